@@ -1,0 +1,133 @@
+/*
+ * cpfit_gpu.h — C-ABI of the B200-native cpfit hot path (libcpfit_gpu.so).
+ *
+ * Drop-in boundary for the reference's solver API in proj/core/include/cpfit/ (C++20,
+ * Eigen). Every entry point below replaces one reference function; the citation names the
+ * reference declaration it stands for. Conventions:
+ *   - host pointers in and out (the library does the H2D/D2H copies); a tensor handle is
+ *     uploaded once and keeps T resident in HBM (DataTensor, tensor.hpp:129-148);
+ *   - factor sets cross the ABI in the reference's pack() layout (kruskal.cpp:195-206):
+ *     factors in mode order, each column-major I_n x R, total length R * sum I_n;
+ *   - return codes mirror the reference's exceptions: 0 ok, 1 std::invalid_argument,
+ *     2 cpfit::numerical_error (errors.hpp:9-12), 3 CUDA / other failure; the message is
+ *     available from cpfit_last_error() (thread-local);
+ *   - distinct tensor handles may be used from different threads concurrently.
+ * Device limits: order <= 8, rank <= 32, dense I_1 <= 512 (mode-0 fibers tile in smem),
+ * sparse mode sizes < 2^31.
+ */
+#ifndef CPFIT_GPU_H
+#define CPFIT_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cpfit_tensor_s* cpfit_tensor;
+typedef struct cpfit_solver_s* cpfit_solver;
+
+/* trace.hpp:18-29 TraceRecord */
+typedef struct {
+    int32_t iter;
+    int32_t restart;
+    double time_s, f, h, gnorm_rel, beta;
+    int64_t fevals, gevals, precond_calls;
+} cpfit_trace_row;
+
+/* ngmres.hpp:50-57 NgmresOptions + line_search.hpp:7-14 LineSearchParams.
+ * gradient_scale: NgmresProblem::gradient_scale (ngmres.hpp:71); <= 0 selects ||T||_F as in
+ * ngmres_solve (ngmres.cpp:219). */
+typedef struct {
+    int32_t window;
+    int32_t max_iters;
+    double epsilon_reg;
+    double tol_grad;
+    double gradient_scale;
+    double ftol, gtol, initial_step;
+    int32_t max_evals;
+    int32_t restart_on_ascent;
+    double step_min, step_max;
+} cpfit_ngmres_options;
+
+/* line_search.hpp:7-14 / 23-29 */
+typedef struct {
+    double ftol, gtol, initial_step;
+    int32_t max_evals;
+    double step_min, step_max;
+} cpfit_line_search_params;
+typedef struct {
+    double step, f, dg;
+    int32_t status; /* 0 Converged, 1 MaxEvals, 2 NotDescent, 3 NumericalStall */
+    int32_t evals;
+} cpfit_line_search_result;
+typedef void (*cpfit_phi_fn)(double step, double* f, double* dg, void* ctx);
+
+const char* cpfit_last_error(void);
+int cpfit_device_count(void);
+void cpfit_default_ngmres_options(cpfit_ngmres_options* o);
+
+/* DataTensor(DenseTensor) — tensor.hpp:46-60, 129-148 (values first-mode-fastest). */
+int cpfit_tensor_create_dense(int order, const int64_t* dims, const double* values, cpfit_tensor* out);
+/* DataTensor(SparseTensor) — tensor.hpp:66-88: coords nnz*N AoS, canonicalised like the
+ * reference constructor (tensor.cpp:56-103). */
+int cpfit_tensor_create_coo(int order, const int64_t* dims, int64_t nnz, const int64_t* coords,
+                            const double* values, cpfit_tensor* out);
+int cpfit_tensor_destroy(cpfit_tensor t);
+/* DataTensor::norm() — tensor.hpp:139 */
+int cpfit_tensor_norm(cpfit_tensor t, double* norm);
+/* SparseTensor::nnz() after canonicalisation — tensor.hpp:75 */
+int cpfit_tensor_nnz(cpfit_tensor t, int64_t* nnz);
+
+/* DataTensor::mttkrp(factors, mode) — tensor.hpp:142; out is I_mode x R column-major. */
+int cpfit_mttkrp(cpfit_tensor t, int64_t rank, const double* u, int mode, double* out);
+/* objective(t, k) — kruskal.hpp:36 */
+int cpfit_objective(cpfit_tensor t, int64_t rank, const double* u, double* f);
+/* objective_and_gradient(t, k, grad) — kruskal.hpp:43; grad in pack() layout. */
+int cpfit_objective_and_gradient(cpfit_tensor t, int64_t rank, const double* u, double* grad, double* f);
+/* gram_hadamard(factors, skip) — tensor.hpp:124; out R x R column-major. */
+int cpfit_gram_hadamard(int order, const int64_t* dims, int64_t rank, const double* u, int skip, double* out);
+/* normalize_and_reorder(k) — kruskal.hpp:54 */
+int cpfit_normalize_and_reorder(int order, const int64_t* dims, int64_t rank, const double* u, double* out);
+/* als_sweep(t, k) — als.hpp:14 */
+int cpfit_als_sweep(cpfit_tensor t, int64_t rank, const double* u, double* out);
+/* accelerate(window, u_bar, g_bar, eps) — ngmres.hpp:44-45. window_u / window_g hold m
+ * vectors of length n, oldest first (AccelWindow order, ngmres.hpp:16-35). */
+int cpfit_accelerate(int64_t n, int64_t m, const double* window_u, const double* window_g, const double* u_bar,
+                     const double* g_bar, double epsilon_reg, double* u_hat, double* alpha, double* residual_rel);
+/* more_thuente(eval, phi0, dphi0, params) — line_search.hpp:41-42 (host state machine shared
+ * with the device line search). */
+int cpfit_more_thuente(cpfit_phi_fn phi, void* ctx, double phi0, double dphi0, const cpfit_line_search_params* p,
+                       cpfit_line_search_result* out);
+/* ngmres_solve(t, initial, opts) — ngmres.hpp:126-127; the whole solve is device resident.
+ * u_best receives the best-f iterate (pack layout), trace up to `cap` rows. */
+int cpfit_ngmres_solve(cpfit_tensor t, int64_t rank, const double* u0, const cpfit_ngmres_options* o, double* u_best,
+                       double* f_best, cpfit_trace_row* trace, int64_t cap, int64_t* rows, int* stop_reason);
+/* als_solve(t, initial, opts) — als.hpp:23 */
+int cpfit_als_solve(cpfit_tensor t, int64_t rank, const double* u0, double tol_grad, int max_iters, double* u_best,
+                    double* f_best, cpfit_trace_row* trace, int64_t cap, int64_t* rows, int* stop_reason);
+
+/* Persistent solver handle for measurement (the same device loop as cpfit_ngmres_solve,
+ * split into init + timed loop launches). method 0: N-GMRES, 1: ALS. */
+int cpfit_solver_create(cpfit_tensor t, int64_t rank, const cpfit_ngmres_options* o, int method, cpfit_solver* out);
+int cpfit_solver_set_initial(cpfit_solver s, const double* u0);
+int cpfit_solver_init(cpfit_solver s);
+/* runs until max_iters_total iterations (or a stop); *ms = CUDA-event time on the solver stream */
+int cpfit_solver_run(cpfit_solver s, int max_iters_total, float* ms);
+int cpfit_solver_state(cpfit_solver s, int* iters, int* stop_reason, double* f, double* best_f, int64_t* fevals);
+int cpfit_solver_trace(cpfit_solver s, cpfit_trace_row* trace, int64_t rows);
+int cpfit_solver_best(cpfit_solver s, double* u);
+/* current (last accepted, canonical) iterate */
+int cpfit_solver_iterate(cpfit_solver s, double* u);
+int cpfit_solver_destroy(cpfit_solver s);
+
+/* Device-resident kernel timing (inputs already in HBM): average ms per call over `reps`
+ * calls timed with CUDA events on the launching stream, L2 flushed between calls when
+ * flush_l2 != 0. kind: 0 mttkrp(mode), 1 objective_and_gradient, 2 als_sweep. */
+int cpfit_bench_kernel(cpfit_tensor t, int64_t rank, const double* u, int kind, int mode, int reps, int flush_l2,
+                       float* ms_per_call);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPFIT_GPU_H */

@@ -1,0 +1,278 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY. ctypes binding of oracle/_build/liboracle.so, the CPU
+restatement of the reference (proj/core/src/*.cpp). Used only as the parity checker and the
+CPU baseline; the product never imports it."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "liboracle.so")
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        build()
+    return C.CDLL(LIB_PATH)
+
+
+lib = _load()
+_i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+
+
+class TraceOut(C.Structure):
+    _fields_ = [("iter", C.c_int32), ("restart", C.c_int32), ("f", C.c_double), ("h", C.c_double),
+                ("gnorm_rel", C.c_double), ("beta", C.c_double), ("fevals", C.c_int64), ("gevals", C.c_int64),
+                ("precond_calls", C.c_int64)]
+
+
+class Opts(C.Structure):
+    _fields_ = [("window", C.c_int32), ("max_iters", C.c_int32), ("epsilon_reg", C.c_double),
+                ("tol_grad", C.c_double), ("ftol", C.c_double), ("gtol", C.c_double), ("initial_step", C.c_double),
+                ("max_evals", C.c_int32), ("restart_on_ascent", C.c_int32), ("step_min", C.c_double),
+                ("step_max", C.c_double)]
+
+
+PHI = C.CFUNCTYPE(None, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
+
+_SIGS = {
+    "oracle_last_error": (C.c_char_p, []),
+    "oracle_tensor_dense": (C.c_int, [C.c_int, _i64p, _f64p, C.POINTER(C.c_void_p)]),
+    "oracle_tensor_sparse": (C.c_int, [C.c_int, _i64p, C.c_int64, _i64p, _f64p, C.POINTER(C.c_void_p)]),
+    "oracle_tensor_nnz": (C.c_int64, [C.c_void_p]),
+    "oracle_tensor_sparse_contents": (C.c_int, [C.c_void_p, _i64p, _f64p]),
+    "oracle_tensor_free": (None, [C.c_void_p]),
+    "oracle_tensor_norm": (C.c_double, [C.c_void_p]),
+    "oracle_mttkrp": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_int, _f64p]),
+    "oracle_objective": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.POINTER(C.c_double)]),
+    "oracle_eval": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p, C.POINTER(C.c_double)]),
+    "oracle_gram_hadamard": (C.c_int, [C.c_int, _i64p, C.c_int64, _f64p, C.c_int, _f64p]),
+    "oracle_normalize": (C.c_int, [C.c_int, _i64p, C.c_int64, _f64p, _f64p]),
+    "oracle_full": (C.c_int, [C.c_int, _i64p, C.c_int64, _f64p, _f64p]),
+    "oracle_als_sweep": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p]),
+    "oracle_accelerate": (C.c_int, [C.c_int64, C.c_int64, _f64p, _f64p, _f64p, _f64p, C.c_double, _f64p, _f64p,
+                                    C.POINTER(C.c_double)]),
+    "oracle_ngmres_cp": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.POINTER(Opts), C.c_double, C.c_int, _f64p,
+                                   C.POINTER(C.c_double), C.POINTER(TraceOut), C.c_int64, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int), C.c_void_p, C.POINTER(C.c_double)]),
+    "oracle_als_solve": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_double, C.c_int, _f64p, C.POINTER(TraceOut),
+                                   C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
+    "oracle_more_thuente": (C.c_int, [PHI, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                      C.c_int, C.c_double, C.c_double, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int)]),
+    "oracle_ngmres_linear": (C.c_int, [C.c_int64, _f64p, _f64p, C.c_double, _f64p, C.c_int, C.c_int, C.c_double,
+                                       C.c_double, C.c_int, C.c_double, C.c_int, _f64p, _f64p,
+                                       C.POINTER(C.c_int64)]),
+    "oracle_ncg_cp": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_double, C.c_int, _f64p, C.POINTER(TraceOut),
+                                C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
+}
+for _n, (_r, _a) in _SIGS.items():
+    _f = getattr(lib, _n)
+    _f.restype = _r
+    _f.argtypes = _a
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+class OracleNumericalError(OracleError):
+    pass
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    msg = lib.oracle_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise OracleNumericalError(msg)
+    raise OracleError(msg)
+
+
+def _f64(x):
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+class Tensor:
+    def __init__(self, h, dims):
+        self.h = h
+        self.dims = tuple(int(d) for d in dims)
+
+    @classmethod
+    def dense(cls, dims, flat):
+        dims = np.ascontiguousarray(dims, dtype=np.int64)
+        flat = _f64(flat).reshape(-1)
+        if flat.size != int(np.prod(dims)):
+            raise ValueError("DenseTensor: value count does not match shape")
+        h = C.c_void_p()
+        _check(lib.oracle_tensor_dense(len(dims), dims, flat, C.byref(h)))
+        return cls(h, dims)
+
+    @classmethod
+    def coo(cls, dims, coords, vals):
+        dims = np.ascontiguousarray(dims, dtype=np.int64)
+        coords = np.ascontiguousarray(coords, dtype=np.int64).reshape(-1)
+        vals = _f64(vals).reshape(-1)
+        h = C.c_void_p()
+        _check(lib.oracle_tensor_sparse(len(dims), dims, vals.size, coords, vals, C.byref(h)))
+        return cls(h, dims)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.oracle_tensor_free(self.h)
+            self.h = None
+
+    def norm(self):
+        return lib.oracle_tensor_norm(self.h)
+
+    def rank_of(self, u):
+        return _f64(u).size // sum(self.dims)
+
+    def sparse_contents(self):
+        n = lib.oracle_tensor_nnz(self.h)
+        c = np.empty(n * len(self.dims), dtype=np.int64)
+        v = np.empty(n)
+        _check(lib.oracle_tensor_sparse_contents(self.h, c, v))
+        return c.reshape(n, -1), v
+
+    def mttkrp(self, u, mode):
+        r = self.rank_of(u)
+        out = np.empty(self.dims[mode] * r)
+        _check(lib.oracle_mttkrp(self.h, r, _f64(u), mode, out))
+        return out.reshape((self.dims[mode], r), order="F")
+
+    def objective(self, u):
+        f = C.c_double()
+        _check(lib.oracle_objective(self.h, self.rank_of(u), _f64(u), C.byref(f)))
+        return f.value
+
+    def eval(self, u):
+        g = np.empty(_f64(u).size)
+        f = C.c_double()
+        _check(lib.oracle_eval(self.h, self.rank_of(u), _f64(u), g, C.byref(f)))
+        return f.value, g
+
+    def als_sweep(self, u):
+        out = np.empty(_f64(u).size)
+        _check(lib.oracle_als_sweep(self.h, self.rank_of(u), _f64(u), out))
+        return out
+
+    def ngmres(self, u0, window=20, max_iters=2000, epsilon_reg=1e-12, tol_grad=1e-9, gradient_scale=None,
+               restart_on_ascent=True, record_iterates=0, ftol=1e-4, gtol=1e-2, initial_step=1.0, max_evals=20):
+        u0 = _f64(u0)
+        r = self.rank_of(u0)
+        o = Opts(window, max_iters, epsilon_reg, tol_grad, ftol, gtol, initial_step, max_evals,
+                 int(restart_on_ascent), 0.0, 1e20)
+        cap = max_iters + 1
+        tr = (TraceOut * cap)()
+        ub = np.empty_like(u0)
+        fb = C.c_double()
+        rows = C.c_int64()
+        stop = C.c_int()
+        secs = C.c_double()
+        its = np.empty((max(record_iterates, 1), u0.size))
+        gs = self.norm() if gradient_scale is None else gradient_scale
+        _check(lib.oracle_ngmres_cp(self.h, r, u0, C.byref(o), gs, record_iterates, ub, C.byref(fb), tr, cap,
+                                    C.byref(rows), C.byref(stop), its.ctypes.data if record_iterates else None,
+                                    C.byref(secs)))
+        return dict(u=ub, f=fb.value, trace=_trace(tr, rows.value), stop=stop.value, seconds=secs.value,
+                    iterates=its[:min(record_iterates, rows.value)] if record_iterates else None)
+
+    def als_solve(self, u0, tol_grad=1e-9, max_iters=2000):
+        u0 = _f64(u0)
+        cap = max_iters + 1
+        tr = (TraceOut * cap)()
+        ub = np.empty_like(u0)
+        rows = C.c_int64()
+        stop = C.c_int()
+        _check(lib.oracle_als_solve(self.h, self.rank_of(u0), u0, tol_grad, max_iters, ub, tr, cap, C.byref(rows),
+                                    C.byref(stop)))
+        return dict(u=ub, trace=_trace(tr, rows.value), stop=stop.value)
+
+    def ncg(self, u0, tol_grad=1e-9, max_iters=2000):
+        u0 = _f64(u0)
+        cap = max_iters + 1
+        tr = (TraceOut * cap)()
+        ub = np.empty_like(u0)
+        rows = C.c_int64()
+        stop = C.c_int()
+        _check(lib.oracle_ncg_cp(self.h, self.rank_of(u0), u0, tol_grad, max_iters, ub, tr, cap, C.byref(rows),
+                                 C.byref(stop)))
+        return dict(u=ub, trace=_trace(tr, rows.value), stop=stop.value)
+
+
+def _trace(tr, rows):
+    return [dict(iter=t.iter, f=t.f, h=t.h, gnorm_rel=t.gnorm_rel, fevals=t.fevals, gevals=t.gevals,
+                 precond_calls=t.precond_calls, restart=bool(t.restart), beta=t.beta) for t in tr[:rows]]
+
+
+def gram_hadamard(dims, rank, u, skip=-1):
+    dims = np.ascontiguousarray(dims, dtype=np.int64)
+    out = np.empty(rank * rank)
+    _check(lib.oracle_gram_hadamard(len(dims), dims, rank, _f64(u), skip, out))
+    return out.reshape((rank, rank), order="F")
+
+
+def normalize(dims, rank, u):
+    dims = np.ascontiguousarray(dims, dtype=np.int64)
+    out = np.empty(_f64(u).size)
+    _check(lib.oracle_normalize(len(dims), dims, rank, _f64(u), out))
+    return out
+
+
+def full(dims, rank, u):
+    dims = np.ascontiguousarray(dims, dtype=np.int64)
+    out = np.empty(int(np.prod(dims)))
+    _check(lib.oracle_full(len(dims), dims, rank, _f64(u), out))
+    return out
+
+
+def accelerate(window_u, window_g, u_bar, g_bar, eps=1e-12):
+    wu = np.ascontiguousarray(np.asarray(window_u, dtype=np.float64).reshape(len(window_u), -1))
+    wg = np.ascontiguousarray(np.asarray(window_g, dtype=np.float64).reshape(len(window_g), -1))
+    m, n = wu.shape
+    uh = np.empty(n)
+    al = np.empty(m)
+    rr = C.c_double()
+    _check(lib.oracle_accelerate(n, m, wu.reshape(-1), wg.reshape(-1), _f64(u_bar), _f64(g_bar), eps, uh, al,
+                                 C.byref(rr)))
+    return uh, al, rr.value
+
+
+def more_thuente(phi, phi0, dphi0, ftol=1e-4, gtol=1e-2, initial_step=1.0, max_evals=20, step_min=0.0,
+                 step_max=1e20):
+    def cb(s, fp, gp, _):
+        f, g = phi(s)
+        fp[0] = f
+        gp[0] = g
+
+    fn = PHI(cb)
+    st, f, g = C.c_double(), C.c_double(), C.c_double()
+    status, ev = C.c_int(), C.c_int()
+    _check(lib.oracle_more_thuente(fn, None, phi0, dphi0, ftol, gtol, initial_step, max_evals, step_min, step_max,
+                                   C.byref(st), C.byref(f), C.byref(g), C.byref(status), C.byref(ev)))
+    return dict(step=st.value, f=f.value, dg=g.value, status=status.value, evals=ev.value)
+
+
+def ngmres_linear(a, b, omega, u0, window, max_iters, epsilon_reg, tol_grad, restart_on_ascent=False,
+                  fixed_step=None):
+    n = len(b)
+    u = np.empty(n)
+    obs = np.empty(max_iters + 2)
+    cnt = C.c_int64()
+    _check(lib.oracle_ngmres_linear(n, _f64(np.asarray(a).reshape(-1, order="F")), _f64(b), omega, _f64(u0), window,
+                                    max_iters, epsilon_reg, tol_grad, int(restart_on_ascent),
+                                    0.0 if fixed_step is None else fixed_step, int(fixed_step is not None), u, obs,
+                                    C.byref(cnt)))
+    return u, obs[:cnt.value]

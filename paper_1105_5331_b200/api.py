@@ -1,0 +1,561 @@
+"""Python host mirror of the reference solver API over the C-ABI (include/cpfit_gpu.h).
+
+Names, argument meaning and error behaviour follow proj/core/include/cpfit/*.hpp:
+``DataTensor`` (tensor.hpp:129-148), ``mttkrp`` (tensor.hpp:119-120), ``gram_hadamard``
+(tensor.hpp:124), ``objective`` / ``objective_and_gradient`` / ``normalize_and_reorder`` /
+``pack`` / ``unpack`` (kruskal.hpp:29-58), ``als_sweep`` / ``als_solve`` (als.hpp:14,23),
+``accelerate`` / ``ngmres_solve`` (ngmres.hpp:44-127), ``more_thuente`` (line_search.hpp:41).
+std::invalid_argument -> ValueError, cpfit::numerical_error -> NumericalError.
+
+All compute goes through libcpfit_gpu.so (sm_100a kernels). There is no CPU fallback: if the
+library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libcpfit_gpu.so")
+
+
+class NumericalError(RuntimeError):
+    """cpfit::numerical_error (errors.hpp:9-12)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the B200 path has no CPU fallback)")
+    return C.CDLL(LIB_PATH)
+
+
+lib = _load()
+
+_i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+
+
+class TraceRow(C.Structure):
+    _fields_ = [("iter", C.c_int32), ("restart", C.c_int32), ("time_s", C.c_double), ("f", C.c_double),
+                ("h", C.c_double), ("gnorm_rel", C.c_double), ("beta", C.c_double), ("fevals", C.c_int64),
+                ("gevals", C.c_int64), ("precond_calls", C.c_int64)]
+
+
+class NgmresOptionsC(C.Structure):
+    _fields_ = [("window", C.c_int32), ("max_iters", C.c_int32), ("epsilon_reg", C.c_double),
+                ("tol_grad", C.c_double), ("gradient_scale", C.c_double), ("ftol", C.c_double),
+                ("gtol", C.c_double), ("initial_step", C.c_double), ("max_evals", C.c_int32),
+                ("restart_on_ascent", C.c_int32), ("step_min", C.c_double), ("step_max", C.c_double)]
+
+
+class LsParamsC(C.Structure):
+    _fields_ = [("ftol", C.c_double), ("gtol", C.c_double), ("initial_step", C.c_double),
+                ("max_evals", C.c_int32), ("step_min", C.c_double), ("step_max", C.c_double)]
+
+
+class LsResultC(C.Structure):
+    _fields_ = [("step", C.c_double), ("f", C.c_double), ("dg", C.c_double), ("status", C.c_int32),
+                ("evals", C.c_int32)]
+
+
+PHI_FN = C.CFUNCTYPE(None, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
+
+# symbol table: name -> (restype, argtypes)
+_SIGS = {
+    "cpfit_last_error": (C.c_char_p, []),
+    "cpfit_device_count": (C.c_int, []),
+    "cpfit_tensor_create_dense": (C.c_int, [C.c_int, _i64p, _f64p, C.POINTER(C.c_void_p)]),
+    "cpfit_tensor_create_coo": (C.c_int, [C.c_int, _i64p, C.c_int64, _i64p, _f64p, C.POINTER(C.c_void_p)]),
+    "cpfit_tensor_destroy": (C.c_int, [C.c_void_p]),
+    "cpfit_tensor_norm": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    "cpfit_tensor_nnz": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "cpfit_mttkrp": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_int, _f64p]),
+    "cpfit_objective": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.POINTER(C.c_double)]),
+    "cpfit_objective_and_gradient": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p, C.POINTER(C.c_double)]),
+    "cpfit_gram_hadamard": (C.c_int, [C.c_int, _i64p, C.c_int64, _f64p, C.c_int, _f64p]),
+    "cpfit_normalize_and_reorder": (C.c_int, [C.c_int, _i64p, C.c_int64, _f64p, _f64p]),
+    "cpfit_als_sweep": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p]),
+    "cpfit_accelerate": (C.c_int, [C.c_int64, C.c_int64, _f64p, _f64p, _f64p, _f64p, C.c_double, _f64p, _f64p,
+                                   C.POINTER(C.c_double)]),
+    "cpfit_more_thuente": (C.c_int, [PHI_FN, C.c_void_p, C.c_double, C.c_double, C.POINTER(LsParamsC),
+                                     C.POINTER(LsResultC)]),
+    "cpfit_ngmres_solve": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.POINTER(NgmresOptionsC), _f64p,
+                                     C.POINTER(C.c_double), C.POINTER(TraceRow), C.c_int64, C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int)]),
+    "cpfit_als_solve": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_double, C.c_int, _f64p, C.POINTER(C.c_double),
+                                  C.POINTER(TraceRow), C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
+    "cpfit_solver_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(NgmresOptionsC), C.c_int,
+                                      C.POINTER(C.c_void_p)]),
+    "cpfit_solver_set_initial": (C.c_int, [C.c_void_p, _f64p]),
+    "cpfit_solver_init": (C.c_int, [C.c_void_p]),
+    "cpfit_solver_run": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_float)]),
+    "cpfit_solver_state": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "cpfit_solver_trace": (C.c_int, [C.c_void_p, C.POINTER(TraceRow), C.c_int64]),
+    "cpfit_solver_best": (C.c_int, [C.c_void_p, _f64p]),
+    "cpfit_solver_iterate": (C.c_int, [C.c_void_p, _f64p]),
+    "cpfit_solver_destroy": (C.c_int, [C.c_void_p]),
+    "cpfit_bench_kernel": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(C.c_float)]),
+    # problems (host)
+    "cpfit_problems_last_error": (C.c_char_p, []),
+    "cpfit_rng_draws": (C.c_int, [C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cpfit_rng_mix": (C.c_uint64, [C.c_uint64]),
+    "cpfit_collinear_factors": (C.c_int, [C.c_int, _i64p, C.c_int64, C.c_double, C.c_uint64, _f64p]),
+    "cpfit_full": (C.c_int, [C.c_int, _i64p, C.c_int64, _f64p, _f64p]),
+    "cpfit_dense_test_problem": (C.c_int, [C.c_int, _i64p, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                           C.c_uint64, C.c_int, _f64p, C.c_void_p, C.c_void_p]),
+    "cpfit_uniform_initial_guess": (C.c_int, [C.c_int, _i64p, C.c_int64, C.c_uint64, _f64p]),
+    "cpfit_laplacian_tensor": (C.c_int, [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "cpfit_random_sparse_problem": (C.c_int, [C.c_int, _i64p, C.c_int64, C.c_int64, C.c_double, C.c_uint64,
+                                              _i64p, _f64p, C.c_void_p]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+EXPORTED_SYMBOLS = sorted(_SIGS)
+
+
+def _check(rc: int, problems: bool = False):
+    if rc == 0:
+        return
+    msg = (lib.cpfit_problems_last_error() if problems else lib.cpfit_last_error()).decode(errors="replace")
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise NumericalError(msg)
+    raise CudaError(msg)
+
+
+def device_count() -> int:
+    return int(lib.cpfit_device_count())
+
+
+def _f64(x) -> np.ndarray:
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def _dims(d) -> np.ndarray:
+    return np.ascontiguousarray(d, dtype=np.int64)
+
+
+# ---- pack / unpack (kruskal.cpp:195-221) ---------------------------------------------------
+
+def pack(factors) -> np.ndarray:
+    return np.concatenate([np.asarray(a, dtype=np.float64).reshape(-1, order="F") for a in factors])
+
+
+def unpack(u, dims, rank):
+    u = _f64(u)
+    total = sum(int(d) * rank for d in dims)
+    if u.size != total:
+        raise ValueError("unpack: vector length does not match shape and rank")
+    out, at = [], 0
+    for d in dims:
+        out.append(u[at:at + d * rank].reshape((d, rank), order="F"))
+        at += d * rank
+    return out
+
+
+# ---- tensors --------------------------------------------------------------------------------
+
+class DataTensor:
+    """Device-resident DataTensor (tensor.hpp:129-148). T is uploaded once (dense values in
+    first-mode-fastest order, or COO with nnz x N int64 coordinates)."""
+
+    def __init__(self, handle, dims, sparse):
+        self._h = handle
+        self.dims = tuple(int(d) for d in dims)
+        self.order = len(self.dims)
+        self.is_sparse = sparse
+
+    @classmethod
+    def dense(cls, values, dims=None):
+        values = np.asarray(values, dtype=np.float64)
+        if dims is None:
+            dims = values.shape
+            flat = np.ascontiguousarray(values.reshape(-1, order="F"))
+        else:
+            flat = _f64(values).reshape(-1)
+        dims = _dims(dims)
+        if flat.size != int(np.prod(dims)):
+            raise ValueError("DenseTensor: value count does not match shape")
+        h = C.c_void_p()
+        _check(lib.cpfit_tensor_create_dense(len(dims), dims, flat, C.byref(h)))
+        return cls(h, dims, False)
+
+    @classmethod
+    def coo(cls, dims, coords, values):
+        dims = _dims(dims)
+        coords = np.ascontiguousarray(coords, dtype=np.int64).reshape(-1)
+        values = _f64(values).reshape(-1)
+        if coords.size != values.size * len(dims):
+            raise ValueError("SparseTensor: coords/values size mismatch")
+        h = C.c_void_p()
+        _check(lib.cpfit_tensor_create_coo(len(dims), dims, values.size, coords, values, C.byref(h)))
+        return cls(h, dims, True)
+
+    def close(self):
+        if self._h:
+            lib.cpfit_tensor_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def norm(self) -> float:
+        v = C.c_double()
+        _check(lib.cpfit_tensor_norm(self._h, C.byref(v)))
+        return v.value
+
+    def nnz(self) -> int:
+        v = C.c_int64()
+        _check(lib.cpfit_tensor_nnz(self._h, C.byref(v)))
+        return v.value
+
+    def nu(self, rank):
+        return sum(d * rank for d in self.dims)
+
+    def _rank(self, u):
+        u = _f64(u)
+        s = sum(self.dims)
+        if u.size % s:
+            raise ValueError("tensor and Kruskal model shapes must match")
+        return u, u.size // s
+
+    def mttkrp(self, u, mode):
+        u, r = self._rank(u)
+        if not 0 <= mode < self.order:
+            raise ValueError("mttkrp: mode out of range")
+        out = np.empty(self.dims[mode] * r)
+        _check(lib.cpfit_mttkrp(self._h, r, u, mode, out))
+        return out.reshape((self.dims[mode], r), order="F")
+
+
+def mttkrp(t: DataTensor, u, mode):
+    return t.mttkrp(u, mode)
+
+
+def objective(t: DataTensor, u) -> float:
+    u, r = t._rank(u)
+    f = C.c_double()
+    _check(lib.cpfit_objective(t._h, r, u, C.byref(f)))
+    return f.value
+
+
+def objective_and_gradient(t: DataTensor, u):
+    u, r = t._rank(u)
+    g = np.empty(u.size)
+    f = C.c_double()
+    _check(lib.cpfit_objective_and_gradient(t._h, r, u, g, C.byref(f)))
+    return f.value, g
+
+
+def gradient(t, u):
+    return objective_and_gradient(t, u)[1]
+
+
+def fit_h(t: DataTensor, u) -> float:
+    n = t.norm()
+    if not n > 0.0:
+        raise ValueError("fit_h: data tensor must be nonzero")
+    return float(np.sqrt(max(2.0 * objective(t, u), 0.0)) / n)
+
+
+def gram_hadamard(dims, rank, u, skip=-1):
+    dims = _dims(dims)
+    out = np.empty(rank * rank)
+    _check(lib.cpfit_gram_hadamard(len(dims), dims, rank, _f64(u), skip, out))
+    return out.reshape((rank, rank), order="F")
+
+
+def normalize_and_reorder(dims, rank, u):
+    dims = _dims(dims)
+    u = _f64(u)
+    out = np.empty_like(u)
+    _check(lib.cpfit_normalize_and_reorder(len(dims), dims, rank, u, out))
+    return out
+
+
+def als_sweep(t: DataTensor, u):
+    u, r = t._rank(u)
+    out = np.empty_like(u)
+    _check(lib.cpfit_als_sweep(t._h, r, u, out))
+    return out
+
+
+@dataclass
+class AccelOutcome:
+    u_hat: np.ndarray
+    alpha: np.ndarray
+    system_residual_rel: float
+
+
+def accelerate(window_u, window_g, u_bar, g_bar, epsilon_reg=1e-12) -> AccelOutcome:
+    """accelerate(window, u_bar, g_bar, eps) — window lists oldest first (ngmres.hpp:44)."""
+    wu = np.ascontiguousarray(np.asarray(window_u, dtype=np.float64).reshape(len(window_u), -1))
+    wg = np.ascontiguousarray(np.asarray(window_g, dtype=np.float64).reshape(len(window_g), -1))
+    m, n = wu.shape
+    uh = np.empty(n)
+    al = np.empty(max(m, 1))
+    rr = C.c_double()
+    _check(lib.cpfit_accelerate(n, m, wu.reshape(-1), wg.reshape(-1), _f64(u_bar), _f64(g_bar), epsilon_reg, uh, al,
+                                C.byref(rr)))
+    return AccelOutcome(uh, al[:m], rr.value)
+
+
+# ---- line search ----------------------------------------------------------------------------
+
+CONVERGED, MAX_EVALS, NOT_DESCENT, NUMERICAL_STALL = 0, 1, 2, 3
+
+
+@dataclass
+class LineSearchParams:
+    ftol: float = 1e-4
+    gtol: float = 1e-2
+    initial_step: float = 1.0
+    max_evals: int = 20
+    step_min: float = 0.0
+    step_max: float = 1e20
+
+
+@dataclass
+class LineSearchResult:
+    step: float
+    f: float
+    dg: float
+    status: int
+    evals: int
+
+
+def more_thuente(phi, phi0, dphi0, params: LineSearchParams = None) -> LineSearchResult:
+    """phi(step) -> (f, dg). Same state machine the device line search runs."""
+    p = params or LineSearchParams()
+    err = []
+
+    def cb(step, fp, gp, _ctx):
+        try:
+            f, g = phi(step)
+            fp[0] = f
+            gp[0] = g
+        except Exception as e:  # pragma: no cover
+            err.append(e)
+            fp[0] = float("nan")
+            gp[0] = float("nan")
+
+    fn = PHI_FN(cb)
+    cp = LsParamsC(p.ftol, p.gtol, p.initial_step, p.max_evals, p.step_min, p.step_max)
+    out = LsResultC()
+    _check(lib.cpfit_more_thuente(fn, None, phi0, dphi0, C.byref(cp), C.byref(out)))
+    if err:
+        raise err[0]
+    return LineSearchResult(out.step, out.f, out.dg, out.status, out.evals)
+
+
+# ---- solvers --------------------------------------------------------------------------------
+
+GRAD_TOL, MAX_ITERS, STALLED = 0, 1, 2
+
+
+@dataclass
+class NgmresOptions:
+    window: int = 20
+    epsilon_reg: float = 1e-12
+    tol_grad: float = 1e-9
+    max_iters: int = 2000
+    line_search: LineSearchParams = field(default_factory=LineSearchParams)
+    restart_on_ascent: bool = True
+    gradient_scale: float = 0.0  # <= 0: ||T||_F as in ngmres_solve
+
+    def c(self):
+        ls = self.line_search
+        return NgmresOptionsC(self.window, self.max_iters, self.epsilon_reg, self.tol_grad, self.gradient_scale,
+                              ls.ftol, ls.gtol, ls.initial_step, ls.max_evals, int(self.restart_on_ascent),
+                              ls.step_min, ls.step_max)
+
+
+@dataclass
+class SolveResult:
+    solution: np.ndarray  # best-f iterate, pack layout
+    f: float
+    trace: list
+    stop_reason: int
+
+
+def _trace_list(buf, rows):
+    return [dict(iter=r.iter, time_s=r.time_s, f=r.f, h=r.h, gnorm_rel=r.gnorm_rel, fevals=r.fevals,
+                 gevals=r.gevals, precond_calls=r.precond_calls, restart=bool(r.restart), beta=r.beta)
+            for r in buf[:rows]]
+
+
+def ngmres_solve(t: DataTensor, u0, opts: NgmresOptions = None) -> SolveResult:
+    o = opts or NgmresOptions()
+    u0, r = t._rank(u0)
+    cap = o.max_iters + 1
+    trace = (TraceRow * cap)()
+    ub = np.empty_like(u0)
+    fb = C.c_double()
+    rows = C.c_int64()
+    stop = C.c_int()
+    oc = o.c()
+    _check(lib.cpfit_ngmres_solve(t._h, r, u0, C.byref(oc), ub, C.byref(fb), trace, cap, C.byref(rows),
+                                  C.byref(stop)))
+    return SolveResult(ub, fb.value, _trace_list(trace, rows.value), stop.value)
+
+
+def als_solve(t: DataTensor, u0, tol_grad=1e-9, max_iters=2000) -> SolveResult:
+    u0, r = t._rank(u0)
+    cap = max_iters + 1
+    trace = (TraceRow * cap)()
+    ub = np.empty_like(u0)
+    fb = C.c_double()
+    rows = C.c_int64()
+    stop = C.c_int()
+    _check(lib.cpfit_als_solve(t._h, r, u0, tol_grad, max_iters, ub, C.byref(fb), trace, cap, C.byref(rows),
+                               C.byref(stop)))
+    return SolveResult(ub, fb.value, _trace_list(trace, rows.value), stop.value)
+
+
+class Solver:
+    """Persistent device solver (measurement surface): init once, then timed loop launches."""
+
+    def __init__(self, t: DataTensor, rank: int, opts: NgmresOptions, method: int = 0):
+        self.t = t
+        h = C.c_void_p()
+        oc = opts.c()
+        _check(lib.cpfit_solver_create(t._h, rank, C.byref(oc), method, C.byref(h)))
+        self._h = h
+        self.rank = rank
+        self.max_iters = opts.max_iters
+
+    def set_initial(self, u0):
+        _check(lib.cpfit_solver_set_initial(self._h, _f64(u0)))
+
+    def init(self):
+        _check(lib.cpfit_solver_init(self._h))
+
+    def run(self, max_iters_total) -> float:
+        ms = C.c_float()
+        _check(lib.cpfit_solver_run(self._h, int(max_iters_total), C.byref(ms)))
+        return ms.value
+
+    def state(self):
+        it, st, fe = C.c_int(), C.c_int(), C.c_int64()
+        f, bf = C.c_double(), C.c_double()
+        _check(lib.cpfit_solver_state(self._h, C.byref(it), C.byref(st), C.byref(f), C.byref(bf), C.byref(fe)))
+        return dict(iters=it.value, stop=st.value, f=f.value, best_f=bf.value, fevals=fe.value)
+
+    def trace(self, rows):
+        buf = (TraceRow * rows)()
+        _check(lib.cpfit_solver_trace(self._h, buf, rows))
+        return _trace_list(buf, rows)
+
+    def best(self):
+        out = np.empty(self.t.nu(self.rank))
+        _check(lib.cpfit_solver_best(self._h, out))
+        return out
+
+    def iterate(self):
+        out = np.empty(self.t.nu(self.rank))
+        _check(lib.cpfit_solver_iterate(self._h, out))
+        return out
+
+    def close(self):
+        if self._h:
+            lib.cpfit_solver_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def bench_kernel(t: DataTensor, u, kind: int, mode: int = 0, reps: int = 10, flush_l2: bool = True) -> float:
+    u, r = t._rank(u)
+    ms = C.c_float()
+    _check(lib.cpfit_bench_kernel(t._h, r, u, kind, mode, reps, int(flush_l2), C.byref(ms)))
+    return ms.value
+
+
+# ---- problems (host generators) ---------------------------------------------------------------
+
+def rng_draws(seed, n):
+    u64 = np.empty(n, dtype=np.uint64)
+    uni = np.empty(n)
+    nor = np.empty(n)
+    _check(lib.cpfit_rng_draws(seed, n, u64.ctypes.data, uni.ctypes.data, nor.ctypes.data), True)
+    return u64, uni, nor
+
+
+def rng_mix(x):
+    return int(lib.cpfit_rng_mix(x))
+
+
+def collinear_factors(dims, rank, c, seed):
+    dims = _dims(dims)
+    out = np.empty(int(dims.sum()) * rank)
+    _check(lib.cpfit_collinear_factors(len(dims), dims, rank, c, seed, out), True)
+    return out
+
+
+def full(dims, rank, u):
+    dims = _dims(dims)
+    out = np.empty(int(np.prod(dims)))
+    _check(lib.cpfit_full(len(dims), dims, rank, _f64(u), out), True)
+    return out
+
+
+def dense_test_problem(dims, rank, c, l1, l2, seed, noise_mode=1, want_truth=False, want_noise_free=False):
+    """Returns (T flat first-mode-fastest, truth packed or None, noise-free T or None).
+    noise_mode 0: reference scaling (100/l-1)^(-1/2); 1: BASELINE l/100."""
+    dims = _dims(dims)
+    K = int(np.prod(dims))
+    t = np.empty(K)
+    truth = np.empty(int(dims.sum()) * rank) if want_truth else None
+    nf = np.empty(K) if want_noise_free else None
+    _check(lib.cpfit_dense_test_problem(len(dims), dims, rank, c, l1, l2, seed, noise_mode, t,
+                                        truth.ctypes.data if truth is not None else None,
+                                        nf.ctypes.data if nf is not None else None), True)
+    return t, truth, nf
+
+
+def uniform_initial_guess(dims, rank, seed):
+    dims = _dims(dims)
+    out = np.empty(int(dims.sum()) * rank)
+    _check(lib.cpfit_uniform_initial_guess(len(dims), dims, rank, seed, out), True)
+    return out
+
+
+def laplacian_tensor(d, s):
+    n = C.c_int64()
+    _check(lib.cpfit_laplacian_tensor(d, s, None, None, C.byref(n)), True)
+    coords = np.empty(n.value * 2 * d, dtype=np.int64)
+    vals = np.empty(n.value)
+    _check(lib.cpfit_laplacian_tensor(d, s, coords.ctypes.data, vals.ctypes.data, C.byref(n)), True)
+    return (s,) * (2 * d), coords.reshape(-1, 2 * d), vals
+
+
+def random_sparse_problem(dims, nnz, rank, noise, seed, want_truth=False):
+    dims = _dims(dims)
+    coords = np.empty(nnz * len(dims), dtype=np.int64)
+    vals = np.empty(nnz)
+    truth = np.empty(int(dims.sum()) * rank) if want_truth else None
+    _check(lib.cpfit_random_sparse_problem(len(dims), dims, nnz, rank, noise, seed, coords, vals,
+                                           truth.ctypes.data if truth is not None else None), True)
+    return coords.reshape(-1, len(dims)), vals, truth

@@ -1,0 +1,491 @@
+// N-GMRES Step II on device (accelerate, ngmres.cpp:27-63).
+//
+// The reference solves min ||P a + g||^2 + delta ||a||^2 (P columns g_bar - g_j, delta =
+// eps * max diag P^T P) by a column-pivoted Householder QR of the stacked n_u+m by m matrix.
+// Here the tall part is reduced first by a communication-avoiding TSQR of X = [P | -g_bar]
+// (one streaming pass over the window, Householder in shared memory per row block, then a
+// tree of merges of the (m+1)x(m+1) R factors). Because Q is orthogonal,
+//   ||P a + g_bar||^2 = ||R_P a - r_c||^2 + rho^2,  ||P e_j|| = ||R_P e_j||,  P^T g_bar = -R_P^T r_c,
+// so delta, the right-hand side and the damped problem are recovered exactly from R, and the
+// small (2m x m) stacked system [R_P; sqrt(delta) I] a = [r_c; 0] is solved with the same
+// column-pivoted Householder algorithm (pivot order by column norms, which equal the tall
+// matrix's) in one warp. u_hat = u_bar + sum_j a_j (u_bar - u_j), d = u_hat - u_bar and the
+// descent slope g_bar.d are formed in a final streaming pass.
+#include "device.cuh"
+
+#include <algorithm>
+
+namespace cpfit_gpu {
+
+namespace {
+
+constexpr int kLeafRows = 256;
+constexpr int kTsqrThreads = 256;
+
+struct TsqrParams {
+    int64_t n;
+    int cap;
+    const int* ring;  // [0] = m, [1] = head slot
+    const double* wg;
+    const double* gb;
+    const double* rin;   // merge input (stacked R's) or null for leaf
+    int64_t nin;         // number of input R's (merge)
+    double* rout;        // output R's [cta][C*C] (col-major C x C, ld = C)
+    int64_t blocks_per_cta;
+    int64_t nblocks;
+    int per_block;       // rows (leaf) or R's (merge) per block
+};
+
+// Householder QR (no pivoting; Eigen makeHouseholder / applyHouseholderOnTheLeft) of the
+// H x C column-major smem matrix x (ld = H); upper triangle left in rows 0..C-1, the rest
+// zeroed.
+__device__ void smem_qr(double* x, int H, int C, double* tau_s) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int K = min(H, C);
+    for (int k = 0; k < K; ++k) {
+        if (warp == 0) {
+            double* col = x + (size_t)k * H;
+            double tail = 0.0;
+            for (int i = k + 1 + lane; i < H; i += 32) tail += col[i] * col[i];
+            tail = warp_sum(tail);
+            const double c0 = col[k];
+            double tau, beta;
+            if (tail <= 2.2250738585072014e-308) {
+                tau = 0.0;
+                beta = c0;
+                for (int i = k + 1 + lane; i < H; i += 32) col[i] = 0.0;
+            } else {
+                beta = sqrt(c0 * c0 + tail);
+                if (c0 >= 0.0) beta = -beta;
+                const double inv = c0 - beta;
+                for (int i = k + 1 + lane; i < H; i += 32) col[i] /= inv;
+                tau = (beta - c0) / beta;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                col[k] = beta;
+                tau_s[0] = tau;
+            }
+        }
+        __syncthreads();
+        const double tau = tau_s[0];
+        const double* v = x + (size_t)k * H;
+        if (tau != 0.0) {
+            for (int j = k + 1 + warp; j < C; j += nw) {
+                double* cj = x + (size_t)j * H;
+                double t = 0.0;
+                for (int i = k + 1 + lane; i < H; i += 32) t += v[i] * cj[i];
+                t = warp_sum(t) + cj[k];
+                if (lane == 0) cj[k] -= tau * t;
+                for (int i = k + 1 + lane; i < H; i += 32) cj[i] -= tau * v[i] * t;
+            }
+        }
+        __syncthreads();
+    }
+    // zero everything below the diagonal (essential parts)
+    for (int e = threadIdx.x; e < H * C; e += blockDim.x) {
+        const int j = e / H, i = e % H;
+        if (i > j) x[e] = 0.0;
+    }
+    __syncthreads();
+}
+
+__global__ void tsqr_kernel(const TsqrParams p) {
+    extern __shared__ double xs[];
+    __shared__ double tau_s[1];
+    const int m = p.ring[0], head = p.ring[1];
+    const int C = m + 1;
+    const int H = C + p.per_block * (p.rin ? C : 1);
+    const int64_t b0 = blockIdx.x * p.blocks_per_cta;
+    const int64_t b1 = imin64(p.nblocks, b0 + p.blocks_per_cta);
+    bool have = false;
+    for (int e = threadIdx.x; e < H * C; e += blockDim.x) xs[e] = 0.0;
+    __syncthreads();
+    for (int64_t b = b0; b < b1; ++b) {
+        const int top = have ? C : 0;
+        if (!p.rin) {
+            const int64_t r0 = b * p.per_block;
+            for (int e = threadIdx.x; e < p.per_block * C; e += blockDim.x) {
+                const int j = e / p.per_block, ii = e % p.per_block;
+                const int64_t i = r0 + ii;
+                double v = 0.0;
+                if (i < p.n) {
+                    const double g = p.gb[i];
+                    if (j < m) {
+                        const int slot = (head + j) % p.cap;
+                        v = g - p.wg[(int64_t)slot * p.n + i];
+                    } else {
+                        v = -g;
+                    }
+                }
+                xs[(size_t)j * H + top + ii] = v;
+            }
+            for (int e = threadIdx.x; e < (H - top - p.per_block) * C; e += blockDim.x) {
+                const int rows = H - top - p.per_block;
+                const int j = e / rows, ii = e % rows;
+                xs[(size_t)j * H + top + p.per_block + ii] = 0.0;
+            }
+        } else {
+            const int64_t k0 = b * p.per_block;
+            for (int e = threadIdx.x; e < p.per_block * C * C; e += blockDim.x) {
+                const int kk = e / (C * C), rem = e % (C * C);
+                const int j = rem / C, i = rem % C;
+                const int64_t src = k0 + kk;
+                xs[(size_t)j * H + top + kk * C + i] = (src < p.nin) ? p.rin[src * C * C + (size_t)j * C + i] : 0.0;
+            }
+            for (int e = threadIdx.x; e < (H - top - p.per_block * C) * C; e += blockDim.x) {
+                const int rows = H - top - p.per_block * C;
+                const int j = e / rows, ii = e % rows;
+                xs[(size_t)j * H + top + p.per_block * C + ii] = 0.0;
+            }
+        }
+        __syncthreads();
+        smem_qr(xs, H, C, tau_s);
+        have = true;
+    }
+    double* out = p.rout + (size_t)blockIdx.x * C * C;
+    for (int e = threadIdx.x; e < C * C; e += blockDim.x) {
+        const int j = e / C, i = e % C;
+        out[e] = have ? xs[(size_t)j * H + i] : 0.0;
+    }
+}
+
+// One warp: damped least squares from the final R, Eigen ColPivHouseholderQR semantics.
+__global__ void accel_solve_kernel(const double* rfin, const int* ring, double eps, double* alpha, double* scal) {
+    extern __shared__ double a[];  // 2m x m stacked system
+    __shared__ double bvec[128];
+    __shared__ double upd[64], dir[64], hc[64], rhs[64], al[64];
+    __shared__ int perm[64], transp[64];
+    const int lane = threadIdx.x;
+    const int m = ring[0];
+    const int C = m + 1;
+    const int rows = 2 * m;
+    // R_P (m x m), r_c (m)
+    double dmax = 0.0;
+    for (int j = 0; j < m; ++j) {
+        double s = 0.0;
+        for (int i = 0; i <= j; ++i) s += rfin[(size_t)j * C + i] * rfin[(size_t)j * C + i];
+        dmax = (j == 0) ? s : fmax(dmax, s);
+    }
+    const double delta = (dmax > 0.0) ? eps * dmax : eps;
+    for (int j = lane; j < m; j += 32) {
+        double s = 0.0;
+        for (int i = 0; i <= j; ++i) s += rfin[(size_t)j * C + i] * rfin[(size_t)m * C + i];
+        rhs[j] = s;  // = -(P^T g_bar)_j
+    }
+    __syncwarp();
+    double rn = 0.0;
+    for (int j = 0; j < m; ++j) rn += rhs[j] * rhs[j];
+    rn = sqrt(rn);
+    if (rn == 0.0) {
+        for (int j = lane; j < m; j += 32) alpha[j] = 0.0;
+        if (lane == 0) {
+            scal[0] = 0.0;
+            scal[2] = delta;
+        }
+        return;
+    }
+    const double sd = sqrt(delta);
+    for (int e = lane; e < rows * m; e += 32) {
+        const int j = e / rows, i = e % rows;
+        double v;
+        if (i < m)
+            v = (i <= j) ? rfin[(size_t)j * C + i] : 0.0;
+        else
+            v = (i - m == j) ? sd : 0.0;
+        a[(size_t)j * rows + i] = v;
+    }
+    for (int i = lane; i < rows; i += 32) bvec[i] = (i < m) ? rfin[(size_t)m * C + i] : 0.0;
+    __syncwarp();
+    const double epsm = 2.220446049250313e-16;
+    for (int j = lane; j < m; j += 32) {
+        double s = 0.0;
+        for (int i = 0; i < rows; ++i) s += a[(size_t)j * rows + i] * a[(size_t)j * rows + i];
+        upd[j] = dir[j] = sqrt(s);
+        perm[j] = j;
+    }
+    __syncwarp();
+    double maxcol = 0.0;
+    for (int j = 0; j < m; ++j) maxcol = fmax(maxcol, upd[j]);
+    const double thr_help = (maxcol * epsm) * (maxcol * epsm) / rows;
+    const double down_thr = sqrt(epsm);
+    int nzp = m;
+    double maxpivot = 0.0;
+    const int size = m;
+    for (int k = 0; k < size; ++k) {
+        int big = k;
+        for (int j = k + 1; j < m; ++j)
+            if (upd[j] > upd[big]) big = j;
+        const double bsq = upd[big] * upd[big];
+        if (nzp == size && bsq < thr_help * (rows - k)) nzp = k;
+        if (lane == 0) transp[k] = big;
+        if (k != big) {
+            for (int i = lane; i < rows; i += 32) {
+                const double t = a[(size_t)k * rows + i];
+                a[(size_t)k * rows + i] = a[(size_t)big * rows + i];
+                a[(size_t)big * rows + i] = t;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                double t = upd[k];
+                upd[k] = upd[big];
+                upd[big] = t;
+                t = dir[k];
+                dir[k] = dir[big];
+                dir[big] = t;
+            }
+        }
+        __syncwarp();
+        // Householder on column k rows k..rows-1
+        double* col = a + (size_t)k * rows;
+        double tail = 0.0;
+        for (int i = k + 1 + lane; i < rows; i += 32) tail += col[i] * col[i];
+        tail = warp_sum(tail);
+        const double c0 = col[k];
+        double tau, beta;
+        if (tail <= 2.2250738585072014e-308) {
+            tau = 0.0;
+            beta = c0;
+            for (int i = k + 1 + lane; i < rows; i += 32) col[i] = 0.0;
+        } else {
+            beta = sqrt(c0 * c0 + tail);
+            if (c0 >= 0.0) beta = -beta;
+            const double inv = c0 - beta;
+            for (int i = k + 1 + lane; i < rows; i += 32) col[i] /= inv;
+            tau = (beta - c0) / beta;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            col[k] = beta;
+            hc[k] = tau;
+        }
+        maxpivot = fmax(maxpivot, fabs(beta));
+        __syncwarp();
+        // apply to columns k+1.. (one lane per column)
+        for (int j = k + 1 + lane; j < m; j += 32) {
+            double* cj = a + (size_t)j * rows;
+            if (rows - k == 1) {
+                cj[k] *= (1.0 - tau);
+            } else if (tau != 0.0) {
+                double t = cj[k];
+                for (int i = k + 1; i < rows; ++i) t += col[i] * cj[i];
+                cj[k] -= tau * t;
+                for (int i = k + 1; i < rows; ++i) cj[i] -= tau * col[i] * t;
+            }
+            // norm downdate
+            if (upd[j] != 0.0) {
+                double t = fabs(cj[k]) / upd[j];
+                t = (1.0 + t) * (1.0 - t);
+                if (t < 0.0) t = 0.0;
+                const double ratio = upd[j] / dir[j];
+                const double t2 = t * ratio * ratio;
+                if (t2 <= down_thr) {
+                    double s = 0.0;
+                    for (int i = k + 1; i < rows; ++i) s += cj[i] * cj[i];
+                    dir[j] = sqrt(s);
+                    upd[j] = dir[j];
+                } else {
+                    upd[j] *= sqrt(t);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        for (int k = 0; k < size; ++k) {
+            const int t = perm[k];
+            perm[k] = perm[transp[k]];
+            perm[transp[k]] = t;
+        }
+        const double thr = maxpivot * epsm * size;
+        int nz = 0;
+        for (int i = 0; i < nzp; ++i) nz += (fabs(a[(size_t)i * rows + i]) > thr) ? 1 : 0;
+        for (int j = 0; j < m; ++j) al[j] = 0.0;
+        if (nz > 0) {
+            double c[128];
+            for (int i = 0; i < rows; ++i) c[i] = bvec[i];
+            for (int k = 0; k < nz; ++k) {
+                const double tau = hc[k];
+                const int n = rows - k;
+                if (n == 1) {
+                    c[k] *= (1.0 - tau);
+                    continue;
+                }
+                if (tau == 0.0) continue;
+                double t = c[k];
+                for (int i = 1; i < n; ++i) t += a[(size_t)k * rows + k + i] * c[k + i];
+                c[k] -= tau * t;
+                for (int i = 1; i < n; ++i) c[k + i] -= tau * a[(size_t)k * rows + k + i] * t;
+            }
+            for (int i = nz - 1; i >= 0; --i) {
+                double s = c[i];
+                for (int j = i + 1; j < nz; ++j) s -= a[(size_t)j * rows + i] * c[j];
+                c[i] = s / a[(size_t)i * rows + i];
+            }
+            for (int i = 0; i < nz; ++i) al[perm[i]] = c[i];
+        }
+        // residual_rel = ||(R_P^T R_P + delta I) alpha - rhs|| / ||rhs||
+        double rr = 0.0;
+        for (int i = 0; i < m; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < m; ++j) {
+                double gij = 0.0;
+                const int top = min(i, j);
+                for (int q = 0; q <= top; ++q) gij += rfin[(size_t)i * C + q] * rfin[(size_t)j * C + q];
+                if (i == j) gij += delta;
+                s += gij * al[j];
+            }
+            s -= rhs[i];
+            rr += s * s;
+        }
+        scal[0] = sqrt(rr) / rn;
+        scal[2] = delta;
+    }
+    __syncwarp();
+    for (int j = lane; j < m; j += 32) alpha[j] = al[j];
+}
+
+struct UpdParams {
+    int64_t n;
+    int cap;
+    const int* ring;
+    const double* wu;
+    const double* ub;
+    const double* gb;
+    const double* alpha;
+    double* uhat;
+    double* d;
+    double* red;
+};
+
+__global__ void accel_update_kernel(const UpdParams p) {
+    __shared__ double red[32];
+    const int m = p.ring[0], head = p.ring[1];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double ub = p.ub[i];
+        double uh = ub;
+        for (int j = 0; j < m; ++j) {
+            const int slot = (head + j) % p.cap;
+            uh += p.alpha[j] * (ub - p.wu[(int64_t)slot * p.n + i]);
+        }
+        if (p.uhat) p.uhat[i] = uh;
+        const double dv = uh - ub;
+        p.d[i] = dv;
+        s += p.gb[i] * dv;
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        p.red[blockIdx.x] = t;
+    }
+}
+
+__global__ void accel_slope_kernel(const double* red, int nblk, double* scal) {
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int b = 0; b < nblk; ++b) t += red[b];
+        scal[1] = t;
+    }
+}
+
+}  // namespace
+
+AccelWork* accel_create(int64_t n, int cap) {
+    if (cap < 1 || cap > 63) throw std::invalid_argument("device accelerate supports window 1..63");
+    auto* a = new AccelWork();
+    a->n = n;
+    a->cap = cap;
+    const int C = cap + 1;
+    a->leaf_rows = kLeafRows;
+    const int64_t nblocks = (n + kLeafRows - 1) / kLeafRows;
+    a->leaf_grid = (int)std::min<int64_t>(nblocks, 148);
+    int64_t cnt = a->leaf_grid;
+    while (cnt > 1) {
+        const int per = std::max(1, kLeafRows / C);
+        const int64_t nb = (cnt + per - 1) / per;
+        const int g = (int)std::min<int64_t>(nb, 148);
+        a->merge_grid.push_back(g);
+        cnt = g;
+    }
+    const size_t rsz = sizeof(double) * (size_t)std::max<int64_t>(a->leaf_grid, 1) * C * C;
+    CPFIT_CUDA(cudaMalloc(&a->rbuf[0], rsz));
+    CPFIT_CUDA(cudaMalloc(&a->rbuf[1], rsz));
+    CPFIT_CUDA(cudaMalloc(&a->alpha, sizeof(double) * 64));
+    CPFIT_CUDA(cudaMalloc(&a->scal, sizeof(double) * 8));
+    CPFIT_CUDA(cudaMalloc(&a->red, sizeof(double) * 1024));
+    return a;
+}
+
+void accel_destroy(AccelWork* a) {
+    if (!a) return;
+    cudaFree(a->rbuf[0]);
+    cudaFree(a->rbuf[1]);
+    cudaFree(a->alpha);
+    cudaFree(a->scal);
+    cudaFree(a->red);
+    delete a;
+}
+
+void accelerate_device(AccelWork& a, const double* wu, const double* wg, const int* ring, const double* ub,
+                       const double* gb, double eps, double* uhat, double* d, cudaStream_t st) {
+    const int C = a.cap + 1;  // smem sized for the full window
+    TsqrParams p{};
+    p.n = a.n;
+    p.cap = a.cap;
+    p.ring = ring;
+    p.wg = wg;
+    p.gb = gb;
+    p.per_block = kLeafRows;
+    p.nblocks = (a.n + kLeafRows - 1) / kLeafRows;
+    p.blocks_per_cta = (p.nblocks + a.leaf_grid - 1) / a.leaf_grid;
+    p.rout = a.rbuf[0];
+    size_t smem = sizeof(double) * (size_t)(C + kLeafRows) * C;
+    CPFIT_CUDA(cudaFuncSetAttribute(tsqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int g0 = (int)((p.nblocks + p.blocks_per_cta - 1) / p.blocks_per_cta);
+    tsqr_kernel<<<g0, kTsqrThreads, smem, st>>>(p);
+    CPFIT_CUDA(cudaGetLastError());
+    int64_t cnt = g0;
+    int src = 0;
+    const int per = std::max(1, kLeafRows / C);
+    while (cnt > 1) {
+        TsqrParams q = p;
+        q.rin = a.rbuf[src];
+        q.nin = cnt;
+        q.rout = a.rbuf[src ^ 1];
+        q.per_block = per;
+        q.nblocks = (cnt + per - 1) / per;
+        const int gmax = 148;
+        q.blocks_per_cta = (q.nblocks + gmax - 1) / gmax;
+        const int g = (int)((q.nblocks + q.blocks_per_cta - 1) / q.blocks_per_cta);
+        smem = sizeof(double) * (size_t)(C + per * C) * C;
+        tsqr_kernel<<<g, kTsqrThreads, smem, st>>>(q);
+        CPFIT_CUDA(cudaGetLastError());
+        cnt = g;
+        src ^= 1;
+    }
+    const size_t ssmem = sizeof(double) * 2 * (size_t)a.cap * a.cap;
+    CPFIT_CUDA(cudaFuncSetAttribute(accel_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+    accel_solve_kernel<<<1, 32, ssmem, st>>>(a.rbuf[src], ring, eps, a.alpha, a.scal);
+    CPFIT_CUDA(cudaGetLastError());
+    UpdParams u{};
+    u.n = a.n;
+    u.cap = a.cap;
+    u.ring = ring;
+    u.wu = wu;
+    u.ub = ub;
+    u.gb = gb;
+    u.alpha = a.alpha;
+    u.uhat = uhat;
+    u.d = d;
+    u.red = a.red;
+    const int nb = (int)std::min<int64_t>(1024, (a.n + 255) / 256);
+    accel_update_kernel<<<nb, 256, 0, st>>>(u);
+    accel_slope_kernel<<<1, 32, 0, st>>>(a.red, nb, a.scal);
+    CPFIT_CUDA(cudaGetLastError());
+}
+
+}  // namespace cpfit_gpu

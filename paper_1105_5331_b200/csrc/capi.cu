@@ -1,0 +1,530 @@
+// extern "C" surface (include/cpfit_gpu.h). Exceptions become status codes here.
+#include "../../include/cpfit_gpu.h"
+#include "device.cuh"
+#include "linesearch.cuh"
+#include "solver.cuh"
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace cpfit_gpu;
+
+struct cpfit_tensor_s {
+    DevTensor* t = nullptr;
+    cudaStream_t st = nullptr;
+    std::map<int, EvalWork*> works;
+    std::mutex mu;
+    double* scratch = nullptr;  // device buffers for per-call ops
+    size_t scratch_n = 0;
+    ~cpfit_tensor_s() {
+        for (auto& kv : works) work_destroy(kv.second);
+        cudaFree(scratch);
+        tensor_destroy(t);
+        if (st) cudaStreamDestroy(st);
+    }
+    EvalWork& work(int R) {
+        auto it = works.find(R);
+        if (it != works.end()) return *it->second;
+        EvalWork* w = work_create(*t, R);
+        works[R] = w;
+        return *w;
+    }
+    double* buf(size_t n) {
+        if (n > scratch_n) {
+            cudaFree(scratch);
+            CPFIT_CUDA(cudaMalloc(&scratch, sizeof(double) * n));
+            scratch_n = n;
+        }
+        return scratch;
+    }
+};
+
+struct cpfit_solver_s {
+    std::unique_ptr<Solver> s;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ~cpfit_solver_s() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const cpfit_gpu::numerical_error& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+int64_t packed_len(int order, const int64_t* dims, int64_t R) {
+    int64_t s = 0;
+    for (int n = 0; n < order; ++n) s += dims[n] * R;
+    return s;
+}
+
+void check_rank(int64_t R) {
+    if (R < 1) throw std::invalid_argument("KruskalTensor: rank must be >= 1");
+    if (R > kMaxRank) throw std::invalid_argument("device path supports rank <= 32");
+}
+
+void check_finite(const double* u, int64_t n) {
+    for (int64_t i = 0; i < n; ++i)
+        if (!std::isfinite(u[i])) throw std::invalid_argument("KruskalTensor: entries must be finite");
+}
+
+// Factor-only context (gram_hadamard / normalize need no tensor).
+struct FactorCtx {
+    DevTensor t;
+    EvalWork* w = nullptr;
+    cudaStream_t st = nullptr;
+    FactorCtx(int order, const int64_t* dims, int R) {
+        if (order < 1 || order > kMaxOrder) throw std::invalid_argument("order must be in [1, 8] on device");
+        t.order = order;
+        t.sparse = true;
+        for (int n = 0; n < order; ++n) {
+            if (dims[n] < 1) throw std::invalid_argument("Shape: every mode size must be >= 1");
+            t.dims[n] = dims[n];
+        }
+        CPFIT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        w = work_create(t, R);
+    }
+    ~FactorCtx() {
+        work_destroy(w);
+        cudaStreamDestroy(st);
+    }
+};
+
+struct DevBuf {
+    double* p = nullptr;
+    explicit DevBuf(size_t n) { CPFIT_CUDA(cudaMalloc(&p, sizeof(double) * std::max<size_t>(n, 1))); }
+    ~DevBuf() { cudaFree(p); }
+};
+
+SolverOptions to_opts(const cpfit_ngmres_options* o, double tnorm) {
+    SolverOptions s;
+    s.window = o->window;
+    s.max_iters = o->max_iters;
+    s.epsilon_reg = o->epsilon_reg;
+    s.tol_grad = o->tol_grad;
+    s.gradient_scale = (o->gradient_scale > 0.0) ? o->gradient_scale : tnorm;
+    s.ftol = o->ftol;
+    s.gtol = o->gtol;
+    s.initial_step = o->initial_step;
+    s.max_evals = o->max_evals;
+    s.step_min = o->step_min;
+    s.step_max = o->step_max;
+    s.restart_on_ascent = o->restart_on_ascent;
+    if (s.window < 1) throw std::invalid_argument("ngmres: window must be >= 1");
+    if (!(s.tol_grad > 0.0)) throw std::invalid_argument("ngmres: tol_grad must be > 0");
+    if (s.epsilon_reg < 0.0) throw std::invalid_argument("ngmres: epsilon_reg must be >= 0");
+    if (!(s.ftol > 0.0 && s.ftol < s.gtol && s.gtol < 1.0))
+        throw std::invalid_argument("more_thuente: need 0 < ftol < gtol < 1");
+    if (!(s.initial_step > 0.0)) throw std::invalid_argument("more_thuente: initial_step must be > 0");
+    if (s.max_evals < 1) throw std::invalid_argument("more_thuente: max_evals must be >= 1");
+    if (!(s.step_min >= 0.0 && s.step_min < s.step_max))
+        throw std::invalid_argument("more_thuente: need 0 <= step_min < step_max");
+    if (s.max_iters < 0) throw std::invalid_argument("ngmres: max_iters must be >= 0");
+    return s;
+}
+
+void finish_solve(Solver& sv, double* u_best, double* f_best, cpfit_trace_row* trace, int64_t cap, int64_t* rows,
+                  int* stop) {
+    const SolverSummary sm = sv.summary();
+    if (sm.status) {
+        if (sm.status & 1)
+            throw cpfit_gpu::numerical_error(
+                "als_sweep: normal matrix is singular after regularization (structurally rank-deficient iterate)");
+        throw cpfit_gpu::numerical_error("als_sweep: non-finite solution of the normal equations");
+    }
+    const int nrows = sm.iters + 1;
+    if (rows) *rows = nrows;
+    if (trace && cap > 0) {
+        std::vector<TraceRow> tr((size_t)nrows);
+        sv.copy_trace(tr.data(), nrows);
+        for (int64_t i = 0; i < std::min<int64_t>(cap, nrows); ++i) std::memcpy(&trace[i], &tr[(size_t)i], sizeof(TraceRow));
+    }
+    if (u_best) {
+        sv.copy_best(u_best, true);
+        sv.sync();
+    }
+    if (f_best) *f_best = sm.best_f;
+    if (stop) *stop = (sm.stop < 0) ? 1 : sm.stop;
+}
+}  // namespace
+
+static_assert(sizeof(cpfit_trace_row) == sizeof(TraceRow), "trace row layout");
+
+extern "C" {
+
+const char* cpfit_last_error(void) { return g_err.c_str(); }
+
+int cpfit_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+void cpfit_default_ngmres_options(cpfit_ngmres_options* o) {
+    *o = cpfit_ngmres_options{20, 2000, 1e-12, 1e-9, 0.0, 1e-4, 1e-2, 1.0, 20, 1, 0.0, 1e20};
+}
+
+int cpfit_tensor_create_dense(int order, const int64_t* dims, const double* values, cpfit_tensor* out) {
+    return guard([&] {
+        auto h = std::make_unique<cpfit_tensor_s>();
+        CPFIT_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+        h->t = tensor_create_dense(order, dims, values, h->st);
+        *out = h.release();
+    });
+}
+
+int cpfit_tensor_create_coo(int order, const int64_t* dims, int64_t nnz, const int64_t* coords, const double* values,
+                            cpfit_tensor* out) {
+    return guard([&] {
+        if (nnz < 0) throw std::invalid_argument("SparseTensor: coords/values size mismatch");
+        auto h = std::make_unique<cpfit_tensor_s>();
+        CPFIT_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+        h->t = tensor_create_coo(order, dims, nnz, coords, values, h->st);
+        *out = h.release();
+    });
+}
+
+int cpfit_tensor_destroy(cpfit_tensor t) {
+    return guard([&] { delete t; });
+}
+
+int cpfit_tensor_norm(cpfit_tensor t, double* norm) {
+    return guard([&] { *norm = t->t->norm; });
+}
+
+int cpfit_tensor_nnz(cpfit_tensor t, int64_t* nnz) {
+    return guard([&] { *nnz = t->t->sparse ? t->t->nnz : t->t->K; });
+}
+
+int cpfit_mttkrp(cpfit_tensor t, int64_t rank, const double* u, int mode, double* out) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(t->mu);
+        check_rank(rank);
+        if (mode < 0 || mode >= t->t->order) throw std::invalid_argument("mttkrp: mode out of range");
+        EvalWork& w = t->work((int)rank);
+        check_finite(u, w.nu);
+        double* du = t->buf((size_t)w.nu + (size_t)t->t->dims[mode] * rank);
+        double* dout = du + w.nu;
+        CPFIT_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * w.nu, cudaMemcpyHostToDevice, t->st));
+        mttkrp_device(*t->t, w, du, mode, dout, t->st);
+        CPFIT_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * t->t->dims[mode] * rank, cudaMemcpyDeviceToHost, t->st));
+        CPFIT_CUDA(cudaStreamSynchronize(t->st));
+    });
+}
+
+static int eval_impl(cpfit_tensor t, int64_t rank, const double* u, double* grad, double* f) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(t->mu);
+        check_rank(rank);
+        EvalWork& w = t->work((int)rank);
+        check_finite(u, w.nu);
+        double* du = t->buf(2 * (size_t)w.nu + 8);
+        double* dg = du + w.nu;
+        EvalScalars* sc = reinterpret_cast<EvalScalars*>(dg + w.nu);
+        CPFIT_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * w.nu, cudaMemcpyHostToDevice, t->st));
+        eval_device(*t->t, w, du, dg, sc, nullptr, nullptr, t->st, grad != nullptr);
+        EvalScalars hs;
+        CPFIT_CUDA(cudaMemcpyAsync(&hs, sc, sizeof(EvalScalars), cudaMemcpyDeviceToHost, t->st));
+        if (grad) CPFIT_CUDA(cudaMemcpyAsync(grad, dg, sizeof(double) * w.nu, cudaMemcpyDeviceToHost, t->st));
+        CPFIT_CUDA(cudaStreamSynchronize(t->st));
+        *f = hs.f;
+    });
+}
+
+int cpfit_objective(cpfit_tensor t, int64_t rank, const double* u, double* f) { return eval_impl(t, rank, u, nullptr, f); }
+
+int cpfit_objective_and_gradient(cpfit_tensor t, int64_t rank, const double* u, double* grad, double* f) {
+    return eval_impl(t, rank, u, grad, f);
+}
+
+int cpfit_gram_hadamard(int order, const int64_t* dims, int64_t rank, const double* u, int skip, double* out) {
+    return guard([&] {
+        check_rank(rank);
+        FactorCtx c(order, dims, (int)rank);
+        const int64_t n = packed_len(order, dims, rank);
+        DevBuf du((size_t)n + (size_t)rank * rank);
+        CPFIT_CUDA(cudaMemcpyAsync(du.p, u, sizeof(double) * n, cudaMemcpyHostToDevice, c.st));
+        grams_device(*c.w, du.p, c.st);
+        gram_hadamard_device(*c.w, skip, du.p + n, c.st);
+        CPFIT_CUDA(cudaMemcpyAsync(out, du.p + n, sizeof(double) * rank * rank, cudaMemcpyDeviceToHost, c.st));
+        CPFIT_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int cpfit_normalize_and_reorder(int order, const int64_t* dims, int64_t rank, const double* u, double* out) {
+    return guard([&] {
+        check_rank(rank);
+        FactorCtx c(order, dims, (int)rank);
+        const int64_t n = packed_len(order, dims, rank);
+        DevBuf du(2 * (size_t)n);
+        CPFIT_CUDA(cudaMemcpyAsync(du.p, u, sizeof(double) * n, cudaMemcpyHostToDevice, c.st));
+        grams_device(*c.w, du.p, c.st);
+        normalize_device(*c.w, du.p, du.p + n, c.st);
+        CPFIT_CUDA(cudaMemcpyAsync(out, du.p + n, sizeof(double) * n, cudaMemcpyDeviceToHost, c.st));
+        CPFIT_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int cpfit_als_sweep(cpfit_tensor t, int64_t rank, const double* u, double* out) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(t->mu);
+        check_rank(rank);
+        EvalWork& w = t->work((int)rank);
+        check_finite(u, w.nu);
+        int64_t maxI = 1;
+        for (int k = 0; k < t->t->order; ++k) maxI = std::max(maxI, t->t->dims[k]);
+        DevBuf b(3 * (size_t)w.nu + (size_t)maxI * rank + 1);
+        double* du = b.p;
+        double* dout = du + w.nu;
+        double* work = dout + w.nu;
+        double* mbuf = work + w.nu;
+        int* status = reinterpret_cast<int*>(mbuf + maxI * rank);
+        CPFIT_CUDA(cudaMemsetAsync(status, 0, sizeof(int), t->st));
+        CPFIT_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * w.nu, cudaMemcpyHostToDevice, t->st));
+        als_sweep_device_ws(*t->t, w, du, dout, work, mbuf, status, t->st);
+        int hs = 0;
+        CPFIT_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, t->st));
+        CPFIT_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * w.nu, cudaMemcpyDeviceToHost, t->st));
+        CPFIT_CUDA(cudaStreamSynchronize(t->st));
+        if (hs & 1)
+            throw cpfit_gpu::numerical_error(
+                "als_sweep: normal matrix is singular after regularization (structurally rank-deficient iterate)");
+        if (hs) throw cpfit_gpu::numerical_error("als_sweep: non-finite solution of the normal equations");
+    });
+}
+
+int cpfit_accelerate(int64_t n, int64_t m, const double* wu, const double* wg, const double* ub, const double* gb,
+                     double eps, double* u_hat, double* alpha, double* residual_rel) {
+    return guard([&] {
+        if (m < 1) throw std::invalid_argument("accelerate: window must be nonempty");
+        cudaStream_t st;
+        CPFIT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        struct S {
+            cudaStream_t s;
+            ~S() { cudaStreamDestroy(s); }
+        } sg{st};
+        std::unique_ptr<AccelWork, void (*)(AccelWork*)> a(accel_create(n, (int)m), accel_destroy);
+        DevBuf b(2 * (size_t)(n * m) + 4 * (size_t)n + 2);
+        double* dwu = b.p;
+        double* dwg = dwu + n * m;
+        double* dub = dwg + n * m;
+        double* dgb = dub + n;
+        double* duh = dgb + n;
+        double* dd_ = duh + n;
+        int* ring = reinterpret_cast<int*>(dd_ + n);
+        const int hr[2] = {(int)m, 0};
+        CPFIT_CUDA(cudaMemcpyAsync(dwu, wu, sizeof(double) * n * m, cudaMemcpyHostToDevice, st));
+        CPFIT_CUDA(cudaMemcpyAsync(dwg, wg, sizeof(double) * n * m, cudaMemcpyHostToDevice, st));
+        CPFIT_CUDA(cudaMemcpyAsync(dub, ub, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        CPFIT_CUDA(cudaMemcpyAsync(dgb, gb, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        CPFIT_CUDA(cudaMemcpyAsync(ring, hr, sizeof(hr), cudaMemcpyHostToDevice, st));
+        accelerate_device(*a, dwu, dwg, ring, dub, dgb, eps, duh, dd_, st);
+        CPFIT_CUDA(cudaMemcpyAsync(u_hat, duh, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        CPFIT_CUDA(cudaMemcpyAsync(alpha, a->alpha, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+        double sc[3];
+        CPFIT_CUDA(cudaMemcpyAsync(sc, a->scal, sizeof(sc), cudaMemcpyDeviceToHost, st));
+        CPFIT_CUDA(cudaStreamSynchronize(st));
+        *residual_rel = sc[0];
+    });
+}
+
+int cpfit_more_thuente(cpfit_phi_fn phi, void* ctx, double phi0, double dphi0, const cpfit_line_search_params* p,
+                       cpfit_line_search_result* out) {
+    return guard([&] {
+        if (!(p->ftol > 0.0 && p->ftol < p->gtol && p->gtol < 1.0))
+            throw std::invalid_argument("more_thuente: need 0 < ftol < gtol < 1");
+        if (!(p->initial_step > 0.0)) throw std::invalid_argument("more_thuente: initial_step must be > 0");
+        if (p->max_evals < 1) throw std::invalid_argument("more_thuente: max_evals must be >= 1");
+        if (!(p->step_min >= 0.0 && p->step_min < p->step_max))
+            throw std::invalid_argument("more_thuente: need 0 <= step_min < step_max");
+        MoreThuente mt;
+        LsParams lp{p->ftol, p->gtol, p->initial_step, p->max_evals, p->step_min, p->step_max};
+        if (mt.begin(lp, phi0, dphi0)) {
+            for (;;) {
+                double f = 0.0, g = 0.0;
+                phi(mt.stp, &f, &g, ctx);
+                if (mt.update(f, g)) break;
+            }
+        }
+        *out = cpfit_line_search_result{mt.out_step, mt.out_f, mt.out_g, mt.status, mt.evals};
+    });
+}
+
+int cpfit_ngmres_solve(cpfit_tensor t, int64_t rank, const double* u0, const cpfit_ngmres_options* o, double* u_best,
+                       double* f_best, cpfit_trace_row* trace, int64_t cap, int64_t* rows, int* stop_reason) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(t->mu);
+        check_rank(rank);
+        const SolverOptions so = to_opts(o, t->t->norm);
+        Solver sv(t->t, (int)rank, so, 0);
+        check_finite(u0, sv.n());
+        sv.set_initial(u0, true);
+        sv.run_init();
+        sv.run_loop(so.max_iters);
+        finish_solve(sv, u_best, f_best, trace, cap, rows, stop_reason);
+    });
+}
+
+int cpfit_als_solve(cpfit_tensor t, int64_t rank, const double* u0, double tol_grad, int max_iters, double* u_best,
+                    double* f_best, cpfit_trace_row* trace, int64_t cap, int64_t* rows, int* stop_reason) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(t->mu);
+        check_rank(rank);
+        SolverOptions so;
+        so.tol_grad = tol_grad;
+        so.max_iters = max_iters;
+        so.gradient_scale = t->t->norm;  // als.cpp:74 (||g|| / ||T||)
+        Solver sv(t->t, (int)rank, so, 1);
+        check_finite(u0, sv.n());
+        sv.set_initial(u0, true);
+        sv.run_init();
+        sv.run_loop(so.max_iters);
+        finish_solve(sv, u_best, f_best, trace, cap, rows, stop_reason);
+    });
+}
+
+int cpfit_solver_create(cpfit_tensor t, int64_t rank, const cpfit_ngmres_options* o, int method, cpfit_solver* out) {
+    return guard([&] {
+        check_rank(rank);
+        SolverOptions so = to_opts(o, t->t->norm);
+        if (method == 1) so.gradient_scale = (o->gradient_scale > 0.0) ? o->gradient_scale : t->t->norm;
+        auto h = std::make_unique<cpfit_solver_s>();
+        h->s = std::make_unique<Solver>(t->t, (int)rank, so, method);
+        CPFIT_CUDA(cudaEventCreate(&h->e0));
+        CPFIT_CUDA(cudaEventCreate(&h->e1));
+        *out = h.release();
+    });
+}
+
+int cpfit_solver_set_initial(cpfit_solver s, const double* u0) {
+    return guard([&] {
+        s->s->set_initial(u0, true);
+        s->s->sync();
+    });
+}
+
+int cpfit_solver_init(cpfit_solver s) {
+    return guard([&] {
+        s->s->run_init();
+        s->s->sync();
+    });
+}
+
+int cpfit_solver_run(cpfit_solver s, int max_iters_total, float* ms) {
+    return guard([&] {
+        Solver& sv = *s->s;
+        CPFIT_CUDA(cudaEventRecord(s->e0, sv.stream()));
+        sv.run_loop(max_iters_total);
+        CPFIT_CUDA(cudaEventRecord(s->e1, sv.stream()));
+        CPFIT_CUDA(cudaEventSynchronize(s->e1));
+        float t = 0.f;
+        CPFIT_CUDA(cudaEventElapsedTime(&t, s->e0, s->e1));
+        if (ms) *ms = t;
+    });
+}
+
+int cpfit_solver_state(cpfit_solver s, int* iters, int* stop_reason, double* f, double* best_f, int64_t* fevals) {
+    return guard([&] {
+        const SolverSummary sm = s->s->summary();
+        if (iters) *iters = sm.iters;
+        if (stop_reason) *stop_reason = sm.stop;
+        if (f) *f = sm.f;
+        if (best_f) *best_f = sm.best_f;
+        if (fevals) *fevals = sm.fevals;
+        if (sm.status) throw cpfit_gpu::numerical_error("solver: numerical failure in the ALS normal equations");
+    });
+}
+
+int cpfit_solver_trace(cpfit_solver s, cpfit_trace_row* trace, int64_t rows) {
+    return guard([&] { s->s->copy_trace(reinterpret_cast<TraceRow*>(trace), (int)rows); });
+}
+
+int cpfit_solver_best(cpfit_solver s, double* u) {
+    return guard([&] {
+        s->s->copy_best(u, true);
+        s->s->sync();
+    });
+}
+
+int cpfit_solver_iterate(cpfit_solver s, double* u) {
+    return guard([&] {
+        s->s->copy_current(u);
+        s->s->sync();
+    });
+}
+
+int cpfit_solver_destroy(cpfit_solver s) {
+    return guard([&] { delete s; });
+}
+
+int cpfit_bench_kernel(cpfit_tensor t, int64_t rank, const double* u, int kind, int mode, int reps, int flush_l2,
+                       float* ms_per_call) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(t->mu);
+        check_rank(rank);
+        EvalWork& w = t->work((int)rank);
+        int64_t maxI = 1;
+        for (int k = 0; k < t->t->order; ++k) maxI = std::max(maxI, t->t->dims[k]);
+        DevBuf b(4 * (size_t)w.nu + (size_t)maxI * rank + 16);
+        double* du = b.p;
+        double* dg = du + w.nu;
+        double* work = dg + w.nu;
+        double* dout = work + w.nu;
+        double* mbuf = dout + w.nu;
+        EvalScalars* sc = reinterpret_cast<EvalScalars*>(mbuf + maxI * rank);
+        int* status = reinterpret_cast<int*>(sc + 1);
+        CPFIT_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * w.nu, cudaMemcpyHostToDevice, t->st));
+        CPFIT_CUDA(cudaMemsetAsync(status, 0, sizeof(int), t->st));
+        const size_t flush_bytes = 256ull << 20;  // > 126 MB L2
+        DevBuf flush(flush_l2 ? flush_bytes / 8 : 1);
+        cudaEvent_t e0, e1;
+        CPFIT_CUDA(cudaEventCreate(&e0));
+        CPFIT_CUDA(cudaEventCreate(&e1));
+        auto call = [&] {
+            if (kind == 0)
+                mttkrp_device(*t->t, w, du, mode, dout, t->st);
+            else if (kind == 1)
+                eval_device(*t->t, w, du, dg, sc, nullptr, status, t->st);
+            else
+                als_sweep_device_ws(*t->t, w, du, dout, work, mbuf, status, t->st);
+        };
+        for (int i = 0; i < 3; ++i) call();
+        float total = 0.f;
+        for (int i = 0; i < reps; ++i) {
+            if (flush_l2) CPFIT_CUDA(cudaMemsetAsync(flush.p, i & 0xff, flush_bytes, t->st));
+            CPFIT_CUDA(cudaEventRecord(e0, t->st));
+            call();
+            CPFIT_CUDA(cudaEventRecord(e1, t->st));
+            CPFIT_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CPFIT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            total += ms;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ms_per_call = total / std::max(1, reps);
+    });
+}
+
+}  // extern "C"

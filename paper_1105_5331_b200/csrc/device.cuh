@@ -1,0 +1,121 @@
+// Internal device-side API of the cpfit B200 path (not part of the C-ABI).
+//
+// Data layout in HBM:
+//   * dense T: first-mode-fastest like the reference (tensor.hpp:42-60), but each mode-0
+//     fiber is padded to ldT = round_up(I_0, 4) doubles (zeros) so every fiber starts
+//     32-byte aligned and can be moved by one bulk async copy;
+//   * iterates u / gradients g: the reference's packed layout (pack(), kruskal.cpp:195-206):
+//     factors in mode order, each column-major — vectors cross the C-ABI unchanged;
+//   * S = T x_1 A^(0) (per mode-0 fiber, RP doubles, row-major [fiber][r]) is materialised
+//     by the fiber pass and consumed by the level contractions for modes >= 1;
+//   * sparse T: canonical COO (sorted lexicographically, tensor.cpp:56-103) uploaded as
+//     structure-of-arrays int64 indices + fp64 values.
+#pragma once
+
+#include "common.cuh"
+
+#include <vector>
+
+namespace cpfit_gpu {
+
+struct DevTensor {
+    int order = 0;
+    int64_t dims[kMaxOrder] = {};
+    int64_t K = 0;
+    bool sparse = false;
+    double norm = 0.0, norm_sq = 0.0;
+    // dense
+    double* T = nullptr;
+    int64_t ldT = 0;  // padded fiber stride
+    int64_t J = 0;    // number of mode-0 fibers (K / I_0)
+    double* fiber_norm2 = nullptr;  // ||t_f||^2 per fiber (dd-accurate), for the per-fiber objective
+    // sparse: canonical nnz and the per-mode sorted copies (sparse.cuh)
+    int64_t nnz = 0;
+    struct SparseModes* modes = nullptr;
+};
+
+DevTensor* tensor_create_dense(int order, const int64_t* dims, const double* host_vals, cudaStream_t st);
+DevTensor* tensor_create_coo(int order, const int64_t* dims, int64_t nnz, const int64_t* coords_aos,
+                             const double* vals, cudaStream_t st);
+void tensor_destroy(DevTensor* t);
+
+// Scratch for one evaluation context (sized from tensor + rank).
+struct EvalWork {
+    int R = 0, RP = 0;
+    int64_t nu = 0;              // R * sum I_n
+    int order = 0;
+    int64_t dims[kMaxOrder] = {};
+    int64_t off[kMaxOrder + 1] = {};  // packed offsets (R * prefix sum)
+    // dense fiber pass
+    int fiber_grid = 0, fiber_F = 16, fiber_nchunk = 0;
+    size_t fiber_smem = 0;
+    double* S = nullptr;        // J x RP
+    double* m0_part = nullptr;  // fiber_grid x RP x (32*nchunk)
+    double* f_part = nullptr;   // fiber_grid (+ sparse/other scalars)
+    // level contractions (modes 1..N-2 heads)
+    int lvl_grid[kMaxOrder] = {};
+    double* lvl_part[kMaxOrder] = {};  // partial M_h per CTA (grid x I_h x RP)
+    double* lvl_S[kMaxOrder] = {};     // S_{h} outputs (slabs x RP)
+    // Grams
+    int gram_chunks[kMaxOrder] = {};
+    dd* gram_part = nullptr;    // [mode][chunk][R*R]
+    double* gram = nullptr;     // [mode][RP*RP] (rounded from dd; padded entries 0)
+    // sparse
+    double* sp_part = nullptr;  // per-mode outputs I_n x RP
+    double* frows = nullptr;    // row-major RP-padded factor copies (sum I_n x RP)
+    // reductions
+    double* red = nullptr;      // per-CTA partials for norms/dots
+    int red_grid = 0;
+};
+
+EvalWork* work_create(const DevTensor& t, int R);
+void work_destroy(EvalWork* w);
+
+// Device scalars written by the evaluation and read by control kernels.
+struct EvalScalars {
+    double f;      // objective
+    double gnorm2; // ||g||^2
+    double gdotd;  // g . d (when a direction is supplied)
+    double inner;  // <M0, A0>
+};
+
+// objective_and_gradient (kruskal.cpp:127-149) at device iterate u; writes g (packed),
+// scalars->f, ->gnorm2 and (if d != nullptr) ->gdotd.  Grams of u are computed first.
+// mode = 0 gradient+f; mode = 1 f only (objective()).
+void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
+                 int* status, cudaStream_t st, bool need_grad = true);
+
+// mttkrp(T, factors(u), mode) (tensor.cpp:206-259) -> out (I_mode x R col-major).
+void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st);
+
+// Grams G_n = A_n^T A_n for all modes (double-double accumulation) -> w.gram.
+void grams_device(EvalWork& w, const double* u, cudaStream_t st);
+// gram_hadamard(factors(u), skip) (tensor.cpp:261-274) -> out (R x R col-major), from w.gram.
+void gram_hadamard_device(EvalWork& w, int skip, double* out, cudaStream_t st);
+// normalize_and_reorder (kruskal.cpp:156-193): u -> out, Grams in w.gram updated to match.
+void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st);
+// One ALS sweep (als.cpp:38-48): u -> out (normalized); work: n_u scratch, mbuf: max I_n x R
+// scratch. status: bit0 singular normal matrix after the ridge retry, bit1 non-finite solve.
+void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
+                         int* status, cudaStream_t st);
+void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
+
+// Accelerate (ngmres.cpp:27-63) on device.
+struct AccelWork {
+    int64_t n = 0;
+    int cap = 0;
+    int leaf_grid = 0, leaf_rows = 0;
+    std::vector<int> merge_grid;  // per merge level
+    double* rbuf[2] = {nullptr, nullptr};
+    double* alpha = nullptr;  // cap
+    double* scal = nullptr;   // [0] residual_rel, [1] slope, [2] delta, [3] m
+    double* red = nullptr;
+};
+AccelWork* accel_create(int64_t n, int cap);
+void accel_destroy(AccelWork* a);
+// Window as ring slots: wu/wg base pointers with slot stride n; order[j] = slot of j-th
+// oldest entry; m entries (device int). Produces uhat and d = uhat - ubar, slope = gbar.d.
+void accelerate_device(AccelWork& a, const double* wu, const double* wg, const int* ring, const double* ub,
+                       const double* gb, double eps, double* uhat, double* d, cudaStream_t st);
+
+}  // namespace cpfit_gpu

@@ -1,0 +1,472 @@
+// Device-resident solvers: ALS-preconditioned N-GMRES (ngmres.cpp:73-226) and stand-alone
+// ALS (als.cpp:50-96) for the CP objective.
+//
+// The whole iteration loop runs on the GPU with no host round-trip: it is captured once into
+// a CUDA graph whose outer WHILE node repeats one N-GMRES iteration
+//   [ALS sweep -> u_bar] [eval(u_bar)] [accelerate -> d, slope] [line-search init]
+//   WHILE(searching) { u_t = u_bar + stp d ; eval(u_t) ; More–Thuente update }
+//   IF(accepted) { canonical(u_bar + beta d) ; eval }          (ngmres.cpp:137-142)
+//   [commit: window push/reset, trace row, best-f, stall / gradient / budget stop tests]
+// and the scalar control (restart test, Moré–Thuente state machine, counters) lives in
+// device memory, executed by single-thread kernels between the streaming passes.
+#include "device.cuh"
+#include "linesearch.cuh"
+#include "solver.cuh"
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+namespace cpfit_gpu {
+
+void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
+                         int* status, cudaStream_t st);
+
+namespace {
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+struct DevState {
+    // iteration bookkeeping
+    int iter, max_iters, stop, stalls, status;
+    int restart, stalled, searching, accepted;
+    long long fevals, gevals;
+    double f, gnorm2, f_bar, slope, beta, best_f;
+    int ring[2];  // window: m, head slot
+    int slot;     // slot written by this iteration's push/reset
+    int is_best;
+    unsigned long long t0;
+    MoreThuente mt;
+};
+
+struct Ctl {
+    DevState* s;
+    const EvalScalars* sc_cur;
+    const EvalScalars* sc_bar;
+    const EvalScalars* sc_trial;
+    const EvalScalars* sc_next;
+    const double* accel_scal;
+    TraceRow* trace;
+    int trace_cap;
+    double gradient_scale, hscale, tol_grad;
+    int cap;
+    int restart_on_ascent;
+    LsParams ls;
+    int als_mode;  // 1: stand-alone ALS trace semantics
+};
+
+__device__ double fit_h(double f, double scale) { return sqrt(fmax(2.0 * f, 0.0)) / scale; }
+
+__global__ void k_reset(Ctl c, int max_iters) {
+    DevState& s = *c.s;
+    s.iter = 0;
+    s.max_iters = max_iters;
+    s.stop = -1;
+    s.stalls = 0;
+    s.status = 0;
+    s.restart = s.stalled = s.searching = s.accepted = 0;
+    s.fevals = s.gevals = 0;
+    s.ring[0] = 0;
+    s.ring[1] = 0;
+    s.slot = 0;
+    s.beta = 0.0;
+    s.t0 = globaltimer();
+}
+
+// after canonical(u0) + eval: window seeded with (u, g), trace row 0, best = u
+__global__ void k_after_init(Ctl c) {
+    DevState& s = *c.s;
+    s.f = c.sc_cur->f;
+    s.gnorm2 = c.sc_cur->gnorm2;
+    s.fevals = s.gevals = 1;
+    s.best_f = s.f;
+    s.ring[0] = 1;
+    s.ring[1] = 0;
+    s.slot = 0;
+    const double gn = sqrt(s.gnorm2);
+    c.trace[0] = TraceRow{0, 0, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, c.hscale), gn / c.gradient_scale,
+                          0.0, s.fevals, s.gevals, 0};
+    if (s.status) s.stop = 100 + s.status;
+    if (c.als_mode && gn / c.gradient_scale <= c.tol_grad) s.stop = 0;  // als.cpp:74-77
+}
+
+__global__ void k_set_cond_running(Ctl c, cudaGraphConditionalHandle h) {
+    const DevState& s = *c.s;
+    cudaGraphSetConditional(h, (s.stop < 0 && s.iter < s.max_iters) ? 1u : 0u);
+}
+
+__global__ void k_after_bar(Ctl c) {
+    DevState& s = *c.s;
+    s.f_bar = c.sc_bar->f;
+    s.fevals += 1;
+    s.gevals += 1;
+}
+
+// Step III entry (ngmres.cpp:104-124): restart test or start of the line search.
+__global__ void k_ls_init(Ctl c, cudaGraphConditionalHandle ls_h) {
+    DevState& s = *c.s;
+    s.slope = c.accel_scal[1];
+    s.restart = 0;
+    s.stalled = 0;
+    s.accepted = 0;
+    s.beta = 0.0;
+    s.searching = 0;
+    if (s.status) {
+        // numerical failure earlier in the iteration: stop searching, commit will stop the solve
+    } else if (c.restart_on_ascent && s.slope >= 0.0) {
+        s.restart = 1;
+    } else if (s.slope >= 0.0) {
+        // restarts disabled and no descent: keep u_bar
+    } else {
+        s.searching = s.mt.begin(c.ls, s.f_bar, s.slope) ? 1 : 0;
+    }
+    cudaGraphSetConditional(ls_h, s.searching ? 1u : 0u);
+}
+
+__global__ void k_trial(const DevState* s, const double* ub, const double* d, double* ut, int64_t n) {
+    const double stp = s->mt.stp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        ut[i] = ub[i] + stp * d[i];
+}
+
+__global__ void k_ls_update(Ctl c, cudaGraphConditionalHandle ls_h) {
+    DevState& s = *c.s;
+    const bool done = s.mt.update(c.sc_trial->f, c.sc_trial->gdotd);
+    if (done || s.status) {
+        s.searching = 0;
+        s.fevals += s.mt.evals;
+        s.gevals += s.mt.evals;
+        s.stalled = (s.mt.status == LS_STALL) ? 1 : 0;
+        if (!s.status && s.mt.out_step > 0.0 && s.mt.out_f <= s.f_bar) {
+            s.accepted = 1;
+            s.beta = s.mt.out_step;
+        }
+    }
+    cudaGraphSetConditional(ls_h, s.searching ? 1u : 0u);
+}
+
+__global__ void k_accept_cond(Ctl c, cudaGraphConditionalHandle h) {
+    cudaGraphSetConditional(h, c.s->accepted ? 1u : 0u);
+}
+
+__global__ void k_step_point(const DevState* s, const double* ub, const double* d, double* out, int64_t n) {
+    const double b = s->beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = ub[i] + b * d[i];
+}
+
+__global__ void k_after_next(Ctl c) {
+    DevState& s = *c.s;
+    s.fevals += 1;
+    s.gevals += 1;
+}
+
+// Scalar part of the commit (ngmres.cpp:150-157, 182-197).
+__global__ void k_commit(Ctl c, cudaGraphConditionalHandle loop_h) {
+    DevState& s = *c.s;
+    if (c.als_mode) {
+        s.f = c.sc_next->f;
+        s.gnorm2 = c.sc_next->gnorm2;
+        s.fevals += 1;
+        s.gevals += 1;
+    } else if (s.accepted) {
+        s.f = c.sc_next->f;
+        s.gnorm2 = c.sc_next->gnorm2;
+    } else {
+        s.f = s.f_bar;
+        s.gnorm2 = c.sc_bar->gnorm2;
+    }
+    if (!c.als_mode) {
+        // window ring
+        int m = s.ring[0], head = s.ring[1];
+        if (s.restart) {
+            head = 0;
+            m = 1;
+            s.slot = 0;
+        } else if (m < c.cap) {
+            s.slot = (head + m) % c.cap;
+            ++m;
+        } else {
+            s.slot = head;
+            head = (head + 1) % c.cap;
+        }
+        s.ring[0] = m;
+        s.ring[1] = head;
+    }
+    s.iter += 1;
+    const double gn = sqrt(s.gnorm2);
+    if (s.iter < c.trace_cap)
+        c.trace[s.iter] = TraceRow{s.iter, s.restart, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, c.hscale),
+                                   gn / c.gradient_scale, s.beta, s.fevals, s.gevals, s.iter};
+    s.is_best = (s.f < s.best_f) ? 1 : 0;
+    if (s.is_best) s.best_f = s.f;
+    if (s.status) {
+        s.stop = 100 + s.status;
+    } else if (c.als_mode) {
+        if (gn / c.gradient_scale <= c.tol_grad) s.stop = 0;
+    } else {
+        s.stalls = s.stalled ? s.stalls + 1 : 0;
+        if (s.stalls >= 2)
+            s.stop = 2;
+        else if (gn / c.gradient_scale <= c.tol_grad)
+            s.stop = 0;
+    }
+    // the iteration budget is not a stored stop: a later run_loop() may extend it
+    cudaGraphSetConditional(loop_h, (s.stop < 0 && s.iter < s.max_iters) ? 1u : 0u);
+}
+
+// Vector part of the commit: u, g <- chosen pair; window slot; best iterate.
+__global__ void k_commit_vec(const DevState* s, int als_mode, const double* ub, const double* gb, const double* un,
+                             const double* gn, double* u, double* g, double* wu, double* wg, double* ubest,
+                             int64_t n) {
+    const bool acc = als_mode || s->accepted;
+    const double* su = acc ? un : ub;
+    const double* sg = acc ? gn : gb;
+    double* wu_s = als_mode ? nullptr : wu + (int64_t)s->slot * n;
+    double* wg_s = als_mode ? nullptr : wg + (int64_t)s->slot * n;
+    const bool best = s->is_best;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double a = su[i], b = sg[i];
+        u[i] = a;
+        g[i] = b;
+        if (wu_s) {
+            wu_s[i] = a;
+            wg_s[i] = b;
+        }
+        if (best) ubest[i] = a;
+    }
+}
+
+__global__ void k_seed_window(const double* u, const double* g, double* wu, double* wg, double* ubest, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        wu[i] = u[i];
+        wg[i] = g[i];
+        ubest[i] = u[i];
+    }
+}
+
+int vec_blocks(int64_t n) { return (int)std::min<int64_t>(592, (n + 255) / 256); }
+
+// Conditional handle owned by the graph currently being captured on `st`.
+cudaGraphConditionalHandle make_handle(cudaStream_t st) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    CPFIT_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, nullptr, nullptr));
+    cudaGraphConditionalHandle h;
+    CPFIT_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+    return h;
+}
+
+// Appends a conditional node (WHILE / IF on handle h) to the capture on `st`; returns its body.
+cudaGraph_t append_conditional(cudaStream_t st, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CPFIT_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = type;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CPFIT_CUDA(cudaGraphAddNode(&node, g, deps, nd, &np));
+    CPFIT_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+    return np.conditional.phGraph_out[0];
+}
+
+}  // namespace
+
+Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
+    : t_(t), R_(R), opt_(o), method_(method) {
+    CPFIT_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    CPFIT_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
+    CPFIT_CUDA(cudaStreamCreateWithFlags(&st3_, cudaStreamNonBlocking));
+    w_ = work_create(*t, R);
+    n_ = w_->nu;
+    cap_ = std::max(1, o.window);
+    if (method_ == 0) a_ = accel_create(n_, cap_);
+    auto alloc = [&](double** p, int64_t cnt) { CPFIT_CUDA(cudaMalloc(p, sizeof(double) * (size_t)std::max<int64_t>(cnt, 1))); };
+    alloc(&u_, n_);
+    alloc(&g_, n_);
+    alloc(&ub_, n_);
+    alloc(&gb_, n_);
+    alloc(&d_, n_);
+    alloc(&ut_, n_);
+    alloc(&gt_, n_);
+    alloc(&un_, n_);
+    alloc(&gn_, n_);
+    alloc(&u0_, n_);
+    alloc(&ubest_, n_);
+    alloc(&work_, n_);
+    int64_t maxI = 1;
+    for (int k = 0; k < t->order; ++k) maxI = std::max(maxI, t->dims[k]);
+    alloc(&mbuf_, maxI * R);
+    if (method_ == 0) {
+        alloc(&wu_, n_ * cap_);
+        alloc(&wg_, n_ * cap_);
+    }
+    CPFIT_CUDA(cudaMalloc(&sc_, sizeof(EvalScalars) * 4));
+    CPFIT_CUDA(cudaMemset(sc_, 0, sizeof(EvalScalars) * 4));
+    CPFIT_CUDA(cudaMalloc(&state_, sizeof(DevState)));
+    CPFIT_CUDA(cudaMemset(state_, 0, sizeof(DevState)));
+    trace_cap_ = o.max_iters + 1;
+    CPFIT_CUDA(cudaMalloc(&trace_, sizeof(TraceRow) * (size_t)trace_cap_));
+    build_graphs();
+}
+
+Solver::~Solver() {
+    if (x_init_) cudaGraphExecDestroy(x_init_);
+    if (x_loop_) cudaGraphExecDestroy(x_loop_);
+    if (g_init_) cudaGraphDestroy(g_init_);
+    if (g_loop_) cudaGraphDestroy(g_loop_);
+    for (double* p : {u_, g_, ub_, gb_, d_, ut_, gt_, un_, gn_, u0_, ubest_, work_, mbuf_, wu_, wg_}) cudaFree(p);
+    cudaFree(sc_);
+    cudaFree(state_);
+    cudaFree(trace_);
+    accel_destroy(a_);
+    work_destroy(w_);
+    cudaStreamDestroy(st_);
+    cudaStreamDestroy(st2_);
+    cudaStreamDestroy(st3_);
+}
+
+void Solver::build_graphs() {
+    EvalScalars* sc_cur = reinterpret_cast<EvalScalars*>(sc_) + 0;
+    EvalScalars* sc_bar = reinterpret_cast<EvalScalars*>(sc_) + 1;
+    EvalScalars* sc_trial = reinterpret_cast<EvalScalars*>(sc_) + 2;
+    EvalScalars* sc_next = reinterpret_cast<EvalScalars*>(sc_) + 3;
+    DevState* s = reinterpret_cast<DevState*>(state_);
+    Ctl c{};
+    c.s = s;
+    c.sc_cur = sc_cur;
+    c.sc_bar = sc_bar;
+    c.sc_trial = sc_trial;
+    c.sc_next = sc_next;
+    c.accel_scal = a_ ? a_->scal : nullptr;
+    c.trace = trace_;
+    c.trace_cap = trace_cap_;
+    c.gradient_scale = opt_.gradient_scale;
+    c.hscale = t_->norm;
+    c.tol_grad = opt_.tol_grad;
+    c.cap = cap_;
+    c.restart_on_ascent = opt_.restart_on_ascent;
+    c.ls = LsParams{opt_.ftol, opt_.gtol, opt_.initial_step, opt_.max_evals, opt_.step_min, opt_.step_max};
+    c.als_mode = (method_ == 1);
+    int* status = &s->status;
+    const int vb = vec_blocks(n_);
+
+    // ---- init graph: canonical(u0), eval, seed window -----------------------------------
+    CPFIT_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
+    k_reset<<<1, 1, 0, st_>>>(c, opt_.max_iters);
+    grams_device(*w_, u0_, st_);
+    normalize_device(*w_, u0_, u_, st_);
+    eval_device(*t_, *w_, u_, g_, sc_cur, nullptr, status, st_);
+    k_after_init<<<1, 1, 0, st_>>>(c);
+    if (method_ == 0)
+        k_seed_window<<<vb, 256, 0, st_>>>(u_, g_, wu_, wg_, ubest_, n_);
+    else
+        k_seed_window<<<vb, 256, 0, st_>>>(u_, g_, ut_, gt_, ubest_, n_);
+    CPFIT_CUDA(cudaGetLastError());
+    CPFIT_CUDA(cudaStreamEndCapture(st_, &g_init_));
+    CPFIT_CUDA(cudaGraphInstantiate(&x_init_, g_init_, 0));
+
+    // ---- loop graph: WHILE(running) { one iteration } -----------------------------------
+    CPFIT_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
+    const cudaGraphConditionalHandle loop_h = make_handle(st_);
+    k_set_cond_running<<<1, 1, 0, st_>>>(c, loop_h);
+    cudaGraph_t body = append_conditional(st_, loop_h, cudaGraphCondTypeWhile);
+    CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st2_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    if (method_ == 0) {
+        // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
+        als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_);
+        eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_);
+        k_after_bar<<<1, 1, 0, st2_>>>(c);
+        // Step II: windowed recombination -> d, slope                        (ngmres.cpp:97-101)
+        accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st2_);
+        // Step III: restart test / Moré–Thuente line search                 (ngmres.cpp:111-147)
+        const cudaGraphConditionalHandle ls_h = make_handle(st2_);
+        k_ls_init<<<1, 1, 0, st2_>>>(c, ls_h);
+        cudaGraph_t lsb = append_conditional(st2_, ls_h, cudaGraphCondTypeWhile);
+        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        k_trial<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
+        eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st3_);
+        k_ls_update<<<1, 1, 0, st3_>>>(c, ls_h);
+        CPFIT_CUDA(cudaGetLastError());
+        CPFIT_CUDA(cudaStreamEndCapture(st3_, &lsb));
+        // accepted step: canonicalize u_bar + beta d and re-evaluate        (ngmres.cpp:137-142)
+        const cudaGraphConditionalHandle acc_h = make_handle(st2_);
+        k_accept_cond<<<1, 1, 0, st2_>>>(c, acc_h);
+        cudaGraph_t ab = append_conditional(st2_, acc_h, cudaGraphCondTypeIf);
+        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, ab, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        k_step_point<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
+        grams_device(*w_, ut_, st3_);
+        normalize_device(*w_, ut_, un_, st3_);
+        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st3_);
+        k_after_next<<<1, 1, 0, st3_>>>(c);
+        CPFIT_CUDA(cudaGetLastError());
+        CPFIT_CUDA(cudaStreamEndCapture(st3_, &ab));
+    } else {
+        // stand-alone ALS iteration (als.cpp:79-95)
+        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_);
+        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_);
+    }
+    k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
+    k_commit_vec<<<vb, 256, 0, st2_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_);
+    CPFIT_CUDA(cudaGetLastError());
+    CPFIT_CUDA(cudaStreamEndCapture(st2_, &body));
+    CPFIT_CUDA(cudaStreamEndCapture(st_, &g_loop_));
+    CPFIT_CUDA(cudaGraphInstantiate(&x_loop_, g_loop_, 0));
+}
+
+void Solver::set_initial(const double* u0, bool host) {
+    CPFIT_CUDA(cudaMemcpyAsync(u0_, u0, sizeof(double) * n_, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                               st_));
+}
+
+void Solver::run_init() { CPFIT_CUDA(cudaGraphLaunch(x_init_, st_)); }
+
+void Solver::run_loop(int max_iters_total) {
+    if (max_iters_total > opt_.max_iters) max_iters_total = opt_.max_iters;
+    host_max_ = max_iters_total;
+    DevState* s = reinterpret_cast<DevState*>(state_);
+    CPFIT_CUDA(cudaMemcpyAsync(&s->max_iters, &host_max_, sizeof(int), cudaMemcpyHostToDevice, st_));
+    CPFIT_CUDA(cudaGraphLaunch(x_loop_, st_));
+}
+
+void Solver::sync() { CPFIT_CUDA(cudaStreamSynchronize(st_)); }
+
+SolverSummary Solver::summary() {
+    DevState hs;
+    CPFIT_CUDA(cudaMemcpyAsync(&hs, state_, sizeof(DevState), cudaMemcpyDeviceToHost, st_));
+    sync();
+    SolverSummary r{};
+    r.iters = hs.iter;
+    r.stop = hs.stop;
+    r.best_f = hs.best_f;
+    r.f = hs.f;
+    r.status = hs.status;
+    r.fevals = hs.fevals;
+    r.gevals = hs.gevals;
+    return r;
+}
+
+void Solver::copy_trace(TraceRow* out, int rows) {
+    CPFIT_CUDA(cudaMemcpyAsync(out, trace_, sizeof(TraceRow) * (size_t)rows, cudaMemcpyDeviceToHost, st_));
+    sync();
+}
+
+void Solver::copy_best(double* out, bool host) {
+    CPFIT_CUDA(cudaMemcpyAsync(out, ubest_, sizeof(double) * n_, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                               st_));
+}
+
+void Solver::copy_current(double* out) {
+    CPFIT_CUDA(cudaMemcpyAsync(out, u_, sizeof(double) * n_, cudaMemcpyDeviceToHost, st_));
+}
+
+}  // namespace cpfit_gpu

@@ -1,0 +1,75 @@
+// Device-resident CP solvers (C++ side of the C-ABI; see solver.cu).
+#pragma once
+
+#include "device.cuh"
+
+namespace cpfit_gpu {
+
+// Mirrors cpfit::NgmresOptions (ngmres.hpp:50-57) + LineSearchParams (line_search.hpp:7-14)
+// and AlsOptions (als.hpp:16-19); gradient_scale is NgmresProblem::gradient_scale.
+struct SolverOptions {
+    int window = 20;
+    int max_iters = 2000;
+    double epsilon_reg = 1e-12;
+    double tol_grad = 1e-9;
+    double gradient_scale = 1.0;
+    double ftol = 1e-4, gtol = 1e-2, initial_step = 1.0;
+    int max_evals = 20;
+    double step_min = 0.0, step_max = 1e20;
+    int restart_on_ascent = 1;
+};
+
+// One trace row (trace.hpp:18-29); layout shared with the C-ABI cpfit_trace_row.
+struct TraceRow {
+    int32_t iter;
+    int32_t restart;
+    double time_s, f, h, gnorm_rel, beta;
+    int64_t fevals, gevals, precond_calls;
+};
+
+struct SolverSummary {
+    int iters, stop, status;
+    double f, best_f;
+    long long fevals, gevals;
+};
+
+class Solver {
+public:
+    // method 0: ALS-preconditioned N-GMRES, 1: stand-alone ALS
+    Solver(DevTensor* t, int R, const SolverOptions& o, int method);
+    ~Solver();
+    void set_initial(const double* u0, bool host);
+    void run_init();
+    void run_loop(int max_iters_total);
+    void sync();
+    SolverSummary summary();
+    void copy_trace(TraceRow* out, int rows);
+    void copy_best(double* out, bool host);
+    void copy_current(double* out);
+    cudaStream_t stream() const { return st_; }
+    int64_t n() const { return n_; }
+
+private:
+    void build_graphs();
+    DevTensor* t_;
+    int R_;
+    SolverOptions opt_;
+    int method_;
+    EvalWork* w_ = nullptr;
+    AccelWork* a_ = nullptr;
+    int64_t n_ = 0;
+    int cap_ = 1;
+    cudaStream_t st_{}, st2_{}, st3_{};
+    double *u_ = nullptr, *g_ = nullptr, *ub_ = nullptr, *gb_ = nullptr, *d_ = nullptr, *ut_ = nullptr,
+           *gt_ = nullptr, *un_ = nullptr, *gn_ = nullptr, *u0_ = nullptr, *ubest_ = nullptr, *work_ = nullptr,
+           *mbuf_ = nullptr, *wu_ = nullptr, *wg_ = nullptr;
+    void* sc_ = nullptr;
+    void* state_ = nullptr;
+    TraceRow* trace_ = nullptr;
+    int trace_cap_ = 0;
+    int host_max_ = 0;
+    cudaGraph_t g_init_ = nullptr, g_loop_ = nullptr;
+    cudaGraphExec_t x_init_ = nullptr, x_loop_ = nullptr;
+};
+
+}  // namespace cpfit_gpu

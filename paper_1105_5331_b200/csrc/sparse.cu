@@ -1,0 +1,173 @@
+// Sparse COO MTTKRP on device (tensor.cpp:242-259) for the sparse objective/gradient
+// (kruskal.cpp:106-111, 127-149).
+//
+// Each mode n has its own mode-n-sorted copy (built at upload), so M_n(i, :) is a
+// segmented sum over rows of that copy: one warp per row, lanes strided over the row's
+// nonzeros, product v * prod_{k != n} A_k(c_k, :) in the reference's mode order, then a
+// warp reduction. Deterministic (no atomics); the streamed bytes per nonzero are the
+// value plus N-1 int32 indices; the factor-row gathers hit L2 (row-major RP-padded
+// copies of the factors, rebuilt per evaluation).
+#include "sparse.cuh"
+
+#include <algorithm>
+
+namespace cpfit_gpu {
+
+namespace {
+
+struct SpParams {
+    int64_t In;
+    int64_t nnz;
+    const int64_t* rowptr;
+    const int32_t* oidx;
+    const double* vals;
+    int nother;
+    const double* frow[kMaxOrder];
+    double* out;  // In x RP
+};
+
+template <int RP>
+__global__ void sp_mttkrp_kernel(const SpParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = gw; i < p.In; i += nw) {
+        double acc[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) acc[r] = 0.0;
+        const int64_t j0 = p.rowptr[i], j1 = p.rowptr[i + 1];
+        for (int64_t j = j0 + lane; j < j1; j += 32) {
+            double prod[RP];
+            const double v = p.vals[j];
+#pragma unroll
+            for (int r = 0; r < RP; ++r) prod[r] = v;
+            for (int k = 0; k < p.nother; ++k) {
+                const int64_t c = p.oidx[(int64_t)k * p.nnz + j];
+                const double2* row = reinterpret_cast<const double2*>(p.frow[k] + c * RP);
+#pragma unroll
+                for (int r = 0; r < RP / 2; ++r) {
+                    const double2 a = __ldg(row + r);
+                    prod[2 * r] *= a.x;
+                    prod[2 * r + 1] *= a.y;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < RP; ++r) acc[r] += prod[r];
+        }
+#pragma unroll
+        for (int r = 0; r < RP; ++r) acc[r] = warp_sum(acc[r]);
+        double mine = 0.0;
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+            if (lane == r) mine = acc[r];
+        if (lane < RP) p.out[i * RP + lane] = mine;
+    }
+}
+
+__global__ void frows_kernel(int order, const int64_t* dims_d, int64_t d0, int64_t d1, int64_t d2, int64_t d3,
+                             int64_t d4, int64_t d5, int64_t d6, int64_t d7, int R, int RP, const double* u,
+                             double* frows) {
+    const int64_t dims[8] = {d0, d1, d2, d3, d4, d5, d6, d7};
+    (void)dims_d;
+    int64_t total = 0;
+    for (int n = 0; n < order; ++n) total += dims[n] * RP;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t rem = e, uoff = 0;
+        int n = 0;
+        while (rem >= dims[n] * RP) {
+            rem -= dims[n] * RP;
+            uoff += dims[n] * R;
+            ++n;
+        }
+        const int64_t i = rem / RP;
+        const int r = (int)(rem % RP);
+        frows[e] = (r < R) ? u[uoff + (int64_t)r * dims[n] + i] : 0.0;
+    }
+}
+
+}  // namespace
+
+void upload_sparse_modes(DevTensor& t, const std::vector<int64_t>& coords, const std::vector<double>& vals,
+                         cudaStream_t st) {
+    auto* sm = new SparseModes();
+    t.modes = sm;
+    const int N = t.order;
+    const int64_t nnz = (int64_t)vals.size();
+    for (int n = 0; n < N; ++n) {
+        const int64_t In = t.dims[n];
+        std::vector<int64_t> rowptr((size_t)In + 1, 0);
+        for (int64_t j = 0; j < nnz; ++j) ++rowptr[(size_t)coords[(size_t)j * N + n] + 1];
+        for (int64_t i = 0; i < In; ++i) rowptr[(size_t)i + 1] += rowptr[(size_t)i];
+        std::vector<int64_t> pos(rowptr.begin(), rowptr.end() - 1);
+        std::vector<int32_t> oidx((size_t)std::max(1, N - 1) * (size_t)nnz);
+        std::vector<double> sv((size_t)nnz);
+        for (int64_t j = 0; j < nnz; ++j) {  // stable counting sort by mode-n index
+            const int64_t dst = pos[(size_t)coords[(size_t)j * N + n]]++;
+            sv[(size_t)dst] = vals[(size_t)j];
+            int k = 0;
+            for (int m = 0; m < N; ++m) {
+                if (m == n) continue;
+                oidx[(size_t)k * nnz + dst] = (int32_t)coords[(size_t)j * N + m];
+                ++k;
+            }
+        }
+        CPFIT_CUDA(cudaMalloc(&sm->rowptr[n], sizeof(int64_t) * rowptr.size()));
+        CPFIT_CUDA(cudaMalloc(&sm->oidx[n], sizeof(int32_t) * std::max<size_t>(oidx.size(), 1)));
+        CPFIT_CUDA(cudaMalloc(&sm->vals[n], sizeof(double) * std::max<size_t>(sv.size(), 1)));
+        CPFIT_CUDA(cudaMemcpyAsync(sm->rowptr[n], rowptr.data(), sizeof(int64_t) * rowptr.size(), cudaMemcpyHostToDevice, st));
+        if (nnz > 0) {
+            CPFIT_CUDA(cudaMemcpyAsync(sm->oidx[n], oidx.data(), sizeof(int32_t) * oidx.size(), cudaMemcpyHostToDevice, st));
+            CPFIT_CUDA(cudaMemcpyAsync(sm->vals[n], sv.data(), sizeof(double) * sv.size(), cudaMemcpyHostToDevice, st));
+        }
+        CPFIT_CUDA(cudaStreamSynchronize(st));  // host staging vectors go out of scope
+    }
+    t.nnz = nnz;
+}
+
+void free_sparse_modes(DevTensor& t) {
+    if (!t.modes) return;
+    for (int n = 0; n < kMaxOrder; ++n) {
+        cudaFree(t.modes->rowptr[n]);
+        cudaFree(t.modes->oidx[n]);
+        cudaFree(t.modes->vals[n]);
+    }
+    delete t.modes;
+    t.modes = nullptr;
+}
+
+void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st) {
+    const int N = t.order;
+    int64_t total = 0;
+    for (int n = 0; n < N; ++n) total += t.dims[n] * w.RP;
+    frows_kernel<<<(int)std::min<int64_t>(1024, (total + 255) / 256), 256, 0, st>>>(
+        N, nullptr, t.dims[0], t.dims[1], t.dims[2], t.dims[3], t.dims[4], t.dims[5], t.dims[6], t.dims[7], w.R, w.RP,
+        u, w.frows);
+    CPFIT_CUDA(cudaGetLastError());
+    int64_t off[kMaxOrder + 1];
+    off[0] = 0;
+    for (int n = 0; n < N; ++n) off[n + 1] = off[n] + t.dims[n] * w.RP;
+    for (int n = 0; n < N; ++n) {
+        if (only_mode >= 0 && n != only_mode) continue;
+        SpParams p{};
+        p.In = t.dims[n];
+        p.nnz = t.nnz;
+        p.rowptr = t.modes->rowptr[n];
+        p.oidx = t.modes->oidx[n];
+        p.vals = t.modes->vals[n];
+        int k = 0;
+        for (int m = 0; m < N; ++m)
+            if (m != n) p.frow[k++] = w.frows + off[m];
+        p.nother = k;
+        p.out = w.sp_part + off[n];
+        const int blocks = (int)std::min<int64_t>(148 * 8, (p.In * 32 + 255) / 256);
+        switch (w.RP) {
+            case 8: sp_mttkrp_kernel<8><<<blocks, 256, 0, st>>>(p); break;
+            case 16: sp_mttkrp_kernel<16><<<blocks, 256, 0, st>>>(p); break;
+            case 24: sp_mttkrp_kernel<24><<<blocks, 256, 0, st>>>(p); break;
+            default: sp_mttkrp_kernel<32><<<blocks, 256, 0, st>>>(p); break;
+        }
+        CPFIT_CUDA(cudaGetLastError());
+    }
+}
+
+}  // namespace cpfit_gpu

@@ -1,0 +1,247 @@
+"""GPU parity: every device entry point through the C-ABI against the CPU oracle on the same
+seeded inputs. Per-call MTTKRP / gradient / f within 1e-12 relative (BASELINE.json north_star);
+ALS sweep / normalize / accelerate within the rounding the reformulations introduce."""
+import numpy as np
+import pytest
+
+from conftest import random_factors, random_sparse, rel
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [((3, 4, 2), 3), ((4, 3, 5), 2), ((5, 5, 5, 5), 3), ((20, 20, 20), 3), ((50, 50, 50), 5),
+          ((64, 64, 64, 64), 10), ((7, 1, 9), 4), ((33, 6, 5), 16), ((2, 3), 2), ((40, 30), 17), ((8, 3, 4, 2, 3), 5)]
+
+
+def _dense(P, O, dims, seed=0):
+    rng = np.random.default_rng(seed)
+    flat = rng.random(int(np.prod(dims))) * 2 - 1
+    return P.DataTensor.dense(flat, dims), O.Tensor.dense(dims, flat), rng
+
+
+@pytest.mark.parametrize("dims,rank", SHAPES)
+def test_mttkrp_dense_all_modes(gpu, O, dims, rank):
+    P = gpu
+    t, o, rng = _dense(P, O, dims)
+    u = random_factors(rng, dims, rank)
+    for mode in range(len(dims)):
+        got = t.mttkrp(u, mode)
+        ref = o.mttkrp(u, mode)
+        assert rel(got, ref) <= 1e-12, (dims, rank, mode, rel(got, ref))
+
+
+@pytest.mark.parametrize("dims,rank", SHAPES)
+def test_objective_and_gradient_dense(gpu, O, dims, rank):
+    P = gpu
+    t, o, rng = _dense(P, O, dims, seed=1)
+    u = random_factors(rng, dims, rank)
+    f, g = P.objective_and_gradient(t, u)
+    fo, go = o.eval(u)
+    assert abs(f - fo) <= 1e-12 * abs(fo), (f, fo)
+    assert rel(g, go) <= 1e-12
+    assert abs(P.objective(t, u) - fo) <= 1e-12 * abs(fo)
+
+
+@pytest.mark.parametrize("dims,rank,density", [((4, 4, 4), 3, 0.3), ((5, 5, 5, 5), 3, 0.3), ((30, 20, 10), 7, 0.05),
+                                               ((4, 4, 4, 4, 4, 4), 2, 0.02)])
+def test_sparse_mttkrp_and_gradient(gpu, O, dims, rank, density):
+    P = gpu
+    rng = np.random.default_rng(3)
+    coords, vals = random_sparse(rng, dims, density)
+    t = P.DataTensor.coo(dims, coords, vals)
+    o = O.Tensor.coo(dims, coords, vals)
+    u = random_factors(rng, dims, rank)
+    for mode in range(len(dims)):
+        assert rel(t.mttkrp(u, mode), o.mttkrp(u, mode)) <= 1e-12
+    f, g = P.objective_and_gradient(t, u)
+    fo, go = o.eval(u)
+    assert abs(f - fo) <= 1e-12 * max(abs(fo), 1.0)
+    assert rel(g, go) <= 1e-12
+
+
+def test_sparse_equals_dense(gpu):
+    # test_tensor.cpp:156-168
+    P = gpu
+    rng = np.random.default_rng(23)
+    dims = (4, 4, 4)
+    coords, vals = random_sparse(rng, dims, 0.3)
+    dense = np.zeros(dims, order="F")
+    dense[tuple(coords.T)] = vals
+    ts = P.DataTensor.coo(dims, coords, vals)
+    td = P.DataTensor.dense(dense)
+    u = random_factors(rng, dims, 3)
+    for n in range(3):
+        b = td.mttkrp(u, n)
+        assert np.linalg.norm(ts.mttkrp(u, n) - b) <= 1e-12 * max(1.0, np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("dims,rank", [((3, 4, 2), 3), ((50, 50, 50), 5), ((6, 7, 8, 9), 10), ((30, 20), 16)])
+def test_gram_and_normalize(gpu, O, dims, rank):
+    P = gpu
+    rng = np.random.default_rng(5)
+    u = random_factors(rng, dims, rank)
+    for skip in [-1] + list(range(len(dims))):
+        assert rel(P.gram_hadamard(dims, rank, u, skip), O.gram_hadamard(dims, rank, u, skip)) <= 1e-13
+    assert rel(P.normalize_and_reorder(dims, rank, u), O.normalize(dims, rank, u)) <= 1e-13
+
+
+@pytest.mark.parametrize("dims,rank", [((5, 4, 6), 3), ((20, 20, 20), 3), ((50, 50, 50), 5), ((12, 10, 8, 6), 4),
+                                       ((30, 25), 6)])
+def test_als_sweep(gpu, O, dims, rank):
+    P = gpu
+    t, o, rng = _dense(P, O, dims, seed=7)
+    u = random_factors(rng, dims, rank)
+    got = P.als_sweep(t, u)
+    ref = o.als_sweep(u)
+    assert rel(got, ref) <= 1e-9, rel(got, ref)
+
+
+def test_als_sweep_sparse(gpu, O):
+    P = gpu
+    rng = np.random.default_rng(8)
+    dims = (5, 4, 6)
+    coords, vals = random_sparse(rng, dims, 0.4)
+    t = P.DataTensor.coo(dims, coords, vals)
+    o = O.Tensor.coo(dims, coords, vals)
+    u = random_factors(rng, dims, 3)
+    assert rel(P.als_sweep(t, u), o.als_sweep(u)) <= 1e-9
+
+
+def test_als_singular_raises(gpu):
+    # test_als.cpp:77-81
+    P = gpu
+    t = P.DataTensor.dense(np.arange(1, 9, dtype=float), (2, 2, 2))
+    with pytest.raises(P.NumericalError):
+        P.als_sweep(t, np.zeros(12))
+
+
+@pytest.mark.parametrize("n,m", [(5, 1), (5, 4), (180, 20), (19200, 20), (1000, 7)])
+def test_accelerate_matches_oracle(gpu, O, n, m):
+    P = gpu
+    rng = np.random.default_rng(n + m)
+    wu = rng.standard_normal((m, n))
+    wg = rng.standard_normal((m, n))
+    ub = rng.standard_normal(n)
+    gb = rng.standard_normal(n)
+    out = P.accelerate(wu, wg, ub, gb, 1e-12)
+    uh, al, rr = O.accelerate(wu, wg, ub, gb, 1e-12)
+    assert rel(out.alpha, al) <= 1e-8
+    assert rel(out.u_hat, uh) <= 1e-10
+    assert out.system_residual_rel <= 1e-8
+
+
+def test_accelerate_degenerate_and_linear(gpu):
+    P = gpu
+    # test_ngmres.cpp:26-35
+    u = np.linspace(1.0, 4.0, 4)
+    g = np.full(4, 0.5)
+    out = P.accelerate([u], [g], u, g, 1e-12)
+    assert out.alpha[0] == 0.0 and np.array_equal(out.u_hat, u)
+    # test_ngmres.cpp:37-45
+    out = P.accelerate([[0.0]], [[-4.0]], np.array([1.0]), np.array([-2.0]), 1e-12)
+    assert abs(out.alpha[0] - 1.0) <= 1e-9 and abs(out.u_hat[0] - 2.0) <= 1e-9
+
+
+def _baseline_case(P, cfg):
+    dims, rank, c, l1, l2 = cfg
+    T, _, _ = P.dense_test_problem(dims, rank, c, l1, l2, 0, noise_mode=1)
+    u0 = P.uniform_initial_guess(dims, rank, 0)
+    return T, u0
+
+
+@pytest.mark.parametrize("cfg", [((20, 20, 20), 3, 0.5, 1.0, 1.0), ((50, 50, 50), 5, 0.9, 10.0, 5.0),
+                                 ((64, 64, 64, 64), 10, 0.7, 5.0, 0.0)])
+def test_baseline_config_per_call(gpu, O, cfg):
+    """BASELINE configs 0, 1, 3 at full size: per-call MTTKRP, gradient and f <= 1e-12."""
+    P = gpu
+    dims, rank = cfg[0], cfg[1]
+    T, u0 = _baseline_case(P, cfg)
+    t = P.DataTensor.dense(T, dims)
+    o = O.Tensor.dense(dims, T)
+    # the oracle sums K squares sequentially (error ~sqrt(K) eps); the device sums in double-double
+    assert abs(t.norm() - o.norm()) <= 1e-12 * o.norm()
+    for mode in range(len(dims)):
+        assert rel(t.mttkrp(u0, mode), o.mttkrp(u0, mode)) <= 1e-12
+    f, g = P.objective_and_gradient(t, u0)
+    fo, go = o.eval(u0)
+    assert abs(f - fo) <= 1e-12 * fo
+    assert rel(g, go) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg", [((20, 20, 20), 3, 0.5, 1.0, 1.0), ((50, 50, 50), 5, 0.9, 10.0, 5.0)])
+def test_ngmres_iterates_match_oracle(gpu, O, cfg):
+    """First 20 iterates within 1e-8; final f within 1e-8 and iterations-to-tol within 2%."""
+    P = gpu
+    dims, rank = cfg[0], cfg[1]
+    T, u0 = _baseline_case(P, cfg)
+    nu = sum(dims) * rank
+    t = P.DataTensor.dense(T, dims)
+    o = O.Tensor.dense(dims, T)
+    k = 20
+    ref = o.ngmres(u0, window=20, max_iters=k, tol_grad=1e-10, gradient_scale=float(nu), record_iterates=k + 1)
+    opts = P.NgmresOptions(window=20, max_iters=k, tol_grad=1e-10, gradient_scale=float(nu))
+    # iterate-by-iterate: run the device solver one iteration at a time
+    s = P.Solver(t, rank, opts, 0)
+    s.set_initial(u0)
+    s.init()
+    iters = ref["iterates"]
+    worst = 0.0
+    for it in range(1, len(iters)):
+        s.run(it)
+        st = s.state()
+        assert st["iters"] == it or st["stop"] >= 0
+        tr = s.trace(it + 1)
+        # compare accepted f and trace bookkeeping against the oracle row
+        ro = ref["trace"][it]
+        assert tr[it]["restart"] == ro["restart"], it
+        assert abs(tr[it]["f"] - ro["f"]) <= 1e-8 * abs(ro["f"]), (it, tr[it]["f"], ro["f"])
+        assert tr[it]["fevals"] == ro["fevals"], it
+        worst = max(worst, abs(tr[it]["beta"] - ro["beta"]) / max(abs(ro["beta"]), 1.0))
+        ui = s.iterate()
+        assert rel(ui, iters[it]) <= 1e-8, (it, rel(ui, iters[it]))
+        if st["stop"] >= 0:
+            break
+    assert worst <= 1e-6
+
+
+@pytest.mark.parametrize("cfg", [((20, 20, 20), 3, 0.5, 1.0, 1.0)])
+def test_ngmres_full_solve_matches_oracle(gpu, O, cfg):
+    P = gpu
+    dims, rank = cfg[0], cfg[1]
+    T, u0 = _baseline_case(P, cfg)
+    nu = sum(dims) * rank
+    t = P.DataTensor.dense(T, dims)
+    o = O.Tensor.dense(dims, T)
+    ref = o.ngmres(u0, window=20, max_iters=2000, tol_grad=1e-10, gradient_scale=float(nu))
+    res = P.ngmres_solve(t, u0, P.NgmresOptions(window=20, max_iters=2000, tol_grad=1e-10, gradient_scale=float(nu)))
+    assert res.stop_reason == ref["stop"]
+    n_ref, n_got = len(ref["trace"]) - 1, len(res.trace) - 1
+    assert abs(n_got - n_ref) <= max(1, int(0.02 * n_ref)), (n_got, n_ref)
+    assert abs(res.f - ref["f"]) <= 1e-8 * ref["f"]
+
+
+def test_ngmres_stationary_start_stops_at_iteration_one(gpu):
+    # test_ngmres.cpp:234-247
+    P = gpu
+    rng = np.random.default_rng(229)
+    dims = (4, 3, 5)
+    u = P.normalize_and_reorder(dims, 2, random_factors(rng, dims, 2))
+    T = P.full(dims, 2, u)
+    t = P.DataTensor.dense(T, dims)
+    res = P.ngmres_solve(t, u, P.NgmresOptions(tol_grad=1e-9))
+    assert res.stop_reason == P.GRAD_TOL
+    assert res.trace[-1]["iter"] == 1
+    assert np.linalg.norm(res.solution - u) <= 1e-10 * (1 + np.linalg.norm(u))
+
+
+def test_als_solve_matches_oracle(gpu, O):
+    P = gpu
+    dims, rank = (20, 20, 20), 3
+    T, _, _ = P.dense_test_problem(dims, rank, 0.5, 1.0, 1.0, 1, noise_mode=1)
+    u0 = P.uniform_initial_guess(dims, rank, 1)
+    t = P.DataTensor.dense(T, dims)
+    o = O.Tensor.dense(dims, T)
+    ref = o.als_solve(u0, tol_grad=1e-9, max_iters=60)
+    res = P.als_solve(t, u0, tol_grad=1e-9, max_iters=60)
+    assert len(res.trace) == len(ref["trace"])
+    for a, b in zip(res.trace, ref["trace"]):
+        assert abs(a["f"] - b["f"]) <= 1e-8 * abs(b["f"])
