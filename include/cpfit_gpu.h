@@ -121,11 +121,22 @@ int cpfit_solver_best(cpfit_solver s, double* u);
 int cpfit_solver_iterate(cpfit_solver s, double* u);
 int cpfit_solver_destroy(cpfit_solver s);
 
+/* kernels of this library launched by the solver's loop graphs since cpfit_solver_init
+ * (counted from the captured graph bodies x the device-side iteration / line-search counters) */
+int cpfit_solver_launches(cpfit_solver s, int64_t* launches);
+
 /* Device-resident kernel timing (inputs already in HBM): average ms per call over `reps`
  * calls timed with CUDA events on the launching stream, L2 flushed between calls when
- * flush_l2 != 0. kind: 0 mttkrp(mode), 1 objective_and_gradient, 2 als_sweep. */
+ * flush_l2 != 0. kind: 0 mttkrp(mode), 1 objective_and_gradient, 2 als_sweep,
+ * 3 fused fiber pass alone (S + M0 + per-fiber f), 4 fiber pass M0 only, 5 fiber pass S only. */
 int cpfit_bench_kernel(cpfit_tensor t, int64_t rank, const double* u, int kind, int mode, int reps, int flush_l2,
                        float* ms_per_call);
+
+/* fp64 peaks measured on the current device (DMMA m8n8k4 and DFMA issue loops), TFLOP/s */
+int cpfit_measure_fp64_peak(double* dmma_tflops, double* dfma_tflops);
+/* page-lock / unlock a host buffer (pinned H2D copies for end-to-end runs) */
+int cpfit_host_register(void* p, int64_t bytes);
+int cpfit_host_unregister(void* p);
 
 #ifdef __cplusplus
 }

@@ -47,13 +47,14 @@ struct TraceOut {
     double f, h, gnorm_rel, beta;
     int64_t fevals, gevals;
     int64_t precond_calls;
+    double time_s;
 };
 
 void write_trace(const std::vector<TraceRecord>& tr, TraceOut* out, int64_t cap, int64_t* rows) {
     *rows = static_cast<int64_t>(tr.size());
     for (size_t i = 0; i < tr.size() && static_cast<int64_t>(i) < cap; ++i)
         out[i] = {tr[i].iter, tr[i].restart ? 1 : 0, tr[i].f, tr[i].h, tr[i].gnorm_rel, tr[i].beta,
-                  tr[i].fevals, tr[i].gevals, tr[i].precond_calls};
+                  tr[i].fevals, tr[i].gevals, tr[i].precond_calls, tr[i].time_s};
 }
 }  // namespace
 

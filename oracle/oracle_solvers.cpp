@@ -383,10 +383,12 @@ NgmresStepReport ngmres_step(const NgmresProblem& p, NgmresState& s, const Ngmre
 MinimizeResult ngmres_minimize(const NgmresProblem& p, const Vector& initial, const NgmresOptions& o,
                                int record_iterates) {
     auto fit = [&](double f) { return p.fit_from_f ? p.fit_from_f(f) : 0.0; };
+    const auto t0 = std::chrono::steady_clock::now();  // ngmres.cpp:162-164
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     NgmresState s = ngmres_init(p, initial, o);
     MinimizeResult res;
     auto record = [&](int it, bool restart, double beta) {
-        res.trace.push_back({it, 0.0, s.f, fit(s.f), norm(s.g) / p.gradient_scale, s.fevals, s.gevals, it, restart, beta});
+        res.trace.push_back({it, elapsed(), s.f, fit(s.f), norm(s.g) / p.gradient_scale, s.fevals, s.gevals, it, restart, beta});
     };
     record(0, false, 0.0);
     if (record_iterates > 0) res.iterates.push_back(s.u);

@@ -31,7 +31,7 @@ _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 class TraceOut(C.Structure):
     _fields_ = [("iter", C.c_int32), ("restart", C.c_int32), ("f", C.c_double), ("h", C.c_double),
                 ("gnorm_rel", C.c_double), ("beta", C.c_double), ("fevals", C.c_int64), ("gevals", C.c_int64),
-                ("precond_calls", C.c_int64)]
+                ("precond_calls", C.c_int64), ("time_s", C.c_double)]
 
 
 class Opts(C.Structure):
@@ -214,7 +214,8 @@ class Tensor:
 
 def _trace(tr, rows):
     return [dict(iter=t.iter, f=t.f, h=t.h, gnorm_rel=t.gnorm_rel, fevals=t.fevals, gevals=t.gevals,
-                 precond_calls=t.precond_calls, restart=bool(t.restart), beta=t.beta) for t in tr[:rows]]
+                 precond_calls=t.precond_calls, restart=bool(t.restart), beta=t.beta, time_s=t.time_s)
+            for t in tr[:rows]]
 
 
 def gram_hadamard(dims, rank, u, skip=-1):

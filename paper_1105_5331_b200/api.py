@@ -103,6 +103,11 @@ _SIGS = {
     "cpfit_solver_trace": (C.c_int, [C.c_void_p, C.POINTER(TraceRow), C.c_int64]),
     "cpfit_solver_best": (C.c_int, [C.c_void_p, _f64p]),
     "cpfit_solver_iterate": (C.c_int, [C.c_void_p, _f64p]),
+    "cpfit_solver_launches": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "cpfit_measure_fp64_peak": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "cpfit_host_register": (C.c_int, [C.c_void_p, C.c_int64]),
+    "cpfit_host_unregister": (C.c_int, [C.c_void_p]),
+    "cpfit_default_ngmres_options": (None, [C.POINTER(NgmresOptionsC)]),
     "cpfit_solver_destroy": (C.c_int, [C.c_void_p]),
     "cpfit_bench_kernel": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_int, C.c_int, C.c_int, C.c_int,
                                      C.POINTER(C.c_float)]),
@@ -474,6 +479,11 @@ class Solver:
         _check(lib.cpfit_solver_iterate(self._h, out))
         return out
 
+    def launches(self) -> int:
+        n = C.c_int64()
+        _check(lib.cpfit_solver_launches(self._h, C.byref(n)))
+        return n.value
+
     def close(self):
         if self._h:
             lib.cpfit_solver_destroy(self._h)
@@ -484,6 +494,21 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def measure_fp64_peak():
+    """(DMMA TFLOP/s, DFMA TFLOP/s) measured on the current device."""
+    a, b = C.c_double(), C.c_double()
+    _check(lib.cpfit_measure_fp64_peak(C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def host_register(arr: np.ndarray):
+    _check(lib.cpfit_host_register(arr.ctypes.data, arr.nbytes))
+
+
+def host_unregister(arr: np.ndarray):
+    _check(lib.cpfit_host_unregister(arr.ctypes.data))
 
 
 def bench_kernel(t: DataTensor, u, kind: int, mode: int = 0, reps: int = 10, flush_l2: bool = True) -> float:

@@ -14,6 +14,11 @@
 
 using namespace cpfit_gpu;
 
+namespace cpfit_gpu {
+void dense_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, cudaStream_t st);
+void dense_fiber_fused(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st);
+}  // namespace cpfit_gpu
+
 struct cpfit_tensor_s {
     DevTensor* t = nullptr;
     cudaStream_t st = nullptr;
@@ -467,6 +472,10 @@ int cpfit_solver_best(cpfit_solver s, double* u) {
     });
 }
 
+int cpfit_solver_launches(cpfit_solver s, int64_t* launches) {
+    return guard([&] { *launches = s->s->summary().launches; });
+}
+
 int cpfit_solver_iterate(cpfit_solver s, double* u) {
     return guard([&] {
         s->s->copy_current(u);
@@ -501,13 +510,18 @@ int cpfit_bench_kernel(cpfit_tensor t, int64_t rank, const double* u, int kind, 
         cudaEvent_t e0, e1;
         CPFIT_CUDA(cudaEventCreate(&e0));
         CPFIT_CUDA(cudaEventCreate(&e1));
+        if (kind >= 3 && t->t->sparse) throw std::invalid_argument("fiber-pass kinds need a dense tensor");
+        if (kind >= 3) grams_device(w, du, t->st);
         auto call = [&] {
-            if (kind == 0)
-                mttkrp_device(*t->t, w, du, mode, dout, t->st);
-            else if (kind == 1)
-                eval_device(*t->t, w, du, dg, sc, nullptr, status, t->st);
-            else
-                als_sweep_device_ws(*t->t, w, du, dout, work, mbuf, status, t->st);
+            switch (kind) {
+                case 0: mttkrp_device(*t->t, w, du, mode, dout, t->st); break;
+                case 1: eval_device(*t->t, w, du, dg, sc, nullptr, status, t->st); break;
+                case 2: als_sweep_device_ws(*t->t, w, du, dout, work, mbuf, status, t->st); break;
+                case 3: dense_fiber_fused(*t->t, w, du, t->st); break;          // S + M0 + f
+                case 4: dense_fiber(*t->t, w, du, false, true, t->st); break;   // M0 only
+                case 5: dense_fiber(*t->t, w, du, true, false, t->st); break;   // S only
+                default: throw std::invalid_argument("bench kind");
+            }
         };
         for (int i = 0; i < 3; ++i) call();
         float total = 0.f;

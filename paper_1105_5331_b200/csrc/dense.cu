@@ -904,6 +904,10 @@ void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, d
 void dense_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, cudaStream_t st) {
     run_fiber(t, w, u, do_s, do_m0, false, nullptr, st);
 }
+// the fused evaluation pass alone (S + M0 + per-fiber objective); Grams of u must be current
+void dense_fiber_fused(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st) {
+    run_fiber(t, w, u, true, true, true, w.gram, st);
+}
 void dense_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
                  double* Sout, cudaStream_t st) {
     run_level(t, w, h, Sin, u, do_m, do_s, Sout, st);

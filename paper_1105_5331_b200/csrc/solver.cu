@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <vector>
 
 namespace cpfit_gpu {
 
@@ -40,6 +41,7 @@ struct DevState {
     int slot;     // slot written by this iteration's push/reset
     int is_best;
     unsigned long long t0;
+    long long total_ls_evals, total_accepted;  // for kernel-launch accounting
     MoreThuente mt;
 };
 
@@ -74,6 +76,7 @@ __global__ void k_reset(Ctl c, int max_iters) {
     s.ring[1] = 0;
     s.slot = 0;
     s.beta = 0.0;
+    s.total_ls_evals = s.total_accepted = 0;
     s.t0 = globaltimer();
 }
 
@@ -140,6 +143,7 @@ __global__ void k_ls_update(Ctl c, cudaGraphConditionalHandle ls_h) {
         s.searching = 0;
         s.fevals += s.mt.evals;
         s.gevals += s.mt.evals;
+        s.total_ls_evals += s.mt.evals;
         s.stalled = (s.mt.status == LS_STALL) ? 1 : 0;
         if (!s.status && s.mt.out_step > 0.0 && s.mt.out_f <= s.f_bar) {
             s.accepted = 1;
@@ -176,6 +180,7 @@ __global__ void k_commit(Ctl c, cudaGraphConditionalHandle loop_h) {
     } else if (s.accepted) {
         s.f = c.sc_next->f;
         s.gnorm2 = c.sc_next->gnorm2;
+        s.total_accepted += 1;
     } else {
         s.f = s.f_bar;
         s.gnorm2 = c.sc_bar->gnorm2;
@@ -252,6 +257,25 @@ __global__ void k_seed_window(const double* u, const double* g, double* wu, doub
 int vec_blocks(int64_t n) { return (int)std::min<int64_t>(592, (n + 255) / 256); }
 
 // Conditional handle owned by the graph currently being captured on `st`.
+// number of kernel nodes directly in g (conditional bodies are counted separately)
+int count_kernels(cudaGraph_t g) {
+    size_t n = 0;
+    CPFIT_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CPFIT_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+    int k = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess) {
+            // conditional nodes are not mappable by this runtime/driver pair; never kernels
+            (void)cudaGetLastError();
+            continue;
+        }
+        if (ty == cudaGraphNodeTypeKernel) ++k;
+    }
+    return k;
+}
+
 cudaGraphConditionalHandle make_handle(cudaStream_t st) {
     cudaStreamCaptureStatus cs;
     cudaGraph_t g;
@@ -381,6 +405,7 @@ void Solver::build_graphs() {
     k_set_cond_running<<<1, 1, 0, st_>>>(c, loop_h);
     cudaGraph_t body = append_conditional(st_, loop_h, cudaGraphCondTypeWhile);
     CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st2_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    cudaGraph_t lsb = nullptr, ab = nullptr;
     if (method_ == 0) {
         // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
         als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_);
@@ -391,7 +416,7 @@ void Solver::build_graphs() {
         // Step III: restart test / Moré–Thuente line search                 (ngmres.cpp:111-147)
         const cudaGraphConditionalHandle ls_h = make_handle(st2_);
         k_ls_init<<<1, 1, 0, st2_>>>(c, ls_h);
-        cudaGraph_t lsb = append_conditional(st2_, ls_h, cudaGraphCondTypeWhile);
+        lsb = append_conditional(st2_, ls_h, cudaGraphCondTypeWhile);
         CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         k_trial<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
         eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st3_);
@@ -401,7 +426,7 @@ void Solver::build_graphs() {
         // accepted step: canonicalize u_bar + beta d and re-evaluate        (ngmres.cpp:137-142)
         const cudaGraphConditionalHandle acc_h = make_handle(st2_);
         k_accept_cond<<<1, 1, 0, st2_>>>(c, acc_h);
-        cudaGraph_t ab = append_conditional(st2_, acc_h, cudaGraphCondTypeIf);
+        ab = append_conditional(st2_, acc_h, cudaGraphCondTypeIf);
         CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, ab, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         k_step_point<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
         grams_device(*w_, ut_, st3_);
@@ -420,6 +445,11 @@ void Solver::build_graphs() {
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaStreamEndCapture(st2_, &body));
     CPFIT_CUDA(cudaStreamEndCapture(st_, &g_loop_));
+    // kernel nodes per graph level, counted once every capture is closed
+    n_prelude_ = count_kernels(g_loop_);
+    n_body_ = count_kernels(body);
+    n_ls_ = lsb ? count_kernels(lsb) : 0;
+    n_acc_ = ab ? count_kernels(ab) : 0;
     CPFIT_CUDA(cudaGraphInstantiate(&x_loop_, g_loop_, 0));
 }
 
@@ -436,6 +466,7 @@ void Solver::run_loop(int max_iters_total) {
     DevState* s = reinterpret_cast<DevState*>(state_);
     CPFIT_CUDA(cudaMemcpyAsync(&s->max_iters, &host_max_, sizeof(int), cudaMemcpyHostToDevice, st_));
     CPFIT_CUDA(cudaGraphLaunch(x_loop_, st_));
+    ++loop_launches_;
 }
 
 void Solver::sync() { CPFIT_CUDA(cudaStreamSynchronize(st_)); }
@@ -452,6 +483,8 @@ SolverSummary Solver::summary() {
     r.status = hs.status;
     r.fevals = hs.fevals;
     r.gevals = hs.gevals;
+    r.launches = (long long)loop_launches_ * n_prelude_ + (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ +
+                 hs.total_accepted * n_acc_;
     return r;
 }
 

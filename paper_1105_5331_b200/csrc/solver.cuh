@@ -31,6 +31,7 @@ struct SolverSummary {
     int iters, stop, status;
     double f, best_f;
     long long fevals, gevals;
+    long long launches;  // kernels launched by the loop graphs since init
 };
 
 class Solver {
@@ -68,6 +69,8 @@ private:
     TraceRow* trace_ = nullptr;
     int trace_cap_ = 0;
     int host_max_ = 0;
+    int n_prelude_ = 0, n_body_ = 0, n_ls_ = 0, n_acc_ = 0;
+    long long loop_launches_ = 0;
     cudaGraph_t g_init_ = nullptr, g_loop_ = nullptr;
     cudaGraphExec_t x_init_ = nullptr, x_loop_ = nullptr;
 };
