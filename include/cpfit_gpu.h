@@ -48,6 +48,14 @@ typedef struct {
     int32_t max_evals;
     int32_t restart_on_ascent;
     double step_min, step_max;
+    /* 1: re-evaluate at the canonicalized accepted point (ngmres.cpp:139-140) — one more pass
+     * over T per accepted step; 0 (default): map the accepted trial's f and gradient through
+     * the exact normalisation rescale (f invariant, G_n -> G_n D_n^-1). Counters are identical. */
+    int32_t reeval_accepted;
+    /* 1: every evaluation uses the residual objective 1/2 sum (T - model)^2 (kruskal.cpp:83-102,
+     * 6KR flops); 0 (default): the per-fiber three-term form (4KR, ~1e-14 relative at h ~ 1e-2)
+     * until f stagnates (relative decrease < 1e-8) or h < 1e-3, then the residual form. */
+    int32_t residual_objective;
 } cpfit_ngmres_options;
 
 /* line_search.hpp:7-14 / 23-29 */
@@ -114,6 +122,9 @@ int cpfit_solver_set_initial(cpfit_solver s, const double* u0);
 int cpfit_solver_init(cpfit_solver s);
 /* runs until max_iters_total iterations (or a stop); *ms = CUDA-event time on the solver stream */
 int cpfit_solver_run(cpfit_solver s, int max_iters_total, float* ms);
+/* new start point (host), init (canonicalize + evaluate + seed window) and run; *ms covers
+ * init + loop on the solver stream */
+int cpfit_solver_restart(cpfit_solver s, const double* u0, int max_iters_total, float* ms);
 int cpfit_solver_state(cpfit_solver s, int* iters, int* stop_reason, double* f, double* best_f, int64_t* fevals);
 int cpfit_solver_trace(cpfit_solver s, cpfit_trace_row* trace, int64_t rows);
 int cpfit_solver_best(cpfit_solver s, double* u);

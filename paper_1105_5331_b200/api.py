@@ -54,7 +54,8 @@ class NgmresOptionsC(C.Structure):
     _fields_ = [("window", C.c_int32), ("max_iters", C.c_int32), ("epsilon_reg", C.c_double),
                 ("tol_grad", C.c_double), ("gradient_scale", C.c_double), ("ftol", C.c_double),
                 ("gtol", C.c_double), ("initial_step", C.c_double), ("max_evals", C.c_int32),
-                ("restart_on_ascent", C.c_int32), ("step_min", C.c_double), ("step_max", C.c_double)]
+                ("restart_on_ascent", C.c_int32), ("step_min", C.c_double), ("step_max", C.c_double),
+                ("reeval_accepted", C.c_int32), ("residual_objective", C.c_int32)]
 
 
 class LsParamsC(C.Structure):
@@ -98,6 +99,7 @@ _SIGS = {
     "cpfit_solver_set_initial": (C.c_int, [C.c_void_p, _f64p]),
     "cpfit_solver_init": (C.c_int, [C.c_void_p]),
     "cpfit_solver_run": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_float)]),
+    "cpfit_solver_restart": (C.c_int, [C.c_void_p, _f64p, C.c_int, C.POINTER(C.c_float)]),
     "cpfit_solver_state": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "cpfit_solver_trace": (C.c_int, [C.c_void_p, C.POINTER(TraceRow), C.c_int64]),
@@ -385,12 +387,14 @@ class NgmresOptions:
     line_search: LineSearchParams = field(default_factory=LineSearchParams)
     restart_on_ascent: bool = True
     gradient_scale: float = 0.0  # <= 0: ||T||_F as in ngmres_solve
+    reeval_accepted: bool = False  # True: the reference's extra evaluation after acceptance
+    residual_objective: bool = False  # True: residual-form f for every evaluation
 
     def c(self):
         ls = self.line_search
         return NgmresOptionsC(self.window, self.max_iters, self.epsilon_reg, self.tol_grad, self.gradient_scale,
                               ls.ftol, ls.gtol, ls.initial_step, ls.max_evals, int(self.restart_on_ascent),
-                              ls.step_min, ls.step_max)
+                              ls.step_min, ls.step_max, int(self.reeval_accepted), int(self.residual_objective))
 
 
 @dataclass
@@ -456,6 +460,12 @@ class Solver:
     def run(self, max_iters_total) -> float:
         ms = C.c_float()
         _check(lib.cpfit_solver_run(self._h, int(max_iters_total), C.byref(ms)))
+        return ms.value
+
+    def restart(self, u0, max_iters_total) -> float:
+        """New start point + init + loop; CUDA-event ms for init + loop."""
+        ms = C.c_float()
+        _check(lib.cpfit_solver_restart(self._h, _f64(u0), int(max_iters_total), C.byref(ms)))
         return ms.value
 
     def state(self):

@@ -121,6 +121,11 @@ struct NormParams {
     const double* gram;
     const double* u;
     double* out;
+    // optional: the gradient at u, mapped to the normalised point (G -> G D^-1, permuted),
+    // and per-block partial sums of its squares
+    const double* g;
+    double* gout;
+    double* red;
 };
 
 // normalize_and_reorder: norms from the (double-double) Gram diagonals, lambda_r =
@@ -157,6 +162,7 @@ __global__ void normalize_kernel(const NormParams p) {
     }
     __syncthreads();
     const int64_t total = p.off[p.order];
+    double g2 = 0.0;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + tid; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         int n = 0;
         while (e >= p.off[n + 1]) ++n;
@@ -165,8 +171,26 @@ __global__ void normalize_kernel(const NormParams p) {
         const int r = (int)(loc / In);
         const int64_t i = loc % In;
         const int src = perm[r];
-        const double v = p.u[p.off[n] + (int64_t)src * In + i];
-        p.out[e] = (lam[src] == 0.0) ? v : v * scale[n][r];
+        const int64_t at = p.off[n] + (int64_t)src * In + i;
+        const double v = p.u[at];
+        const bool keep = (lam[src] == 0.0);
+        p.out[e] = keep ? v : v * scale[n][r];
+        if (p.g) {
+            const double gv = keep ? p.g[at] : p.g[at] / scale[n][r];
+            p.gout[e] = gv;
+            g2 += gv * gv;
+        }
+    }
+    if (p.g) {
+        __shared__ double red[32];
+        g2 = warp_sum(g2);
+        if ((tid & 31) == 0) red[tid >> 5] = g2;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+            p.red[blockIdx.x] = s;
+        }
     }
 }
 
@@ -203,6 +227,29 @@ void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st
     const int blocks = (int)std::min<int64_t>(296, (w.nu + 255) / 256);
     normalize_kernel<<<blocks, 256, 0, st>>>(p);
     CPFIT_CUDA(cudaGetLastError());
+}
+
+int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
+                          cudaStream_t st) {
+    NormParams p{};
+    p.order = w.order;
+    p.R = w.R;
+    p.RP = w.RP;
+    for (int n = 0; n < w.order; ++n) {
+        p.dims[n] = w.dims[n];
+        p.off[n] = w.off[n];
+    }
+    p.off[w.order] = w.off[w.order];
+    p.gram = w.gram;
+    p.u = u;
+    p.out = uout;
+    p.g = g;
+    p.gout = gout;
+    p.red = red;
+    const int blocks = (int)std::min<int64_t>(296, (w.nu + 255) / 256);
+    normalize_kernel<<<blocks, 256, 0, st>>>(p);
+    CPFIT_CUDA(cudaGetLastError());
+    return blocks;
 }
 
 namespace {

@@ -16,7 +16,7 @@ using namespace cpfit_gpu;
 
 namespace cpfit_gpu {
 void dense_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, cudaStream_t st);
-void dense_fiber_fused(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st);
+void dense_fiber_fused(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st, const int* resid_flag);
 }  // namespace cpfit_gpu
 
 struct cpfit_tensor_s {
@@ -26,8 +26,18 @@ struct cpfit_tensor_s {
     std::mutex mu;
     double* scratch = nullptr;  // device buffers for per-call ops
     size_t scratch_n = 0;
+    int* one_ = nullptr;        // device int 1: residual-form objective for per-call evaluations
+    const int* one() {
+        if (!one_) {
+            CPFIT_CUDA(cudaMalloc(&one_, sizeof(int)));
+            const int v = 1;
+            CPFIT_CUDA(cudaMemcpy(one_, &v, sizeof(int), cudaMemcpyHostToDevice));
+        }
+        return one_;
+    }
     ~cpfit_tensor_s() {
         for (auto& kv : works) work_destroy(kv.second);
+        cudaFree(one_);
         cudaFree(scratch);
         tensor_destroy(t);
         if (st) cudaStreamDestroy(st);
@@ -136,6 +146,8 @@ SolverOptions to_opts(const cpfit_ngmres_options* o, double tnorm) {
     s.step_min = o->step_min;
     s.step_max = o->step_max;
     s.restart_on_ascent = o->restart_on_ascent;
+    s.reeval_accepted = o->reeval_accepted;
+    s.residual_objective = o->residual_objective;
     if (s.window < 1) throw std::invalid_argument("ngmres: window must be >= 1");
     if (!(s.tol_grad > 0.0)) throw std::invalid_argument("ngmres: tol_grad must be > 0");
     if (s.epsilon_reg < 0.0) throw std::invalid_argument("ngmres: epsilon_reg must be >= 0");
@@ -187,7 +199,7 @@ int cpfit_device_count(void) {
 }
 
 void cpfit_default_ngmres_options(cpfit_ngmres_options* o) {
-    *o = cpfit_ngmres_options{20, 2000, 1e-12, 1e-9, 0.0, 1e-4, 1e-2, 1.0, 20, 1, 0.0, 1e20};
+    *o = cpfit_ngmres_options{20, 2000, 1e-12, 1e-9, 0.0, 1e-4, 1e-2, 1.0, 20, 1, 0.0, 1e20, 0, 0};
 }
 
 int cpfit_tensor_create_dense(int order, const int64_t* dims, const double* values, cpfit_tensor* out) {
@@ -248,7 +260,8 @@ static int eval_impl(cpfit_tensor t, int64_t rank, const double* u, double* grad
         double* dg = du + w.nu;
         EvalScalars* sc = reinterpret_cast<EvalScalars*>(dg + w.nu);
         CPFIT_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * w.nu, cudaMemcpyHostToDevice, t->st));
-        eval_device(*t->t, w, du, dg, sc, nullptr, nullptr, t->st, grad != nullptr);
+        // per-call objective uses the reference's residual form (kruskal.cpp:83-102)
+        eval_device(*t->t, w, du, dg, sc, nullptr, nullptr, t->st, grad != nullptr, t->one());
         EvalScalars hs;
         CPFIT_CUDA(cudaMemcpyAsync(&hs, sc, sizeof(EvalScalars), cudaMemcpyDeviceToHost, t->st));
         if (grad) CPFIT_CUDA(cudaMemcpyAsync(grad, dg, sizeof(double) * w.nu, cudaMemcpyDeviceToHost, t->st));
@@ -449,6 +462,22 @@ int cpfit_solver_run(cpfit_solver s, int max_iters_total, float* ms) {
     });
 }
 
+int cpfit_solver_restart(cpfit_solver s, const double* u0, int max_iters_total, float* ms) {
+    return guard([&] {
+        Solver& sv = *s->s;
+        sv.set_initial(u0, true);
+        sv.sync();
+        CPFIT_CUDA(cudaEventRecord(s->e0, sv.stream()));
+        sv.run_init();
+        sv.run_loop(max_iters_total);
+        CPFIT_CUDA(cudaEventRecord(s->e1, sv.stream()));
+        CPFIT_CUDA(cudaEventSynchronize(s->e1));
+        float t = 0.f;
+        CPFIT_CUDA(cudaEventElapsedTime(&t, s->e0, s->e1));
+        if (ms) *ms = t;
+    });
+}
+
 int cpfit_solver_state(cpfit_solver s, int* iters, int* stop_reason, double* f, double* best_f, int64_t* fevals) {
     return guard([&] {
         const SolverSummary sm = s->s->summary();
@@ -515,9 +544,11 @@ int cpfit_bench_kernel(cpfit_tensor t, int64_t rank, const double* u, int kind, 
         auto call = [&] {
             switch (kind) {
                 case 0: mttkrp_device(*t->t, w, du, mode, dout, t->st); break;
-                case 1: eval_device(*t->t, w, du, dg, sc, nullptr, status, t->st); break;
+                case 1: eval_device(*t->t, w, du, dg, sc, nullptr, status, t->st, true, t->one()); break;
+                case 7: eval_device(*t->t, w, du, dg, sc, nullptr, status, t->st, true, nullptr); break;
                 case 2: als_sweep_device_ws(*t->t, w, du, dout, work, mbuf, status, t->st); break;
-                case 3: dense_fiber_fused(*t->t, w, du, t->st); break;          // S + M0 + f
+                case 3: dense_fiber_fused(*t->t, w, du, t->st, nullptr); break;   // S + M0 + per-fiber f
+                case 6: dense_fiber_fused(*t->t, w, du, t->st, t->one()); break;  // S + M0 + residual f
                 case 4: dense_fiber(*t->t, w, du, false, true, t->st); break;   // M0 only
                 case 5: dense_fiber(*t->t, w, du, true, false, t->st); break;   // S only
                 default: throw std::invalid_argument("bench kind");

@@ -50,10 +50,14 @@ struct FiberParams {
     double* f_part;                // grid
     const double* gamma0;          // RP x RP
     const double* fnorm2;          // J
+    const int* resid_flag;         // device flag: residual-form objective when nonzero
     int64_t tiles_per_cta;
     int64_t ntiles;
 };
 
+#include "fiber.cuh"
+
+#if 0  // first version (CTA-wide barriers per tile), superseded by fiber.cuh
 constexpr int kStages = 3;
 
 template <int RP, int F>
@@ -289,8 +293,10 @@ size_t fiber_smem(int RP, int nchunk) {
     }
 }
 
+#endif
+
 void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, bool do_f,
-               const double* gamma0, cudaStream_t st) {
+               const double* gamma0, cudaStream_t st, const int* resid_flag = nullptr) {
     FiberParams p{};
     p.T = t.T;
     p.ldT = t.ldT;
@@ -313,6 +319,7 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
     p.f_part = w.f_part;
     p.gamma0 = gamma0;
     p.fnorm2 = t.fiber_norm2;
+    p.resid_flag = resid_flag;
     p.ntiles = (t.J + w.fiber_F - 1) / w.fiber_F;
     p.tiles_per_cta = (p.ntiles + w.fiber_grid - 1) / w.fiber_grid;
     const int grid = (int)((p.ntiles + p.tiles_per_cta - 1) / p.tiles_per_cta);
@@ -326,7 +333,6 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
     switch (w.RP) {
         case 8: launch_fiber<8>(p, grid, w.fiber_nchunk, w.fiber_smem, st); break;
         case 16: launch_fiber<16>(p, grid, w.fiber_nchunk, w.fiber_smem, st); break;
-        case 24: launch_fiber<24>(p, grid, w.fiber_nchunk, w.fiber_smem, st); break;
         default: launch_fiber<32>(p, grid, w.fiber_nchunk, w.fiber_smem, st); break;
     }
 }
@@ -692,7 +698,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
     if (R < 1 || R > kMaxRank) throw std::invalid_argument("device path supports 1 <= rank <= 32");
     auto* w = new EvalWork();
     w->R = R;
-    w->RP = round_up(R, 8);
+    w->RP = (R <= 8) ? 8 : (R <= 16 ? 16 : 32);  // power of two: per-fiber lane groups
     w->order = t.order;
     w->off[0] = 0;
     for (int n = 0; n < t.order; ++n) {
@@ -714,11 +720,12 @@ EvalWork* work_create(const DevTensor& t, int R) {
         if (t.order < 2) throw std::invalid_argument("device dense path needs order >= 2");
         const int I0 = (int)t.dims[0];
         w->fiber_nchunk = (I0 + 31) / 32;
-        if (w->fiber_nchunk > 16) throw std::invalid_argument("device dense path supports I_1 <= 512");
+        if (w->fiber_nchunk > 13) throw std::invalid_argument("device dense path supports I_1 <= 416");
         w->fiber_smem = fiber_smem(w->RP, w->fiber_nchunk);
         if (w->fiber_smem > 227 * 1024) throw std::invalid_argument("fiber tile does not fit shared memory");
         const int64_t ntiles = (t.J + w->fiber_F - 1) / w->fiber_F;
-        const int per_sm = std::max(1, std::min(2048 / (32 * w->fiber_nchunk), (int)((228 * 1024) / (w->fiber_smem + 1024))));
+        const int per_sm = std::max(1, std::min(2048 / (32 * (w->fiber_nchunk + 3)),
+                                                (int)((228 * 1024) / (w->fiber_smem + 1024))));
         w->fiber_grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
         CPFIT_CUDA(cudaMalloc(&w->S, sizeof(double) * (size_t)t.J * w->RP));
         CPFIT_CUDA(cudaMalloc(&w->m0_part, sizeof(double) * (size_t)w->fiber_grid * w->RP * 32 * w->fiber_nchunk));
@@ -819,12 +826,12 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
 }  // namespace
 
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
-                 int* status, cudaStream_t st, bool need_grad) {
+                 int* status, cudaStream_t st, bool need_grad, const int* resid_flag) {
     (void)status;
     grams_device(w, u, st);
     if (!t.sparse) {
         // fused pass: S, M0 partials and per-fiber objective
-        run_fiber(t, w, u, true, true, true, w.gram /* mode-0 Gram */, st);
+        run_fiber(t, w, u, true, true, true, w.gram /* mode-0 Gram */, st, resid_flag);
         // modes 1..N-1 from S
         const double* Sin = w.S;
         for (int h = 1; h < t.order - 1; ++h) {
@@ -905,8 +912,8 @@ void dense_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bo
     run_fiber(t, w, u, do_s, do_m0, false, nullptr, st);
 }
 // the fused evaluation pass alone (S + M0 + per-fiber objective); Grams of u must be current
-void dense_fiber_fused(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st) {
-    run_fiber(t, w, u, true, true, true, w.gram, st);
+void dense_fiber_fused(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st, const int* resid_flag) {
+    run_fiber(t, w, u, true, true, true, w.gram, st, resid_flag);
 }
 void dense_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
                  double* Sout, cudaStream_t st) {

@@ -83,7 +83,7 @@ struct EvalScalars {
 // scalars->f, ->gnorm2 and (if d != nullptr) ->gdotd.  Grams of u are computed first.
 // mode = 0 gradient+f; mode = 1 f only (objective()).
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
-                 int* status, cudaStream_t st, bool need_grad = true);
+                 int* status, cudaStream_t st, bool need_grad = true, const int* resid_flag = nullptr);
 
 // mttkrp(T, factors(u), mode) (tensor.cpp:206-259) -> out (I_mode x R col-major).
 void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st);
@@ -94,6 +94,10 @@ void grams_device(EvalWork& w, const double* u, cudaStream_t st);
 void gram_hadamard_device(EvalWork& w, int skip, double* out, cudaStream_t st);
 // normalize_and_reorder (kruskal.cpp:156-193): u -> out, Grams in w.gram updated to match.
 void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st);
+// normalize u -> uout and map the gradient g at u to the normalised point (G_n D_n^-1,
+// permuted) -> gout; writes per-block partial ||gout||^2 to red, returns the block count.
+int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
+                          cudaStream_t st);
 // One ALS sweep (als.cpp:38-48): u -> out (normalized); work: n_u scratch, mbuf: max I_n x R
 // scratch. status: bit0 singular normal matrix after the ridge retry, bit1 non-finite solve.
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,

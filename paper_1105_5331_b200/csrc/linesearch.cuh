@@ -28,6 +28,7 @@ struct MoreThuente {
     int bracketed, stage1;
     double best_s, best_f, best_g;
     int evals;
+    int last_improved;
     int status;
     double out_step, out_f, out_g;
 
@@ -79,6 +80,7 @@ struct MoreThuente {
     // when the search has terminated (status/out_* set); otherwise stp holds the next trial.
     __host__ __device__ bool update(double f, double g) {
         ++evals;
+        last_improved = (f < best_f) ? 1 : 0;  // lets the caller keep the best trial's data
         if (f < best_f) {
             best_s = stp;
             best_f = f;

@@ -42,6 +42,9 @@ struct DevState {
     int is_best;
     unsigned long long t0;
     long long total_ls_evals, total_accepted;  // for kernel-launch accounting
+    // objective form for every evaluation of this solve: 0 per-fiber three-term (4KR),
+    // 1 residual (6KR, the reference's form); switched on (sticky) once f stagnates or h is small
+    int resid;
     MoreThuente mt;
 };
 
@@ -55,6 +58,7 @@ struct Ctl {
     TraceRow* trace;
     int trace_cap;
     double gradient_scale, hscale, tol_grad;
+    int resid_always;
     int cap;
     int restart_on_ascent;
     LsParams ls;
@@ -77,7 +81,16 @@ __global__ void k_reset(Ctl c, int max_iters) {
     s.slot = 0;
     s.beta = 0.0;
     s.total_ls_evals = s.total_accepted = 0;
+    s.resid = c.resid_always;
     s.t0 = globaltimer();
+}
+
+// Residual form once f stagnates (relative decrease < 1e-8 per iteration) or the fit is
+// nearly exact (h < 1e-3): from there on the Wolfe tests compare f values whose differences
+// are below the per-fiber form's rounding floor (~1e-14 (0.02/h)^2 relative).
+__device__ void update_objective_form(const Ctl& c, DevState& s, double f_old) {
+    if (s.resid) return;
+    if (2.0 * s.f < 1e-6 * c.hscale * c.hscale || (f_old - s.f) < 1e-8 * s.f) s.resid = 1;
 }
 
 // after canonical(u0) + eval: window seeded with (u, g), trace row 0, best = u
@@ -95,6 +108,7 @@ __global__ void k_after_init(Ctl c) {
                           0.0, s.fevals, s.gevals, 0};
     if (s.status) s.stop = 100 + s.status;
     if (c.als_mode && gn / c.gradient_scale <= c.tol_grad) s.stop = 0;  // als.cpp:74-77
+    if (2.0 * s.f < 1e-6 * c.hscale * c.hscale) s.resid = 1;
 }
 
 __global__ void k_set_cond_running(Ctl c, cudaGraphConditionalHandle h) {
@@ -169,9 +183,42 @@ __global__ void k_after_next(Ctl c) {
     s.gevals += 1;
 }
 
+// keep (u, g) of the best trial so far (returned by More–Thuente under MaxEvals / Stall)
+__global__ void k_keep_best(const DevState* s, const double* ut, const double* gt, double* ubl, double* gbl,
+                            int64_t n) {
+    if (!s->mt.last_improved) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        ubl[i] = ut[i];
+        gbl[i] = gt[i];
+    }
+}
+
+// accepted step = the last trial when Converged, else the best trial: bring it into (ut, gt)
+__global__ void k_select_accepted(const DevState* s, const double* ubl, const double* gbl, double* ut, double* gt,
+                                  int64_t n) {
+    if (s->mt.status == LS_CONVERGED) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        ut[i] = ubl[i];
+        gt[i] = gbl[i];
+    }
+}
+
+// f at the canonical point equals f at the accepted trial (normalisation preserves full(K));
+// the gradient was mapped by the exact column rescale; counters as if re-evaluated
+__global__ void k_after_rescale(Ctl c, EvalScalars* scn, const double* red, int nblk) {
+    DevState& s = *c.s;
+    double g2 = 0.0;
+    for (int b = 0; b < nblk; ++b) g2 += red[b];
+    scn->f = s.mt.out_f;
+    scn->gnorm2 = g2;
+    s.fevals += 1;
+    s.gevals += 1;
+}
+
 // Scalar part of the commit (ngmres.cpp:150-157, 182-197).
 __global__ void k_commit(Ctl c, cudaGraphConditionalHandle loop_h) {
     DevState& s = *c.s;
+    const double f_old = s.f;
     if (c.als_mode) {
         s.f = c.sc_next->f;
         s.gnorm2 = c.sc_next->gnorm2;
@@ -209,6 +256,7 @@ __global__ void k_commit(Ctl c, cudaGraphConditionalHandle loop_h) {
                                    gn / c.gradient_scale, s.beta, s.fevals, s.gevals, s.iter};
     s.is_best = (s.f < s.best_f) ? 1 : 0;
     if (s.is_best) s.best_f = s.f;
+    update_objective_form(c, s, f_old);
     if (s.status) {
         s.stop = 100 + s.status;
     } else if (c.als_mode) {
@@ -326,6 +374,9 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     alloc(&gn_, n_);
     alloc(&u0_, n_);
     alloc(&ubest_, n_);
+    alloc(&ubl_, n_);
+    alloc(&gbl_, n_);
+    alloc(&red_, 1024);
     alloc(&work_, n_);
     int64_t maxI = 1;
     for (int k = 0; k < t->order; ++k) maxI = std::max(maxI, t->dims[k]);
@@ -348,7 +399,8 @@ Solver::~Solver() {
     if (x_loop_) cudaGraphExecDestroy(x_loop_);
     if (g_init_) cudaGraphDestroy(g_init_);
     if (g_loop_) cudaGraphDestroy(g_loop_);
-    for (double* p : {u_, g_, ub_, gb_, d_, ut_, gt_, un_, gn_, u0_, ubest_, work_, mbuf_, wu_, wg_}) cudaFree(p);
+    for (double* p : {u_, g_, ub_, gb_, d_, ut_, gt_, un_, gn_, u0_, ubest_, work_, mbuf_, wu_, wg_, ubl_, gbl_, red_})
+        cudaFree(p);
     cudaFree(sc_);
     cudaFree(state_);
     cudaFree(trace_);
@@ -377,6 +429,7 @@ void Solver::build_graphs() {
     c.gradient_scale = opt_.gradient_scale;
     c.hscale = t_->norm;
     c.tol_grad = opt_.tol_grad;
+    c.resid_always = opt_.residual_objective;
     c.cap = cap_;
     c.restart_on_ascent = opt_.restart_on_ascent;
     c.ls = LsParams{opt_.ftol, opt_.gtol, opt_.initial_step, opt_.max_evals, opt_.step_min, opt_.step_max};
@@ -389,7 +442,7 @@ void Solver::build_graphs() {
     k_reset<<<1, 1, 0, st_>>>(c, opt_.max_iters);
     grams_device(*w_, u0_, st_);
     normalize_device(*w_, u0_, u_, st_);
-    eval_device(*t_, *w_, u_, g_, sc_cur, nullptr, status, st_);
+    eval_device(*t_, *w_, u_, g_, sc_cur, nullptr, status, st_, true, &s->resid);
     k_after_init<<<1, 1, 0, st_>>>(c);
     if (method_ == 0)
         k_seed_window<<<vb, 256, 0, st_>>>(u_, g_, wu_, wg_, ubest_, n_);
@@ -397,6 +450,7 @@ void Solver::build_graphs() {
         k_seed_window<<<vb, 256, 0, st_>>>(u_, g_, ut_, gt_, ubest_, n_);
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaStreamEndCapture(st_, &g_init_));
+    n_init_ = count_kernels(g_init_);
     CPFIT_CUDA(cudaGraphInstantiate(&x_init_, g_init_, 0));
 
     // ---- loop graph: WHILE(running) { one iteration } -----------------------------------
@@ -409,7 +463,7 @@ void Solver::build_graphs() {
     if (method_ == 0) {
         // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
         als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_);
-        eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_);
+        eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_, true, &s->resid);
         k_after_bar<<<1, 1, 0, st2_>>>(c);
         // Step II: windowed recombination -> d, slope                        (ngmres.cpp:97-101)
         accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st2_);
@@ -419,8 +473,9 @@ void Solver::build_graphs() {
         lsb = append_conditional(st2_, ls_h, cudaGraphCondTypeWhile);
         CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         k_trial<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
-        eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st3_);
+        eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st3_, true, &s->resid);
         k_ls_update<<<1, 1, 0, st3_>>>(c, ls_h);
+        if (!opt_.reeval_accepted) k_keep_best<<<vb, 256, 0, st3_>>>(s, ut_, gt_, ubl_, gbl_, n_);
         CPFIT_CUDA(cudaGetLastError());
         CPFIT_CUDA(cudaStreamEndCapture(st3_, &lsb));
         // accepted step: canonicalize u_bar + beta d and re-evaluate        (ngmres.cpp:137-142)
@@ -428,17 +483,27 @@ void Solver::build_graphs() {
         k_accept_cond<<<1, 1, 0, st2_>>>(c, acc_h);
         ab = append_conditional(st2_, acc_h, cudaGraphCondTypeIf);
         CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, ab, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        k_step_point<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
-        grams_device(*w_, ut_, st3_);
-        normalize_device(*w_, ut_, un_, st3_);
-        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st3_);
-        k_after_next<<<1, 1, 0, st3_>>>(c);
+        if (opt_.reeval_accepted) {
+            // faithful: canonicalize u_bar + beta d, then a full evaluation there
+            k_step_point<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
+            grams_device(*w_, ut_, st3_);
+            normalize_device(*w_, ut_, un_, st3_);
+            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st3_, true, &s->resid);
+            k_after_next<<<1, 1, 0, st3_>>>(c);
+        } else {
+            // exact rescale: normalize_and_reorder scales columns by D_n with
+            // prod_n D_n = I, so f is unchanged and G_n -> G_n D_n^-1 (permuted)
+            k_select_accepted<<<vb, 256, 0, st3_>>>(s, ubl_, gbl_, ut_, gt_, n_);
+            grams_device(*w_, ut_, st3_);
+            const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st3_);
+            k_after_rescale<<<1, 1, 0, st3_>>>(c, sc_next, red_, nb);
+        }
         CPFIT_CUDA(cudaGetLastError());
         CPFIT_CUDA(cudaStreamEndCapture(st3_, &ab));
     } else {
         // stand-alone ALS iteration (als.cpp:79-95)
         als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_);
-        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_);
+        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid);
     }
     k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
     k_commit_vec<<<vb, 256, 0, st2_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_);
@@ -458,7 +523,20 @@ void Solver::set_initial(const double* u0, bool host) {
                                st_));
 }
 
-void Solver::run_init() { CPFIT_CUDA(cudaGraphLaunch(x_init_, st_)); }
+void Solver::run_init() {
+    // the device iteration counters restart with every init: fold the finished solve's
+    // loop kernels into the running total first
+    if (init_launches_ > 0) launches_done_ += pending_loop_launches();
+    CPFIT_CUDA(cudaGraphLaunch(x_init_, st_));
+    ++init_launches_;
+}
+
+long long Solver::pending_loop_launches() {
+    DevState hs;
+    CPFIT_CUDA(cudaMemcpyAsync(&hs, state_, sizeof(DevState), cudaMemcpyDeviceToHost, st_));
+    sync();
+    return (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + hs.total_accepted * n_acc_;
+}
 
 void Solver::run_loop(int max_iters_total) {
     if (max_iters_total > opt_.max_iters) max_iters_total = opt_.max_iters;
@@ -483,8 +561,8 @@ SolverSummary Solver::summary() {
     r.status = hs.status;
     r.fevals = hs.fevals;
     r.gevals = hs.gevals;
-    r.launches = (long long)loop_launches_ * n_prelude_ + (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ +
-                 hs.total_accepted * n_acc_;
+    r.launches = launches_done_ + loop_launches_ * n_prelude_ + init_launches_ * n_init_ +
+                 (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + hs.total_accepted * n_acc_;
     return r;
 }
 

@@ -17,6 +17,12 @@ struct SolverOptions {
     int max_evals = 20;
     double step_min = 0.0, step_max = 1e20;
     int restart_on_ascent = 1;
+    // 1: re-evaluate at the canonicalized accepted point as ngmres.cpp:139-140 does;
+    // 0: map the accepted trial's (f, g) through the exact normalisation rescale (default)
+    int reeval_accepted = 0;
+    // 1: every evaluation uses the residual objective (kruskal.cpp:83-102); 0: per-fiber
+    // three-term form until f stagnates, then residual (sticky)
+    int residual_objective = 0;
 };
 
 // One trace row (trace.hpp:18-29); layout shared with the C-ABI cpfit_trace_row.
@@ -63,13 +69,15 @@ private:
     cudaStream_t st_{}, st2_{}, st3_{};
     double *u_ = nullptr, *g_ = nullptr, *ub_ = nullptr, *gb_ = nullptr, *d_ = nullptr, *ut_ = nullptr,
            *gt_ = nullptr, *un_ = nullptr, *gn_ = nullptr, *u0_ = nullptr, *ubest_ = nullptr, *work_ = nullptr,
-           *mbuf_ = nullptr, *wu_ = nullptr, *wg_ = nullptr;
+           *mbuf_ = nullptr, *wu_ = nullptr, *wg_ = nullptr, *ubl_ = nullptr, *gbl_ = nullptr, *red_ = nullptr;
     void* sc_ = nullptr;
     void* state_ = nullptr;
     TraceRow* trace_ = nullptr;
     int trace_cap_ = 0;
     int host_max_ = 0;
-    int n_prelude_ = 0, n_body_ = 0, n_ls_ = 0, n_acc_ = 0;
+    int n_prelude_ = 0, n_body_ = 0, n_ls_ = 0, n_acc_ = 0, n_init_ = 0;
+    long long init_launches_ = 0, launches_done_ = 0;
+    long long pending_loop_launches();
     long long loop_launches_ = 0;
     cudaGraph_t g_init_ = nullptr, g_loop_ = nullptr;
     cudaGraphExec_t x_init_ = nullptr, x_loop_ = nullptr;

@@ -163,7 +163,6 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
         switch (w.RP) {
             case 8: sp_mttkrp_kernel<8><<<blocks, 256, 0, st>>>(p); break;
             case 16: sp_mttkrp_kernel<16><<<blocks, 256, 0, st>>>(p); break;
-            case 24: sp_mttkrp_kernel<24><<<blocks, 256, 0, st>>>(p); break;
             default: sp_mttkrp_kernel<32><<<blocks, 256, 0, st>>>(p); break;
         }
         CPFIT_CUDA(cudaGetLastError());
