@@ -288,7 +288,7 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
     } else {
         // mode 0: tail contraction with the old modes >= 1
         dense_fiber(t, w, work, false, true, st);
-        gather_m(t.dims[0], w, w.m0_part, w.fiber_grid, 32 * w.fiber_nchunk, 0, mbuf, st);
+        gather_m(t.dims[0], w, w.m0, 1, 32 * w.fiber_nchunk, 0, mbuf, st);
         solve_mode(w, 0, mbuf, work + w.off[0], status, st);
         gram_mode_device(w, work, 0, st);
         // S' = T x_1 A0'
@@ -297,7 +297,7 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
         for (int n = 1; n < N; ++n) {
             if (n < N - 1) {
                 dense_level(t, w, n, Sin, work, true, false, nullptr, st);
-                gather_m(t.dims[n], w, w.lvl_part[n], w.lvl_grid[n], 0, 1, mbuf, st);
+                gather_m(t.dims[n], w, w.lvl_m[n], 1, 0, 1, mbuf, st);
             } else {
                 gather_m(t.dims[n], w, Sin, 1, 0, 1, mbuf, st);
             }

@@ -295,6 +295,12 @@ size_t fiber_smem(int RP, int nchunk) {
 
 #endif
 
+// M0 = sum over the fiber-pass CTAs of their [RP][32 NC] partials (fixed order)
+void reduce_parts(const double* part, int nparts, int64_t nout, double* out, cudaStream_t st);
+void reduce_m0(EvalWork& w, cudaStream_t st) {
+    reduce_parts(w.m0_part, w.fiber_grid, (int64_t)w.RP * 32 * w.fiber_nchunk, w.m0, st);
+}
+
 void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, bool do_f,
                const double* gamma0, cudaStream_t st, const int* resid_flag = nullptr) {
     FiberParams p{};
@@ -430,33 +436,125 @@ __global__ void __launch_bounds__(kLevelThreads) level_kernel(const LevelParams 
     }
 }
 
+// Fixed-order reduction of `nparts` contiguous partial vectors: out[o] = sum_c part[c*nout+o].
+// Block = 32 outputs x 8 part-slices (coalesced across lanes), slices combined in order.
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const double* __restrict__ part, int nparts, int64_t nout,
+                                                           double* __restrict__ out) {
+    __shared__ double sl[8][33];
+    const int lane = threadIdx.x & 31, ws = threadIdx.x >> 5;
+    const int64_t o = (int64_t)blockIdx.x * 32 + lane;
+    double v = 0.0;
+    if (o < nout)
+        for (int c = ws; c < nparts; c += 8) v += part[(int64_t)c * nout + o];
+    sl[ws][lane] = v;
+    __syncthreads();
+    if (ws == 0 && o < nout) {
+        double s = 0.0;
+        for (int k = 0; k < 8; ++k) s += sl[k][lane];
+        out[o] = s;
+    }
+}
+
+void reduce_parts(const double* part, int nparts, int64_t nout, double* out, cudaStream_t st) {
+    reduce_parts_kernel<<<(unsigned)((nout + 31) / 32), 256, 0, st>>>(part, nparts, nout, out);
+    CPFIT_CUDA(cudaGetLastError());
+}
+
+// M_h(jh, r) = sum_s Sin(jh, s, r) Wt(s, r) over a chunk of slabs per CTA: thread (jh, r),
+// coalesced over consecutive (jh, r) for each slab; chunk partials -> reduce_parts.
+struct LevelMParams {
+    const double* Sin;
+    int64_t Ih, Jt;
+    int R, RP;
+    int ntail;
+    int64_t tdims[kMaxOrder];
+    const double* tfac[kMaxOrder];
+    int64_t chunk;  // slabs per chunk
+    double* part;   // [chunk][Ih*RP]
+};
+
+__global__ void __launch_bounds__(256) level_m_kernel(const LevelMParams p) {
+    extern __shared__ double wt[];  // [chunk][RP]
+    const int64_t npairs = p.Ih * p.RP;
+    const int64_t s0 = (int64_t)blockIdx.y * p.chunk;
+    const int64_t s1 = imin64(p.Jt, s0 + p.chunk);
+    const int ns = (int)(s1 - s0);
+    for (int e = threadIdx.x; e < ns * p.RP; e += blockDim.x) {
+        const int sl = e / p.RP, r = e % p.RP;
+        double w = 0.0;
+        if (r < p.R) {
+            w = 1.0;
+            int64_t rem = s0 + sl;
+            for (int m = 0; m < p.ntail; ++m) {
+                const int64_t jm = rem % p.tdims[m];
+                rem /= p.tdims[m];
+                w *= p.tfac[m][(int64_t)r * p.tdims[m] + jm];
+            }
+        }
+        wt[e] = w;
+    }
+    __syncthreads();
+    const int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pr >= npairs) return;
+    const int r = (int)(pr % p.RP);
+    const double* src = p.Sin + s0 * npairs + pr;
+    double a0 = 0.0, a1 = 0.0;
+    int sl = 0;
+    for (; sl + 1 < ns; sl += 2) {
+        a0 += src[(int64_t)sl * npairs] * wt[sl * p.RP + r];
+        a1 += src[(int64_t)(sl + 1) * npairs] * wt[(sl + 1) * p.RP + r];
+    }
+    if (sl < ns) a0 += src[(int64_t)sl * npairs] * wt[sl * p.RP + r];
+    p.part[(int64_t)blockIdx.y * npairs + pr] = a0 + a1;
+}
+
 void run_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
                double* Sout, cudaStream_t st) {
+    const int64_t Ih = t.dims[h];
+    int64_t Jt = 1;
+    for (int m = h + 1; m < t.order; ++m) Jt *= t.dims[m];
+    const int64_t npairs = Ih * w.RP;
+    if (do_m) {
+        LevelMParams q{};
+        q.Sin = Sin;
+        q.Ih = Ih;
+        q.Jt = Jt;
+        q.R = w.R;
+        q.RP = w.RP;
+        q.ntail = t.order - h - 1;
+        for (int m = h + 1; m < t.order; ++m) {
+            q.tdims[m - h - 1] = t.dims[m];
+            q.tfac[m - h - 1] = u + w.off[m];
+        }
+        q.chunk = w.lvl_chunk[h];
+        q.part = w.lvl_part[h];
+        const int nchunk = (int)((Jt + q.chunk - 1) / q.chunk);
+        dim3 grid((unsigned)((npairs + 255) / 256), (unsigned)nchunk);
+        level_m_kernel<<<grid, 256, sizeof(double) * q.chunk * w.RP, st>>>(q);
+        CPFIT_CUDA(cudaGetLastError());
+        reduce_parts(w.lvl_part[h], nchunk, npairs, w.lvl_m[h], st);
+    }
+    if (!do_s) return;
     LevelParams p{};
     p.Sin = Sin;
-    p.Ih = t.dims[h];
-    p.Jt = 1;
-    for (int m = h + 1; m < t.order; ++m) p.Jt *= t.dims[m];
+    p.Ih = Ih;
+    p.Jt = Jt;
     p.R = w.R;
     p.RP = w.RP;
-    p.Ah = do_s ? u + w.off[h] : nullptr;
+    p.Ah = u + w.off[h];
     p.ntail = t.order - h - 1;
     for (int m = h + 1; m < t.order; ++m) {
         p.tdims[m - h - 1] = t.dims[m];
         p.tfac[m - h - 1] = u + w.off[m];
     }
-    p.mh_part = do_m ? w.lvl_part[h] : nullptr;
-    p.Sout = do_s ? Sout : nullptr;
+    p.mh_part = nullptr;
+    p.Sout = Sout;
     const int gmax = w.lvl_grid[h];
     p.slabs_per_cta = (p.Jt + gmax - 1) / gmax;
     const int grid = (int)((p.Jt + p.slabs_per_cta - 1) / p.slabs_per_cta);
-    const int B = (w.RP == 24) ? 192 : kLevelThreads;
-    const int64_t npairs = p.Ih * w.RP;
+    const int B = kLevelThreads;
     const int kmax = (int)((npairs + B - 1) / B);
     const size_t smem = sizeof(double) * ((size_t)2 * kmax * B + kSlabBatch * w.RP + (size_t)kSlabBatch * B);
-    if (do_m && grid < gmax)
-        CPFIT_CUDA(cudaMemsetAsync(w.lvl_part[h] + (size_t)grid * npairs, 0,
-                                   sizeof(double) * (size_t)(gmax - grid) * npairs, st));
     CPFIT_CUDA(cudaFuncSetAttribute(level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     level_kernel<<<grid, B, smem, st>>>(p);
     CPFIT_CUDA(cudaGetLastError());
@@ -562,15 +660,22 @@ struct GradParams {
     double* g;
     const double* d;
     const double* gram;  // [mode][RP*RP]
-    const double* m0_part;
-    int m0_grid, m0_ld;
-    const double* lvl_part[kMaxOrder];
-    int lvl_grid[kMaxOrder];
+    const double* m0;    // reduced M_0 [r][m0_ld]
+    int m0_ld;
+    const double* lvl_m[kMaxOrder];  // reduced M_h [i][r], 1 <= h <= N-2
     const double* mlast;   // [i][r] complete M_{N-1} (dense) or null
     const double* sp_out;  // sparse: per-mode complete M_n [mode offset][i][r] (null for dense)
     int64_t sp_off[kMaxOrder];
     double* red;           // gridDim x 3
     int need_grad;
+    // finalisation by the last block to finish (fixed-order sums of the block partials)
+    const double* f_part;
+    int f_grid;
+    int sparse;  // three-term objective (kruskal.cpp:146-148)
+    double norm_sq;
+    EvalScalars* sc;
+    int has_d;
+    unsigned int* counter;
 };
 
 __device__ double gamma_entry(const GradParams& p, int n, int q, int r) {
@@ -599,16 +704,15 @@ __global__ void grad_kernel(const GradParams p) {
         const int64_t In = p.dims[n];
         const int r = (int)(loc / In);
         const int64_t i = loc % In;
-        double m = 0.0;
-        if (p.sp_out) {
+        double m;
+        if (p.sp_out)
             m = p.sp_out[p.sp_off[n] + i * p.RP + r];
-        } else if (n == 0) {
-            for (int c = 0; c < p.m0_grid; ++c) m += p.m0_part[((size_t)c * p.RP + r) * p.m0_ld + i];
-        } else if (n == p.order - 1) {
+        else if (n == 0)
+            m = p.m0[(size_t)r * p.m0_ld + i];
+        else if (n == p.order - 1)
             m = p.mlast[i * p.RP + r];
-        } else {
-            for (int c = 0; c < p.lvl_grid[n]; ++c) m += p.lvl_part[n][((size_t)c * In + i) * p.RP + r];
-        }
+        else
+            m = p.lvl_m[n][i * p.RP + r];
         if (n == 0) inner += m * p.u[e];
         if (p.need_grad) {
             const double* a = p.u + p.off[n];
@@ -630,6 +734,7 @@ __global__ void grad_kernel(const GradParams p) {
         red[2][warp] = inner;
     }
     __syncthreads();
+    __shared__ bool last;
     if (tid == 0) {
         double a = 0, b = 0, c = 0;
         for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) {
@@ -640,50 +745,42 @@ __global__ void grad_kernel(const GradParams p) {
         p.red[blockIdx.x * 3 + 0] = a;
         p.red[blockIdx.x * 3 + 1] = b;
         p.red[blockIdx.x * 3 + 2] = c;
+        __threadfence();
+        last = (atomicAdd(p.counter, 1u) == gridDim.x - 1);
     }
-}
-
-struct FinalParams {
-    const double* red;
-    int red_grid;
-    const double* f_part;
-    int f_grid;
-    int sparse;  // three-term objective
-    double norm_sq;
-    const double* gram;
-    int order, R, RP;
-    EvalScalars* sc;
-    int has_d;
-};
-
-__global__ void final_kernel(const FinalParams p) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double g2 = 0, gd = 0, inner = 0;
-    for (int c = 0; c < p.red_grid; ++c) {
-        g2 += p.red[c * 3 + 0];
-        gd += p.red[c * 3 + 1];
-        inner += p.red[c * 3 + 2];
+    __syncthreads();
+    if (!last || warp != 0) return;
+    // last block, one warp: lane-strided partial sums then a fixed shuffle tree (deterministic)
+    __threadfence();
+    double a = 0.0, b = 0.0, c = 0.0, fs = 0.0;
+    for (int k = lane; k < (int)gridDim.x; k += 32) {
+        a += p.red[k * 3 + 0];
+        b += p.red[k * 3 + 1];
+        c += p.red[k * 3 + 2];
     }
-    double f;
+    for (int k = lane; k < p.f_grid; k += 32) fs += p.f_part[k];
+    a = warp_sum(a);
+    b = warp_sum(b);
+    c = warp_sum(c);
+    fs = warp_sum(fs);
+    double gs = 0.0;
     if (p.sparse) {
-        // kruskal.cpp:146-148: 1/2||T||^2 - <M0, A0> + 1/2 1^T Gamma 1
-        double gs = 0.0;
-        for (int q = 0; q < p.R; ++q)
-            for (int r = 0; r < p.R; ++r) {
-                double v = 1.0;
-                for (int m = 0; m < p.order; ++m) v *= p.gram[(size_t)m * p.RP * p.RP + q * p.RP + r];
-                gs += v;
-            }
-        f = 0.5 * p.norm_sq - inner + 0.5 * gs;
-    } else {
-        double s = 0.0;
-        for (int c = 0; c < p.f_grid; ++c) s += p.f_part[c];
-        f = 0.5 * s;
+        // kruskal.cpp:146-148: 1/2||T||^2 - <M0, A0> + 1/2 1^T Gamma 1, Gamma = gram_hadamard(-1)
+        for (int e = lane; e < p.R * p.R; e += 32) {
+            const int q = e / p.R, r = e % p.R;
+            double v = 1.0;
+            for (int m = 0; m < p.order; ++m) v *= p.gram[(size_t)m * p.RP * p.RP + q * p.RP + r];
+            gs += v;
+        }
+        gs = warp_sum(gs);
     }
-    p.sc->f = f;
-    p.sc->gnorm2 = g2;
-    p.sc->inner = inner;
-    if (p.has_d) p.sc->gdotd = gd;
+    if (lane == 0) {
+        p.sc->f = p.sparse ? 0.5 * p.norm_sq - c + 0.5 * gs : 0.5 * fs;
+        p.sc->gnorm2 = a;
+        p.sc->inner = c;
+        if (p.has_d) p.sc->gdotd = b;
+        *p.counter = 0u;  // ready for the next evaluation (stream order)
+    }
 }
 
 }  // namespace
@@ -716,6 +813,8 @@ EvalWork* work_create(const DevTensor& t, int R) {
     CPFIT_CUDA(cudaMalloc(&w->gram, sizeof(double) * (size_t)t.order * w->RP * w->RP));
     w->red_grid = sms * 2;
     CPFIT_CUDA(cudaMalloc(&w->red, sizeof(double) * 3 * (size_t)w->red_grid));
+    CPFIT_CUDA(cudaMalloc(&w->counter, sizeof(unsigned int)));
+    CPFIT_CUDA(cudaMemset(w->counter, 0, sizeof(unsigned int)));
     if (!t.sparse) {
         if (t.order < 2) throw std::invalid_argument("device dense path needs order >= 2");
         const int I0 = (int)t.dims[0];
@@ -729,12 +828,19 @@ EvalWork* work_create(const DevTensor& t, int R) {
         w->fiber_grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
         CPFIT_CUDA(cudaMalloc(&w->S, sizeof(double) * (size_t)t.J * w->RP));
         CPFIT_CUDA(cudaMalloc(&w->m0_part, sizeof(double) * (size_t)w->fiber_grid * w->RP * 32 * w->fiber_nchunk));
+        CPFIT_CUDA(cudaMalloc(&w->m0, sizeof(double) * (size_t)w->RP * 32 * w->fiber_nchunk));
         CPFIT_CUDA(cudaMalloc(&w->f_part, sizeof(double) * (size_t)w->fiber_grid));
         for (int h = 1; h < t.order - 1; ++h) {
             int64_t Jt = 1;
             for (int m = h + 1; m < t.order; ++m) Jt *= t.dims[m];
             w->lvl_grid[h] = (int)std::min<int64_t>(Jt, (int64_t)sms);
-            CPFIT_CUDA(cudaMalloc(&w->lvl_part[h], sizeof(double) * (size_t)w->lvl_grid[h] * t.dims[h] * w->RP));
+            const int64_t npairs = t.dims[h] * w->RP;
+            const int64_t bx = (npairs + 255) / 256;
+            const int64_t want = std::max<int64_t>(1, (2 * sms + bx - 1) / bx);
+            w->lvl_chunk[h] = std::max<int64_t>(1, std::min<int64_t>((Jt + want - 1) / want, 6144 / w->RP));
+            const int64_t nch = (Jt + w->lvl_chunk[h] - 1) / w->lvl_chunk[h];
+            CPFIT_CUDA(cudaMalloc(&w->lvl_part[h], sizeof(double) * (size_t)nch * npairs));
+            CPFIT_CUDA(cudaMalloc(&w->lvl_m[h], sizeof(double) * (size_t)npairs));
             CPFIT_CUDA(cudaMalloc(&w->lvl_S[h], sizeof(double) * (size_t)Jt * w->RP));
         }
     } else {
@@ -754,11 +860,14 @@ void work_destroy(EvalWork* w) {
     cudaFree(w->red);
     cudaFree(w->S);
     cudaFree(w->m0_part);
+    cudaFree(w->m0);
     cudaFree(w->f_part);
     cudaFree(w->sp_part);
     cudaFree(w->frows);
+    cudaFree(w->counter);
     for (int h = 0; h < kMaxOrder; ++h) {
         cudaFree(w->lvl_part[h]);
+        cudaFree(w->lvl_m[h]);
         cudaFree(w->lvl_S[h]);
     }
     delete w;
@@ -789,7 +898,7 @@ void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st) {
 
 namespace {
 void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const double* d, bool need_grad,
-              cudaStream_t st) {
+              EvalScalars* sc, cudaStream_t st) {
     GradParams p{};
     p.order = t.order;
     p.R = w.R;
@@ -797,8 +906,7 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
     for (int n = 0; n < t.order; ++n) {
         p.dims[n] = t.dims[n];
         p.off[n] = w.off[n];
-        p.lvl_part[n] = w.lvl_part[n];
-        p.lvl_grid[n] = w.lvl_grid[n];
+        p.lvl_m[n] = w.lvl_m[n];
     }
     p.off[t.order] = w.off[t.order];
     p.u = u;
@@ -814,13 +922,21 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
             acc += t.dims[n] * w.RP;
         }
     } else {
-        p.m0_part = w.m0_part;
-        p.m0_grid = w.fiber_grid;
+        p.m0 = w.m0;
         p.m0_ld = 32 * w.fiber_nchunk;
         p.mlast = (t.order == 2) ? w.S : w.lvl_S[t.order - 2];
     }
     p.red = w.red;
-    grad_kernel<<<w.red_grid, 256, sizeof(double) * t.order * w.R * w.R, st>>>(p);
+    p.f_part = w.f_part;
+    p.f_grid = t.sparse ? 0 : w.fiber_grid;
+    p.sparse = t.sparse ? 1 : 0;
+    p.norm_sq = t.norm_sq;
+    p.sc = sc;
+    p.has_d = d ? 1 : 0;
+    p.counter = w.counter;
+    // enough blocks to cover n_u once (latency-bound epilogue, no grid-stride tail)
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(w.red_grid, (w.nu + 255) / 256));
+    grad_kernel<<<blocks, 256, sizeof(double) * t.order * w.R * w.R, st>>>(p);
     CPFIT_CUDA(cudaGetLastError());
 }
 }  // namespace
@@ -832,6 +948,7 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
     if (!t.sparse) {
         // fused pass: S, M0 partials and per-fiber objective
         run_fiber(t, w, u, true, true, true, w.gram /* mode-0 Gram */, st, resid_flag);
+        reduce_m0(w, st);
         // modes 1..N-1 from S
         const double* Sin = w.S;
         for (int h = 1; h < t.order - 1; ++h) {
@@ -841,22 +958,7 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
     } else {
         sparse_all_modes(t, w, u, -1, st);
     }
-    run_grad(t, w, u, g, d, need_grad, st);
-    FinalParams fp{};
-    fp.red = w.red;
-    fp.red_grid = w.red_grid;
-    fp.f_part = w.f_part;
-    fp.f_grid = t.sparse ? 0 : w.fiber_grid;
-    fp.sparse = t.sparse ? 1 : 0;
-    fp.norm_sq = t.norm_sq;
-    fp.gram = w.gram;
-    fp.order = t.order;
-    fp.R = w.R;
-    fp.RP = w.RP;
-    fp.sc = sc;
-    fp.has_d = d ? 1 : 0;
-    final_kernel<<<1, 32, 0, st>>>(fp);
-    CPFIT_CUDA(cudaGetLastError());
+    run_grad(t, w, u, g, d, need_grad, sc, st);
 }
 
 namespace {
@@ -890,7 +992,8 @@ void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, d
     }
     if (mode == 0) {
         run_fiber(t, w, u, false, true, false, nullptr, st);
-        gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, w.m0_part, w.fiber_grid, 32 * w.fiber_nchunk, 0, out);
+        reduce_m0(w, st);
+        gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, w.m0, 1, 32 * w.fiber_nchunk, 0, out);
     } else {
         run_fiber(t, w, u, true, false, false, nullptr, st);
         const double* Sin = w.S;
@@ -902,7 +1005,7 @@ void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, d
         if (mode == t.order - 1)
             gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, Sin, 1, 0, 1, out);
         else
-            gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, w.lvl_part[mode], w.lvl_grid[mode], 0, 1, out);
+            gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, w.lvl_m[mode], 1, 0, 1, out);
     }
     CPFIT_CUDA(cudaGetLastError());
 }
@@ -910,6 +1013,7 @@ void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, d
 // exported for als.cu
 void dense_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, cudaStream_t st) {
     run_fiber(t, w, u, do_s, do_m0, false, nullptr, st);
+    if (do_m0) reduce_m0(w, st);  // -> w.m0
 }
 // the fused evaluation pass alone (S + M0 + per-fiber objective); Grams of u must be current
 void dense_fiber_fused(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st, const int* resid_flag) {

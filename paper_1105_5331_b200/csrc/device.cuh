@@ -52,10 +52,14 @@ struct EvalWork {
     double* S = nullptr;        // J x RP
     double* m0_part = nullptr;  // fiber_grid x RP x (32*nchunk)
     double* f_part = nullptr;   // fiber_grid (+ sparse/other scalars)
+    double* m0 = nullptr;       // reduced M0 [RP][32*nchunk]
     // level contractions (modes 1..N-2 heads)
     int lvl_grid[kMaxOrder] = {};
-    double* lvl_part[kMaxOrder] = {};  // partial M_h per CTA (grid x I_h x RP)
+    int64_t lvl_chunk[kMaxOrder] = {};  // slabs per M_h chunk
+    double* lvl_part[kMaxOrder] = {};  // M_h chunk partials (chunks x I_h x RP)
+    double* lvl_m[kMaxOrder] = {};     // reduced M_h [i][r]
     double* lvl_S[kMaxOrder] = {};     // S_{h} outputs (slabs x RP)
+    unsigned int* counter = nullptr;   // last-block-done counter of the gradient epilogue
     // Grams
     int gram_chunks[kMaxOrder] = {};
     dd* gram_part = nullptr;    // [mode][chunk][R*R]
