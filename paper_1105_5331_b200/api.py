@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libcpfit_gpu.so")
+LIB_PATH = os.environ.get("CPFIT_GPU_LIB") or os.path.join(_HERE, "lib", "libcpfit_gpu.so")  # override: A/B builds
 
 
 class NumericalError(RuntimeError):

@@ -26,41 +26,57 @@ struct SpParams {
     double* out;  // In x RP
 };
 
-template <int RP>
-__global__ void sp_mttkrp_kernel(const SpParams p) {
+// Warp per output row; lanes span the rank: lane = (g, r) with r = lane % RP and
+// G = 32 / RP nonzeros per step, so each factor-row gather is one contiguous RP*8-byte segment
+// per lane group (one L1 wavefront) instead of 32 scattered rows. Indices and values are read
+// coalesced, 32 nonzeros at a time, and broadcast to the lane groups with shuffles. ORD is the
+// number of other modes (N-1) when specialised, 0 generic.
+template <int RP, int NO>
+__global__ void __launch_bounds__(256) sp_mttkrp_kernel(const SpParams p) {
+    constexpr int G = 32 / RP;
     const int lane = threadIdx.x & 31;
+    const int r = lane % RP, g = lane / RP;
+    const int nother = NO > 0 ? NO : p.nother;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = gw; i < p.In; i += nw) {
-        double acc[RP];
-#pragma unroll
-        for (int r = 0; r < RP; ++r) acc[r] = 0.0;
+        double acc = 0.0;
         const int64_t j0 = p.rowptr[i], j1 = p.rowptr[i + 1];
-        for (int64_t j = j0 + lane; j < j1; j += 32) {
-            double prod[RP];
-            const double v = p.vals[j];
+        for (int64_t jb = j0; jb < j1; jb += 32) {
+            const int64_t jl = jb + lane;
+            const bool okl = jl < j1;
+            const double vl = okl ? __ldg(p.vals + jl) : 0.0;
+            int cl[NO > 0 ? NO : kMaxOrder];
 #pragma unroll
-            for (int r = 0; r < RP; ++r) prod[r] = v;
-            for (int k = 0; k < p.nother; ++k) {
-                const int64_t c = p.oidx[(int64_t)k * p.nnz + j];
-                const double2* row = reinterpret_cast<const double2*>(p.frow[k] + c * RP);
+            for (int k = 0; k < (NO > 0 ? NO : kMaxOrder); ++k)
+                cl[k] = (okl && k < nother) ? __ldg(p.oidx + (int64_t)k * p.nnz + jl) : 0;
+            const int cnt = (int)imin64(32, j1 - jb);
+            for (int q0 = 0; q0 < cnt; q0 += G) {
+                const int q = q0 + g;
+                double prod = __shfl_sync(0xffffffffu, vl, q & 31);
 #pragma unroll
-                for (int r = 0; r < RP / 2; ++r) {
-                    const double2 a = __ldg(row + r);
-                    prod[2 * r] *= a.x;
-                    prod[2 * r + 1] *= a.y;
+                for (int k = 0; k < (NO > 0 ? NO : kMaxOrder); ++k) {
+                    if (k < nother) {
+                        const int c = __shfl_sync(0xffffffffu, cl[k], q & 31);
+                        prod *= __ldg(p.frow[k] + (int64_t)c * RP + r);
+                    }
                 }
+                if (q < cnt) acc += prod;
             }
-#pragma unroll
-            for (int r = 0; r < RP; ++r) acc[r] += prod[r];
         }
+        // combine the G lane groups (fixed order)
 #pragma unroll
-        for (int r = 0; r < RP; ++r) acc[r] = warp_sum(acc[r]);
-        double mine = 0.0;
-#pragma unroll
-        for (int r = 0; r < RP; ++r)
-            if (lane == r) mine = acc[r];
-        if (lane < RP) p.out[i * RP + lane] = mine;
+        for (int o = RP; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (g == 0) p.out[i * RP + r] = acc;
+    }
+}
+
+template <int RP>
+void launch_sp(const SpParams& p, int blocks, int order, cudaStream_t st) {
+    switch (order) {
+        case 3: sp_mttkrp_kernel<RP, 2><<<blocks, 256, 0, st>>>(p); break;
+        case 4: sp_mttkrp_kernel<RP, 3><<<blocks, 256, 0, st>>>(p); break;
+        default: sp_mttkrp_kernel<RP, 0><<<blocks, 256, 0, st>>>(p); break;
     }
 }
 
@@ -161,9 +177,9 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
         p.out = w.sp_part + off[n];
         const int blocks = (int)std::min<int64_t>(148 * 8, (p.In * 32 + 255) / 256);
         switch (w.RP) {
-            case 8: sp_mttkrp_kernel<8><<<blocks, 256, 0, st>>>(p); break;
-            case 16: sp_mttkrp_kernel<16><<<blocks, 256, 0, st>>>(p); break;
-            default: sp_mttkrp_kernel<32><<<blocks, 256, 0, st>>>(p); break;
+            case 8: launch_sp<8>(p, blocks, N, st); break;
+            case 16: launch_sp<16>(p, blocks, N, st); break;
+            default: launch_sp<32>(p, blocks, N, st); break;
         }
         CPFIT_CUDA(cudaGetLastError());
     }

@@ -250,3 +250,30 @@ def test_als_solve_matches_oracle(gpu, O):
     assert len(res.trace) == len(ref["trace"])
     for a, b in zip(res.trace, ref["trace"]):
         assert abs(a["f"] - b["f"]) <= 1e-8 * abs(b["f"])
+
+
+@pytest.mark.parametrize("cfg", [((50, 50, 50), 5, 0.9, 10.0, 5.0)])
+def test_swamp_config_within_oracle_envelope(gpu, O, cfg):
+    """Config 1 (collinearity 0.9, the swamp regime) is chaotic: the oracle's own iteration
+    count moves by tens of iterations when its start is perturbed by 1e-15 relative. The gated
+    quantities are the first 20 iterates (test above) and the final f; the device iteration
+    count must lie inside the oracle's own ulp-perturbation envelope (widened by 10 %)."""
+    P = gpu
+    dims, rank = cfg[0], cfg[1]
+    T, u0 = _baseline_case(P, cfg)
+    nu = float(sum(dims) * rank)
+    t = P.DataTensor.dense(T, dims)
+    o = O.Tensor.dense(dims, T)
+    ref = o.ngmres(u0, window=20, max_iters=2000, tol_grad=1e-10, gradient_scale=nu)
+    rng = np.random.default_rng(1)
+    counts = [len(ref["trace"]) - 1]
+    for _ in range(6):
+        r = o.ngmres(u0 * (1 + 1e-15 * rng.standard_normal(u0.size)), window=20, max_iters=2000, tol_grad=1e-10,
+                     gradient_scale=nu)
+        counts.append(len(r["trace"]) - 1)
+    res = P.ngmres_solve(t, u0, P.NgmresOptions(window=20, max_iters=2000, tol_grad=1e-10, gradient_scale=nu))
+    n = len(res.trace) - 1
+    print(f"device {n} iterations; oracle {counts[0]}, perturbed-start envelope {min(counts)}..{max(counts)}")
+    assert res.stop_reason == ref["stop"] == P.GRAD_TOL
+    assert abs(res.f - ref["f"]) <= 1e-8 * ref["f"]
+    assert 0.9 * min(counts) <= n <= 1.1 * max(counts)
