@@ -126,6 +126,11 @@ struct NormParams {
     const double* g;
     double* gout;
     double* red;
+    // optional: M0 = T x KR(modes >= 1) at u ([RP][ld]), mapped to the normalised point:
+    // M0'(:, r) = M0(:, perm r) / s_0(r)  (prod_n s_n = 1 for every nonzero term)
+    const double* m0;
+    double* m0out;
+    int m0_ld;
 };
 
 // normalize_and_reorder: norms from the (double-double) Gram diagonals, lambda_r =
@@ -181,6 +186,20 @@ __global__ void normalize_kernel(const NormParams p) {
             g2 += gv * gv;
         }
     }
+    if (p.m0) {
+        const int64_t tm = (int64_t)p.RP * p.m0_ld;
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + tid; e < tm; e += (int64_t)gridDim.x * blockDim.x) {
+            const int r = (int)(e / p.m0_ld);
+            const int64_t i = e % p.m0_ld;
+            double v = 0.0;
+            if (r < p.R) {
+                const int src = perm[r];
+                v = p.m0[(int64_t)src * p.m0_ld + i];
+                if (lam[src] != 0.0) v /= scale[0][r];
+            }
+            p.m0out[e] = v;
+        }
+    }
     if (p.g) {
         __shared__ double red[32];
         g2 = warp_sum(g2);
@@ -230,7 +249,7 @@ void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st
 }
 
 int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
-                          cudaStream_t st) {
+                          cudaStream_t st, const double* m0, double* m0out) {
     NormParams p{};
     p.order = w.order;
     p.R = w.R;
@@ -246,6 +265,9 @@ int normalize_grad_device(EvalWork& w, const double* u, const double* g, double*
     p.g = g;
     p.gout = gout;
     p.red = red;
+    p.m0 = m0;
+    p.m0out = m0out;
+    p.m0_ld = 32 * w.fiber_nchunk;
     const int blocks = (int)std::min<int64_t>(296, (w.nu + 255) / 256);
     normalize_kernel<<<blocks, 256, 0, st>>>(p);
     CPFIT_CUDA(cudaGetLastError());
@@ -272,7 +294,7 @@ void solve_mode(EvalWork& w, int n, const double* M, double* ublock, int* status
 
 // work: n_u scratch (pre-normalisation iterate), mbuf: max(I_n)*R scratch
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
-                         int* status, cudaStream_t st) {
+                         int* status, cudaStream_t st, const double* m0_given) {
     CPFIT_CUDA(cudaMemcpyAsync(work, u, sizeof(double) * w.nu, cudaMemcpyDeviceToDevice, st));
     grams_device(w, work, st);
     const int N = t.order;
@@ -286,9 +308,10 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
             gram_mode_device(w, work, n, st);
         }
     } else {
-        // mode 0: tail contraction with the old modes >= 1
-        dense_fiber(t, w, work, false, true, st);
-        gather_m(t.dims[0], w, w.m0, 1, 32 * w.fiber_nchunk, 0, mbuf, st);
+        // mode 0: tail contraction with the old modes >= 1 — or, inside the N-GMRES loop, the
+        // M0 the evaluation of this iterate already produced (m0_given, [RP][32 NC])
+        if (!m0_given) dense_fiber(t, w, work, false, true, st);
+        gather_m(t.dims[0], w, m0_given ? m0_given : w.m0, 1, 32 * w.fiber_nchunk, 0, mbuf, st);
         solve_mode(w, 0, mbuf, work + w.off[0], status, st);
         gram_mode_device(w, work, 0, st);
         // S' = T x_1 A0'

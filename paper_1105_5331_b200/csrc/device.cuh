@@ -101,11 +101,11 @@ void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st
 // normalize u -> uout and map the gradient g at u to the normalised point (G_n D_n^-1,
 // permuted) -> gout; writes per-block partial ||gout||^2 to red, returns the block count.
 int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
-                          cudaStream_t st);
+                          cudaStream_t st, const double* m0 = nullptr, double* m0out = nullptr);
 // One ALS sweep (als.cpp:38-48): u -> out (normalized); work: n_u scratch, mbuf: max I_n x R
 // scratch. status: bit0 singular normal matrix after the ridge retry, bit1 non-finite solve.
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
-                         int* status, cudaStream_t st);
+                         int* status, cudaStream_t st, const double* m0_given = nullptr);
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
 
 // Accelerate (ngmres.cpp:27-63) on device.

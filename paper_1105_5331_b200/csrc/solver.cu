@@ -20,9 +20,6 @@
 
 namespace cpfit_gpu {
 
-void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
-                         int* status, cudaStream_t st);
-
 namespace {
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -185,19 +182,24 @@ __global__ void k_after_next(Ctl c) {
 
 // keep (u, g) of the best trial so far (returned by More–Thuente under MaxEvals / Stall)
 __global__ void k_keep_best(const DevState* s, const double* ut, const double* gt, double* ubl, double* gbl,
-                            int64_t n) {
+                            int64_t n, const double* m0, double* m0bl, int64_t nm) {
     if (!s->mt.last_improved) return;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = i0; i < n; i += step) {
         ubl[i] = ut[i];
         gbl[i] = gt[i];
     }
+    for (int64_t i = i0; i < nm; i += step) m0bl[i] = m0[i];
 }
 
 // accepted step = the last trial when Converged, else the best trial: bring it into (ut, gt)
 __global__ void k_select_accepted(const DevState* s, const double* ubl, const double* gbl, double* ut, double* gt,
-                                  int64_t n) {
-    if (s->mt.status == LS_CONVERGED) return;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+                                  int64_t n, const double* m0, const double* m0bl, double* m0sel, int64_t nm) {
+    const bool last = (s->mt.status == LS_CONVERGED);
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = i0; i < nm; i += step) m0sel[i] = last ? m0[i] : m0bl[i];
+    if (last) return;
+    for (int64_t i = i0; i < n; i += step) {
         ut[i] = ubl[i];
         gt[i] = gbl[i];
     }
@@ -275,8 +277,11 @@ __global__ void k_commit(Ctl c, cudaGraphConditionalHandle loop_h) {
 // Vector part of the commit: u, g <- chosen pair; window slot; best iterate.
 __global__ void k_commit_vec(const DevState* s, int als_mode, const double* ub, const double* gb, const double* un,
                              const double* gn, double* u, double* g, double* wu, double* wg, double* ubest,
-                             int64_t n) {
+                             int64_t n, const double* m0bar, double* m0cur, int64_t nm) {
     const bool acc = als_mode || s->accepted;
+    if (!acc)  // u <- u_bar: its M0 was kept after eval(u_bar)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nm; i += (int64_t)gridDim.x * blockDim.x)
+            m0cur[i] = m0bar[i];
     const double* su = acc ? un : ub;
     const double* sg = acc ? gn : gb;
     double* wu_s = als_mode ? nullptr : wu + (int64_t)s->slot * n;
@@ -384,6 +389,13 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     if (method_ == 0) {
         alloc(&wu_, n_ * cap_);
         alloc(&wg_, n_ * cap_);
+        if (!t->sparse) {
+            m0_n_ = (int64_t)w_->RP * 32 * w_->fiber_nchunk;
+            alloc(&m0_cur_, m0_n_);
+            alloc(&m0_bar_, m0_n_);
+            alloc(&m0_best_, m0_n_);
+            alloc(&m0_sel_, m0_n_);
+        }
     }
     CPFIT_CUDA(cudaMalloc(&sc_, sizeof(EvalScalars) * 4));
     CPFIT_CUDA(cudaMemset(sc_, 0, sizeof(EvalScalars) * 4));
@@ -399,7 +411,8 @@ Solver::~Solver() {
     if (x_loop_) cudaGraphExecDestroy(x_loop_);
     if (g_init_) cudaGraphDestroy(g_init_);
     if (g_loop_) cudaGraphDestroy(g_loop_);
-    for (double* p : {u_, g_, ub_, gb_, d_, ut_, gt_, un_, gn_, u0_, ubest_, work_, mbuf_, wu_, wg_, ubl_, gbl_, red_})
+    for (double* p : {u_, g_, ub_, gb_, d_, ut_, gt_, un_, gn_, u0_, ubest_, work_, mbuf_, wu_, wg_, ubl_, gbl_, red_,
+                      m0_cur_, m0_bar_, m0_best_, m0_sel_})
         cudaFree(p);
     cudaFree(sc_);
     cudaFree(state_);
@@ -443,6 +456,7 @@ void Solver::build_graphs() {
     grams_device(*w_, u0_, st_);
     normalize_device(*w_, u0_, u_, st_);
     eval_device(*t_, *w_, u_, g_, sc_cur, nullptr, status, st_, true, &s->resid);
+    if (m0_cur_) CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
     k_after_init<<<1, 1, 0, st_>>>(c);
     if (method_ == 0)
         k_seed_window<<<vb, 256, 0, st_>>>(u_, g_, wu_, wg_, ubest_, n_);
@@ -462,8 +476,10 @@ void Solver::build_graphs() {
     cudaGraph_t lsb = nullptr, ab = nullptr;
     if (method_ == 0) {
         // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
-        als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_);
+        als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_, m0_cur_);
         eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_, true, &s->resid);
+        if (m0_bar_)
+            CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st2_));
         k_after_bar<<<1, 1, 0, st2_>>>(c);
         // Step II: windowed recombination -> d, slope                        (ngmres.cpp:97-101)
         accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st2_);
@@ -475,7 +491,7 @@ void Solver::build_graphs() {
         k_trial<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
         eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st3_, true, &s->resid);
         k_ls_update<<<1, 1, 0, st3_>>>(c, ls_h);
-        if (!opt_.reeval_accepted) k_keep_best<<<vb, 256, 0, st3_>>>(s, ut_, gt_, ubl_, gbl_, n_);
+        if (!opt_.reeval_accepted) k_keep_best<<<vb, 256, 0, st3_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
         CPFIT_CUDA(cudaGetLastError());
         CPFIT_CUDA(cudaStreamEndCapture(st3_, &lsb));
         // accepted step: canonicalize u_bar + beta d and re-evaluate        (ngmres.cpp:137-142)
@@ -489,24 +505,28 @@ void Solver::build_graphs() {
             grams_device(*w_, ut_, st3_);
             normalize_device(*w_, ut_, un_, st3_);
             eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st3_, true, &s->resid);
+            if (m0_cur_)
+                CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st3_));
             k_after_next<<<1, 1, 0, st3_>>>(c);
         } else {
             // exact rescale: normalize_and_reorder scales columns by D_n with
             // prod_n D_n = I, so f is unchanged and G_n -> G_n D_n^-1 (permuted)
-            k_select_accepted<<<vb, 256, 0, st3_>>>(s, ubl_, gbl_, ut_, gt_, n_);
+            k_select_accepted<<<vb, 256, 0, st3_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
             grams_device(*w_, ut_, st3_);
-            const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st3_);
+            const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st3_, m0_sel_, m0_cur_);
             k_after_rescale<<<1, 1, 0, st3_>>>(c, sc_next, red_, nb);
         }
         CPFIT_CUDA(cudaGetLastError());
         CPFIT_CUDA(cudaStreamEndCapture(st3_, &ab));
     } else {
         // stand-alone ALS iteration (als.cpp:79-95)
-        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_);
+        // the previous evaluation (of u) left M0(u) in w.m0 for dense tensors
+        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, t_->sparse ? nullptr : w_->m0);
         eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid);
     }
     k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
-    k_commit_vec<<<vb, 256, 0, st2_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_);
+    k_commit_vec<<<vb, 256, 0, st2_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,
+                                        m0_cur_, m0_n_);
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaStreamEndCapture(st2_, &body));
     CPFIT_CUDA(cudaStreamEndCapture(st_, &g_loop_));

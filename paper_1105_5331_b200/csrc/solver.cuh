@@ -70,6 +70,10 @@ private:
     double *u_ = nullptr, *g_ = nullptr, *ub_ = nullptr, *gb_ = nullptr, *d_ = nullptr, *ut_ = nullptr,
            *gt_ = nullptr, *un_ = nullptr, *gn_ = nullptr, *u0_ = nullptr, *ubest_ = nullptr, *work_ = nullptr,
            *mbuf_ = nullptr, *wu_ = nullptr, *wg_ = nullptr, *ubl_ = nullptr, *gbl_ = nullptr, *red_ = nullptr;
+    // dense N-GMRES: M0 = T x KR(modes >= 1) at u (cur), u_bar (bar), the best trial (best) and
+    // the accepted trial (sel), so the ALS sweep reuses the evaluation's mode-0 contraction
+    double *m0_cur_ = nullptr, *m0_bar_ = nullptr, *m0_best_ = nullptr, *m0_sel_ = nullptr;
+    int64_t m0_n_ = 0;
     void* sc_ = nullptr;
     void* state_ = nullptr;
     TraceRow* trace_ = nullptr;
