@@ -336,7 +336,7 @@ def main():
             "e2e": {"value": round(e2e_value, 3), "unit": "iters/s", "h2d_bytes_per_step": h2d // max(e_it, 1),
                     "d2h_bytes_per_step": d2h // max(e_it, 1),
                     "note": f"cpfit_tensor_create_dense + {e_solves} cpfit_ngmres_solve calls from pinned host "
-                            "buffers (graph build per call), wall clock"},
+                            "buffers (graphs built on the first call, cached on the tensor handle), wall clock"},
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -135,6 +135,14 @@ int cpfit_solver_destroy(cpfit_solver s);
 /* kernels of this library launched by the solver's loop graphs since cpfit_solver_init
  * (counted from the captured graph bodies x the device-side iteration / line-search counters) */
 int cpfit_solver_launches(cpfit_solver s, int64_t* launches);
+/* Diagnostic: fiber-pass barrier-wait cycles by role (12 counters; nonzero only in a library
+ * built with -DCPFIT_FIBER_PROF, see tools/fiber_prof.py); reset != 0 clears them. */
+int cpfit_fiber_prof(uint64_t* out, int reset);
+/* Diagnostic: per-phase device time of the solver loop (8 phases: ALS sweep, eval(u_bar),
+ * accelerate + LS init, LS trial eval, LS update, accepted step, commit, loop re-entry), in us,
+ * and visit counts. Only when CPFIT_PHASE_PROFILE=1 was set before cpfit_solver_create (the
+ * stamps add one tiny kernel per phase); otherwise returns 1 (invalid_argument). */
+int cpfit_solver_phase_times(cpfit_solver s, double* us, int64_t* visits);
 
 /* Device-resident kernel timing (inputs already in HBM): average ms per call over `reps`
  * calls timed with CUDA events on the launching stream, L2 flushed between calls when

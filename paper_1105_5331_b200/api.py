@@ -106,6 +106,7 @@ _SIGS = {
     "cpfit_solver_best": (C.c_int, [C.c_void_p, _f64p]),
     "cpfit_solver_iterate": (C.c_int, [C.c_void_p, _f64p]),
     "cpfit_solver_launches": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "cpfit_solver_phase_times": (C.c_int, [C.c_void_p, _f64p, C.POINTER(C.c_int64)]),
     "cpfit_measure_fp64_peak": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "cpfit_host_register": (C.c_int, [C.c_void_p, C.c_int64]),
     "cpfit_host_unregister": (C.c_int, [C.c_void_p]),
@@ -493,6 +494,16 @@ class Solver:
         n = C.c_int64()
         _check(lib.cpfit_solver_launches(self._h, C.byref(n)))
         return n.value
+
+    PHASES = ("als_sweep", "eval_bar", "accel_ls_init", "ls_trial_eval", "ls_update", "accepted_step", "commit",
+              "loop_reentry")
+
+    def phase_times(self):
+        """{phase: (us, visits)} — needs CPFIT_PHASE_PROFILE=1 before the Solver is created."""
+        us = np.zeros(8)
+        cnt = (C.c_int64 * 8)()
+        _check(lib.cpfit_solver_phase_times(self._h, us, cnt))
+        return {k: (float(us[i]), int(cnt[i])) for i, k in enumerate(self.PHASES)}
 
     def close(self):
         if self._h:

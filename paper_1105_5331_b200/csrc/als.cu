@@ -7,14 +7,19 @@
 //   mode 1      : S' = T x_1 A0'  (stored) then the level contraction   (T pass 2)
 //   modes >= 2  : level contractions of S' with the freshly solved heads (no T pass)
 // so a sweep streams T twice instead of N times. The R x R normal matrix
-// Gamma_n = *_{m!=n} A_m^T A_m is factored by a warp-parallel left-looking Cholesky in the
-// column order of Eigen's unblocked LLT, with the reference's one ridge retry
-// (1e-12 * trace) before reporting numerical failure.
+// Gamma_n = *_{m!=n} A_m^T A_m is factored by a one-warp left-looking Cholesky in the column
+// order of Eigen's unblocked LLT, with the reference's one ridge retry (1e-12 * trace) before
+// reporting numerical failure; the factorisation of Gamma_n runs on a side stream while the
+// pass producing M_n streams (its Grams are final once mode n-1 is solved).
 #include "device.cuh"
+
+#include <cooperative_groups.h>
 
 #include <algorithm>
 
 namespace cpfit_gpu {
+
+namespace cg = cooperative_groups;
 
 void dense_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, cudaStream_t st);
 void dense_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
@@ -26,92 +31,165 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
 
 namespace {
 
-struct SolveParams {
+// Mode update (als.cpp:38-48 for one mode) in two kernels:
+//   chol_kernel       Gamma_n = *_{m != n} G_m and its Cholesky factor (one warp);
+//   solve_gram_kernel A_n <- M_n Gamma_n^-1 row by row, then the dd Gram of the new A_n.
+// The factorisation is a serial chain of R square roots, so it is launched on a side stream
+// as soon as the Grams it needs exist, overlapping the streaming pass that produces M_n.
+struct CholParams {
     int order, R, RP, mode;
-    int64_t In;
     const double* gram;  // [mode][RP*RP]
-    const double* M;     // col-major In x R
-    double* out;         // col-major In x R (block of the packed iterate)
+    double* fac;         // [R*R] L row-major, [R] 1 / l_kk, [1] ok flag (1.0 / 0.0)
     int* status;
 };
 
-// Left-looking LLT of g (R x R, row-major in smem) into l; returns false on pivot <= 0.
-__device__ bool warp_llt(const double* g, double* l, int R, double ridge) {
+// Left-looking LLT (Eigen's unblocked llt_inplace order: l_ik = (g_ik - sum_{j<k} l_ij l_kj)
+// / l_kk, j ascending; the pivot likewise, the ridge added to g_kk first), one warp: lane i
+// keeps row i of Gamma and of L in registers and receives row k by shuffles, so a column costs
+// one k-long DFMA chain plus one reciprocal square root. The division by l_kk = sqrt(x) is a
+// multiplication by rsqrt(x) (<= 1 ulp from the quotient). Returns false (uniformly) on a
+// pivot <= 0; a NaN pivot passes as in Eigen and surfaces as a non-finite solve.
+template <int RP>
+__device__ bool warp_llt(const double (&gr)[RP], double (&lr)[RP], double& dinv, int R, double ridge) {
     const int lane = threadIdx.x & 31;
     bool ok = true;
-    for (int k = 0; k < R; ++k) {
-        // pivot: x = a_kk - sum_j l_kj^2  (j ascending, as Eigen's A10.squaredNorm())
-        double x = g[k * R + k] + ridge;
-        for (int j = 0; j < k; ++j) x -= l[k * R + j] * l[k * R + j];
-        if (!(x > 0.0)) {
-            if (x <= 0.0) ok = false;  // NaN passes Eigen's (x <= 0) test
+#pragma unroll
+    for (int j = 0; j < RP; ++j) lr[j] = 0.0;
+#pragma unroll
+    for (int k = 0; k < RP; ++k) {
+        if (k < R) {
+            double s = gr[k] + (lane == k ? ridge : 0.0);
+#pragma unroll
+            for (int j = 0; j < k; ++j) s -= lr[j] * __shfl_sync(0xffffffffu, lr[j], k);
+            const double x = __shfl_sync(0xffffffffu, s, k);
+            if (x <= 0.0) ok = false;
+            const double inv = rsqrt(x);
+            if (lane == k) {
+                lr[k] = sqrt(x);
+                dinv = inv;
+            } else if (lane > k) {
+                lr[k] = s * inv;
+            }
         }
-        if (x <= 0.0) return false;
-        x = sqrt(x);
-        __syncwarp();
-        for (int i = k + 1 + lane; i < R; i += 32) {
-            double s = g[i * R + k];
-            for (int j = 0; j < k; ++j) s -= l[i * R + j] * l[k * R + j];
-            l[i * R + k] = s / x;
-        }
-        if (lane == 0) l[k * R + k] = x;
-        __syncwarp();
     }
     return ok;
 }
 
-__global__ void solve_kernel(const SolveParams p) {
-    __shared__ double g[kMaxRank * kMaxRank];
-    __shared__ double l[kMaxRank * kMaxRank];
-    __shared__ int ok_s;
+template <int RP>
+__global__ void __launch_bounds__(32) chol_kernel(const CholParams p) {
+    extern __shared__ double gs[];  // [order][RP*RP]
+    const int R = p.R, lane = threadIdx.x;
+    const bool row = lane < R;
+    // stage every Gram first (independent loads), then the Hadamard product from shared memory
+    for (int e = lane; e < p.order * RP * RP; e += 32) gs[e] = p.gram[e];
+    __syncwarp();
+    double gr[RP], lr[RP], dinv = 0.0;
+#pragma unroll
+    for (int j = 0; j < RP; ++j) {
+        double v = 0.0;
+        if (row && j < R) {
+            v = 1.0;
+            for (int m = 0; m < p.order; ++m)
+                if (m != p.mode) v *= gs[m * RP * RP + lane * RP + j];
+        }
+        gr[j] = v;
+    }
+    bool ok = warp_llt<RP>(gr, lr, dinv, R, 0.0);
+    if (!ok) {
+        // one ridge retry (1e-12 trace), as the reference's solve_spd
+        double tr = 0.0;
+#pragma unroll
+        for (int j = 0; j < RP; ++j) tr += __shfl_sync(0xffffffffu, gr[j], j);  // diagonal, j ascending
+        const double ridge = 1e-12 * tr;
+        ok = (ridge > 0.0) && warp_llt<RP>(gr, lr, dinv, R, ridge);
+    }
+    if (row) {
+#pragma unroll
+        for (int j = 0; j < RP; ++j)
+            if (j < R) p.fac[lane * R + j] = (j <= lane) ? lr[j] : 0.0;
+        p.fac[R * R + lane] = dinv;
+    }
+    if (lane == 0) {
+        p.fac[R * R + R] = ok ? 1.0 : 0.0;
+        if (!ok) atomicOr(p.status, 1);
+    }
+}
+
+struct SolveGramParams {
+    int R, RP, mode;
+    int64_t In;
+    double* gram;        // [mode][RP*RP]: this mode rewritten by the last block
+    const double* fac;   // chol_kernel output for this mode
+    const double* M;     // layout 0: M[r * ld + i]; layout 1: M[i * RP + r]
+    int layout;
+    int64_t ld;
+    double* out;         // col-major In x R (block of the packed iterate)
+    int* status;
+    dd* part;            // this mode's Gram partials [chunk][npair]
+    int nchunk;
+    int64_t rows;        // rows per Gram chunk
+    unsigned int* counter;
+};
+
+constexpr int kSolveThreads = 256;
+
+// Phase 1: threads solve rows i = global thread id (+ grid stride) against the factor from
+// chol_kernel. Grid barrier. Phase 2: the Gram of the new A_n as warp (chunk, pair) tasks
+// (gram.cuh); the last block combines and rounds into gram[mode].
+template <int RP>
+__global__ void __launch_bounds__(kSolveThreads) solve_gram_kernel(const SolveGramParams p) {
+    __shared__ double l[RP * RP];
+    __shared__ double dinv[RP];
     const int R = p.R;
     const int tid = threadIdx.x;
-    for (int e = tid; e < R * R; e += blockDim.x) {
-        const int q = e / R, r = e % R;
-        double v = 1.0;
-        for (int m = 0; m < p.order; ++m)
-            if (m != p.mode) v *= p.gram[(size_t)m * p.RP * p.RP + q * p.RP + r];
-        g[e] = v;
-        l[e] = 0.0;
-    }
+    if (p.fac[R * R + R] == 0.0) return;  // factorisation failed (status set): uniform exit
+    for (int e = tid; e < R * R; e += blockDim.x) l[e] = p.fac[e];
+    for (int e = tid; e < R; e += blockDim.x) dinv[e] = p.fac[R * R + e];
     __syncthreads();
-    if (tid < 32) {
-        bool ok = warp_llt(g, l, R, 0.0);
-        if (!ok) {
-            double tr = 0.0;
-            for (int i = 0; i < R; ++i) tr += g[i * R + i];
-            const double ridge = 1e-12 * tr;
-            __syncwarp();
-            for (int e = tid; e < R * R; e += 32) l[e] = 0.0;
-            __syncwarp();
-            ok = (ridge > 0.0) && warp_llt(g, l, R, ridge);
+    bool fin = true;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + tid; i < p.In; i += (int64_t)gridDim.x * blockDim.x) {
+        double y[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+            y[r] = (r < R) ? (p.layout == 0 ? p.M[(int64_t)r * p.ld + i] : p.M[i * RP + r]) : 0.0;
+        // L y = m, then L^T x = y (dot-product order of the reference's triangular solves)
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+            if (r < R) {
+                double s = y[r];
+#pragma unroll
+                for (int j = 0; j < r; ++j) s -= l[r * R + j] * y[j];
+                y[r] = s * dinv[r];
+            }
         }
-        if (tid == 0) ok_s = ok ? 1 : 0;
+#pragma unroll
+        for (int r = RP - 1; r >= 0; --r) {
+            if (r < R) {
+                double s = y[r];
+#pragma unroll
+                for (int j = r + 1; j < RP; ++j)
+                    if (j < R) s -= l[j * R + r] * y[j];
+                y[r] = s * dinv[r];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+            if (r < R) {
+                p.out[(int64_t)r * p.In + i] = y[r];
+                fin = fin && isfinite(y[r]);
+            }
     }
-    __syncthreads();
-    if (!ok_s) {
-        if (tid == 0 && blockIdx.x == 0) atomicOr(p.status, 1);
-        return;
-    }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + tid; i < p.In; i += (int64_t)gridDim.x * blockDim.x) {
-        double y[kMaxRank];
-        for (int r = 0; r < R; ++r) {  // L y = m_i
-            double s = p.M[(int64_t)r * p.In + i];
-            for (int j = 0; j < r; ++j) s -= l[r * R + j] * y[j];
-            y[r] = s / l[r * R + r];
-        }
-        for (int r = R - 1; r >= 0; --r) {  // L^T x = y
-            double s = y[r];
-            for (int j = r + 1; j < R; ++j) s -= l[j * R + r] * y[j];
-            y[r] = s / l[r * R + r];
-        }
-        bool fin = true;
-        for (int r = 0; r < R; ++r) {
-            p.out[(int64_t)r * p.In + i] = y[r];
-            fin = fin && isfinite(y[r]);
-        }
-        if (!fin) atomicOr(p.status, 2);
-    }
+    if (!fin) atomicOr(p.status, 2);
+    __threadfence();
+    cg::this_grid().sync();
+    const int npair = R * (R + 1) / 2;
+    const int warp = (int)((blockIdx.x * blockDim.x + tid) >> 5);
+    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int t = warp; t < p.nchunk * npair; t += nwarps) gram_task(p.out, p.In, p.rows, R, t, p.part);
+    if (!last_block_arrives(p.counter)) return;
+    double* gout = p.gram + (size_t)p.mode * p.RP * p.RP;
+    gram_zero_pads(R, p.RP, gout);
+    for (int q = tid; q < npair; q += blockDim.x) gram_combine_pair(p.part, p.nchunk, q, R, p.RP, gout);
 }
 
 struct NormParams {
@@ -141,11 +219,15 @@ __global__ void normalize_kernel(const NormParams p) {
     __shared__ double lam[kMaxRank];
     __shared__ int perm[kMaxRank];
     __shared__ double scale[kMaxOrder][kMaxRank];
+    __shared__ double diag[kMaxOrder][kMaxRank];
     const int tid = threadIdx.x;
+    for (int e = tid; e < p.order * p.R; e += blockDim.x)  // Gram diagonals, independent loads
+        diag[e / p.R][e % p.R] = p.gram[(size_t)(e / p.R) * p.RP * p.RP + (e % p.R) * (p.RP + 1)];
+    __syncthreads();
     if (tid < p.R) {
         double l = 1.0;
         for (int n = 0; n < p.order; ++n) {
-            const double v = sqrt(p.gram[(size_t)n * p.RP * p.RP + tid * p.RP + tid]);
+            const double v = sqrt(diag[n][tid]);
             nrm[n][tid] = v;
             l *= v;
         }
@@ -275,21 +357,74 @@ int normalize_grad_device(EvalWork& w, const double* u, const double* g, double*
 }
 
 namespace {
-void solve_mode(EvalWork& w, int n, const double* M, double* ublock, int* status, cudaStream_t st) {
-    SolveParams p{};
+// Cholesky factor of Gamma_n from the current Grams -> w.chol + mode slot
+void chol_mode(EvalWork& w, int n, int* status, cudaStream_t st) {
+    CholParams p{};
     p.order = w.order;
+    p.R = w.R;
+    p.RP = w.RP;
+    p.mode = n;
+    p.gram = w.gram;
+    p.fac = w.chol + (size_t)n * w.chol_stride;
+    p.status = status;
+    const size_t smem = sizeof(double) * (size_t)w.order * w.RP * w.RP;
+    switch (w.RP) {
+        case 8: chol_kernel<8><<<1, 32, smem, st>>>(p); break;
+        case 16: chol_kernel<16><<<1, 32, smem, st>>>(p); break;
+        default:
+            CPFIT_CUDA(cudaFuncSetAttribute(chol_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            chol_kernel<32><<<1, 32, smem, st>>>(p);
+            break;
+    }
+    CPFIT_CUDA(cudaGetLastError());
+}
+
+// A_n <- M_n Gamma_n^-1 (factor from chol_mode) and G_n <- A_n^T A_n
+void solve_gram(EvalWork& w, int n, const double* M, int layout, int64_t ld, double* ublock, int* status,
+                cudaStream_t st) {
+    SolveGramParams p{};
     p.R = w.R;
     p.RP = w.RP;
     p.mode = n;
     p.In = w.dims[n];
     p.gram = w.gram;
+    p.fac = w.chol + (size_t)n * w.chol_stride;
     p.M = M;
+    p.layout = layout;
+    p.ld = ld;
     p.out = ublock;
     p.status = status;
-    const int blocks = (int)std::min<int64_t>(296, (p.In + 127) / 128);
-    solve_kernel<<<blocks, 128, 0, st>>>(p);
-    CPFIT_CUDA(cudaGetLastError());
+    p.part = w.gram_part + (size_t)w.gram_chunk0[n] * (w.R * (w.R + 1) / 2);
+    p.nchunk = w.gram_nchunk[n];
+    p.rows = gram_chunk_rows(p.In);
+    p.counter = w.counter + kCounterSolve;
+    const int tasks = p.nchunk * (w.R * (w.R + 1) / 2);
+    const int64_t need = std::max<int64_t>((p.In + kSolveThreads - 1) / kSolveThreads, (tasks + 7) / 8);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(need, sm_count())));
+    cfg.blockDim = dim3(kSolveThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeCooperative;
+    attr.val.cooperative = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    switch (w.RP) {
+        case 8: CPFIT_CUDA(cudaLaunchKernelEx(&cfg, solve_gram_kernel<8>, p)); break;
+        case 16: CPFIT_CUDA(cudaLaunchKernelEx(&cfg, solve_gram_kernel<16>, p)); break;
+        default: CPFIT_CUDA(cudaLaunchKernelEx(&cfg, solve_gram_kernel<32>, p)); break;
+    }
 }
+
+// chol_mode(n) on the side stream once everything queued on st so far is done; the next
+// solve_gram(n) on st waits for it (join_chol)
+void fork_chol(EvalWork& w, int n, int* status, cudaStream_t st) {
+    CPFIT_CUDA(cudaEventRecord(w.ev_fork, st));
+    CPFIT_CUDA(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
+    chol_mode(w, n, status, w.side);
+    CPFIT_CUDA(cudaEventRecord(w.ev_join, w.side));
+}
+void join_chol(EvalWork& w, cudaStream_t st) { CPFIT_CUDA(cudaStreamWaitEvent(st, w.ev_join, 0)); }
 }  // namespace
 
 // work: n_u scratch (pre-normalisation iterate), mbuf: max(I_n)*R scratch
@@ -298,37 +433,37 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
     CPFIT_CUDA(cudaMemcpyAsync(work, u, sizeof(double) * w.nu, cudaMemcpyDeviceToDevice, st));
     grams_device(w, work, st);
     const int N = t.order;
+    // Gamma_0 from the Grams of u; each later Gamma_n as soon as G_{n-1}' exists (side stream)
+    chol_mode(w, 0, status, st);
     if (t.sparse) {
         for (int n = 0; n < N; ++n) {
+            if (n > 0) fork_chol(w, n, status, st);
             sparse_all_modes(t, w, work, n, st);
             int64_t off = 0;
             for (int m = 0; m < n; ++m) off += t.dims[m] * w.RP;
-            gather_m(t.dims[n], w, w.sp_part + off, 1, 0, 1, mbuf, st);
-            solve_mode(w, n, mbuf, work + w.off[n], status, st);
-            gram_mode_device(w, work, n, st);
+            if (n > 0) join_chol(w, st);
+            solve_gram(w, n, w.sp_part + off, 1, 0, work + w.off[n], status, st);
         }
     } else {
         // mode 0: tail contraction with the old modes >= 1 — or, inside the N-GMRES loop, the
         // M0 the evaluation of this iterate already produced (m0_given, [RP][32 NC])
         if (!m0_given) dense_fiber(t, w, work, false, true, st);
-        gather_m(t.dims[0], w, m0_given ? m0_given : w.m0, 1, 32 * w.fiber_nchunk, 0, mbuf, st);
-        solve_mode(w, 0, mbuf, work + w.off[0], status, st);
-        gram_mode_device(w, work, 0, st);
+        solve_gram(w, 0, m0_given ? m0_given : w.m0, 0, 32 * w.fiber_nchunk, work + w.off[0], status, st);
+        fork_chol(w, 1, status, st);
         // S' = T x_1 A0'
         dense_fiber(t, w, work, true, false, st);
         const double* Sin = w.S;
         for (int n = 1; n < N; ++n) {
             if (n < N - 1) {
                 dense_level(t, w, n, Sin, work, true, false, nullptr, st);
-                gather_m(t.dims[n], w, w.lvl_m[n], 1, 0, 1, mbuf, st);
-            } else {
-                gather_m(t.dims[n], w, Sin, 1, 0, 1, mbuf, st);
-            }
-            solve_mode(w, n, mbuf, work + w.off[n], status, st);
-            gram_mode_device(w, work, n, st);
-            if (n < N - 1) {
+                join_chol(w, st);
+                solve_gram(w, n, w.lvl_m[n], 1, 0, work + w.off[n], status, st);
+                fork_chol(w, n + 1, status, st);
                 dense_level(t, w, n, Sin, work, false, true, w.lvl_S[n], st);
                 Sin = w.lvl_S[n];
+            } else {
+                join_chol(w, st);
+                solve_gram(w, n, Sin, 1, 0, work + w.off[n], status, st);
             }
         }
     }

@@ -35,7 +35,20 @@ struct cpfit_tensor_s {
         }
         return one_;
     }
+    // solvers of the one-shot solve calls, kept between calls (graph capture and instantiation
+    // cost milliseconds): one per method, reused while rank and graph-baked options match
+    std::unique_ptr<Solver> solvers[2];
+    Solver& solver(int R, const SolverOptions& o, int method) {
+        std::unique_ptr<Solver>& s = solvers[method];
+        if (!s || s->rank() != R || !s->options().serves(o)) {
+            s.reset();
+            s = std::make_unique<Solver>(t, R, o, method);
+        }
+        return *s;
+    }
     ~cpfit_tensor_s() {
+        solvers[0].reset();
+        solvers[1].reset();
         for (auto& kv : works) work_destroy(kv.second);
         cudaFree(one_);
         cudaFree(scratch);
@@ -395,7 +408,7 @@ int cpfit_ngmres_solve(cpfit_tensor t, int64_t rank, const double* u0, const cpf
         std::lock_guard<std::mutex> lk(t->mu);
         check_rank(rank);
         const SolverOptions so = to_opts(o, t->t->norm);
-        Solver sv(t->t, (int)rank, so, 0);
+        Solver& sv = t->solver((int)rank, so, 0);
         check_finite(u0, sv.n());
         sv.set_initial(u0, true);
         sv.run_init();
@@ -413,7 +426,7 @@ int cpfit_als_solve(cpfit_tensor t, int64_t rank, const double* u0, double tol_g
         so.tol_grad = tol_grad;
         so.max_iters = max_iters;
         so.gradient_scale = t->t->norm;  // als.cpp:74 (||g|| / ||T||)
-        Solver sv(t->t, (int)rank, so, 1);
+        Solver& sv = t->solver((int)rank, so, 1);
         check_finite(u0, sv.n());
         sv.set_initial(u0, true);
         sv.run_init();
@@ -503,6 +516,22 @@ int cpfit_solver_best(cpfit_solver s, double* u) {
 
 int cpfit_solver_launches(cpfit_solver s, int64_t* launches) {
     return guard([&] { *launches = s->s->summary().launches; });
+}
+
+int cpfit_fiber_prof(uint64_t* out, int reset) {
+    return guard([&] {
+        unsigned long long* b = cpfit_gpu::fiber_prof_buffer();
+        CPFIT_CUDA(cudaDeviceSynchronize());
+        CPFIT_CUDA(cudaMemcpy(out, b, sizeof(unsigned long long) * cpfit_gpu::kFiberProfSlots, cudaMemcpyDeviceToHost));
+        if (reset) CPFIT_CUDA(cudaMemset(b, 0, sizeof(unsigned long long) * cpfit_gpu::kFiberProfSlots));
+    });
+}
+
+int cpfit_solver_phase_times(cpfit_solver s, double* us, int64_t* visits) {
+    return guard([&] {
+        if (!s->s->phase_times(us, visits))
+            throw std::invalid_argument("phase profiling is off (set CPFIT_PHASE_PROFILE=1 before cpfit_solver_create)");
+    });
 }
 
 int cpfit_solver_iterate(cpfit_solver s, double* u) {

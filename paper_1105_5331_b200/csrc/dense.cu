@@ -17,8 +17,6 @@
 
 namespace cpfit_gpu {
 
-namespace {
-
 int sm_count() {
     static int n = [] {
         int d = 0, c = 0;
@@ -29,16 +27,24 @@ int sm_count() {
     return n;
 }
 
+namespace {
+
 // ---------------------------------------------------------------------------------------
 // Fiber pass
 // ---------------------------------------------------------------------------------------
+constexpr int kMaxM0W = 16;  // M0 warps per fiber CTA (fiber.cuh FiberRoles)
+
 struct FiberParams {
     const double* T;
     int64_t ldT;
     int I0;
     int64_t J;
-    int nchunk;  // warps per CTA; each owns 32 rows of the fiber
+    int nchunk;  // 32-row chunks of the fiber (smem stride / M0 ld = 32*nchunk)
     int I0s;     // smem row stride (32*nchunk + 4)
+    // M0 warps and their 8-row m-tiles: warp m owns m-tiles [mt_start[m], +mt_cnt[m]),
+    // balanced across the SM's four schedulers (fiber_schedule)
+    int mt_cnt[kMaxM0W];
+    int mt_start[kMaxM0W];
     int do_s, do_m0, do_f;
     int R;
     const double* A0;  // col-major I0 x R
@@ -53,247 +59,25 @@ struct FiberParams {
     const int* resid_flag;         // device flag: residual-form objective when nonzero
     int64_t tiles_per_cta;
     int64_t ntiles;
+    unsigned long long* prof;  // diagnostic build only (fiber.cuh FIBER_WAIT)
 };
 
 #include "fiber.cuh"
 
-#if 0  // first version (CTA-wide barriers per tile), superseded by fiber.cuh
-constexpr int kStages = 3;
 
-template <int RP, int F>
-__host__ __device__ constexpr int ws_ld() {
-    return RP + 4;  // RP + 4 is 4 or 12 mod 16 for RP in {8,16,24,32}: conflict-free frags
+}  // namespace
+
+// diagnostic counters of the -DCPFIT_FIBER_PROF build (zeros otherwise)
+unsigned long long* fiber_prof_buffer() {
+    static unsigned long long* buf = nullptr;
+    if (!buf) {
+        CPFIT_CUDA(cudaMalloc(&buf, sizeof(unsigned long long) * kProfSlots));
+        CPFIT_CUDA(cudaMemset(buf, 0, sizeof(unsigned long long) * kProfSlots));
+    }
+    return buf;
 }
 
-template <int RP, int F>
-size_t fiber_smem_bytes(int nchunk) {
-    const int I0s = 32 * nchunk + 4;
-    size_t b = 0;
-    b += sizeof(double) * (size_t)kStages * F * I0s;          // T tiles
-    b += sizeof(double) * (size_t)nchunk * F * RP;             // S partials per warp
-    b += sizeof(double) * 2 * (size_t)F * ws_ld<RP, F>();      // W tile (double buffered)
-    b += sizeof(double) * (size_t)F * RP;                      // per-fiber objective terms
-    b += sizeof(uint64_t) * kStages;
-    return b;
-}
-
-template <int RP, int F, bool A0REG>
-__global__ void __launch_bounds__(512) fiber_kernel(const FiberParams p) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int WLD = ws_ld<RP, F>();
-    constexpr int NRT = RP / 8;
-    const int I0s = p.I0s;
-    double* tiles = reinterpret_cast<double*>(smem_raw);
-    double* spart = tiles + (size_t)kStages * F * I0s;
-    double* wsb = spart + (size_t)p.nchunk * F * RP;
-    double* fterm = wsb + 2 * F * WLD;
-    uint64_t* full = reinterpret_cast<uint64_t*>(fterm + F * RP);
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nthr = blockDim.x;
-    const int64_t t_begin = (int64_t)blockIdx.x * p.tiles_per_cta;
-    const int64_t t_end = imin64(p.ntiles, t_begin + p.tiles_per_cta);
-    const int64_t ntl = t_end > t_begin ? t_end - t_begin : 0;
-
-    // zero tiles once (padding rows beyond ldT must read as 0)
-    for (int64_t e = tid; e < (int64_t)kStages * F * I0s; e += nthr) tiles[e] = 0.0;
-    if (tid == 0)
-        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-    mbar_fence_init();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-
-    auto issue = [&](int64_t t, int s) {
-        // thread 0 only
-        const int64_t f0 = t * F;
-        const int nvalid = (int)cpfit_gpu::imin64(F, p.J - f0);
-        mbar_arrive_expect_tx(&full[s], (uint32_t)(nvalid * p.ldT * 8));
-        for (int f = 0; f < nvalid; ++f)
-            bulk_g2s(tiles + ((size_t)s * F + f) * I0s, p.T + (f0 + f) * p.ldT, (uint32_t)(p.ldT * 8), &full[s]);
-    };
-    auto zero_invalid = [&](int64_t t, int s) {
-        const int64_t f0 = t * F;
-        const int nvalid = (int)cpfit_gpu::imin64(F, p.J - f0);
-        for (int e = tid; e < (F - nvalid) * I0s; e += nthr) tiles[((size_t)s * F + nvalid) * I0s + e] = 0.0;
-    };
-    if (tid == 0)
-        for (int64_t k = 0; k < cpfit_gpu::imin64(kStages, ntl); ++k) issue(t_begin + k, (int)k);
-    for (int64_t k = 0; k < cpfit_gpu::imin64(kStages, ntl); ++k) zero_invalid(t_begin + k, (int)k);
-
-    const int c = warp;  // this warp's 32-row chunk
-    // A0 fragments (B operand of the S contraction): A0[i][r], i = c*32 + ks*4 + lane%4
-    double a0f[A0REG ? 8 : 1][A0REG ? NRT : 1];
-    auto a0_at = [&](int ks, int rt) -> double {
-        const int i = c * 32 + ks * 4 + (lane & 3);
-        const int r = rt * 8 + (lane >> 2);
-        return (i < p.I0 && r < p.R) ? p.A0[(int64_t)r * p.I0 + i] : 0.0;
-    };
-    if (A0REG && p.do_s) {
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-            for (int rt = 0; rt < NRT; ++rt) a0f[ks][rt] = a0_at(ks, rt);
-    }
-    double macc[NRT][4][2];
-#pragma unroll
-    for (int rt = 0; rt < NRT; ++rt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) macc[rt][nt][0] = macc[rt][nt][1] = 0.0;
-    double facc = 0.0;
-    const bool need_w = p.do_m0 || p.do_f;
-
-    for (int64_t k = 0; k < ntl; ++k) {
-        const int64_t t = t_begin + k;
-        const int s = (int)(k % kStages);
-        const uint32_t parity = (uint32_t)((k / kStages) & 1);
-        double* wsv = wsb + (k & 1) * F * WLD;
-        if (need_w) {
-            for (int e = tid; e < F * RP; e += nthr) {
-                const int f = e / RP, r = e % RP;
-                const int64_t fib = t * F + f;
-                double w = 0.0;
-                if (fib < p.J && r < p.R) {
-                    w = 1.0;
-                    int64_t rem = fib;
-                    for (int m = 1; m < p.order; ++m) {
-                        const int64_t jm = rem % p.dims[m];
-                        rem /= p.dims[m];
-                        w *= p.fac[m][(int64_t)r * p.dims[m] + jm];
-                    }
-                }
-                wsv[f * WLD + r] = w;
-            }
-        }
-        __syncthreads();
-        mbar_wait(&full[s], parity);
-        const double* tt = tiles + (size_t)s * F * I0s;
-        if (p.do_s) {
-            double sacc[F / 8][NRT][2];
-#pragma unroll
-            for (int ft = 0; ft < F / 8; ++ft)
-#pragma unroll
-                for (int rt = 0; rt < NRT; ++rt) sacc[ft][rt][0] = sacc[ft][rt][1] = 0.0;
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                const int i = c * 32 + ks * 4 + (lane & 3);
-                double a[F / 8];
-#pragma unroll
-                for (int ft = 0; ft < F / 8; ++ft) a[ft] = tt[(ft * 8 + (lane >> 2)) * I0s + i];
-#pragma unroll
-                for (int rt = 0; rt < NRT; ++rt) {
-                    const double b = A0REG ? a0f[A0REG ? ks : 0][A0REG ? rt : 0] : a0_at(ks, rt);
-#pragma unroll
-                    for (int ft = 0; ft < F / 8; ++ft) dmma_8x8x4(sacc[ft][rt][0], sacc[ft][rt][1], a[ft], b);
-                }
-            }
-            double* sp = spart + (size_t)warp * F * RP;
-#pragma unroll
-            for (int ft = 0; ft < F / 8; ++ft)
-#pragma unroll
-                for (int rt = 0; rt < NRT; ++rt) {
-                    const int f = ft * 8 + (lane >> 2), r = rt * 8 + 2 * (lane & 3);
-                    *reinterpret_cast<double2*>(sp + f * RP + r) = make_double2(sacc[ft][rt][0], sacc[ft][rt][1]);
-                }
-        }
-        if (p.do_m0) {
-#pragma unroll
-            for (int kf = 0; kf < F / 4; ++kf) {
-                const int f = kf * 4 + (lane & 3);
-                double wa[NRT];
-#pragma unroll
-                for (int rt = 0; rt < NRT; ++rt) wa[rt] = wsv[f * WLD + rt * 8 + (lane >> 2)];
-#pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                    const double b = tt[f * I0s + c * 32 + nt * 8 + (lane >> 2)];
-#pragma unroll
-                    for (int rt = 0; rt < NRT; ++rt) dmma_8x8x4(macc[rt][nt][0], macc[rt][nt][1], wa[rt], b);
-                }
-            }
-        }
-        __syncthreads();  // stage s and spart complete
-        if (k + kStages < ntl) {
-            if (tid == 0) issue(t + kStages, s);
-            zero_invalid(t + kStages, s);
-        }
-        if (p.do_s) {
-            const int64_t f0 = t * F;
-            for (int e = tid; e < F * RP; e += nthr) {
-                const int f = e / RP, r = e % RP;
-                double v = 0.0;
-                for (int ww = 0; ww < p.nchunk; ++ww) v += spart[((size_t)ww * F + f) * RP + r];
-                if (f0 + f < p.J) p.S_out[(f0 + f) * RP + r] = v;
-                if (p.do_f) {
-                    // per-fiber objective term: w_r * ((G0 w)_r - 2 s_r)
-                    double q = 0.0;
-#pragma unroll 8
-                    for (int qq = 0; qq < RP; ++qq) q += p.gamma0[r * RP + qq] * wsv[f * WLD + qq];
-                    const double w = wsv[f * WLD + r];
-                    fterm[f * RP + r] = w * (q - 2.0 * v);
-                }
-            }
-            if (p.do_f) {
-                __syncthreads();
-                if (tid < F && f0 + tid < p.J) {
-                    double pf = p.fnorm2[f0 + tid];
-                    for (int r = 0; r < RP; ++r) pf += fterm[tid * RP + r];
-                    facc += pf;
-                }
-            }
-        }
-    }
-    // write M0 partials: M0^T[r][i] tile fragments
-    if (p.do_m0) {
-        const int ld = 32 * p.nchunk;
-        double* out = p.m0_part + (size_t)blockIdx.x * RP * ld;
-#pragma unroll
-        for (int rt = 0; rt < NRT; ++rt)
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-                const int r = rt * 8 + (lane >> 2);
-                const int i = c * 32 + nt * 8 + 2 * (lane & 3);
-                out[(size_t)r * ld + i] = macc[rt][nt][0];
-                out[(size_t)r * ld + i + 1] = macc[rt][nt][1];
-            }
-    }
-    if (p.do_f) {
-        // fixed-order block reduction of the per-fiber sums (threads < F hold them)
-        __shared__ double red[32];
-        double v = warp_sum(facc);
-        if (lane == 0) red[warp] = v;
-        __syncthreads();
-        if (tid == 0) {
-            double s = 0.0;
-            for (int ww = 0; ww < (nthr + 31) / 32; ++ww) s += red[ww];
-            p.f_part[blockIdx.x] = s;
-        }
-    }
-}
-
-template <int RP>
-void launch_fiber(const FiberParams& p, int grid, int nchunk, size_t smem, cudaStream_t st) {
-    constexpr int F = 16;
-    if (RP <= 16) {
-        auto k = fiber_kernel<RP, F, true>;
-        CPFIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k<<<grid, 32 * nchunk, smem, st>>>(p);
-    } else {
-        auto k = fiber_kernel<RP, F, false>;
-        CPFIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k<<<grid, 32 * nchunk, smem, st>>>(p);
-    }
-    CPFIT_CUDA(cudaGetLastError());
-}
-
-size_t fiber_smem(int RP, int nchunk) {
-    switch (RP) {
-        case 8: return fiber_smem_bytes<8, 16>(nchunk);
-        case 16: return fiber_smem_bytes<16, 16>(nchunk);
-        case 24: return fiber_smem_bytes<24, 16>(nchunk);
-        default: return fiber_smem_bytes<32, 16>(nchunk);
-    }
-}
-
-#endif
+namespace {
 
 // M0 = sum over the fiber-pass CTAs of their [RP][32 NC] partials (fixed order)
 void reduce_parts(const double* part, int nparts, int64_t nout, double* out, cudaStream_t st);
@@ -310,6 +94,10 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
     p.J = t.J;
     p.nchunk = w.fiber_nchunk;
     p.I0s = 32 * w.fiber_nchunk + 4;
+    fiber_schedule(w.RP, p.I0, do_s, p);
+#ifdef CPFIT_FIBER_PROF
+    p.prof = fiber_prof_buffer();
+#endif
     p.do_s = do_s;
     p.do_m0 = do_m0;
     p.do_f = do_f;
@@ -337,102 +125,123 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
         if (do_f) CPFIT_CUDA(cudaMemsetAsync(w.f_part + grid, 0, sizeof(double) * (w.fiber_grid - grid), st));
     }
     switch (w.RP) {
-        case 8: launch_fiber<8>(p, grid, w.fiber_nchunk, w.fiber_smem, st); break;
-        case 16: launch_fiber<16>(p, grid, w.fiber_nchunk, w.fiber_smem, st); break;
-        default: launch_fiber<32>(p, grid, w.fiber_nchunk, w.fiber_smem, st); break;
+        case 8: launch_fiber<8>(p, grid, w.fiber_smem, st); break;
+        case 16: launch_fiber<16>(p, grid, w.fiber_smem, st); break;
+        default: launch_fiber<32>(p, grid, w.fiber_smem, st); break;
     }
 }
 
 // ---------------------------------------------------------------------------------------
-// Level contraction: Sin viewed as (Ih x Jt x RP) [(jh + Ih*s)*RP + r]
-//   Mh(jh, r)   = sum_s Sin(jh, s, r) * Wt(s, r),  Wt = KR of modes h+1..N-1
-//   Sout(s, r)  = sum_jh Sin(jh, s, r) * Ah(jh, r)
-// Thread t owns pairs p = t + k*B of (jh, r) (B % RP == 0 so r = t % RP is fixed).
+// Level contraction: Sin viewed as Jt slabs of (Ih x RP) doubles [(s*Ih + jh)*RP + r]
+//   M_h(jh, r) = sum_s Sin(s, jh, r) * Wt(s, r),  Wt = KR rows of modes h+1..N-1
+//   Sout(s, r) = sum_jh Sin(s, jh, r) * A_h(jh, r)
+// Both from one read of Sin. CTA (x, y) streams slabs [x*spc, (x+1)*spc) over the pair range
+// [y*256*KM, (y+1)*256*KM); a thread owns pairs base + tid + 256 k (k < KM; 256 % RP == 0 so
+// r = tid % RP) with its M accumulators and A_h entries in registers. M partials per x go
+// through reduce_parts (fixed order); Sout per (y, slab) from a shuffle + shared-memory tree.
 // ---------------------------------------------------------------------------------------
 struct LevelParams {
     const double* Sin;
     int64_t Ih, Jt;
-    int R, RP;
-    const double* Ah;  // col-major Ih x R (head factor) or null (no Sout)
+    int R;
+    const double* Ah;  // col-major Ih x R (Sout) or null
     int ntail;
     int64_t tdims[kMaxOrder];
     const double* tfac[kMaxOrder];
-    double* mh_part;  // grid x Ih x RP  (null: skip Mh)
-    double* Sout;     // Jt x RP (null: skip)
-    int64_t slabs_per_cta;
+    double* m_part;  // [gridDim.x][Ih*RP] or null (no M_h)
+    double* s_out;   // [gridDim.y][Jt][RP] or null (no Sout)
+    int64_t spc;     // slabs per CTA
 };
 
 constexpr int kLevelThreads = 256;
-constexpr int kSlabBatch = 8;
+constexpr int kSlabBatch = 4;
 
+template <int RP, int KM>
 __global__ void __launch_bounds__(kLevelThreads) level_kernel(const LevelParams p) {
-    extern __shared__ __align__(16) double lsm[];
-    const int tid = threadIdx.x, B = blockDim.x;
-    const int RP = p.RP;
-    const int64_t npairs = p.Ih * RP;
-    const int kmax = (int)((npairs + B - 1) / B);
-    double* acc = lsm;                          // kmax * B (private per thread)
-    double* ah = acc + (size_t)kmax * B;        // kmax * B
-    double* wt = ah + (size_t)kmax * B;         // kSlabBatch * RP
-    double* spart = wt + kSlabBatch * RP;       // kSlabBatch * B
-    const int64_t s_begin = (int64_t)blockIdx.x * p.slabs_per_cta;
-    const int64_t s_end = imin64(p.Jt, s_begin + p.slabs_per_cta);
+    constexpr int B = kLevelThreads, NW = B / 32;
+    __shared__ double wt[kSlabBatch][RP];
+    __shared__ double sred[kSlabBatch][NW][RP];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r = tid % RP;
-    for (int k = 0; k < kmax; ++k) {
-        const int64_t pr = tid + (int64_t)k * B;
-        acc[k * B + tid] = 0.0;
-        double a = 0.0;
-        if (p.Ah && pr < npairs && r < p.R) a = p.Ah[(int64_t)r * p.Ih + pr / RP];
-        ah[k * B + tid] = a;
+    const int64_t npairs = p.Ih * RP;
+    const int64_t pbase = (int64_t)blockIdx.y * B * KM + tid;
+    const int64_t s_begin = (int64_t)blockIdx.x * p.spc;
+    const int64_t s_end = imin64(p.Jt, s_begin + p.spc);
+    const bool do_m = p.m_part != nullptr, do_s = p.s_out != nullptr;
+    double acc[KM], ah[KM];
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+        const int64_t pr = pbase + (int64_t)k * B;
+        acc[k] = 0.0;
+        ah[k] = (do_s && pr < npairs && r < p.R) ? p.Ah[(int64_t)r * p.Ih + pr / RP] : 0.0;
     }
     for (int64_t s0 = s_begin; s0 < s_end; s0 += kSlabBatch) {
-        const int nb = (int)cpfit_gpu::imin64(kSlabBatch, s_end - s0);
-        __syncthreads();
-        for (int e = tid; e < nb * RP; e += B) {
-            const int sl = e / RP, rr = e % RP;
-            double w = 0.0;
-            if (rr < p.R) {
-                w = 1.0;
-                int64_t rem = s0 + sl;
-                for (int m = 0; m < p.ntail; ++m) {
-                    const int64_t jm = rem % p.tdims[m];
-                    rem /= p.tdims[m];
-                    w *= p.tfac[m][(int64_t)rr * p.tdims[m] + jm];
+        const int nb = (int)imin64(kSlabBatch, s_end - s0);
+        __syncthreads();  // previous batch's wt / sred consumers are done
+        if (do_m) {
+            for (int e = tid; e < nb * RP; e += B) {
+                const int sl = e / RP, rr = e % RP;
+                double w = 0.0;
+                if (rr < p.R) {
+                    w = 1.0;
+                    int64_t rem = s0 + sl;
+                    for (int m = 0; m < p.ntail; ++m) {
+                        const int64_t jm = rem % p.tdims[m];
+                        rem /= p.tdims[m];
+                        w *= p.tfac[m][(int64_t)rr * p.tdims[m] + jm];
+                    }
                 }
+                wt[sl][rr] = w;
             }
-            wt[sl * RP + rr] = w;
+            __syncthreads();
         }
-        __syncthreads();
         for (int sl = 0; sl < nb; ++sl) {
-            const double* src = p.Sin + (s0 + sl) * p.Ih * RP;
-            const double wv = wt[sl * RP + r];
+            const double* src = p.Sin + (s0 + sl) * npairs;
+            const double wv = do_m ? wt[sl][r] : 0.0;
             double sp = 0.0;
-            for (int k = 0; k < kmax; ++k) {
-                const int64_t pr = tid + (int64_t)k * B;
+#pragma unroll
+            for (int k = 0; k < KM; ++k) {
+                const int64_t pr = pbase + (int64_t)k * B;
                 if (pr < npairs) {
-                    const double v = src[pr];
-                    acc[k * B + tid] += v * wv;
-                    sp += v * ah[k * B + tid];
+                    const double v = __ldg(src + pr);
+                    acc[k] = fma(v, wv, acc[k]);
+                    sp = fma(v, ah[k], sp);
                 }
             }
-            spart[sl * B + tid] = sp;
+            if (do_s) {
+#pragma unroll
+                for (int o = 16; o >= RP; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
+                if (lane < RP) sred[sl][warp][lane] = sp;
+            }
         }
-        __syncthreads();
-        if (p.Sout) {
+        if (do_s) {
+            __syncthreads();
             for (int e = tid; e < nb * RP; e += B) {
                 const int sl = e / RP, rr = e % RP;
                 double v = 0.0;
-                for (int t2 = rr; t2 < B; t2 += RP) v += spart[sl * B + t2];
-                p.Sout[(s0 + sl) * RP + rr] = v;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) v += sred[sl][w][rr];
+                p.s_out[((int64_t)blockIdx.y * p.Jt + s0 + sl) * RP + rr] = v;
             }
         }
     }
-    if (p.mh_part) {
-        double* out = p.mh_part + (size_t)blockIdx.x * npairs;
-        for (int k = 0; k < kmax; ++k) {
-            const int64_t pr = tid + (int64_t)k * B;
-            if (pr < npairs) out[pr] = acc[k * B + tid];
+    if (do_m) {
+        double* out = p.m_part + (int64_t)blockIdx.x * npairs;
+#pragma unroll
+        for (int k = 0; k < KM; ++k) {
+            const int64_t pr = pbase + (int64_t)k * B;
+            if (pr < npairs) out[pr] = acc[k];
         }
+    }
+}
+
+template <int RP>
+void launch_level_rp(const LevelParams& p, dim3 grid, int km, cudaStream_t st) {
+    switch (km) {
+        case 4: level_kernel<RP, 4><<<grid, kLevelThreads, 0, st>>>(p); break;
+        case 8: level_kernel<RP, 8><<<grid, kLevelThreads, 0, st>>>(p); break;
+        case 16: level_kernel<RP, 16><<<grid, kLevelThreads, 0, st>>>(p); break;
+        default: level_kernel<RP, 32><<<grid, kLevelThreads, 0, st>>>(p); break;
     }
 }
 
@@ -445,7 +254,16 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const double* __restr
     const int64_t o = (int64_t)blockIdx.x * 32 + lane;
     double v = 0.0;
     if (o < nout)
-        for (int c = ws; c < nparts; c += 8) v += part[(int64_t)c * nout + o];
+        for (int c0 = ws; c0 < nparts; c0 += 8 * 8) {
+            double x[8];  // loads batched ahead of the in-order adds
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int c = c0 + 8 * k;
+                x[k] = c < nparts ? part[(int64_t)c * nout + o] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v += x[k];
+        }
     sl[ws][lane] = v;
     __syncthreads();
     if (ws == 0 && o < nout) {
@@ -460,190 +278,97 @@ void reduce_parts(const double* part, int nparts, int64_t nout, double* out, cud
     CPFIT_CUDA(cudaGetLastError());
 }
 
-// M_h(jh, r) = sum_s Sin(jh, s, r) Wt(s, r) over a chunk of slabs per CTA: thread (jh, r),
-// coalesced over consecutive (jh, r) for each slab; chunk partials -> reduce_parts.
-struct LevelMParams {
-    const double* Sin;
-    int64_t Ih, Jt;
-    int R, RP;
-    int ntail;
-    int64_t tdims[kMaxOrder];
-    const double* tfac[kMaxOrder];
-    int64_t chunk;  // slabs per chunk
-    double* part;   // [chunk][Ih*RP]
-};
-
-__global__ void __launch_bounds__(256) level_m_kernel(const LevelMParams p) {
-    extern __shared__ double wt[];  // [chunk][RP]
-    const int64_t npairs = p.Ih * p.RP;
-    const int64_t s0 = (int64_t)blockIdx.y * p.chunk;
-    const int64_t s1 = imin64(p.Jt, s0 + p.chunk);
-    const int ns = (int)(s1 - s0);
-    for (int e = threadIdx.x; e < ns * p.RP; e += blockDim.x) {
-        const int sl = e / p.RP, r = e % p.RP;
-        double w = 0.0;
-        if (r < p.R) {
-            w = 1.0;
-            int64_t rem = s0 + sl;
-            for (int m = 0; m < p.ntail; ++m) {
-                const int64_t jm = rem % p.tdims[m];
-                rem /= p.tdims[m];
-                w *= p.tfac[m][(int64_t)r * p.tdims[m] + jm];
-            }
-        }
-        wt[e] = w;
-    }
-    __syncthreads();
-    const int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pr >= npairs) return;
-    const int r = (int)(pr % p.RP);
-    const double* src = p.Sin + s0 * npairs + pr;
-    double a0 = 0.0, a1 = 0.0;
-    int sl = 0;
-    for (; sl + 1 < ns; sl += 2) {
-        a0 += src[(int64_t)sl * npairs] * wt[sl * p.RP + r];
-        a1 += src[(int64_t)(sl + 1) * npairs] * wt[(sl + 1) * p.RP + r];
-    }
-    if (sl < ns) a0 += src[(int64_t)sl * npairs] * wt[sl * p.RP + r];
-    p.part[(int64_t)blockIdx.y * npairs + pr] = a0 + a1;
-}
-
 void run_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
                double* Sout, cudaStream_t st) {
-    const int64_t Ih = t.dims[h];
-    int64_t Jt = 1;
-    for (int m = h + 1; m < t.order; ++m) Jt *= t.dims[m];
-    const int64_t npairs = Ih * w.RP;
-    if (do_m) {
-        LevelMParams q{};
-        q.Sin = Sin;
-        q.Ih = Ih;
-        q.Jt = Jt;
-        q.R = w.R;
-        q.RP = w.RP;
-        q.ntail = t.order - h - 1;
-        for (int m = h + 1; m < t.order; ++m) {
-            q.tdims[m - h - 1] = t.dims[m];
-            q.tfac[m - h - 1] = u + w.off[m];
-        }
-        q.chunk = w.lvl_chunk[h];
-        q.part = w.lvl_part[h];
-        const int nchunk = (int)((Jt + q.chunk - 1) / q.chunk);
-        dim3 grid((unsigned)((npairs + 255) / 256), (unsigned)nchunk);
-        level_m_kernel<<<grid, 256, sizeof(double) * q.chunk * w.RP, st>>>(q);
-        CPFIT_CUDA(cudaGetLastError());
-        reduce_parts(w.lvl_part[h], nchunk, npairs, w.lvl_m[h], st);
-    }
-    if (!do_s) return;
+    if (!do_m && !do_s) return;
     LevelParams p{};
     p.Sin = Sin;
-    p.Ih = Ih;
-    p.Jt = Jt;
+    p.Ih = t.dims[h];
+    p.Jt = 1;
+    for (int m = h + 1; m < t.order; ++m) p.Jt *= t.dims[m];
     p.R = w.R;
-    p.RP = w.RP;
-    p.Ah = u + w.off[h];
+    p.Ah = do_s ? u + w.off[h] : nullptr;
     p.ntail = t.order - h - 1;
     for (int m = h + 1; m < t.order; ++m) {
         p.tdims[m - h - 1] = t.dims[m];
         p.tfac[m - h - 1] = u + w.off[m];
     }
-    p.mh_part = nullptr;
-    p.Sout = Sout;
-    const int gmax = w.lvl_grid[h];
-    p.slabs_per_cta = (p.Jt + gmax - 1) / gmax;
-    const int grid = (int)((p.Jt + p.slabs_per_cta - 1) / p.slabs_per_cta);
-    const int B = kLevelThreads;
-    const int kmax = (int)((npairs + B - 1) / B);
-    const size_t smem = sizeof(double) * ((size_t)2 * kmax * B + kSlabBatch * w.RP + (size_t)kSlabBatch * B);
-    CPFIT_CUDA(cudaFuncSetAttribute(level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    level_kernel<<<grid, B, smem, st>>>(p);
+    const int ny = w.lvl_ny[h];
+    p.m_part = do_m ? w.lvl_part[h] : nullptr;
+    p.s_out = do_s ? (ny > 1 ? w.lvl_spart[h] : Sout) : nullptr;
+    p.spc = w.lvl_spc[h];
+    const dim3 grid((unsigned)w.lvl_nx[h], (unsigned)ny);
+    switch (w.RP) {
+        case 8: launch_level_rp<8>(p, grid, w.lvl_km[h], st); break;
+        case 16: launch_level_rp<16>(p, grid, w.lvl_km[h], st); break;
+        default: launch_level_rp<32>(p, grid, w.lvl_km[h], st); break;
+    }
     CPFIT_CUDA(cudaGetLastError());
+    if (do_m) reduce_parts(w.lvl_part[h], w.lvl_nx[h], p.Ih * w.RP, w.lvl_m[h], st);
+    if (do_s && ny > 1) reduce_parts(w.lvl_spart[h], ny, p.Jt * w.RP, Sout, st);
 }
 
 // ---------------------------------------------------------------------------------------
-// Grams in double-double: G_n(r,q) = sum_i A_n(i,r) A_n(i,q); one warp per (mode, pair,
-// row chunk). Then a combine kernel sums chunks in order and rounds.
+// Grams in double-double (gram.cuh): blocks [blk0[n], blk0[n] + nblk[n]) own mode n's row
+// tiles; the last block to finish combines the partials of modes [mode_lo, mode_hi).
 // ---------------------------------------------------------------------------------------
 struct GramParams {
-    int order, R, RP;
+    int order, R, RP, mode_lo, mode_hi;
     int64_t dims[kMaxOrder];
     const double* fac[kMaxOrder];
-    int chunks[kMaxOrder];
-    int64_t chunk_rows;
-    dd* part;    // [mode][chunk][R*R]
-    double* out; // [mode][RP*RP]
-    int maxchunks;
-    int mode0;
+    int nchunk[kMaxOrder], chunk0[kMaxOrder];  // chunks per mode, prefix over all modes
+    int64_t rows[kMaxOrder];                   // rows per chunk
+    dd* part;     // [global chunk][npair]
+    double* out;  // [mode][RP*RP]
+    unsigned int* counter;
 };
 
-__global__ void gram_partial_kernel(const GramParams p) {
-    const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__global__ void __launch_bounds__(256) gram_kernel(const GramParams p) {
     const int npair = p.R * (p.R + 1) / 2;
-    // decode (mode, chunk, pair)
-    int rem = gw;
-    for (int n = 0; n < p.order; ++n) {
-        const int cnt = p.chunks[n] * npair;
-        if (rem < cnt) {
-            const int chunk = rem / npair, pr = rem % npair;
-            int r = 0, acc = 0;
-            while (acc + (p.R - r) <= pr) {
-                acc += p.R - r;
-                ++r;
-            }
-            const int q = r + (pr - acc);
-            const int64_t i0 = (int64_t)chunk * p.chunk_rows;
-            const int64_t i1 = min(p.dims[n], i0 + p.chunk_rows);
-            const double* a = p.fac[n] + (int64_t)r * p.dims[n];
-            const double* b = p.fac[n] + (int64_t)q * p.dims[n];
-            dd s{0.0, 0.0};
-            for (int64_t i = i0 + lane; i < i1; i += 32) s = dd_fma(s, a[i], b[i]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                dd t{__shfl_xor_sync(0xffffffffu, s.hi, o), __shfl_xor_sync(0xffffffffu, s.lo, o)};
-                s = dd_add(s, t);
-            }
-            if (lane == 0) {
-                dd* dst = p.part + ((size_t)n * p.maxchunks + chunk) * p.R * p.R;
-                dst[r * p.R + q] = s;
-            }
-            return;
+    const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+    // tasks of modes [lo, hi) back to back
+    int total = 0;
+    for (int m = p.mode_lo; m < p.mode_hi; ++m) total += p.nchunk[m] * npair;
+    for (int t = warp; t < total; t += nwarps) {
+        int m = p.mode_lo, tl = t;
+        while (tl >= p.nchunk[m] * npair) {
+            tl -= p.nchunk[m] * npair;
+            ++m;
         }
-        rem -= cnt;
+        gram_task(p.fac[m], p.dims[m], p.rows[m], p.R, tl, p.part + (size_t)p.chunk0[m] * npair);
+    }
+    if (!last_block_arrives(p.counter)) return;
+    for (int m = p.mode_lo; m < p.mode_hi; ++m) gram_zero_pads(p.R, p.RP, p.out + (size_t)m * p.RP * p.RP);
+    for (int f = threadIdx.x; f < (p.mode_hi - p.mode_lo) * npair; f += blockDim.x) {
+        const int m = p.mode_lo + f / npair;
+        gram_combine_pair(p.part + (size_t)p.chunk0[m] * npair, p.nchunk[m], f % npair, p.R, p.RP,
+                          p.out + (size_t)m * p.RP * p.RP);
     }
 }
 
-__global__ void gram_combine_kernel(const GramParams p) {
-    const int n = p.mode0 + blockIdx.x;
-    for (int e = threadIdx.x; e < p.RP * p.RP; e += blockDim.x) {
-        const int r = e / p.RP, q = e % p.RP;
-        double v = 0.0;
-        if (r < p.R && q < p.R) {
-            const int a = min(r, q), b = max(r, q);
-            dd s{0.0, 0.0};
-            for (int c = 0; c < p.chunks[n]; ++c) s = dd_add(s, p.part[((size_t)n * p.maxchunks + c) * p.R * p.R + a * p.R + b]);
-            v = s.hi + s.lo;
-        }
-        p.out[(size_t)n * p.RP * p.RP + e] = v;
-    }
-}
-
-GramParams gram_params(EvalWork& w, const double* u) {
+void launch_gram(EvalWork& w, const double* u, int lo, int hi, cudaStream_t st) {
     GramParams p{};
     p.order = w.order;
     p.R = w.R;
     p.RP = w.RP;
-    p.chunk_rows = 2048;
-    p.maxchunks = 1;
+    p.mode_lo = lo;
+    p.mode_hi = hi;
     for (int n = 0; n < w.order; ++n) {
         p.dims[n] = w.dims[n];
         p.fac[n] = u + w.off[n];
-        p.chunks[n] = w.gram_chunks[n];
-        p.maxchunks = std::max(p.maxchunks, p.chunks[n]);
+        p.nchunk[n] = w.gram_nchunk[n];
+        p.chunk0[n] = w.gram_chunk0[n];
+        p.rows[n] = gram_chunk_rows(w.dims[n]);
     }
     p.part = w.gram_part;
     p.out = w.gram;
-    return p;
+    p.counter = w.counter + kCounterGram;
+    int tasks = 0;
+    for (int n = lo; n < hi; ++n) tasks += w.gram_nchunk[n] * (w.R * (w.R + 1) / 2);
+    const int grid = std::max(1, std::min((tasks + 7) / 8, 4 * sm_count()));
+    gram_kernel<<<grid, 256, 0, st>>>(p);
+    CPFIT_CUDA(cudaGetLastError());
 }
 
 // ---------------------------------------------------------------------------------------
@@ -716,8 +441,13 @@ __global__ void grad_kernel(const GradParams p) {
         if (n == 0) inner += m * p.u[e];
         if (p.need_grad) {
             const double* a = p.u + p.off[n];
+            double av[kMaxRank];  // row i of A_n, loaded before the in-order dot product
+#pragma unroll
+            for (int q = 0; q < kMaxRank; ++q) av[q] = q < p.R ? a[(int64_t)q * In + i] : 0.0;
             double ag = 0.0;
-            for (int q = 0; q < p.R; ++q) ag += a[(int64_t)q * In + i] * gsm[n * RR + q * p.R + r];
+#pragma unroll
+            for (int q = 0; q < kMaxRank; ++q)
+                if (q < p.R) ag += av[q] * gsm[n * RR + q * p.R + r];
             const double gv = -m + ag;
             p.g[e] = gv;
             g2 += gv * gv;
@@ -804,44 +534,55 @@ EvalWork* work_create(const DevTensor& t, int R) {
     }
     w->nu = w->off[t.order];
     const int sms = sm_count();
-    int maxchunks = 1;
+    int chunks = 0;
     for (int n = 0; n < t.order; ++n) {
-        w->gram_chunks[n] = (int)((t.dims[n] + 2047) / 2048);
-        maxchunks = std::max(maxchunks, w->gram_chunks[n]);
+        w->gram_nchunk[n] = gram_chunks(t.dims[n]);
+        w->gram_chunk0[n] = chunks;
+        chunks += w->gram_nchunk[n];
     }
-    CPFIT_CUDA(cudaMalloc(&w->gram_part, sizeof(dd) * (size_t)t.order * maxchunks * R * R));
+    CPFIT_CUDA(cudaMalloc(&w->gram_part, sizeof(dd) * (size_t)chunks * (R * (R + 1) / 2)));
     CPFIT_CUDA(cudaMalloc(&w->gram, sizeof(double) * (size_t)t.order * w->RP * w->RP));
     w->red_grid = sms * 2;
     CPFIT_CUDA(cudaMalloc(&w->red, sizeof(double) * 3 * (size_t)w->red_grid));
-    CPFIT_CUDA(cudaMalloc(&w->counter, sizeof(unsigned int)));
-    CPFIT_CUDA(cudaMemset(w->counter, 0, sizeof(unsigned int)));
+    w->chol_stride = (int64_t)R * R + R + 1;
+    CPFIT_CUDA(cudaMalloc(&w->chol, sizeof(double) * (size_t)t.order * w->chol_stride));
+    CPFIT_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
+    CPFIT_CUDA(cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming));
+    CPFIT_CUDA(cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming));
+    CPFIT_CUDA(cudaMalloc(&w->counter, sizeof(unsigned int) * kCounters));
+    CPFIT_CUDA(cudaMemset(w->counter, 0, sizeof(unsigned int) * kCounters));
     if (!t.sparse) {
         if (t.order < 2) throw std::invalid_argument("device dense path needs order >= 2");
         const int I0 = (int)t.dims[0];
         w->fiber_nchunk = (I0 + 31) / 32;
         if (w->fiber_nchunk > 13) throw std::invalid_argument("device dense path supports I_1 <= 416");
-        w->fiber_smem = fiber_smem(w->RP, w->fiber_nchunk);
+        w->fiber_smem = fiber_smem(w->RP, w->fiber_nchunk, I0);
         if (w->fiber_smem > 227 * 1024) throw std::invalid_argument("fiber tile does not fit shared memory");
         const int64_t ntiles = (t.J + w->fiber_F - 1) / w->fiber_F;
-        const int per_sm = std::max(1, std::min(2048 / (32 * (w->fiber_nchunk + 3)),
+        const int per_sm = std::max(1, std::min(2048 / fiber_threads(w->RP),
                                                 (int)((228 * 1024) / (w->fiber_smem + 1024))));
         w->fiber_grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
         CPFIT_CUDA(cudaMalloc(&w->S, sizeof(double) * (size_t)t.J * w->RP));
         CPFIT_CUDA(cudaMalloc(&w->m0_part, sizeof(double) * (size_t)w->fiber_grid * w->RP * 32 * w->fiber_nchunk));
+        // rows >= 8 ceil(I0 / 8) of the partials are never written: keep them zero
+        CPFIT_CUDA(cudaMemset(w->m0_part, 0, sizeof(double) * (size_t)w->fiber_grid * w->RP * 32 * w->fiber_nchunk));
         CPFIT_CUDA(cudaMalloc(&w->m0, sizeof(double) * (size_t)w->RP * 32 * w->fiber_nchunk));
         CPFIT_CUDA(cudaMalloc(&w->f_part, sizeof(double) * (size_t)w->fiber_grid));
         for (int h = 1; h < t.order - 1; ++h) {
             int64_t Jt = 1;
             for (int m = h + 1; m < t.order; ++m) Jt *= t.dims[m];
-            w->lvl_grid[h] = (int)std::min<int64_t>(Jt, (int64_t)sms);
             const int64_t npairs = t.dims[h] * w->RP;
-            const int64_t bx = (npairs + 255) / 256;
-            const int64_t want = std::max<int64_t>(1, (2 * sms + bx - 1) / bx);
-            w->lvl_chunk[h] = std::max<int64_t>(1, std::min<int64_t>((Jt + want - 1) / want, 6144 / w->RP));
-            const int64_t nch = (Jt + w->lvl_chunk[h] - 1) / w->lvl_chunk[h];
-            CPFIT_CUDA(cudaMalloc(&w->lvl_part[h], sizeof(double) * (size_t)nch * npairs));
+            const int64_t need = (npairs + kLevelThreads - 1) / kLevelThreads;
+            w->lvl_km[h] = need <= 4 ? 4 : need <= 8 ? 8 : need <= 16 ? 16 : 32;
+            w->lvl_ny[h] = (int)((npairs + (int64_t)kLevelThreads * w->lvl_km[h] - 1) / (kLevelThreads * w->lvl_km[h]));
+            const int64_t nx_want = std::max<int64_t>(1, std::min<int64_t>(Jt, (sms + w->lvl_ny[h] - 1) / w->lvl_ny[h]));
+            w->lvl_spc[h] = (Jt + nx_want - 1) / nx_want;
+            w->lvl_nx[h] = (int)((Jt + w->lvl_spc[h] - 1) / w->lvl_spc[h]);
+            CPFIT_CUDA(cudaMalloc(&w->lvl_part[h], sizeof(double) * (size_t)w->lvl_nx[h] * npairs));
             CPFIT_CUDA(cudaMalloc(&w->lvl_m[h], sizeof(double) * (size_t)npairs));
             CPFIT_CUDA(cudaMalloc(&w->lvl_S[h], sizeof(double) * (size_t)Jt * w->RP));
+            if (w->lvl_ny[h] > 1)
+                CPFIT_CUDA(cudaMalloc(&w->lvl_spart[h], sizeof(double) * (size_t)w->lvl_ny[h] * Jt * w->RP));
         }
     } else {
         int64_t tot = 0;
@@ -865,35 +606,23 @@ void work_destroy(EvalWork* w) {
     cudaFree(w->sp_part);
     cudaFree(w->frows);
     cudaFree(w->counter);
+    cudaFree(w->chol);
+    if (w->ev_fork) cudaEventDestroy(w->ev_fork);
+    if (w->ev_join) cudaEventDestroy(w->ev_join);
+    if (w->side) cudaStreamDestroy(w->side);
     for (int h = 0; h < kMaxOrder; ++h) {
         cudaFree(w->lvl_part[h]);
         cudaFree(w->lvl_m[h]);
         cudaFree(w->lvl_S[h]);
+        cudaFree(w->lvl_spart[h]);
     }
     delete w;
 }
 
-void grams_device(EvalWork& w, const double* u, cudaStream_t st) {
-    GramParams p = gram_params(w, u);
-    const int npair = w.R * (w.R + 1) / 2;
-    int warps = 0;
-    for (int n = 0; n < w.order; ++n) warps += w.gram_chunks[n] * npair;
-    gram_partial_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(p);
-    gram_combine_kernel<<<w.order, 256, 0, st>>>(p);
-    CPFIT_CUDA(cudaGetLastError());
-}
+void grams_device(EvalWork& w, const double* u, cudaStream_t st) { launch_gram(w, u, 0, w.order, st); }
 
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st) {
-    GramParams p = gram_params(w, u);
-    const int npair = w.R * (w.R + 1) / 2;
-    // restrict to one mode by zeroing the other chunk counts and offsetting pointers
-    GramParams q = p;
-    for (int n = 0; n < w.order; ++n) q.chunks[n] = (n == mode) ? p.chunks[n] : 0;
-    const int warps = p.chunks[mode] * npair;
-    q.mode0 = mode;
-    gram_partial_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(q);
-    gram_combine_kernel<<<1, 256, 0, st>>>(q);
-    CPFIT_CUDA(cudaGetLastError());
+    launch_gram(w, u, mode, mode + 1, st);
 }
 
 namespace {
@@ -933,7 +662,7 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
     p.norm_sq = t.norm_sq;
     p.sc = sc;
     p.has_d = d ? 1 : 0;
-    p.counter = w.counter;
+    p.counter = w.counter + kCounterGrad;
     // enough blocks to cover n_u once (latency-bound epilogue, no grid-stride tail)
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(w.red_grid, (w.nu + 255) / 256));
     grad_kernel<<<blocks, 256, sizeof(double) * t.order * w.R * w.R, st>>>(p);

@@ -13,6 +13,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "gram.cuh"
 
 #include <vector>
 
@@ -34,10 +35,18 @@ struct DevTensor {
     struct SparseModes* modes = nullptr;
 };
 
+int sm_count();  // SMs of the current device (cached)
+// fiber-pass barrier-wait counters (filled only by a -DCPFIT_FIBER_PROF build)
+constexpr int kFiberProfSlots = 12;
+unsigned long long* fiber_prof_buffer();
+
 DevTensor* tensor_create_dense(int order, const int64_t* dims, const double* host_vals, cudaStream_t st);
 DevTensor* tensor_create_coo(int order, const int64_t* dims, int64_t nnz, const int64_t* coords_aos,
                              const double* vals, cudaStream_t st);
 void tensor_destroy(DevTensor* t);
+
+// last-block-done counters (one per kernel family; each resets its own after use)
+constexpr int kCounterGrad = 0, kCounterGram = 1, kCounterSolve = 2, kCounters = 4;
 
 // Scratch for one evaluation context (sized from tensor + rank).
 struct EvalWork {
@@ -54,15 +63,16 @@ struct EvalWork {
     double* f_part = nullptr;   // fiber_grid (+ sparse/other scalars)
     double* m0 = nullptr;       // reduced M0 [RP][32*nchunk]
     // level contractions (modes 1..N-2 heads)
-    int lvl_grid[kMaxOrder] = {};
-    int64_t lvl_chunk[kMaxOrder] = {};  // slabs per M_h chunk
-    double* lvl_part[kMaxOrder] = {};  // M_h chunk partials (chunks x I_h x RP)
+    int lvl_nx[kMaxOrder] = {}, lvl_ny[kMaxOrder] = {}, lvl_km[kMaxOrder] = {};  // grid, pairs/thread
+    int64_t lvl_spc[kMaxOrder] = {};   // slabs per CTA
+    double* lvl_part[kMaxOrder] = {};  // M_h partials (nx x I_h x RP)
+    double* lvl_spart[kMaxOrder] = {}; // Sout partials over pair chunks (ny x Jt x RP; ny > 1 only)
     double* lvl_m[kMaxOrder] = {};     // reduced M_h [i][r]
     double* lvl_S[kMaxOrder] = {};     // S_{h} outputs (slabs x RP)
-    unsigned int* counter = nullptr;   // last-block-done counter of the gradient epilogue
-    // Grams
-    int gram_chunks[kMaxOrder] = {};
-    dd* gram_part = nullptr;    // [mode][chunk][R*R]
+    unsigned int* counter = nullptr;   // last-block-done counters [kCounters]
+    // Grams (gram.cuh): per-mode row chunks, dd partials [global chunk][R(R+1)/2]
+    int gram_nchunk[kMaxOrder] = {}, gram_chunk0[kMaxOrder] = {};
+    dd* gram_part = nullptr;
     double* gram = nullptr;     // [mode][RP*RP] (rounded from dd; padded entries 0)
     // sparse
     double* sp_part = nullptr;  // per-mode outputs I_n x RP
@@ -70,6 +80,12 @@ struct EvalWork {
     // reductions
     double* red = nullptr;      // per-CTA partials for norms/dots
     int red_grid = 0;
+    // ALS: Cholesky factors of Gamma_n per mode (als.cu chol_kernel) and the side stream the
+    // factorisations run on, overlapping the streaming passes
+    double* chol = nullptr;
+    int64_t chol_stride = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 EvalWork* work_create(const DevTensor& t, int R);

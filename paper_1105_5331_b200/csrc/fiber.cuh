@@ -1,48 +1,70 @@
 // Warp-specialized fiber pass (included by dense.cu inside cpfit_gpu::(anonymous)).
 //
-// One CTA per SM streams a contiguous range of F-fiber tiles of T (mode-0 fibers, padded to
-// ldT doubles) through a kFStages-deep shared-memory ring. Roles:
-//   warp 0                 producer: one bulk async copy per fiber into the ring (mbarrier
-//                          complete_tx), and the W tile (Khatri-Rao rows of modes >= 1,
-//                          never materialised in HBM) into a double-buffered smem tile — the
-//                          factor gathers are independent and issued back to back, and run
-//                          ahead of the consumers instead of on their critical path;
-//   warps 1 .. NC          compute: each owns 32 rows i of the fiber; per tile it runs
-//                            S^T partial (F x RP)  = T(rows, F)^T A0(rows, :)   DMMA m8n8k4
-//                            M0^T      (RP x 32)  += W(F, :)^T T(rows, F)^T     DMMA m8n8k4
-//                          (+ model(rows, F) = A0 W^T and the squared residual in the
-//                          residual-objective mode), with the M0 accumulators held in
-//                          registers for the whole pass;
-//   warps NC+1, NC+2       epilogue: sum the NC per-warp S partials (fixed order), store S,
-//                          and fold the per-fiber objective ||t||^2 - 2 w.s + w^T G0 w
-//                          (G0 w on DMMA, per-fiber sums by lane shuffles).
-// Hand-offs are mbarrier phases only; there is no CTA-wide barrier in the steady state.
-// Shared-memory fragment layouts: T rows padded to I0s = 32 NC + 4 doubles and W rows to
-// RP + 4 doubles (both 4 or 12 mod 16), which makes every DMMA operand load conflict free.
+// One CTA per SM streams a contiguous range of F = 16-fiber tiles of T (mode-0 fibers, padded
+// to ldT doubles) through a kFStages-deep shared-memory ring. Roles:
+//   T producer (warp 0)    one bulk async copy per fiber into the ring, issued by 16 lanes at
+//                          once (mbarrier complete_tx);
+//   W producer (warp 1)    the W tile — Khatri-Rao rows of modes >= 1, never materialised in
+//                          HBM — into a double-buffered smem tile (independent gathers);
+//   S warps                warp s owns 8 x 8 sub-tile(s) (m-tile ft of fibers x r-tile rt) of
+//                            S(F x RP) = T(:, F)^T A0    DMMA m8n8k4 over the FULL fiber length,
+//                          four interleaved accumulator chains, A0 fragments from a shared-memory
+//                          copy of A0 staged once per CTA; then the epilogue of its sub-tile:
+//                          store S, Q = W G0 (DMMA) and the per-fiber objective
+//                          ||t||^2 - 2 w.s + w^T G0 w folded into a per-warp sum;
+//   M0 warps               warp m owns a run of 8-row m-tiles of the fiber:
+//                            M0^T (RP x rows) += W(F, :)^T T(rows, F)^T   DMMA m8n8k4,
+//                          accumulators in registers for the whole pass (+ the squared
+//                          residual against A0 W^T in the residual-objective mode).
+// S needs no cross-warp partial sums, so no scalar fp64 reduction competes with the DMMAs for
+// the fp64 pipe. The M0 m-tiles are spread so each SM scheduler (warp w issues on w % 4) gets
+// the same DMMA work (fiber_schedule). Hand-offs are mbarrier phases only.
+// Shared-memory layouts: T rows padded to I0s = 32 NC + 4 doubles (4 mod 16) and W rows to
+// RP + 4 doubles; A0 rows of RP doubles with the column index XOR-swizzled by (row & 1) * 8 for
+// RP = 16 — every DMMA fragment load is conflict free (two wavefronts per 32 doubles).
 #pragma once
 
 constexpr int kFStages = 3;
-constexpr int kEpiWarps = 2;
-constexpr int kFiberF = 16;  // fibers per tile (2 DMMA m-tiles; one per epilogue warp)
+constexpr int kFiberF = 16;
 
 template <int RP>
 __host__ __device__ constexpr int w_ld() {
     return RP + 4;
 }
 
+// role counts per padded rank
+template <int RP>
+struct FiberRoles {
+    static constexpr int NRT = RP / 8;
+    static constexpr bool SEPW = RP <= 16;                  // W producer in its own warp
+    static constexpr int NQ = 2 * NRT;                      // 8x8 S sub-tiles per tile
+    static constexpr int NS = RP == 32 ? 4 : NQ;            // S warps
+    static constexpr int SPW = NQ / NS;                     // sub-tiles per S warp
+    static constexpr int NM = RP == 32 ? 11 : 8;            // M0 warps
+    static constexpr int MAXMT = RP == 8 ? 14 : (RP == 16 ? 7 : 5);  // m-tiles per M0 warp
+    static constexpr bool A0SMEM = RP <= 16;                // A0 staged in shared memory
+    static constexpr int S0 = 1 + (SEPW ? 1 : 0);           // first S warp
+    static constexpr int M0W = S0 + NS;                     // first M0 warp
+    static constexpr int WARPS = M0W + NM;
+};
+static_assert(FiberRoles<32>::WARPS <= 16 && FiberRoles<16>::WARPS <= 16, "<= 512 threads (128 registers)");
+
 struct FiberSmem {
-    size_t tiles, spart, wbuf, gam, bars, total;
+    size_t tiles, a0, wbuf, gam, bars, total;
 };
 
+// A0 rows staged in shared memory: every row an M0 warp's m-tiles touch (8 ceil(I0 / 8) >= ldT)
+__host__ __device__ inline int64_t a0_rows(int64_t I0) { return (I0 + 7) / 8 * 8; }
+
 template <int RP, int F>
-__host__ __device__ FiberSmem fiber_layout(int nchunk) {
+__host__ __device__ FiberSmem fiber_layout(int nchunk, int64_t I0) {
     const int I0s = 32 * nchunk + 4;
     FiberSmem s{};
     size_t off = 0;
     s.tiles = off;
     off += sizeof(double) * (size_t)kFStages * F * I0s;
-    s.spart = off;
-    off += sizeof(double) * 2 * (size_t)nchunk * F * RP;
+    s.a0 = off;
+    if (FiberRoles<RP>::A0SMEM) off += sizeof(double) * (size_t)a0_rows(I0) * RP;
     s.wbuf = off;
     off += sizeof(double) * 2 * (size_t)F * w_ld<RP>();
     s.gam = off;
@@ -52,6 +74,68 @@ __host__ __device__ FiberSmem fiber_layout(int nchunk) {
     s.total = off;
     return s;
 }
+
+// Spread the ceil(I0 / 8) m-tiles over the M0 warps so the DMMA work per SM scheduler is as even
+// as possible (the S warps' k-steps and the producers count as loads), at most MAXMT per warp.
+template <int RP>
+inline void fiber_schedule_rp(int I0, bool do_s, FiberParams& p) {
+    using Ro = FiberRoles<RP>;
+    const int MT = (I0 + 7) / 8;
+    const int KS = (I0 + 3) / 4;
+    double load[4] = {0.0, 0.0, 0.0, 0.0};
+    load[0] += 2.0;
+    if (Ro::SEPW) load[1] += 2.0;
+    if (do_s)
+        for (int s = 0; s < Ro::NS; ++s) load[(Ro::S0 + s) % 4] += (double)KS * Ro::SPW + 6.0 * Ro::SPW;
+    const double mt_w = 4.0 * Ro::NRT;  // DMMAs per m-tile per tile
+    int cnt[16] = {};
+    for (int t = 0; t < MT; ++t) {
+        int best = -1;
+        for (int m = 0; m < Ro::NM; ++m) {
+            if (cnt[m] >= Ro::MAXMT) continue;
+            if (best < 0 || load[(Ro::M0W + m) % 4] < load[(Ro::M0W + best) % 4] ||
+                (load[(Ro::M0W + m) % 4] == load[(Ro::M0W + best) % 4] && cnt[m] < cnt[best]))
+                best = m;
+        }
+        if (best < 0) throw std::invalid_argument("fiber pass: I_1 too large for the M0 warps");
+        ++cnt[best];
+        load[(Ro::M0W + best) % 4] += mt_w;
+    }
+    int acc = 0;
+    for (int m = 0; m < Ro::NM; ++m) {
+        p.mt_cnt[m] = cnt[m];
+        p.mt_start[m] = acc;
+        acc += cnt[m];
+    }
+}
+inline void fiber_schedule(int RP, int I0, bool do_s, FiberParams& p) {
+    switch (RP) {
+        case 8: fiber_schedule_rp<8>(I0, do_s, p); break;
+        case 16: fiber_schedule_rp<16>(I0, do_s, p); break;
+        default: fiber_schedule_rp<32>(I0, do_s, p); break;
+    }
+}
+inline int fiber_threads(int RP) {
+    switch (RP) {
+        case 8: return 32 * FiberRoles<8>::WARPS;
+        case 16: return 32 * FiberRoles<16>::WARPS;
+        default: return 32 * FiberRoles<32>::WARPS;
+    }
+}
+
+// Diagnostic build (-DCPFIT_FIBER_PROF): cycles each warp role spends in every barrier wait,
+// accumulated into FiberParams::prof[kProfSlots] (tools/fiber_prof.py).
+constexpr int kProfSlots = 12;
+#ifdef CPFIT_FIBER_PROF
+#define FIBER_WAIT(slot, bar, par)                      \
+    do {                                                \
+        const long long t0_ = clock64();                \
+        mbar_wait(bar, par);                            \
+        prof_acc[slot] += clock64() - t0_;              \
+    } while (0)
+#else
+#define FIBER_WAIT(slot, bar, par) mbar_wait(bar, par)
+#endif
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -110,160 +194,242 @@ __device__ __forceinline__ FiberIndex<ORD> advance_fiber(const FiberParams& p, F
     return x;
 }
 
-template <int RP, int F, bool A0REG, int ORD>
-__global__ void __launch_bounds__(512) fiber_ws_kernel(const FiberParams p) {
+// shared-memory A0 position of (i, r): rows of RP doubles, XOR swizzle for RP = 16
+template <int RP>
+__device__ __forceinline__ int a0s_index(int i, int r) {
+    return i * RP + (RP == 16 ? (r ^ ((i & 1) << 3)) : r);
+}
+
+template <int RP, int F, int ORD>
+__global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel(const FiberParams p) {
+    using Ro = FiberRoles<RP>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int NRT = RP / 8;
+    constexpr int NRT = Ro::NRT;
     constexpr int WLD = w_ld<RP>();
-    static_assert(F == 16, "two epilogue warps cover two 8-fiber m-tiles");
-    const FiberSmem L = fiber_layout<RP, F>(p.nchunk);
-    const int NC = p.nchunk;
+    static_assert(F == 16, "two 8-fiber m-tiles per tile");
+    const FiberSmem L = fiber_layout<RP, F>(p.nchunk, p.I0);
     const int I0s = p.I0s;
+    const int KS = (int)(p.ldT / 4);  // k-steps of 4 rows (ldT = I0 rounded up to 4; pad rows are 0)
     double* tiles = reinterpret_cast<double*>(smem_raw + L.tiles);
-    double* spart = reinterpret_cast<double*>(smem_raw + L.spart);  // [2][NC][F][RP]
-    double* wbuf = reinterpret_cast<double*>(smem_raw + L.wbuf);    // [2][F][WLD]
-    double* gam = reinterpret_cast<double*>(smem_raw + L.gam);      // [RP][RP]
+    double* a0s = reinterpret_cast<double*>(smem_raw + L.a0);    // [a0_rows][RP] swizzled
+    double* wbuf = reinterpret_cast<double*>(smem_raw + L.wbuf);  // [2][F][WLD]
+    double* gam = reinterpret_cast<double*>(smem_raw + L.gam);    // [RP][RP]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
-    uint64_t* tfull = bars;        // [kFStages] tx bytes
-    uint64_t* tempty = bars + 3;   // [kFStages] NC arrivals
-    uint64_t* sfull = bars + 6;    // [2] NC
-    uint64_t* sempty = bars + 8;   // [2] kEpiWarps
-    uint64_t* wfull = bars + 10;   // [2] producer
-    uint64_t* wempty = bars + 12;  // [2] NC (+ kEpiWarps for the per-fiber objective)
+    uint64_t* tfull = bars;       // [kFStages] tx bytes
+    uint64_t* tempty = bars + 3;  // [kFStages] T consumers
+    uint64_t* wfull = bars + 6;   // [2] W producer
+    uint64_t* wempty = bars + 8;  // [2] W consumers
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef CPFIT_FIBER_PROF
+    long long prof_acc[kProfSlots] = {};
+    const long long prof_t0 = clock64();
+#endif
     const int64_t t_begin = (int64_t)blockIdx.x * p.tiles_per_cta;
     const int64_t t_end = imin64(p.ntiles, t_begin + p.tiles_per_cta);
     const int64_t ntl = t_end > t_begin ? t_end - t_begin : 0;
     // objective form: residual 1/2 sum (T - model)^2 (kruskal.cpp:83-102) when requested,
-    // else the per-fiber three-term form folded by the epilogue
+    // else the per-fiber three-term form folded by the S warps
     const bool resid = p.do_f && p.resid_flag && *p.resid_flag;
     const bool need_w = p.do_m0 || p.do_f;
-    const bool epi_w = p.do_f && !resid;  // epilogue reads W
+    const bool m0w_on = p.do_m0 || resid;  // M0 warps consume T (and W)
+    const bool epi_w = p.do_f && !resid;   // S warps consume W
+    const bool need_a0 = p.do_s || resid;
     dd racc{0.0, 0.0};
 
     for (int64_t e = tid; e < (int64_t)kFStages * F * I0s; e += blockDim.x) tiles[e] = 0.0;
+    if (Ro::A0SMEM && need_a0)
+        for (int64_t e = tid; e < a0_rows(p.I0) * RP; e += blockDim.x) {
+            const int i = (int)(e / RP), r = (int)(e % RP);
+            a0s[a0s_index<RP>(i, r)] = (i < p.I0 && r < p.R) ? p.A0[(int64_t)r * p.I0 + i] : 0.0;
+        }
     if (p.do_f)
         for (int e = tid; e < RP * RP; e += blockDim.x) gam[e] = p.gamma0[e];
     if (tid == 0) {
+        const int t_cons = (p.do_s ? Ro::NS : 0) + (m0w_on ? Ro::NM : 0);
+        const int w_cons = (m0w_on ? Ro::NM : 0) + (epi_w ? Ro::NS : 0);
         for (int s = 0; s < kFStages; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], NC);
+            mbar_init(&tempty[s], t_cons);
         }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&sfull[b], NC);
-            mbar_init(&sempty[b], kEpiWarps);
             mbar_init(&wfull[b], 1);
-            mbar_init(&wempty[b], NC + (epi_w ? kEpiWarps : 0));
+            mbar_init(&wempty[b], w_cons);
         }
     }
     mbar_fence_init();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
 
+    auto a0_at = [&](int i, int r) -> double {  // fragment operand A0(i, r)
+        if (Ro::A0SMEM) return a0s[a0s_index<RP>(i, r)];
+        return (i < p.I0 && r < p.R) ? __ldg(p.A0 + (int64_t)r * p.I0 + i) : 0.0;
+    };
+
     double facc = 0.0;
-    if (warp == 0) {
-        // ---------------- producer ----------------
-        // W lane mapping: fiber f = lane % F, r-slice h = lane / F (RS = RP / 2 values)
+    // W tile k: lane = (fiber fw, r-slice hw); gathers first (independent), then the buffer
+    auto w_producer = [&](int64_t k, FiberIndex<ORD>& xw, int fw, int hw) {
         constexpr int RS = RP * F / 32;
+        const int b = (int)(k & 1);
+        const int64_t f0 = (t_begin + k) * F;
+        if (k > 0) xw = advance_fiber<ORD>(p, xw, F, f0 + fw);
+        double w[RS];
+#pragma unroll
+        for (int j = 0; j < RS; ++j) {
+            const int r = hw * RS + j;
+            const bool ok = xw.valid && r < p.R;
+            double v = ok ? 1.0 : 0.0;
+#pragma unroll
+            for (int m = 1; m < (ORD > 0 ? ORD : kMaxOrder); ++m)
+                if (ok && mode_active<ORD>(p, m)) v *= __ldg(p.fac[m] + (int64_t)r * p.dims[m] + xw.j[m]);
+            w[j] = v;
+        }
+        if (k >= 2) FIBER_WAIT(1, &wempty[b], (uint32_t)(((k / 2) - 1) & 1));
+        double* wv = wbuf + (size_t)b * F * WLD;
+#pragma unroll
+        for (int j = 0; j < RS; ++j) wv[fw * WLD + hw * RS + j] = w[j];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wfull[b]);
+    };
+
+    if (warp == 0) {
+        // ---------------- T producer (+ W when RP = 32) ----------------
         const int fw = lane % F, hw = lane / F;
-        FiberIndex<ORD> xw = decode_fiber<ORD>(p, t_begin * F + fw);
+        FiberIndex<ORD> xw;
+        if (!Ro::SEPW && need_w) xw = decode_fiber<ORD>(p, t_begin * F + fw);
         for (int64_t k = 0; k < ntl; ++k) {
-            const int64_t t = t_begin + k;
             const int s = (int)(k % kFStages);
-            const int64_t f0 = t * F;
-            if (k >= kFStages) mbar_wait(&tempty[s], (uint32_t)(((k / kFStages) - 1) & 1));
+            const int64_t f0 = (t_begin + k) * F;
+            if (k >= kFStages) FIBER_WAIT(0, &tempty[s], (uint32_t)(((k / kFStages) - 1) & 1));
             const int nvalid = (int)imin64(F, p.J - f0);
             double* st = tiles + (size_t)s * F * I0s;
             if (nvalid < F)
                 for (int e = lane; e < (F - nvalid) * I0s; e += 32) st[(size_t)nvalid * I0s + e] = 0.0;
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
-                for (int f = 0; f < nvalid; ++f)
-                    bulk_g2s(st + (size_t)f * I0s, p.T + (f0 + f) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s]);
-            }
-            if (need_w) {
+            if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
+            __syncwarp();
+            if (lane < nvalid)
+                bulk_g2s(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s]);
+            if (!Ro::SEPW && need_w) w_producer(k, xw, fw, hw);
+        }
+    } else if (Ro::SEPW && warp == 1) {
+        // ---------------- W producer ----------------
+        if (need_w) {
+            const int fw = lane % F, hw = lane / F;
+            FiberIndex<ORD> xw = decode_fiber<ORD>(p, t_begin * F + fw);
+            for (int64_t k = 0; k < ntl; ++k) w_producer(k, xw, fw, hw);
+        }
+    } else if (warp < Ro::M0W) {
+        // ---------------- S warps ----------------
+        if (p.do_s) {
+            const int sw = warp - Ro::S0;
+            for (int64_t k = 0; k < ntl; ++k) {
+                const int s = (int)(k % kFStages);
                 const int b = (int)(k & 1);
-                if (k > 0) xw = advance_fiber<ORD>(p, xw, F, f0 + fw);
-                // gathers first (independent), then wait for the buffer
-                double w[RS];
+                const int64_t f0 = (t_begin + k) * F;
+                double fn[Ro::SPW];  // ||t_f||^2 of this lane's fiber, prefetched (r-tile 0 only)
 #pragma unroll
-                for (int j = 0; j < RS; ++j) {
-                    const int r = hw * RS + j;
-                    const bool ok = xw.valid && r < p.R;
-                    double v = ok ? 1.0 : 0.0;
-#pragma unroll
-                    for (int m = 1; m < (ORD > 0 ? ORD : kMaxOrder); ++m)
-                        if (ok && mode_active<ORD>(p, m)) v *= __ldg(p.fac[m] + (int64_t)r * p.dims[m] + xw.j[m]);
-                    w[j] = v;
+                for (int j = 0; j < Ro::SPW; ++j) {
+                    const int q = sw * Ro::SPW + j, ft = q / NRT, nt = q % NRT;
+                    const int64_t f = f0 + ft * 8 + (lane >> 2);
+                    fn[j] = (epi_w && nt == 0 && f < p.J) ? p.fnorm2[f] : 0.0;
                 }
-                if (k >= 2) mbar_wait(&wempty[b], (uint32_t)(((k / 2) - 1) & 1));
-                double* wv = wbuf + (size_t)b * F * WLD;
+                FIBER_WAIT(2, &tfull[s], (uint32_t)((k / kFStages) & 1));
+                const double* tt = tiles + (size_t)s * F * I0s;
+                double sv[Ro::SPW][2];
 #pragma unroll
-                for (int j = 0; j < RS; ++j) wv[fw * WLD + hw * RS + j] = w[j];
+                for (int j = 0; j < Ro::SPW; ++j) {
+                    const int q = sw * Ro::SPW + j, ft = q / NRT, nt = q % NRT;
+                    const double* ta = tt + (ft * 8 + (lane >> 2)) * I0s + (lane & 3);
+                    const int rr = nt * 8 + (lane >> 2);
+                    // eight interleaved accumulator chains over the k-steps; each group's 16
+                    // fragment loads issue before its 8 DMMAs
+                    constexpr int U = 8;
+                    double acc[U][2];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) acc[u][0] = acc[u][1] = 0.0;
+                    int ks = 0;
+                    for (; ks + U <= KS; ks += U) {
+                        double a[U], bb[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            a[u] = ta[(ks + u) * 4];
+                            bb[u] = a0_at((ks + u) * 4 + (lane & 3), rr);
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) dmma_8x8x4(acc[u][0], acc[u][1], a[u], bb[u]);
+                    }
+                    {
+                        double a[U - 1], bb[U - 1];
+#pragma unroll
+                        for (int u = 0; u < U - 1; ++u) {
+                            a[u] = ks + u < KS ? ta[(ks + u) * 4] : 0.0;
+                            bb[u] = ks + u < KS ? a0_at((ks + u) * 4 + (lane & 3), rr) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U - 1; ++u)
+                            if (ks + u < KS) dmma_8x8x4(acc[u][0], acc[u][1], a[u], bb[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        acc[u][0] += acc[u + 4][0];
+                        acc[u][1] += acc[u + 4][1];
+                    }
+                    sv[j][0] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+                    sv[j][1] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+                }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&wfull[b]);
+                if (lane == 0) mbar_arrive(&tempty[s]);
+                // epilogue of the sub-tile(s): lane holds D fragment items f = 8 ft + lane/4,
+                // r = 8 nt + 2 (lane%4) + {0, 1}
+                if (epi_w) FIBER_WAIT(6, &wfull[b], (uint32_t)((k / 2) & 1));
+                const double* wv = wbuf + (size_t)b * F * WLD;
+#pragma unroll
+                for (int j = 0; j < Ro::SPW; ++j) {
+                    const int q = sw * Ro::SPW + j, ft = q / NRT, nt = q % NRT;
+                    const int fl = ft * 8 + (lane >> 2);
+                    const int r = nt * 8 + 2 * (lane & 3);
+                    if (f0 + fl < p.J)
+                        *reinterpret_cast<double2*>(p.S_out + (f0 + fl) * RP + r) = make_double2(sv[j][0], sv[j][1]);
+                    if (epi_w) {
+                        // Q = W G0 for this r-tile (DMMA over k = r')
+                        double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+                        for (int kr = 0; kr < RP / 4; ++kr) {
+                            const double gb = gam[(kr * 4 + (lane & 3)) * RP + nt * 8 + (lane >> 2)];
+                            dmma_8x8x4(q0, q1, wv[fl * WLD + kr * 4 + (lane & 3)], gb);
+                        }
+                        const double2 wd = *reinterpret_cast<const double2*>(wv + fl * WLD + r);
+                        double term = wd.x * (q0 - 2.0 * sv[j][0]) + wd.y * (q1 - 2.0 * sv[j][1]);
+                        term += __shfl_xor_sync(0xffffffffu, term, 1);
+                        term += __shfl_xor_sync(0xffffffffu, term, 2);
+                        if ((lane & 3) == 0 && f0 + fl < p.J) facc += fn[j] + term;
+                    }
+                }
+                if (epi_w) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&wempty[b]);
+                }
             }
         }
-    } else if (warp <= NC) {
-        // ---------------- compute ----------------
-        const int c = warp - 1;
-        double a0f[A0REG ? 8 : 1][A0REG ? NRT : 1];
-        auto a0_at = [&](int ks, int rt) -> double {
-            const int i = c * 32 + ks * 4 + (lane & 3);
-            const int r = rt * 8 + (lane >> 2);
-            return (i < p.I0 && r < p.R) ? __ldg(p.A0 + (int64_t)r * p.I0 + i) : 0.0;
-        };
-        if (A0REG && p.do_s) {
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-                for (int rt = 0; rt < NRT; ++rt) a0f[ks][rt] = a0_at(ks, rt);
-        }
-        double macc[NRT][4][2];
+    } else {
+        // ---------------- M0 warps ----------------
+        // rows [rb, rb + 8 cnt) of the fiber (cnt <= MAXMT m-tiles)
+        const int m = warp - Ro::M0W;
+        const int cnt = p.mt_cnt[m];
+        const int rb = 8 * p.mt_start[m];
+        double macc[NRT][Ro::MAXMT][2];
 #pragma unroll
         for (int rt = 0; rt < NRT; ++rt)
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) macc[rt][nt][0] = macc[rt][nt][1] = 0.0;
-        for (int64_t k = 0; k < ntl; ++k) {
-            const int s = (int)(k % kFStages);
-            const int b = (int)(k & 1);
-            mbar_wait(&tfull[s], (uint32_t)((k / kFStages) & 1));
-            const double* tt = tiles + (size_t)s * F * I0s;
-            if (p.do_s) {
-                double sacc[F / 8][NRT][2];
-#pragma unroll
-                for (int ft = 0; ft < F / 8; ++ft)
-#pragma unroll
-                    for (int rt = 0; rt < NRT; ++rt) sacc[ft][rt][0] = sacc[ft][rt][1] = 0.0;
-#pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    const int i = c * 32 + ks * 4 + (lane & 3);
-                    double a[F / 8];
-#pragma unroll
-                    for (int ft = 0; ft < F / 8; ++ft) a[ft] = tt[(ft * 8 + (lane >> 2)) * I0s + i];
-#pragma unroll
-                    for (int rt = 0; rt < NRT; ++rt) {
-                        const double bb = A0REG ? a0f[A0REG ? ks : 0][A0REG ? rt : 0] : a0_at(ks, rt);
-#pragma unroll
-                        for (int ft = 0; ft < F / 8; ++ft) dmma_8x8x4(sacc[ft][rt][0], sacc[ft][rt][1], a[ft], bb);
-                    }
-                }
-                if (k >= 2) mbar_wait(&sempty[b], (uint32_t)(((k / 2) - 1) & 1));
-                double* sp = spart + ((size_t)b * NC + c) * F * RP;
-#pragma unroll
-                for (int ft = 0; ft < F / 8; ++ft)
-#pragma unroll
-                    for (int rt = 0; rt < NRT; ++rt) {
-                        const int f = ft * 8 + (lane >> 2), r = rt * 8 + 2 * (lane & 3);
-                        *reinterpret_cast<double2*>(sp + f * RP + r) = make_double2(sacc[ft][rt][0], sacc[ft][rt][1]);
-                    }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sfull[b]);
-            }
-            if (need_w) {
-                mbar_wait(&wfull[b], (uint32_t)((k / 2) & 1));
+            for (int nt = 0; nt < Ro::MAXMT; ++nt) macc[rt][nt][0] = macc[rt][nt][1] = 0.0;
+        if (m0w_on) {
+            for (int64_t k = 0; k < ntl; ++k) {
+                const int s = (int)(k % kFStages);
+                const int b = (int)(k & 1);
+                FIBER_WAIT(3, &tfull[s], (uint32_t)((k / kFStages) & 1));
+                FIBER_WAIT(4, &wfull[b], (uint32_t)((k / 2) & 1));
+                const double* tt = tiles + (size_t)s * F * I0s;
                 const double* wv = wbuf + (size_t)b * F * WLD;
                 if (p.do_m0) {
 #pragma unroll
@@ -273,108 +439,75 @@ __global__ void __launch_bounds__(512) fiber_ws_kernel(const FiberParams p) {
 #pragma unroll
                         for (int rt = 0; rt < NRT; ++rt) wa[rt] = wv[f * WLD + rt * 8 + (lane >> 2)];
 #pragma unroll
-                        for (int nt = 0; nt < 4; ++nt) {
-                            const double bb = tt[f * I0s + c * 32 + nt * 8 + (lane >> 2)];
+                        for (int nt = 0; nt < Ro::MAXMT; ++nt) {
+                            if (nt < cnt) {
+                                const double bb = tt[f * I0s + rb + nt * 8 + (lane >> 2)];
 #pragma unroll
-                            for (int rt = 0; rt < NRT; ++rt) dmma_8x8x4(macc[rt][nt][0], macc[rt][nt][1], wa[rt], bb);
+                                for (int rt = 0; rt < NRT; ++rt)
+                                    dmma_8x8x4(macc[rt][nt][0], macc[rt][nt][1], wa[rt], bb);
+                            }
                         }
                     }
                 }
                 if (resid) {
-                    // model(i, f) = sum_r A0(i, r) W(f, r) for this warp's 32 rows on DMMA,
-                    // then the squared residual against the tile (padding is 0 - 0)
+                    // model(i, f) = sum_r A0(i, r) W(f, r) for this warp's rows on DMMA, then the
+                    // squared residual against the tile (padding is 0 - 0)
                     double tsum = 0.0;
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) {
-                        const int i = c * 32 + mt * 8 + (lane >> 2);
-                        double a0r[RP / 4];
+                    for (int mt = 0; mt < Ro::MAXMT; ++mt) {
+                        if (mt < cnt) {
+                            const int i = rb + mt * 8 + (lane >> 2);
+                            double a0r[RP / 4];
 #pragma unroll
-                        for (int kr = 0; kr < RP / 4; ++kr) {
-                            const int r = kr * 4 + (lane & 3);
-                            a0r[kr] = (i < p.I0 && r < p.R) ? __ldg(p.A0 + (int64_t)r * p.I0 + i) : 0.0;
-                        }
+                            for (int kr = 0; kr < RP / 4; ++kr) a0r[kr] = a0_at(i, kr * 4 + (lane & 3));
 #pragma unroll
-                        for (int nt = 0; nt < F / 8; ++nt) {
-                            double d0 = 0.0, d1 = 0.0;
+                            for (int nt = 0; nt < F / 8; ++nt) {
+                                double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-                            for (int kr = 0; kr < RP / 4; ++kr)
-                                dmma_8x8x4(d0, d1, a0r[kr], wv[(nt * 8 + (lane >> 2)) * WLD + kr * 4 + (lane & 3)]);
-                            const int f = nt * 8 + 2 * (lane & 3);
-                            const double r0 = tt[f * I0s + i] - d0;
-                            const double r1 = tt[(f + 1) * I0s + i] - d1;
-                            tsum += r0 * r0 + r1 * r1;
+                                for (int kr = 0; kr < RP / 4; ++kr)
+                                    dmma_8x8x4(d0, d1, a0r[kr], wv[(nt * 8 + (lane >> 2)) * WLD + kr * 4 + (lane & 3)]);
+                                const int f = nt * 8 + 2 * (lane & 3);
+                                const double r0 = tt[f * I0s + i] - d0;
+                                const double r1 = tt[(f + 1) * I0s + i] - d1;
+                                tsum += r0 * r0 + r1 * r1;
+                            }
                         }
                     }
                     racc = dd_add(racc, dd{tsum, 0.0});
                 }
-            }
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&tempty[s]);
-                if (need_w) mbar_arrive(&wempty[b]);
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&tempty[s]);
+                    mbar_arrive(&wempty[b]);
+                }
             }
         }
         if (p.do_m0) {
-            const int ld = 32 * NC;
+            const int ld = 32 * p.nchunk;
             double* out = p.m0_part + (size_t)blockIdx.x * RP * ld;
 #pragma unroll
             for (int rt = 0; rt < NRT; ++rt)
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                    const int r = rt * 8 + (lane >> 2);
-                    const int i = c * 32 + nt * 8 + 2 * (lane & 3);
-                    *reinterpret_cast<double2*>(out + (size_t)r * ld + i) =
-                        make_double2(macc[rt][nt][0], macc[rt][nt][1]);
-                }
-        }
-    } else if (p.do_s) {
-        // ---------------- epilogue ----------------
-        // warp ew owns fibers m0 = 8 ew .. 8 ew + 7; lane holds the (f, r) items of a DMMA
-        // D fragment: f = m0 + lane/4, r = 8 nt + 2 (lane%4) + {0, 1}
-        const int m0 = (warp - NC - 1) * 8;
-        const int fl = m0 + (lane >> 2);
-        for (int64_t k = 0; k < ntl; ++k) {
-            const int b = (int)(k & 1);
-            const int64_t f0 = (t_begin + k) * F;
-            mbar_wait(&sfull[b], (uint32_t)((k / 2) & 1));
-            if (epi_w) mbar_wait(&wfull[b], (uint32_t)((k / 2) & 1));
-            const double* sp = spart + (size_t)b * NC * F * RP;
-            const double* wv = wbuf + (size_t)b * F * WLD;
-            double term = 0.0;
-#pragma unroll
-            for (int nt = 0; nt < NRT; ++nt) {
-                const int r = nt * 8 + 2 * (lane & 3);
-                double2 sv = make_double2(0.0, 0.0);
-                for (int ww = 0; ww < NC; ++ww) {
-                    const double2 v = *reinterpret_cast<const double2*>(sp + ((size_t)ww * F + fl) * RP + r);
-                    sv.x += v.x;
-                    sv.y += v.y;
-                }
-                if (f0 + fl < p.J) *reinterpret_cast<double2*>(p.S_out + (f0 + fl) * RP + r) = sv;
-                if (epi_w) {
-                    // Q = W G0 for this n-tile (DMMA over k = r')
-                    double q0 = 0.0, q1 = 0.0;
-#pragma unroll
-                    for (int ks = 0; ks < RP / 4; ++ks) {
-                        const double gb = gam[(ks * 4 + (lane & 3)) * RP + nt * 8 + (lane >> 2)];
-                        dmma_8x8x4(q0, q1, wv[fl * WLD + ks * 4 + (lane & 3)], gb);
+                for (int nt = 0; nt < Ro::MAXMT; ++nt) {
+                    if (nt < cnt) {
+                        const int r = rt * 8 + (lane >> 2);
+                        const int i = rb + nt * 8 + 2 * (lane & 3);
+                        *reinterpret_cast<double2*>(out + (size_t)r * ld + i) =
+                            make_double2(macc[rt][nt][0], macc[rt][nt][1]);
                     }
-                    const double2 wd = *reinterpret_cast<const double2*>(wv + fl * WLD + r);
-                    term += wd.x * (q0 - 2.0 * sv.x) + wd.y * (q1 - 2.0 * sv.y);
                 }
-            }
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&sempty[b]);
-                if (epi_w) mbar_arrive(&wempty[b]);
-            }
-            if (epi_w) {
-                term += __shfl_xor_sync(0xffffffffu, term, 1);
-                term += __shfl_xor_sync(0xffffffffu, term, 2);
-                if ((lane & 3) == 0 && f0 + fl < p.J) facc += p.fnorm2[f0 + fl] + term;
-            }
         }
     }
+#ifdef CPFIT_FIBER_PROF
+    {
+        // slot 7/8/9: producer / S-warp / M0-warp lifetime
+        const int role = warp < Ro::S0 ? 7 : (warp < Ro::M0W ? 8 : 9);
+        prof_acc[role] = clock64() - prof_t0;
+        if (lane == 0 && p.prof)
+            for (int q = 0; q < kProfSlots; ++q)
+                if (prof_acc[q]) atomicAdd(p.prof + q, (unsigned long long)prof_acc[q]);
+    }
+#endif
     if (resid) facc = racc.hi + racc.lo;
     if (p.do_f) {
         __shared__ double red[32];
@@ -390,28 +523,27 @@ __global__ void __launch_bounds__(512) fiber_ws_kernel(const FiberParams p) {
 }
 
 template <int RP, int ORD>
-void launch_fiber_ord(const FiberParams& p, int grid, int threads, size_t smem, cudaStream_t st) {
-    auto k = fiber_ws_kernel<RP, kFiberF, (RP <= 16), ORD>;
+void launch_fiber_ord(const FiberParams& p, int grid, size_t smem, cudaStream_t st) {
+    auto k = fiber_ws_kernel<RP, kFiberF, ORD>;
     CPFIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, threads, smem, st>>>(p);
+    k<<<grid, 32 * FiberRoles<RP>::WARPS, smem, st>>>(p);
 }
 
 template <int RP>
-void launch_fiber(const FiberParams& p, int grid, int nchunk, size_t smem, cudaStream_t st) {
-    const int threads = 32 * (1 + nchunk + (p.do_s ? kEpiWarps : 0));
+void launch_fiber(const FiberParams& p, int grid, size_t smem, cudaStream_t st) {
     switch (p.order) {
-        case 2: launch_fiber_ord<RP, 2>(p, grid, threads, smem, st); break;
-        case 3: launch_fiber_ord<RP, 3>(p, grid, threads, smem, st); break;
-        case 4: launch_fiber_ord<RP, 4>(p, grid, threads, smem, st); break;
-        default: launch_fiber_ord<RP, 0>(p, grid, threads, smem, st); break;
+        case 2: launch_fiber_ord<RP, 2>(p, grid, smem, st); break;
+        case 3: launch_fiber_ord<RP, 3>(p, grid, smem, st); break;
+        case 4: launch_fiber_ord<RP, 4>(p, grid, smem, st); break;
+        default: launch_fiber_ord<RP, 0>(p, grid, smem, st); break;
     }
     CPFIT_CUDA(cudaGetLastError());
 }
 
-size_t fiber_smem(int RP, int nchunk) {
+size_t fiber_smem(int RP, int nchunk, int64_t I0) {
     switch (RP) {
-        case 8: return fiber_layout<8, kFiberF>(nchunk).total;
-        case 16: return fiber_layout<16, kFiberF>(nchunk).total;
-        default: return fiber_layout<32, kFiberF>(nchunk).total;
+        case 8: return fiber_layout<8, kFiberF>(nchunk, I0).total;
+        case 16: return fiber_layout<16, kFiberF>(nchunk, I0).total;
+        default: return fiber_layout<32, kFiberF>(nchunk, I0).total;
     }
 }

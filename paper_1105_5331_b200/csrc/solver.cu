@@ -14,6 +14,7 @@
 #include "solver.cuh"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <vector>
@@ -307,6 +308,16 @@ __global__ void k_seed_window(const double* u, const double* g, double* wu, doub
     }
 }
 
+// phase profiler: time since the previous stamp is charged to `phase`
+__global__ void k_stamp(unsigned long long* ph, int phase) {
+    const unsigned long long t = globaltimer();
+    if (phase >= 0) {
+        ph[phase] += t - ph[2 * Solver::kPhases];
+        ph[Solver::kPhases + phase] += 1;
+    }
+    ph[2 * Solver::kPhases] = t;
+}
+
 int vec_blocks(int64_t n) { return (int)std::min<int64_t>(592, (n + 255) / 256); }
 
 // Conditional handle owned by the graph currently being captured on `st`.
@@ -401,6 +412,10 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     CPFIT_CUDA(cudaMemset(sc_, 0, sizeof(EvalScalars) * 4));
     CPFIT_CUDA(cudaMalloc(&state_, sizeof(DevState)));
     CPFIT_CUDA(cudaMemset(state_, 0, sizeof(DevState)));
+    if (const char* e = std::getenv("CPFIT_PHASE_PROFILE"); e && e[0] == '1') {
+        CPFIT_CUDA(cudaMalloc(&phase_, sizeof(unsigned long long) * (2 * kPhases + 1)));
+        CPFIT_CUDA(cudaMemset(phase_, 0, sizeof(unsigned long long) * (2 * kPhases + 1)));
+    }
     trace_cap_ = o.max_iters + 1;
     CPFIT_CUDA(cudaMalloc(&trace_, sizeof(TraceRow) * (size_t)trace_cap_));
     build_graphs();
@@ -416,6 +431,7 @@ Solver::~Solver() {
         cudaFree(p);
     cudaFree(sc_);
     cudaFree(state_);
+    if (phase_) cudaFree(phase_);
     cudaFree(trace_);
     accel_destroy(a_);
     work_destroy(w_);
@@ -449,6 +465,11 @@ void Solver::build_graphs() {
     c.als_mode = (method_ == 1);
     int* status = &s->status;
     const int vb = vec_blocks(n_);
+    // phases: 0 ALS sweep, 1 eval(u_bar), 2 accelerate + LS init, 3 LS trial eval, 4 LS update,
+    // 5 accepted-step body, 6 commit, 7 loop turnaround (graph WHILE re-entry)
+    auto stamp = [&](cudaStream_t sx, int phase) {
+        if (phase_) k_stamp<<<1, 1, 0, sx>>>(phase_, phase);
+    };
 
     // ---- init graph: canonical(u0), eval, seed window -----------------------------------
     CPFIT_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
@@ -471,27 +492,34 @@ void Solver::build_graphs() {
     CPFIT_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
     const cudaGraphConditionalHandle loop_h = make_handle(st_);
     k_set_cond_running<<<1, 1, 0, st_>>>(c, loop_h);
+    stamp(st_, -1);
     cudaGraph_t body = append_conditional(st_, loop_h, cudaGraphCondTypeWhile);
     CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st2_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    stamp(st2_, 7);
     cudaGraph_t lsb = nullptr, ab = nullptr;
     if (method_ == 0) {
         // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
         als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_, m0_cur_);
+        stamp(st2_, 0);
         eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_, true, &s->resid);
         if (m0_bar_)
             CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st2_));
         k_after_bar<<<1, 1, 0, st2_>>>(c);
+        stamp(st2_, 1);
         // Step II: windowed recombination -> d, slope                        (ngmres.cpp:97-101)
         accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st2_);
         // Step III: restart test / Moré–Thuente line search                 (ngmres.cpp:111-147)
         const cudaGraphConditionalHandle ls_h = make_handle(st2_);
         k_ls_init<<<1, 1, 0, st2_>>>(c, ls_h);
+        stamp(st2_, 2);
         lsb = append_conditional(st2_, ls_h, cudaGraphCondTypeWhile);
         CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         k_trial<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
         eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st3_, true, &s->resid);
+        stamp(st3_, 3);
         k_ls_update<<<1, 1, 0, st3_>>>(c, ls_h);
         if (!opt_.reeval_accepted) k_keep_best<<<vb, 256, 0, st3_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
+        stamp(st3_, 4);
         CPFIT_CUDA(cudaGetLastError());
         CPFIT_CUDA(cudaStreamEndCapture(st3_, &lsb));
         // accepted step: canonicalize u_bar + beta d and re-evaluate        (ngmres.cpp:137-142)
@@ -516,6 +544,7 @@ void Solver::build_graphs() {
             const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st3_, m0_sel_, m0_cur_);
             k_after_rescale<<<1, 1, 0, st3_>>>(c, sc_next, red_, nb);
         }
+        stamp(st3_, 5);
         CPFIT_CUDA(cudaGetLastError());
         CPFIT_CUDA(cudaStreamEndCapture(st3_, &ab));
     } else {
@@ -527,6 +556,7 @@ void Solver::build_graphs() {
     k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
     k_commit_vec<<<vb, 256, 0, st2_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,
                                         m0_cur_, m0_n_);
+    stamp(st2_, 6);
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaStreamEndCapture(st2_, &body));
     CPFIT_CUDA(cudaStreamEndCapture(st_, &g_loop_));
@@ -565,6 +595,18 @@ void Solver::run_loop(int max_iters_total) {
     CPFIT_CUDA(cudaMemcpyAsync(&s->max_iters, &host_max_, sizeof(int), cudaMemcpyHostToDevice, st_));
     CPFIT_CUDA(cudaGraphLaunch(x_loop_, st_));
     ++loop_launches_;
+}
+
+bool Solver::phase_times(double* out, int64_t* cnt) {
+    if (!phase_) return false;
+    unsigned long long h[2 * kPhases + 1];
+    CPFIT_CUDA(cudaMemcpyAsync(h, phase_, sizeof(h), cudaMemcpyDeviceToHost, st_));
+    sync();
+    for (int k = 0; k < kPhases; ++k) {
+        out[k] = h[k] * 1e-3;
+        cnt[k] = (int64_t)h[kPhases + k];
+    }
+    return true;
 }
 
 void Solver::sync() { CPFIT_CUDA(cudaStreamSynchronize(st_)); }

@@ -23,6 +23,16 @@ struct SolverOptions {
     // 1: every evaluation uses the residual objective (kruskal.cpp:83-102); 0: per-fiber
     // three-term form until f stagnates, then residual (sticky)
     int residual_objective = 0;
+
+    // a solver built for *this can run a solve with options o (graphs bake in everything but
+    // the iteration budget, which only needs to fit the trace buffer)
+    bool serves(const SolverOptions& o) const {
+        return window == o.window && o.max_iters <= max_iters && epsilon_reg == o.epsilon_reg &&
+               tol_grad == o.tol_grad && gradient_scale == o.gradient_scale && ftol == o.ftol && gtol == o.gtol &&
+               initial_step == o.initial_step && max_evals == o.max_evals && step_min == o.step_min &&
+               step_max == o.step_max && restart_on_ascent == o.restart_on_ascent &&
+               reeval_accepted == o.reeval_accepted && residual_objective == o.residual_objective;
+    }
 };
 
 // One trace row (trace.hpp:18-29); layout shared with the C-ABI cpfit_trace_row.
@@ -53,7 +63,14 @@ public:
     void copy_trace(TraceRow* out, int rows);
     void copy_best(double* out, bool host);
     void copy_current(double* out);
+    // CPFIT_PHASE_PROFILE=1 at construction: globaltimer stamps between the phases of each
+    // iteration; out[k] = accumulated us, cnt[k] = visits (kPhases entries each)
+    static constexpr int kPhases = 8;
+    bool phase_times(double* out, int64_t* cnt);
     cudaStream_t stream() const { return st_; }
+    int rank() const { return R_; }
+    int method() const { return method_; }
+    const SolverOptions& options() const { return opt_; }
     int64_t n() const { return n_; }
 
 private:
@@ -74,6 +91,7 @@ private:
     // the accepted trial (sel), so the ALS sweep reuses the evaluation's mode-0 contraction
     double *m0_cur_ = nullptr, *m0_bar_ = nullptr, *m0_best_ = nullptr, *m0_sel_ = nullptr;
     int64_t m0_n_ = 0;
+    unsigned long long* phase_ = nullptr;  // [kPhases] ns, [kPhases] counts, [1] last stamp
     void* sc_ = nullptr;
     void* state_ = nullptr;
     TraceRow* trace_ = nullptr;
