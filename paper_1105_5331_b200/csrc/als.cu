@@ -13,13 +13,11 @@
 // pass producing M_n streams (its Grams are final once mode n-1 is solved).
 #include "device.cuh"
 
-#include <cooperative_groups.h>
 
 #include <algorithm>
 
 namespace cpfit_gpu {
 
-namespace cg = cooperative_groups;
 
 void dense_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, cudaStream_t st);
 void dense_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
@@ -32,23 +30,66 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
 namespace {
 
 // Mode update (als.cpp:38-48 for one mode) in two kernels:
-//   chol_kernel       Gamma_n = *_{m != n} G_m and its Cholesky factor (one warp);
-//   solve_gram_kernel A_n <- M_n Gamma_n^-1 row by row, then the dd Gram of the new A_n.
-// The factorisation is a serial chain of R square roots, so it is launched on a side stream
-// as soon as the Grams it needs exist, overlapping the streaming pass that produces M_n.
+//   chol_kernel       finalise the Gram the previous mode's solve left as block partials,
+//                     Gamma_n = *_{m != n} G_m, and its Cholesky factor;
+//   solve_gram_kernel A_n <- M_n Gamma_n^-1 (RP lanes per row, substitution by shuffles) and
+//                     per-block dd partials of the Gram of the new A_n.
+// The factorisation is a serial chain of R reciprocal square roots, so it runs on a side stream
+// as soon as the Grams it needs exist, overlapping the streaming pass that produces M_n; the
+// solve has no grid-wide step (its Gram is finished by the next consumer).
+constexpr int kCholThreads = 256;
+constexpr int kSolveThreads = 256;
+constexpr int kSolveMaxBlocks = 148;
+
+struct GramPending {
+    int mode;          // mode whose Gram is still in block partials (-1: none)
+    const dd* part;    // [nblk][npair]
+    int nblk;
+};
+
 struct CholParams {
     int order, R, RP, mode;
-    const double* gram;  // [mode][RP*RP]
+    double* gram;        // [mode][RP*RP] (the pending mode is finalised in place)
+    GramPending pend;
     double* fac;         // [R*R] L row-major, [R] 1 / l_kk, [1] ok flag (1.0 / 0.0)
     int* status;
 };
+
+// dd sum over blocks (in order) of one Gram pair, loads batched ahead of the serial chain
+__device__ __forceinline__ double pending_pair(const GramPending& g, int npair, int p) {
+    constexpr int B = 32;  // one round of loads in flight for the usual <= 32 partials
+    dd s{0.0, 0.0};
+    for (int b0 = 0; b0 < g.nblk; b0 += B) {
+        dd v[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) v[j] = (b0 + j < g.nblk) ? g.part[(size_t)(b0 + j) * npair + p] : dd{0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+            if (b0 + j < g.nblk) s = dd_add(s, v[j]);
+    }
+    return s.hi + s.lo;
+}
+// all threads of the block: G_pending <- rounded sum of its partials (pads zero)
+__device__ void finalize_pending(const GramPending& g, int R, int RP, double* gram) {
+    if (g.mode < 0) return;
+    const int npair = R * (R + 1) / 2;
+    double* out = gram + (size_t)g.mode * RP * RP;
+    gram_zero_pads(R, RP, out);
+    for (int p = threadIdx.x; p < npair; p += blockDim.x) {
+        const double v = pending_pair(g, npair, p);
+        int r, q;
+        pair_rq(p, R, r, q);
+        out[r * RP + q] = v;
+        out[q * RP + r] = v;
+    }
+}
 
 // Left-looking LLT (Eigen's unblocked llt_inplace order: l_ik = (g_ik - sum_{j<k} l_ij l_kj)
 // / l_kk, j ascending; the pivot likewise, the ridge added to g_kk first), one warp: lane i
 // keeps row i of Gamma and of L in registers and receives row k by shuffles, so a column costs
 // one k-long DFMA chain plus one reciprocal square root. The division by l_kk = sqrt(x) is a
-// multiplication by rsqrt(x) (<= 1 ulp from the quotient). Returns false (uniformly) on a
-// pivot <= 0; a NaN pivot passes as in Eigen and surfaces as a non-finite solve.
+// multiplication by rsqrt(x) (<= 1 ulp from the quotient) and l_kk = x rsqrt(x). Returns false
+// (uniformly) on a pivot <= 0; a NaN pivot passes as in Eigen and surfaces as a non-finite solve.
 template <int RP>
 __device__ bool warp_llt(const double (&gr)[RP], double (&lr)[RP], double& dinv, int R, double ridge) {
     const int lane = threadIdx.x & 31;
@@ -65,7 +106,7 @@ __device__ bool warp_llt(const double (&gr)[RP], double (&lr)[RP], double& dinv,
             if (x <= 0.0) ok = false;
             const double inv = rsqrt(x);
             if (lane == k) {
-                lr[k] = sqrt(x);
+                lr[k] = x * inv;
                 dinv = inv;
             } else if (lane > k) {
                 lr[k] = s * inv;
@@ -76,24 +117,28 @@ __device__ bool warp_llt(const double (&gr)[RP], double (&lr)[RP], double& dinv,
 }
 
 template <int RP>
-__global__ void __launch_bounds__(32) chol_kernel(const CholParams p) {
-    extern __shared__ double gs[];  // [order][RP*RP]
-    const int R = p.R, lane = threadIdx.x;
-    const bool row = lane < R;
-    // stage every Gram first (independent loads), then the Hadamard product from shared memory
-    for (int e = lane; e < p.order * RP * RP; e += 32) gs[e] = p.gram[e];
-    __syncwarp();
-    double gr[RP], lr[RP], dinv = 0.0;
-#pragma unroll
-    for (int j = 0; j < RP; ++j) {
+__global__ void __launch_bounds__(kCholThreads) chol_kernel(const CholParams p) {
+    __shared__ double gam[RP * RP];
+    const int R = p.R, tid = threadIdx.x, lane = tid & 31;
+    finalize_pending(p.pend, R, RP, p.gram);
+    __syncthreads();
+    // Gamma_n = Hadamard product of the other modes' Grams (independent loads, one per thread)
+    for (int e = tid; e < RP * RP; e += blockDim.x) {
+        const int q = e / RP, r = e % RP;
         double v = 0.0;
-        if (row && j < R) {
+        if (q < R && r < R) {
             v = 1.0;
             for (int m = 0; m < p.order; ++m)
-                if (m != p.mode) v *= gs[m * RP * RP + lane * RP + j];
+                if (m != p.mode) v *= p.gram[(size_t)m * RP * RP + e];
         }
-        gr[j] = v;
+        gam[e] = v;
     }
+    __syncthreads();
+    if (tid >= 32) return;
+    const bool row = lane < R;
+    double gr[RP], lr[RP], dinv = 0.0;
+#pragma unroll
+    for (int j = 0; j < RP; ++j) gr[j] = row ? gam[lane * RP + j] : 0.0;
     bool ok = warp_llt<RP>(gr, lr, dinv, R, 0.0);
     if (!ok) {
         // one ridge retry (1e-12 trace), as the reference's solve_spd
@@ -116,80 +161,87 @@ __global__ void __launch_bounds__(32) chol_kernel(const CholParams p) {
 }
 
 struct SolveGramParams {
-    int R, RP, mode;
+    int R, mode;
     int64_t In;
-    double* gram;        // [mode][RP*RP]: this mode rewritten by the last block
     const double* fac;   // chol_kernel output for this mode
     const double* M;     // layout 0: M[r * ld + i]; layout 1: M[i * RP + r]
     int layout;
     int64_t ld;
     double* out;         // col-major In x R (block of the packed iterate)
     int* status;
-    dd* part;            // this mode's Gram partials [chunk][npair]
-    int nchunk;
-    int64_t rows;        // rows per Gram chunk
-    unsigned int* counter;
+    dd* part;            // this mode's Gram partials [gridDim.x][npair]
 };
 
-constexpr int kSolveThreads = 256;
-
-// Phase 1: threads solve rows i = global thread id (+ grid stride) against the factor from
-// chol_kernel. Grid barrier. Phase 2: the Gram of the new A_n as warp (chunk, pair) tasks
-// (gram.cuh); the last block combines and rounds into gram[mode].
+// RP lanes own one row i (lane r holds m_ir): L y = m by columns (y_j on lane j, broadcast,
+// lanes r > j subtract l_rj y_j — the same j-ascending operation order as the dot-product
+// form), then L^T x = y by columns (j descending). The block's rows are staged in shared memory
+// and its Gram partial is accumulated in double-double, one upper-triangle pair per thread.
 template <int RP>
 __global__ void __launch_bounds__(kSolveThreads) solve_gram_kernel(const SolveGramParams p) {
+    constexpr int RPB = kSolveThreads / RP;  // rows per block step
+    constexpr int NPT = (RP * (RP + 1) / 2 + kSolveThreads - 1) / kSolveThreads;
     __shared__ double l[RP * RP];
     __shared__ double dinv[RP];
+    __shared__ double xs[RPB][RP + 1];
     const int R = p.R;
     const int tid = threadIdx.x;
     if (p.fac[R * R + R] == 0.0) return;  // factorisation failed (status set): uniform exit
     for (int e = tid; e < R * R; e += blockDim.x) l[e] = p.fac[e];
     for (int e = tid; e < R; e += blockDim.x) dinv[e] = p.fac[R * R + e];
+    const int npair = R * (R + 1) / 2;
+    int pa[NPT], pb[NPT];
+    dd acc[NPT];
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        acc[k] = dd{0.0, 0.0};
+        const int q = tid + k * kSolveThreads;
+        if (q < npair) {
+            pair_rq(q, R, pa[k], pb[k]);
+        } else {
+            pa[k] = pb[k] = -1;
+        }
+    }
     __syncthreads();
+    const int r = tid % RP, rl = tid / RP;
     bool fin = true;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + tid; i < p.In; i += (int64_t)gridDim.x * blockDim.x) {
-        double y[RP];
+    for (int64_t i0 = (int64_t)blockIdx.x * RPB; i0 < p.In; i0 += (int64_t)gridDim.x * RPB) {
+        const int64_t i = i0 + rl;
+        const bool live = i < p.In && r < R;
+        double s = live ? (p.layout == 0 ? p.M[(int64_t)r * p.ld + i] : p.M[i * RP + r]) : 0.0;
+        double y = 0.0;
 #pragma unroll
-        for (int r = 0; r < RP; ++r)
-            y[r] = (r < R) ? (p.layout == 0 ? p.M[(int64_t)r * p.ld + i] : p.M[i * RP + r]) : 0.0;
-        // L y = m, then L^T x = y (dot-product order of the reference's triangular solves)
-#pragma unroll
-        for (int r = 0; r < RP; ++r) {
-            if (r < R) {
-                double s = y[r];
-#pragma unroll
-                for (int j = 0; j < r; ++j) s -= l[r * R + j] * y[j];
-                y[r] = s * dinv[r];
+        for (int j = 0; j < RP; ++j) {
+            if (j < R) {
+                const double yj = __shfl_sync(0xffffffffu, s * dinv[j], j, RP);
+                if (r == j) y = yj;
+                if (r > j) s -= l[r * R + j] * yj;
             }
         }
+        double t = y, x = 0.0;
 #pragma unroll
-        for (int r = RP - 1; r >= 0; --r) {
-            if (r < R) {
-                double s = y[r];
-#pragma unroll
-                for (int j = r + 1; j < RP; ++j)
-                    if (j < R) s -= l[j * R + r] * y[j];
-                y[r] = s * dinv[r];
+        for (int j = RP - 1; j >= 0; --j) {
+            if (j < R) {
+                const double xj = __shfl_sync(0xffffffffu, t * dinv[j], j, RP);
+                if (r == j) x = xj;
+                if (r < j) t -= l[j * R + r] * xj;
             }
         }
+        if (live) {
+            p.out[(int64_t)r * p.In + i] = x;
+            fin = fin && isfinite(x);
+        }
+        __syncthreads();  // previous step's Gram reads of xs are done
+        xs[rl][r] = live ? x : 0.0;
+        __syncthreads();
 #pragma unroll
-        for (int r = 0; r < RP; ++r)
-            if (r < R) {
-                p.out[(int64_t)r * p.In + i] = y[r];
-                fin = fin && isfinite(y[r]);
-            }
+        for (int k = 0; k < NPT; ++k)
+            if (pa[k] >= 0)
+                for (int rr = 0; rr < RPB; ++rr) acc[k] = dd_fma(acc[k], xs[rr][pa[k]], xs[rr][pb[k]]);
     }
     if (!fin) atomicOr(p.status, 2);
-    __threadfence();
-    cg::this_grid().sync();
-    const int npair = R * (R + 1) / 2;
-    const int warp = (int)((blockIdx.x * blockDim.x + tid) >> 5);
-    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
-    for (int t = warp; t < p.nchunk * npair; t += nwarps) gram_task(p.out, p.In, p.rows, R, t, p.part);
-    if (!last_block_arrives(p.counter)) return;
-    double* gout = p.gram + (size_t)p.mode * p.RP * p.RP;
-    gram_zero_pads(R, p.RP, gout);
-    for (int q = tid; q < npair; q += blockDim.x) gram_combine_pair(p.part, p.nchunk, q, R, p.RP, gout);
+#pragma unroll
+    for (int k = 0; k < NPT; ++k)
+        if (pa[k] >= 0) p.part[(size_t)blockIdx.x * npair + tid + k * kSolveThreads] = acc[k];
 }
 
 struct NormParams {
@@ -209,6 +261,10 @@ struct NormParams {
     const double* m0;
     double* m0out;
     int m0_ld;
+    // optional: a Gram still in block partials (the last mode of an ALS sweep): its diagonal is
+    // summed from the partials here, and block 0 finalises it into gram_w
+    GramPending pend;
+    double* gram_w;
 };
 
 // normalize_and_reorder: norms from the (double-double) Gram diagonals, lambda_r =
@@ -221,8 +277,12 @@ __global__ void normalize_kernel(const NormParams p) {
     __shared__ double scale[kMaxOrder][kMaxRank];
     __shared__ double diag[kMaxOrder][kMaxRank];
     const int tid = threadIdx.x;
-    for (int e = tid; e < p.order * p.R; e += blockDim.x)  // Gram diagonals, independent loads
-        diag[e / p.R][e % p.R] = p.gram[(size_t)(e / p.R) * p.RP * p.RP + (e % p.R) * (p.RP + 1)];
+    for (int e = tid; e < p.order * p.R; e += blockDim.x) {  // Gram diagonals, independent loads
+        const int n = e / p.R, r = e % p.R;
+        diag[n][r] = (n == p.pend.mode) ? pending_pair(p.pend, p.R * (p.R + 1) / 2, r * p.R - r * (r - 1) / 2)
+                                        : p.gram[(size_t)n * p.RP * p.RP + r * (p.RP + 1)];
+    }
+    if (blockIdx.x == 0) finalize_pending(p.pend, p.R, p.RP, p.gram_w);
     __syncthreads();
     if (tid < p.R) {
         double l = 1.0;
@@ -307,13 +367,31 @@ __global__ void gram_hadamard_kernel(const double* gram, int order, int R, int R
 
 }  // namespace
 
+namespace {
+int solve_blocks(const EvalWork& w, int n) {
+    const int rpb = kSolveThreads / w.RP;
+    return (int)std::max<int64_t>(1, std::min<int64_t>((w.dims[n] + rpb - 1) / rpb, kSolveMaxBlocks));
+}
+GramPending pending_of(const EvalWork& w, int n) {
+    GramPending g{};
+    g.mode = n;
+    g.part = w.solve_part + (size_t)n * w.solve_part_stride;
+    g.nblk = n >= 0 ? solve_blocks(w, n) : 0;
+    if (n < 0) g.part = nullptr;
+    return g;
+}
+
+}  // namespace
+
 void gram_hadamard_device(EvalWork& w, int skip, double* out, cudaStream_t st) {
     gram_hadamard_kernel<<<1, 256, 0, st>>>(w.gram, w.order, w.R, w.RP, skip, out);
     CPFIT_CUDA(cudaGetLastError());
 }
 
-void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st) {
+void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st, int pending) {
     NormParams p{};
+    p.pend = pending_of(w, pending);
+    p.gram_w = w.gram;
     p.order = w.order;
     p.R = w.R;
     p.RP = w.RP;
@@ -333,6 +411,7 @@ void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st
 int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
                           cudaStream_t st, const double* m0, double* m0out) {
     NormParams p{};
+    p.pend.mode = -1;
     p.order = w.order;
     p.R = w.R;
     p.RP = w.RP;
@@ -357,63 +436,46 @@ int normalize_grad_device(EvalWork& w, const double* u, const double* g, double*
 }
 
 namespace {
-// Cholesky factor of Gamma_n from the current Grams -> w.chol + mode slot
-void chol_mode(EvalWork& w, int n, int* status, cudaStream_t st) {
+// Cholesky factor of Gamma_n -> w.chol + mode slot; first finalises mode `pending`'s Gram
+void chol_mode(EvalWork& w, int n, int pending, int* status, cudaStream_t st) {
     CholParams p{};
     p.order = w.order;
     p.R = w.R;
     p.RP = w.RP;
     p.mode = n;
     p.gram = w.gram;
+    p.pend = pending_of(w, pending);
     p.fac = w.chol + (size_t)n * w.chol_stride;
     p.status = status;
-    const size_t smem = sizeof(double) * (size_t)w.order * w.RP * w.RP;
     switch (w.RP) {
-        case 8: chol_kernel<8><<<1, 32, smem, st>>>(p); break;
-        case 16: chol_kernel<16><<<1, 32, smem, st>>>(p); break;
-        default:
-            CPFIT_CUDA(cudaFuncSetAttribute(chol_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            chol_kernel<32><<<1, 32, smem, st>>>(p);
-            break;
+        case 8: chol_kernel<8><<<1, kCholThreads, 0, st>>>(p); break;
+        case 16: chol_kernel<16><<<1, kCholThreads, 0, st>>>(p); break;
+        default: chol_kernel<32><<<1, kCholThreads, 0, st>>>(p); break;
     }
     CPFIT_CUDA(cudaGetLastError());
 }
 
-// A_n <- M_n Gamma_n^-1 (factor from chol_mode) and G_n <- A_n^T A_n
+// A_n <- M_n Gamma_n^-1 (factor from chol_mode); G_n left as block partials (pending)
 void solve_gram(EvalWork& w, int n, const double* M, int layout, int64_t ld, double* ublock, int* status,
                 cudaStream_t st) {
     SolveGramParams p{};
     p.R = w.R;
-    p.RP = w.RP;
     p.mode = n;
     p.In = w.dims[n];
-    p.gram = w.gram;
     p.fac = w.chol + (size_t)n * w.chol_stride;
     p.M = M;
     p.layout = layout;
     p.ld = ld;
     p.out = ublock;
     p.status = status;
-    p.part = w.gram_part + (size_t)w.gram_chunk0[n] * (w.R * (w.R + 1) / 2);
-    p.nchunk = w.gram_nchunk[n];
-    p.rows = gram_chunk_rows(p.In);
-    p.counter = w.counter + kCounterSolve;
-    const int tasks = p.nchunk * (w.R * (w.R + 1) / 2);
-    const int64_t need = std::max<int64_t>((p.In + kSolveThreads - 1) / kSolveThreads, (tasks + 7) / 8);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(need, sm_count())));
-    cfg.blockDim = dim3(kSolveThreads);
-    cfg.stream = st;
-    cudaLaunchAttribute attr{};
-    attr.id = cudaLaunchAttributeCooperative;
-    attr.val.cooperative = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
+    p.part = w.solve_part + (size_t)n * w.solve_part_stride;
+    const int grid = solve_blocks(w, n);
     switch (w.RP) {
-        case 8: CPFIT_CUDA(cudaLaunchKernelEx(&cfg, solve_gram_kernel<8>, p)); break;
-        case 16: CPFIT_CUDA(cudaLaunchKernelEx(&cfg, solve_gram_kernel<16>, p)); break;
-        default: CPFIT_CUDA(cudaLaunchKernelEx(&cfg, solve_gram_kernel<32>, p)); break;
+        case 8: solve_gram_kernel<8><<<grid, kSolveThreads, 0, st>>>(p); break;
+        case 16: solve_gram_kernel<16><<<grid, kSolveThreads, 0, st>>>(p); break;
+        default: solve_gram_kernel<32><<<grid, kSolveThreads, 0, st>>>(p); break;
     }
+    CPFIT_CUDA(cudaGetLastError());
 }
 
 // chol_mode(n) on the side stream once everything queued on st so far is done; the next
@@ -421,7 +483,7 @@ void solve_gram(EvalWork& w, int n, const double* M, int layout, int64_t ld, dou
 void fork_chol(EvalWork& w, int n, int* status, cudaStream_t st) {
     CPFIT_CUDA(cudaEventRecord(w.ev_fork, st));
     CPFIT_CUDA(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
-    chol_mode(w, n, status, w.side);
+    chol_mode(w, n, n - 1, status, w.side);
     CPFIT_CUDA(cudaEventRecord(w.ev_join, w.side));
 }
 void join_chol(EvalWork& w, cudaStream_t st) { CPFIT_CUDA(cudaStreamWaitEvent(st, w.ev_join, 0)); }
@@ -434,7 +496,7 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
     grams_device(w, work, st);
     const int N = t.order;
     // Gamma_0 from the Grams of u; each later Gamma_n as soon as G_{n-1}' exists (side stream)
-    chol_mode(w, 0, status, st);
+    chol_mode(w, 0, -1, status, st);
     if (t.sparse) {
         for (int n = 0; n < N; ++n) {
             if (n > 0) fork_chol(w, n, status, st);
@@ -467,7 +529,7 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
             }
         }
     }
-    normalize_device(w, work, out, st);
+    normalize_device(w, work, out, st, N - 1);
 }
 
 }  // namespace cpfit_gpu

@@ -154,67 +154,85 @@ struct LevelParams {
 };
 
 constexpr int kLevelThreads = 256;
-constexpr int kSlabBatch = 4;
+constexpr int kSlabBatch = 8;
 
-template <int RP, int KM>
+// Slabs are processed two at a time (both slabs' loads issue before the FMAs: two rounds of
+// L2 latency in flight per thread); the Khatri-Rao tail rows of a batch of slabs are built once
+// per batch with 32-bit index math.
+template <int RP, int KM, bool DO_M, bool DO_S>
 __global__ void __launch_bounds__(kLevelThreads) level_kernel(const LevelParams p) {
     constexpr int B = kLevelThreads, NW = B / 32;
     __shared__ double wt[kSlabBatch][RP];
     __shared__ double sred[kSlabBatch][NW][RP];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r = tid % RP;
-    const int64_t npairs = p.Ih * RP;
-    const int64_t pbase = (int64_t)blockIdx.y * B * KM + tid;
-    const int64_t s_begin = (int64_t)blockIdx.x * p.spc;
-    const int64_t s_end = imin64(p.Jt, s_begin + p.spc);
-    const bool do_m = p.m_part != nullptr, do_s = p.s_out != nullptr;
+    const int npairs = (int)(p.Ih * RP);
+    const int pbase = blockIdx.y * B * KM + tid;
+    const int s_begin = (int)(blockIdx.x * p.spc);
+    const int s_end = (int)imin64(p.Jt, s_begin + p.spc);
     double acc[KM], ah[KM];
 #pragma unroll
     for (int k = 0; k < KM; ++k) {
-        const int64_t pr = pbase + (int64_t)k * B;
+        const int pr = pbase + k * B;
         acc[k] = 0.0;
-        ah[k] = (do_s && pr < npairs && r < p.R) ? p.Ah[(int64_t)r * p.Ih + pr / RP] : 0.0;
+        ah[k] = (DO_S && pr < npairs && r < p.R) ? p.Ah[(int64_t)r * p.Ih + pr / RP] : 0.0;
     }
-    for (int64_t s0 = s_begin; s0 < s_end; s0 += kSlabBatch) {
-        const int nb = (int)imin64(kSlabBatch, s_end - s0);
+    for (int s0 = s_begin; s0 < s_end; s0 += kSlabBatch) {
+        const int nb = min(kSlabBatch, s_end - s0);
         __syncthreads();  // previous batch's wt / sred consumers are done
-        if (do_m) {
+        if (DO_M) {
             for (int e = tid; e < nb * RP; e += B) {
                 const int sl = e / RP, rr = e % RP;
                 double w = 0.0;
                 if (rr < p.R) {
                     w = 1.0;
-                    int64_t rem = s0 + sl;
+                    int rem = s0 + sl;
                     for (int m = 0; m < p.ntail; ++m) {
-                        const int64_t jm = rem % p.tdims[m];
-                        rem /= p.tdims[m];
-                        w *= p.tfac[m][(int64_t)rr * p.tdims[m] + jm];
+                        const int d = (int)p.tdims[m];
+                        const int q = rem / d;
+                        w *= p.tfac[m][(int64_t)rr * d + (rem - q * d)];
+                        rem = q;
                     }
                 }
                 wt[sl][rr] = w;
             }
             __syncthreads();
         }
-        for (int sl = 0; sl < nb; ++sl) {
-            const double* src = p.Sin + (s0 + sl) * npairs;
-            const double wv = do_m ? wt[sl][r] : 0.0;
-            double sp = 0.0;
+        for (int sl = 0; sl < nb; sl += 2) {
+            const bool two = sl + 1 < nb;
+            const double* src0 = p.Sin + (int64_t)(s0 + sl) * npairs;
+            const double* src1 = src0 + npairs;
+            double v0[KM], v1[KM];
 #pragma unroll
             for (int k = 0; k < KM; ++k) {
-                const int64_t pr = pbase + (int64_t)k * B;
-                if (pr < npairs) {
-                    const double v = __ldg(src + pr);
-                    acc[k] = fma(v, wv, acc[k]);
-                    sp = fma(v, ah[k], sp);
+                const int pr = pbase + k * B;
+                v0[k] = pr < npairs ? __ldg(src0 + pr) : 0.0;
+                v1[k] = (two && pr < npairs) ? __ldg(src1 + pr) : 0.0;
+            }
+            if (DO_M) {
+                const double w0 = wt[sl][r], w1 = two ? wt[sl + 1][r] : 0.0;
+#pragma unroll
+                for (int k = 0; k < KM; ++k) acc[k] = fma(v1[k], w1, fma(v0[k], w0, acc[k]));
+            }
+            if (DO_S) {
+                double sp0 = 0.0, sp1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < KM; ++k) {
+                    sp0 = fma(v0[k], ah[k], sp0);
+                    sp1 = fma(v1[k], ah[k], sp1);
+                }
+#pragma unroll
+                for (int o = 16; o >= RP; o >>= 1) {
+                    sp0 += __shfl_xor_sync(0xffffffffu, sp0, o);
+                    sp1 += __shfl_xor_sync(0xffffffffu, sp1, o);
+                }
+                if (lane < RP) {
+                    sred[sl][warp][lane] = sp0;
+                    if (two) sred[sl + 1][warp][lane] = sp1;
                 }
             }
-            if (do_s) {
-#pragma unroll
-                for (int o = 16; o >= RP; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
-                if (lane < RP) sred[sl][warp][lane] = sp;
-            }
         }
-        if (do_s) {
+        if (DO_S) {
             __syncthreads();
             for (int e = tid; e < nb * RP; e += B) {
                 const int sl = e / RP, rr = e % RP;
@@ -225,23 +243,32 @@ __global__ void __launch_bounds__(kLevelThreads) level_kernel(const LevelParams 
             }
         }
     }
-    if (do_m) {
+    if (DO_M) {
         double* out = p.m_part + (int64_t)blockIdx.x * npairs;
 #pragma unroll
         for (int k = 0; k < KM; ++k) {
-            const int64_t pr = pbase + (int64_t)k * B;
+            const int pr = pbase + k * B;
             if (pr < npairs) out[pr] = acc[k];
         }
     }
 }
 
+template <int RP, int KM>
+void launch_level_km(const LevelParams& p, dim3 grid, cudaStream_t st) {
+    const bool m = p.m_part != nullptr, s = p.s_out != nullptr;
+    if (m && s)
+        level_kernel<RP, KM, true, true><<<grid, kLevelThreads, 0, st>>>(p);
+    else if (m)
+        level_kernel<RP, KM, true, false><<<grid, kLevelThreads, 0, st>>>(p);
+    else
+        level_kernel<RP, KM, false, true><<<grid, kLevelThreads, 0, st>>>(p);
+}
 template <int RP>
 void launch_level_rp(const LevelParams& p, dim3 grid, int km, cudaStream_t st) {
     switch (km) {
-        case 4: level_kernel<RP, 4><<<grid, kLevelThreads, 0, st>>>(p); break;
-        case 8: level_kernel<RP, 8><<<grid, kLevelThreads, 0, st>>>(p); break;
-        case 16: level_kernel<RP, 16><<<grid, kLevelThreads, 0, st>>>(p); break;
-        default: level_kernel<RP, 32><<<grid, kLevelThreads, 0, st>>>(p); break;
+        case 4: launch_level_km<RP, 4>(p, grid, st); break;
+        case 8: launch_level_km<RP, 8>(p, grid, st); break;
+        default: launch_level_km<RP, 16>(p, grid, st); break;
     }
 }
 
@@ -544,6 +571,9 @@ EvalWork* work_create(const DevTensor& t, int R) {
     CPFIT_CUDA(cudaMalloc(&w->gram, sizeof(double) * (size_t)t.order * w->RP * w->RP));
     w->red_grid = sms * 2;
     CPFIT_CUDA(cudaMalloc(&w->red, sizeof(double) * 3 * (size_t)w->red_grid));
+    // ALS solve Gram partials: <= 148 blocks per mode (als.cu solve_blocks)
+    w->solve_part_stride = (int64_t)148 * (R * (R + 1) / 2);
+    CPFIT_CUDA(cudaMalloc(&w->solve_part, sizeof(dd) * (size_t)t.order * w->solve_part_stride));
     w->chol_stride = (int64_t)R * R + R + 1;
     CPFIT_CUDA(cudaMalloc(&w->chol, sizeof(double) * (size_t)t.order * w->chol_stride));
     CPFIT_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
@@ -573,9 +603,10 @@ EvalWork* work_create(const DevTensor& t, int R) {
             for (int m = h + 1; m < t.order; ++m) Jt *= t.dims[m];
             const int64_t npairs = t.dims[h] * w->RP;
             const int64_t need = (npairs + kLevelThreads - 1) / kLevelThreads;
-            w->lvl_km[h] = need <= 4 ? 4 : need <= 8 ? 8 : need <= 16 ? 16 : 32;
+            w->lvl_km[h] = need <= 4 ? 4 : need <= 8 ? 8 : 16;
             w->lvl_ny[h] = (int)((npairs + (int64_t)kLevelThreads * w->lvl_km[h] - 1) / (kLevelThreads * w->lvl_km[h]));
-            const int64_t nx_want = std::max<int64_t>(1, std::min<int64_t>(Jt, (sms + w->lvl_ny[h] - 1) / w->lvl_ny[h]));
+            const int64_t nx_want =
+                std::max<int64_t>(1, std::min<int64_t>(Jt, (2 * sms + w->lvl_ny[h] - 1) / w->lvl_ny[h]));
             w->lvl_spc[h] = (Jt + nx_want - 1) / nx_want;
             w->lvl_nx[h] = (int)((Jt + w->lvl_spc[h] - 1) / w->lvl_spc[h]);
             CPFIT_CUDA(cudaMalloc(&w->lvl_part[h], sizeof(double) * (size_t)w->lvl_nx[h] * npairs));
@@ -607,6 +638,7 @@ void work_destroy(EvalWork* w) {
     cudaFree(w->frows);
     cudaFree(w->counter);
     cudaFree(w->chol);
+    cudaFree(w->solve_part);
     if (w->ev_fork) cudaEventDestroy(w->ev_fork);
     if (w->ev_join) cudaEventDestroy(w->ev_join);
     if (w->side) cudaStreamDestroy(w->side);

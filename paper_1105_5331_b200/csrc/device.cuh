@@ -84,6 +84,8 @@ struct EvalWork {
     // factorisations run on, overlapping the streaming passes
     double* chol = nullptr;
     int64_t chol_stride = 0;
+    dd* solve_part = nullptr;        // per-mode Gram partials of the ALS solves
+    int64_t solve_part_stride = 0;   // dd per mode ([blocks][npair])
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -113,7 +115,7 @@ void grams_device(EvalWork& w, const double* u, cudaStream_t st);
 // gram_hadamard(factors(u), skip) (tensor.cpp:261-274) -> out (R x R col-major), from w.gram.
 void gram_hadamard_device(EvalWork& w, int skip, double* out, cudaStream_t st);
 // normalize_and_reorder (kruskal.cpp:156-193): u -> out, Grams in w.gram updated to match.
-void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st);
+void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st, int pending = -1);
 // normalize u -> uout and map the gradient g at u to the normalised point (G_n D_n^-1,
 // permuted) -> gout; writes per-block partial ||gout||^2 to red, returns the block count.
 int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
