@@ -4,8 +4,9 @@
 // to ldT doubles) through a kFStages-deep shared-memory ring. Roles:
 //   T producer (warp 0)    one bulk async copy per fiber into the ring, issued by 16 lanes at
 //                          once (mbarrier complete_tx);
-//   W producer (warp 1)    the W tile — Khatri-Rao rows of modes >= 1, never materialised in
-//                          HBM — into a double-buffered smem tile (independent gathers);
+//   W producers (warps 1-2) the W tile — Khatri-Rao rows of modes >= 1, never materialised in
+//                          HBM — into a double-buffered smem tile (independent gathers; two
+//                          warps, since their multiplies queue behind DMMAs on the fp64 pipe);
 //   S warps                warp s owns 8 x 8 sub-tile(s) (m-tile ft of fibers x r-tile rt) of
 //                            S(F x RP) = T(:, F)^T A0    DMMA m8n8k4 over the FULL fiber length,
 //                          four interleaved accumulator chains, A0 fragments from a shared-memory
@@ -36,14 +37,15 @@ __host__ __device__ constexpr int w_ld() {
 template <int RP>
 struct FiberRoles {
     static constexpr int NRT = RP / 8;
-    static constexpr bool SEPW = RP <= 16;                  // W producer in its own warp
+    static constexpr int NWP = RP <= 16 ? 2 : 0;            // W producer warps (0: the T producer)
+    static constexpr bool SEPW = NWP > 0;
     static constexpr int NQ = 2 * NRT;                      // 8x8 S sub-tiles per tile
     static constexpr int NS = RP == 32 ? 4 : NQ;            // S warps
     static constexpr int SPW = NQ / NS;                     // sub-tiles per S warp
     static constexpr int NM = RP == 32 ? 11 : 8;            // M0 warps
     static constexpr int MAXMT = RP == 8 ? 14 : (RP == 16 ? 7 : 5);  // m-tiles per M0 warp
     static constexpr bool A0SMEM = RP <= 16;                // A0 staged in shared memory
-    static constexpr int S0 = 1 + (SEPW ? 1 : 0);           // first S warp
+    static constexpr int S0 = 1 + NWP;                      // first S warp
     static constexpr int M0W = S0 + NS;                     // first M0 warp
     static constexpr int WARPS = M0W + NM;
 };
@@ -84,7 +86,7 @@ inline void fiber_schedule_rp(int I0, bool do_s, FiberParams& p) {
     const int KS = (I0 + 3) / 4;
     double load[4] = {0.0, 0.0, 0.0, 0.0};
     load[0] += 2.0;
-    if (Ro::SEPW) load[1] += 2.0;
+    for (int w = 0; w < Ro::NWP; ++w) load[(1 + w) % 4] += 2.0;
     if (do_s)
         for (int s = 0; s < Ro::NS; ++s) load[(Ro::S0 + s) % 4] += (double)KS * Ro::SPW + 6.0 * Ro::SPW;
     const double mt_w = 4.0 * Ro::NRT;  // DMMAs per m-tile per tile
@@ -206,6 +208,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int NRT = Ro::NRT;
     constexpr int WLD = w_ld<RP>();
+    constexpr int NW = Ro::NWP > 0 ? Ro::NWP : 1;  // warps building W
     static_assert(F == 16, "two 8-fiber m-tiles per tile");
     const FiberSmem L = fiber_layout<RP, F>(p.nchunk, p.I0);
     const int I0s = p.I0s;
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
             mbar_init(&tempty[s], t_cons);
         }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&wfull[b], 1);
+            mbar_init(&wfull[b], NW);
             mbar_init(&wempty[b], w_cons);
         }
     }
@@ -267,9 +270,10 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     };
 
     double facc = 0.0;
-    // W tile k: lane = (fiber fw, r-slice hw); gathers first (independent), then the buffer
+    // W tile k: lane = (fiber fw, r-slice hw) of one of the NW producer warps; gathers first
+    // (independent), then the buffer
     auto w_producer = [&](int64_t k, FiberIndex<ORD>& xw, int fw, int hw) {
-        constexpr int RS = RP * F / 32;
+        constexpr int RS = RP * F / (32 * NW);
         const int b = (int)(k & 1);
         const int64_t f0 = (t_begin + k) * F;
         if (k > 0) xw = advance_fiber<ORD>(p, xw, F, f0 + fw);
@@ -312,10 +316,10 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                 bulk_g2s(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s]);
             if (!Ro::SEPW && need_w) w_producer(k, xw, fw, hw);
         }
-    } else if (Ro::SEPW && warp == 1) {
-        // ---------------- W producer ----------------
+    } else if (Ro::SEPW && warp <= Ro::NWP) {
+        // ---------------- W producers ----------------
         if (need_w) {
-            const int fw = lane % F, hw = lane / F;
+            const int fw = lane % F, hw = (warp - 1) * (32 / F) + lane / F;
             FiberIndex<ORD> xw = decode_fiber<ORD>(p, t_begin * F + fw);
             for (int64_t k = 0; k < ntl; ++k) w_producer(k, xw, fw, hw);
         }
@@ -380,6 +384,8 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[s]);
+                // epilogue of the sub-tile(s): lane holds D fragment items f = 8 ft + lane/4,
+                // r = 8 nt + 2 (lane%4) + {0, 1}
                 // epilogue of the sub-tile(s): lane holds D fragment items f = 8 ft + lane/4,
                 // r = 8 nt + 2 (lane%4) + {0, 1}
                 if (epi_w) FIBER_WAIT(6, &wfull[b], (uint32_t)((k / 2) & 1));

@@ -37,5 +37,5 @@ for kind in [int(k) for k in os.environ.get("KINDS", "3,4,5").split(",")]:
     def sh(x, tot):
         return f"{100 * x / tot:5.1f}%" if tot else "  -  "
     print(f"  producers tempty {sh(v[0], prod)}  wempty {sh(v[1], prod)}")
-    print(f"  S warps   tfull  {sh(v[2], sw)}  wfull  {sh(v[6], sw)}")
-    print(f"  M0 warps  tfull  {sh(v[3], mw)}  wfull  {sh(v[4], mw)}")
+    print(f"  compute   tfull  {sh(v[2], sw)}  wfull  {sh(v[4], sw)}  parts {sh(v[3], sw)}")
+
