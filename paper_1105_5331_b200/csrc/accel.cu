@@ -20,7 +20,7 @@ namespace cpfit_gpu {
 namespace {
 
 constexpr int kLeafRows = 256;
-constexpr int kTsqrThreads = 256;
+constexpr int kTsqrThreads = 512;
 
 struct TsqrParams {
     int64_t n;
@@ -37,16 +37,27 @@ struct TsqrParams {
 };
 
 // Householder QR (no pivoting; Eigen makeHouseholder / applyHouseholderOnTheLeft) of the
-// H x C column-major smem matrix x (ld = H); upper triangle left in rows 0..C-1, the rest
-// zeroed.
-__device__ void smem_qr(double* x, int H, int C, double* tau_s) {
+// H x C column-major smem matrix x (ld = H, H <= 32 kQrMaxRpl); upper triangle left in rows
+// 0..C-1, the rest zeroed. Latency-bound (C sequential steps): one warp forms each reflector,
+// then every warp updates its columns with the reflector and the column cached in registers
+// (lanes over rows, loads issued before the dot product).
+constexpr int kQrMaxRpl = 10;
+
+__device__ void smem_qr(double* x, int H, int C, double* tau_s /* [3] */) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int K = min(H, C);
     for (int k = 0; k < K; ++k) {
+        double* col = x + (size_t)k * H;
         if (warp == 0) {
-            double* col = x + (size_t)k * H;
+            double cv[kQrMaxRpl];
+#pragma unroll
+            for (int u = 0; u < kQrMaxRpl; ++u) {
+                const int i = k + 1 + lane + 32 * u;
+                cv[u] = i < H ? col[i] : 0.0;
+            }
             double tail = 0.0;
-            for (int i = k + 1 + lane; i < H; i += 32) tail += col[i] * col[i];
+#pragma unroll
+            for (int u = 0; u < kQrMaxRpl; ++u) tail += cv[u] * cv[u];
             tail = warp_sum(tail);
             const double c0 = col[k];
             double tau, beta;
@@ -57,29 +68,49 @@ __device__ void smem_qr(double* x, int H, int C, double* tau_s) {
             } else {
                 beta = sqrt(c0 * c0 + tail);
                 if (c0 >= 0.0) beta = -beta;
-                const double inv = c0 - beta;
-                for (int i = k + 1 + lane; i < H; i += 32) col[i] /= inv;
                 tau = (beta - c0) / beta;
             }
             __syncwarp();
             if (lane == 0) {
-                col[k] = beta;
                 tau_s[0] = tau;
+                tau_s[1] = beta;
+                tau_s[2] = c0 - beta;  // essential part = tail / (c0 - beta)
             }
         }
         __syncthreads();
         const double tau = tau_s[0];
-        const double* v = x + (size_t)k * H;
         if (tau != 0.0) {
+            // essential part of the reflector, every thread one division
+            const double inv = tau_s[2];
+            for (int i = k + 1 + threadIdx.x; i < H; i += blockDim.x) col[i] /= inv;
+            __syncthreads();
+            double vr[kQrMaxRpl];
+#pragma unroll
+            for (int u = 0; u < kQrMaxRpl; ++u) {
+                const int i = k + 1 + lane + 32 * u;
+                vr[u] = i < H ? col[i] : 0.0;
+            }
             for (int j = k + 1 + warp; j < C; j += nw) {
                 double* cj = x + (size_t)j * H;
+                double cr[kQrMaxRpl];
                 double t = 0.0;
-                for (int i = k + 1 + lane; i < H; i += 32) t += v[i] * cj[i];
+#pragma unroll
+                for (int u = 0; u < kQrMaxRpl; ++u) {
+                    const int i = k + 1 + lane + 32 * u;
+                    cr[u] = i < H ? cj[i] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kQrMaxRpl; ++u) t += vr[u] * cr[u];
                 t = warp_sum(t) + cj[k];
+#pragma unroll
+                for (int u = 0; u < kQrMaxRpl; ++u) {
+                    const int i = k + 1 + lane + 32 * u;
+                    if (i < H) cj[i] = cr[u] - tau * vr[u] * t;
+                }
                 if (lane == 0) cj[k] -= tau * t;
-                for (int i = k + 1 + lane; i < H; i += 32) cj[i] -= tau * v[i] * t;
             }
         }
+        if (threadIdx.x == 0) col[k] = tau_s[1];
         __syncthreads();
     }
     // zero everything below the diagonal (essential parts)
@@ -92,7 +123,7 @@ __device__ void smem_qr(double* x, int H, int C, double* tau_s) {
 
 __global__ void tsqr_kernel(const TsqrParams p) {
     extern __shared__ double xs[];
-    __shared__ double tau_s[1];
+    __shared__ double tau_s[3];
     const int m = p.ring[0], head = p.ring[1];
     const int C = m + 1;
     const int H = C + p.per_block * (p.rin ? C : 1);
@@ -104,15 +135,17 @@ __global__ void tsqr_kernel(const TsqrParams p) {
     for (int64_t b = b0; b < b1; ++b) {
         const int top = have ? C : 0;
         if (!p.rin) {
-            const int64_t r0 = b * p.per_block;
-            for (int e = threadIdx.x; e < p.per_block * C; e += blockDim.x) {
-                const int j = e / p.per_block, ii = e % p.per_block;
+            // leaves hold kLeafRows rows; column j of the window sits in ring slot head + j (mod cap)
+            const int64_t r0 = b * kLeafRows;
+#pragma unroll 4
+            for (int e = threadIdx.x; e < kLeafRows * C; e += blockDim.x) {
+                const int j = e / kLeafRows, ii = e % kLeafRows;
                 const int64_t i = r0 + ii;
                 double v = 0.0;
                 if (i < p.n) {
                     const double g = p.gb[i];
                     if (j < m) {
-                        const int slot = (head + j) % p.cap;
+                        const int slot = head + j < p.cap ? head + j : head + j - p.cap;
                         v = g - p.wg[(int64_t)slot * p.n + i];
                     } else {
                         v = -g;
@@ -150,83 +183,101 @@ __global__ void tsqr_kernel(const TsqrParams p) {
     }
 }
 
-// One warp: damped least squares from the final R, Eigen ColPivHouseholderQR semantics.
-__global__ void accel_solve_kernel(const double* rfin, const int* ring, double eps, double* alpha, double* scal) {
-    extern __shared__ double a[];  // 2m x m stacked system
-    __shared__ double bvec[128];
-    __shared__ double upd[64], dir[64], hc[64], rhs[64], al[64];
+// Damped least squares from the final R with Eigen ColPivHouseholderQR semantics (pivot on the
+// largest updated column norm, LAPACK-style norm downdating with recomputation, threshold rank),
+// one block of kSolveThreads: R staged in shared memory once; each Householder step is one warp's
+// norm + scalars, then the remaining columns are updated one warp per column (lanes over rows).
+constexpr int kSolveThreads = 256;
+
+__global__ void __launch_bounds__(kSolveThreads) accel_solve_kernel(const double* rfin, const int* ring, double eps,
+                                                                    double* alpha, double* scal) {
+    extern __shared__ double sm[];  // a: 2m x m stacked system (col-major), rf: C x C
+    __shared__ double bvec[128], cvec[128], upd[64], dir[64], hc[64], rhs[64], al[64], colsq[64], yv[64];
     __shared__ int perm[64], transp[64];
-    const int lane = threadIdx.x;
+    __shared__ double sh_delta, sh_rn, sh_thr_help, sh_maxpivot, sh_tau, sh_beta, sh_inv;
+    __shared__ int sh_big, sh_nzp, sh_nz;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int m = ring[0];
     const int C = m + 1;
     const int rows = 2 * m;
-    // R_P (m x m), r_c (m)
-    double dmax = 0.0;
-    for (int j = 0; j < m; ++j) {
-        double s = 0.0;
-        for (int i = 0; i <= j; ++i) s += rfin[(size_t)j * C + i] * rfin[(size_t)j * C + i];
-        dmax = (j == 0) ? s : fmax(dmax, s);
+    double* a = sm;
+    double* rf = sm + (size_t)rows * m;
+    for (int e = tid; e < C * C; e += blockDim.x) rf[e] = rfin[e];
+    __syncthreads();
+    // ||R_P e_j||^2 and rhs_j = R_P(:, j) . r_c = -(P^T g_bar)_j
+    for (int j = tid; j < m; j += blockDim.x) {
+        double s2 = 0.0, r = 0.0;
+        for (int i = 0; i <= j; ++i) {
+            const double v = rf[(size_t)j * C + i];
+            s2 += v * v;
+            r += v * rf[(size_t)m * C + i];
+        }
+        colsq[j] = s2;
+        rhs[j] = r;
     }
-    const double delta = (dmax > 0.0) ? eps * dmax : eps;
-    for (int j = lane; j < m; j += 32) {
-        double s = 0.0;
-        for (int i = 0; i <= j; ++i) s += rfin[(size_t)j * C + i] * rfin[(size_t)m * C + i];
-        rhs[j] = s;  // = -(P^T g_bar)_j
+    __syncthreads();
+    if (tid == 0) {
+        double dmax = 0.0, rn = 0.0;
+        for (int j = 0; j < m; ++j) {
+            dmax = (j == 0) ? colsq[j] : fmax(dmax, colsq[j]);
+            rn += rhs[j] * rhs[j];
+        }
+        sh_delta = (dmax > 0.0) ? eps * dmax : eps;
+        sh_rn = sqrt(rn);
     }
-    __syncwarp();
-    double rn = 0.0;
-    for (int j = 0; j < m; ++j) rn += rhs[j] * rhs[j];
-    rn = sqrt(rn);
+    __syncthreads();
+    const double delta = sh_delta, rn = sh_rn;
     if (rn == 0.0) {
-        for (int j = lane; j < m; j += 32) alpha[j] = 0.0;
-        if (lane == 0) {
+        for (int j = tid; j < m; j += blockDim.x) alpha[j] = 0.0;
+        if (tid == 0) {
             scal[0] = 0.0;
             scal[2] = delta;
         }
         return;
     }
     const double sd = sqrt(delta);
-    for (int e = lane; e < rows * m; e += 32) {
+    for (int e = tid; e < rows * m; e += blockDim.x) {
         const int j = e / rows, i = e % rows;
         double v;
         if (i < m)
-            v = (i <= j) ? rfin[(size_t)j * C + i] : 0.0;
+            v = (i <= j) ? rf[(size_t)j * C + i] : 0.0;
         else
             v = (i - m == j) ? sd : 0.0;
         a[(size_t)j * rows + i] = v;
     }
-    for (int i = lane; i < rows; i += 32) bvec[i] = (i < m) ? rfin[(size_t)m * C + i] : 0.0;
-    __syncwarp();
+    for (int i = tid; i < rows; i += blockDim.x) bvec[i] = (i < m) ? rf[(size_t)m * C + i] : 0.0;
+    __syncthreads();
     const double epsm = 2.220446049250313e-16;
-    for (int j = lane; j < m; j += 32) {
-        double s = 0.0;
-        for (int i = 0; i < rows; ++i) s += a[(size_t)j * rows + i] * a[(size_t)j * rows + i];
-        upd[j] = dir[j] = sqrt(s);
-        perm[j] = j;
+    for (int j = warp; j < m; j += nw) {
+        double s2 = 0.0;
+        for (int i = lane; i < rows; i += 32) s2 += a[(size_t)j * rows + i] * a[(size_t)j * rows + i];
+        s2 = warp_sum(s2);
+        if (lane == 0) {
+            upd[j] = dir[j] = sqrt(s2);
+            perm[j] = j;
+        }
     }
-    __syncwarp();
-    double maxcol = 0.0;
-    for (int j = 0; j < m; ++j) maxcol = fmax(maxcol, upd[j]);
-    const double thr_help = (maxcol * epsm) * (maxcol * epsm) / rows;
+    __syncthreads();
+    if (tid == 0) {
+        double maxcol = 0.0;
+        for (int j = 0; j < m; ++j) maxcol = fmax(maxcol, upd[j]);
+        sh_thr_help = (maxcol * epsm) * (maxcol * epsm) / rows;
+        sh_nzp = m;
+        sh_maxpivot = 0.0;
+    }
+    __syncthreads();
     const double down_thr = sqrt(epsm);
-    int nzp = m;
-    double maxpivot = 0.0;
     const int size = m;
     for (int k = 0; k < size; ++k) {
-        int big = k;
-        for (int j = k + 1; j < m; ++j)
-            if (upd[j] > upd[big]) big = j;
-        const double bsq = upd[big] * upd[big];
-        if (nzp == size && bsq < thr_help * (rows - k)) nzp = k;
-        if (lane == 0) transp[k] = big;
-        if (k != big) {
-            for (int i = lane; i < rows; i += 32) {
-                const double t = a[(size_t)k * rows + i];
-                a[(size_t)k * rows + i] = a[(size_t)big * rows + i];
-                a[(size_t)big * rows + i] = t;
-            }
-            __syncwarp();
-            if (lane == 0) {
+        if (tid == 0) {
+            int big = k;
+            for (int j = k + 1; j < m; ++j)
+                if (upd[j] > upd[big]) big = j;
+            const double bsq = upd[big] * upd[big];
+            if (sh_nzp == size && bsq < sh_thr_help * (rows - k)) sh_nzp = k;
+            transp[k] = big;
+            sh_big = big;
+            if (k != big) {
                 double t = upd[k];
                 upd[k] = upd[big];
                 upd[big] = t;
@@ -235,44 +286,59 @@ __global__ void accel_solve_kernel(const double* rfin, const int* ring, double e
                 dir[big] = t;
             }
         }
-        __syncwarp();
-        // Householder on column k rows k..rows-1
+        __syncthreads();
+        const int big = sh_big;
+        if (k != big)
+            for (int i = tid; i < rows; i += blockDim.x) {
+                const double t = a[(size_t)k * rows + i];
+                a[(size_t)k * rows + i] = a[(size_t)big * rows + i];
+                a[(size_t)big * rows + i] = t;
+            }
+        __syncthreads();
+        // Householder on column k rows k..rows-1 (Eigen makeHouseholder)
         double* col = a + (size_t)k * rows;
-        double tail = 0.0;
-        for (int i = k + 1 + lane; i < rows; i += 32) tail += col[i] * col[i];
-        tail = warp_sum(tail);
-        const double c0 = col[k];
-        double tau, beta;
-        if (tail <= 2.2250738585072014e-308) {
-            tau = 0.0;
-            beta = c0;
-            for (int i = k + 1 + lane; i < rows; i += 32) col[i] = 0.0;
-        } else {
-            beta = sqrt(c0 * c0 + tail);
-            if (c0 >= 0.0) beta = -beta;
-            const double inv = c0 - beta;
-            for (int i = k + 1 + lane; i < rows; i += 32) col[i] /= inv;
-            tau = (beta - c0) / beta;
+        if (warp == 0) {
+            double tail = 0.0;
+            for (int i = k + 1 + lane; i < rows; i += 32) tail += col[i] * col[i];
+            tail = warp_sum(tail);
+            if (lane == 0) {
+                const double c0 = col[k];
+                double tau, beta, inv = 0.0;
+                if (tail <= 2.2250738585072014e-308) {
+                    tau = 0.0;
+                    beta = c0;
+                } else {
+                    beta = sqrt(c0 * c0 + tail);
+                    if (c0 >= 0.0) beta = -beta;
+                    inv = c0 - beta;
+                    tau = (beta - c0) / beta;
+                }
+                sh_tau = tau;
+                sh_beta = beta;
+                sh_inv = inv;
+                hc[k] = tau;
+                sh_maxpivot = fmax(sh_maxpivot, fabs(beta));
+            }
         }
-        __syncwarp();
-        if (lane == 0) {
-            col[k] = beta;
-            hc[k] = tau;
-        }
-        maxpivot = fmax(maxpivot, fabs(beta));
-        __syncwarp();
-        // apply to columns k+1.. (one lane per column)
-        for (int j = k + 1 + lane; j < m; j += 32) {
+        __syncthreads();
+        const double tau = sh_tau, inv = sh_inv;
+        for (int i = k + 1 + tid; i < rows; i += blockDim.x) col[i] = (inv == 0.0) ? 0.0 : col[i] / inv;
+        __syncthreads();
+        if (tid == 0) col[k] = sh_beta;
+        // apply to columns k+1.. (one warp per column, lanes over rows) + norm downdate
+        for (int j = k + 1 + warp; j < m; j += nw) {
             double* cj = a + (size_t)j * rows;
             if (rows - k == 1) {
-                cj[k] *= (1.0 - tau);
+                if (lane == 0) cj[k] *= (1.0 - tau);
             } else if (tau != 0.0) {
-                double t = cj[k];
-                for (int i = k + 1; i < rows; ++i) t += col[i] * cj[i];
-                cj[k] -= tau * t;
-                for (int i = k + 1; i < rows; ++i) cj[i] -= tau * col[i] * t;
+                double t = 0.0;
+                for (int i = k + 1 + lane; i < rows; i += 32) t += col[i] * cj[i];
+                t = warp_sum(t) + cj[k];
+                for (int i = k + 1 + lane; i < rows; i += 32) cj[i] -= tau * col[i] * t;
+                __syncwarp();
+                if (lane == 0) cj[k] -= tau * t;
             }
-            // norm downdate
+            __syncwarp();
             if (upd[j] != 0.0) {
                 double t = fabs(cj[k]) / upd[j];
                 t = (1.0 + t) * (1.0 - t);
@@ -280,69 +346,90 @@ __global__ void accel_solve_kernel(const double* rfin, const int* ring, double e
                 const double ratio = upd[j] / dir[j];
                 const double t2 = t * ratio * ratio;
                 if (t2 <= down_thr) {
-                    double s = 0.0;
-                    for (int i = k + 1; i < rows; ++i) s += cj[i] * cj[i];
-                    dir[j] = sqrt(s);
-                    upd[j] = dir[j];
+                    double s2 = 0.0;
+                    for (int i = k + 1 + lane; i < rows; i += 32) s2 += cj[i] * cj[i];
+                    s2 = warp_sum(s2);
+                    __syncwarp();
+                    if (lane == 0) upd[j] = dir[j] = sqrt(s2);
                 } else {
-                    upd[j] *= sqrt(t);
+                    __syncwarp();
+                    if (lane == 0) upd[j] *= sqrt(t);
                 }
             }
+            __syncwarp();
         }
-        __syncwarp();
+        __syncthreads();
     }
-    if (lane == 0) {
+    if (tid == 0) {
         for (int k = 0; k < size; ++k) {
             const int t = perm[k];
             perm[k] = perm[transp[k]];
             perm[transp[k]] = t;
         }
-        const double thr = maxpivot * epsm * size;
+        const double thr = sh_maxpivot * epsm * size;
         int nz = 0;
-        for (int i = 0; i < nzp; ++i) nz += (fabs(a[(size_t)i * rows + i]) > thr) ? 1 : 0;
-        for (int j = 0; j < m; ++j) al[j] = 0.0;
-        if (nz > 0) {
-            double c[128];
-            for (int i = 0; i < rows; ++i) c[i] = bvec[i];
-            for (int k = 0; k < nz; ++k) {
-                const double tau = hc[k];
-                const int n = rows - k;
-                if (n == 1) {
-                    c[k] *= (1.0 - tau);
-                    continue;
-                }
-                if (tau == 0.0) continue;
-                double t = c[k];
-                for (int i = 1; i < n; ++i) t += a[(size_t)k * rows + k + i] * c[k + i];
-                c[k] -= tau * t;
-                for (int i = 1; i < n; ++i) c[k + i] -= tau * a[(size_t)k * rows + k + i] * t;
-            }
-            for (int i = nz - 1; i >= 0; --i) {
-                double s = c[i];
-                for (int j = i + 1; j < nz; ++j) s -= a[(size_t)j * rows + i] * c[j];
-                c[i] = s / a[(size_t)i * rows + i];
-            }
-            for (int i = 0; i < nz; ++i) al[perm[i]] = c[i];
-        }
-        // residual_rel = ||(R_P^T R_P + delta I) alpha - rhs|| / ||rhs||
-        double rr = 0.0;
-        for (int i = 0; i < m; ++i) {
-            double s = 0.0;
-            for (int j = 0; j < m; ++j) {
-                double gij = 0.0;
-                const int top = min(i, j);
-                for (int q = 0; q <= top; ++q) gij += rfin[(size_t)i * C + q] * rfin[(size_t)j * C + q];
-                if (i == j) gij += delta;
-                s += gij * al[j];
-            }
-            s -= rhs[i];
-            rr += s * s;
-        }
-        scal[0] = sqrt(rr) / rn;
-        scal[2] = delta;
+        for (int i = 0; i < sh_nzp; ++i) nz += (fabs(a[(size_t)i * rows + i]) > thr) ? 1 : 0;
+        sh_nz = nz;
     }
-    __syncwarp();
-    for (int j = lane; j < m; j += 32) alpha[j] = al[j];
+    for (int i = tid; i < rows; i += blockDim.x) cvec[i] = bvec[i];
+    for (int j = tid; j < m; j += blockDim.x) al[j] = 0.0;
+    __syncthreads();
+    const int nz = sh_nz;
+    // c <- Q^T b (the nz reflectors in order), then back substitution on the leading nz x nz
+    for (int k = 0; k < nz; ++k) {
+        const double tk = hc[k];
+        const int n = rows - k;
+        if (n == 1) {
+            if (tid == 0) cvec[k] *= (1.0 - tk);
+            __syncthreads();
+            continue;
+        }
+        if (tk == 0.0) continue;
+        if (warp == 0) {
+            double t = 0.0;
+            for (int i = 1 + lane; i < n; i += 32) t += a[(size_t)k * rows + k + i] * cvec[k + i];
+            t = warp_sum(t) + cvec[k];
+            if (lane == 0) sh_tau = t;
+        }
+        __syncthreads();
+        const double t = sh_tau;
+        for (int i = 1 + tid; i < n; i += blockDim.x) cvec[k + i] -= tk * a[(size_t)k * rows + k + i] * t;
+        if (tid == 0) cvec[k] -= tk * t;
+        __syncthreads();
+    }
+    for (int i = nz - 1; i >= 0; --i) {
+        if (warp == 0) {
+            double s2 = 0.0;
+            for (int j = i + 1 + lane; j < nz; j += 32) s2 += a[(size_t)j * rows + i] * cvec[j];
+            s2 = warp_sum(s2);
+            if (lane == 0) cvec[i] = (cvec[i] - s2) / a[(size_t)i * rows + i];
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < nz; i += blockDim.x) al[perm[i]] = cvec[i];
+    __syncthreads();
+    // residual_rel = ||(R_P^T R_P + delta I) alpha - rhs|| / ||rhs||  via y = R_P alpha
+    for (int i = tid; i < m; i += blockDim.x) {
+        double y = 0.0;
+        for (int j = i; j < m; ++j) y += rf[(size_t)j * C + i] * al[j];
+        yv[i] = y;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double rr = 0.0;
+        for (int j = lane; j < m; j += 32) {
+            double z = delta * al[j];
+            for (int i = 0; i <= j; ++i) z += rf[(size_t)j * C + i] * yv[i];
+            z -= rhs[j];
+            rr += z * z;
+        }
+        rr = warp_sum(rr);
+        if (lane == 0) {
+            scal[0] = sqrt(rr) / rn;
+            scal[2] = delta;
+        }
+    }
+    for (int j = tid; j < m; j += blockDim.x) alpha[j] = al[j];
 }
 
 struct UpdParams {
@@ -467,9 +554,9 @@ void accelerate_device(AccelWork& a, const double* wu, const double* wg, const i
         cnt = g;
         src ^= 1;
     }
-    const size_t ssmem = sizeof(double) * 2 * (size_t)a.cap * a.cap;
+    const size_t ssmem = sizeof(double) * (2 * (size_t)a.cap * a.cap + (size_t)C * C);
     CPFIT_CUDA(cudaFuncSetAttribute(accel_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
-    accel_solve_kernel<<<1, 32, ssmem, st>>>(a.rbuf[src], ring, eps, a.alpha, a.scal);
+    accel_solve_kernel<<<1, kSolveThreads, ssmem, st>>>(a.rbuf[src], ring, eps, a.alpha, a.scal);
     CPFIT_CUDA(cudaGetLastError());
     UpdParams u{};
     u.n = a.n;

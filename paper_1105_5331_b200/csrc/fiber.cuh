@@ -21,8 +21,8 @@
 // the fp64 pipe. The M0 m-tiles are spread so each SM scheduler (warp w issues on w % 4) gets
 // the same DMMA work (fiber_schedule). Hand-offs are mbarrier phases only.
 // Shared-memory layouts: T rows padded to I0s = 32 NC + 4 doubles (4 mod 16) and W rows to
-// RP + 4 doubles; A0 rows of RP doubles with the column index XOR-swizzled by (row & 1) * 8 for
-// RP = 16 — every DMMA fragment load is conflict free (two wavefronts per 32 doubles).
+// RP + 4 doubles; A0 rows of RP doubles with an XOR column swizzle (a0s_index) — every DMMA
+// fragment load is conflict free (two wavefronts per 32 doubles).
 #pragma once
 
 constexpr int kFStages = 3;
@@ -196,10 +196,14 @@ __device__ __forceinline__ FiberIndex<ORD> advance_fiber(const FiberParams& p, F
     return x;
 }
 
-// shared-memory A0 position of (i, r): rows of RP doubles, XOR swizzle for RP = 16
+// shared-memory A0 position of (i, r): rows of RP doubles, column XOR-swizzled so the 16 lanes of
+// each half-warp of a DMMA fragment load (rows i = 4k + lane%4, columns r = 8t + lane/4, or the
+// transposed pattern) hit 16 distinct 8-byte bank pairs
 template <int RP>
 __device__ __forceinline__ int a0s_index(int i, int r) {
-    return i * RP + (RP == 16 ? (r ^ ((i & 1) << 3)) : r);
+    if (RP == 16) return i * 16 + (r ^ ((i & 3) << 2));
+    if (RP == 8) return i * 8 + (r ^ ((i & 2) << 1));
+    return i * RP + r;
 }
 
 template <int RP, int F, int ORD>
