@@ -187,15 +187,15 @@ __global__ void tsqr_kernel(const TsqrParams p) {
 // largest updated column norm, LAPACK-style norm downdating with recomputation, threshold rank),
 // one block of kSolveThreads: R staged in shared memory once; each Householder step is one warp's
 // norm + scalars, then the remaining columns are updated one warp per column (lanes over rows).
-constexpr int kSolveThreads = 256;
+constexpr int kSolveThreads = 512;
 
 __global__ void __launch_bounds__(kSolveThreads) accel_solve_kernel(const double* rfin, const int* ring, double eps,
                                                                     double* alpha, double* scal) {
     extern __shared__ double sm[];  // a: 2m x m stacked system (col-major), rf: C x C
     __shared__ double bvec[128], cvec[128], upd[64], dir[64], hc[64], rhs[64], al[64], colsq[64], yv[64];
     __shared__ int perm[64], transp[64];
-    __shared__ double sh_delta, sh_rn, sh_thr_help, sh_maxpivot, sh_tau, sh_beta, sh_inv;
-    __shared__ int sh_big, sh_nzp, sh_nz;
+    __shared__ double sh_delta, sh_rn, sh_thr_help, sh_maxpivot, sh_tau;
+    __shared__ int sh_nzp, sh_nz;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int m = ring[0];
     const int C = m + 1;
@@ -269,62 +269,73 @@ __global__ void __launch_bounds__(kSolveThreads) accel_solve_kernel(const double
     const double down_thr = sqrt(epsm);
     const int size = m;
     for (int k = 0; k < size; ++k) {
-        if (tid == 0) {
-            int big = k;
-            for (int j = k + 1; j < m; ++j)
-                if (upd[j] > upd[big]) big = j;
-            const double bsq = upd[big] * upd[big];
-            if (sh_nzp == size && bsq < sh_thr_help * (rows - k)) sh_nzp = k;
-            transp[k] = big;
-            sh_big = big;
-            if (k != big) {
-                double t = upd[k];
-                upd[k] = upd[big];
-                upd[big] = t;
-                t = dir[k];
-                dir[k] = dir[big];
-                dir[big] = t;
-            }
-        }
-        __syncthreads();
-        const int big = sh_big;
-        if (k != big)
-            for (int i = tid; i < rows; i += blockDim.x) {
-                const double t = a[(size_t)k * rows + i];
-                a[(size_t)k * rows + i] = a[(size_t)big * rows + i];
-                a[(size_t)big * rows + i] = t;
-            }
-        __syncthreads();
-        // Householder on column k rows k..rows-1 (Eigen makeHouseholder)
         double* col = a + (size_t)k * rows;
         if (warp == 0) {
+            // pivot: first column of largest updated norm among k..m-1 (lane-strided candidates,
+            // then a shuffle argmax that keeps the smallest index on ties)
+            double bv = -1.0;
+            int bi = m;
+            for (int j = k + lane; j < m; j += 32)
+                if (upd[j] > bv) {
+                    bv = upd[j];
+                    bi = j;
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ov > bv || (ov == bv && oi < bi)) {
+                    bv = ov;
+                    bi = oi;
+                }
+            }
+            const int big = bi;
+            if (lane == 0) {
+                const double bsq = upd[big] * upd[big];
+                if (sh_nzp == size && bsq < sh_thr_help * (rows - k)) sh_nzp = k;
+                transp[k] = big;
+                if (k != big) {
+                    double t = upd[k];
+                    upd[k] = upd[big];
+                    upd[big] = t;
+                    t = dir[k];
+                    dir[k] = dir[big];
+                    dir[big] = t;
+                }
+            }
+            if (k != big)
+                for (int i = lane; i < rows; i += 32) {
+                    const double t = col[i];
+                    col[i] = a[(size_t)big * rows + i];
+                    a[(size_t)big * rows + i] = t;
+                }
+            __syncwarp();
+            // Householder on column k rows k..rows-1 (Eigen makeHouseholder)
             double tail = 0.0;
             for (int i = k + 1 + lane; i < rows; i += 32) tail += col[i] * col[i];
             tail = warp_sum(tail);
+            const double c0 = col[k];
+            double tau, beta, inv = 0.0;
+            if (tail <= 2.2250738585072014e-308) {
+                tau = 0.0;
+                beta = c0;
+            } else {
+                beta = sqrt(c0 * c0 + tail);
+                if (c0 >= 0.0) beta = -beta;
+                inv = c0 - beta;
+                tau = (beta - c0) / beta;
+            }
+            for (int i = k + 1 + lane; i < rows; i += 32) col[i] = (inv == 0.0) ? 0.0 : col[i] / inv;
+            __syncwarp();
             if (lane == 0) {
-                const double c0 = col[k];
-                double tau, beta, inv = 0.0;
-                if (tail <= 2.2250738585072014e-308) {
-                    tau = 0.0;
-                    beta = c0;
-                } else {
-                    beta = sqrt(c0 * c0 + tail);
-                    if (c0 >= 0.0) beta = -beta;
-                    inv = c0 - beta;
-                    tau = (beta - c0) / beta;
-                }
+                col[k] = beta;
                 sh_tau = tau;
-                sh_beta = beta;
-                sh_inv = inv;
                 hc[k] = tau;
                 sh_maxpivot = fmax(sh_maxpivot, fabs(beta));
             }
         }
         __syncthreads();
-        const double tau = sh_tau, inv = sh_inv;
-        for (int i = k + 1 + tid; i < rows; i += blockDim.x) col[i] = (inv == 0.0) ? 0.0 : col[i] / inv;
-        __syncthreads();
-        if (tid == 0) col[k] = sh_beta;
+        const double tau = sh_tau;
         // apply to columns k+1.. (one warp per column, lanes over rows) + norm downdate
         for (int j = k + 1 + warp; j < m; j += nw) {
             double* cj = a + (size_t)j * rows;
