@@ -61,7 +61,12 @@ struct Ctl {
     int restart_on_ascent;
     LsParams ls;
     int als_mode;  // 1: stand-alone ALS trace semantics
+    int eager;     // 1: host-driven loop (no graph conditionals; profiling / launch lists)
 };
+
+__device__ __forceinline__ void set_cond(const Ctl& c, cudaGraphConditionalHandle h, bool v) {
+    if (!c.eager) cudaGraphSetConditional(h, v ? 1u : 0u);
+}
 
 __device__ double fit_h(double f, double scale) { return sqrt(fmax(2.0 * f, 0.0)) / scale; }
 
@@ -111,7 +116,7 @@ __global__ void k_after_init(Ctl c) {
 
 __global__ void k_set_cond_running(Ctl c, cudaGraphConditionalHandle h) {
     const DevState& s = *c.s;
-    cudaGraphSetConditional(h, (s.stop < 0 && s.iter < s.max_iters) ? 1u : 0u);
+    set_cond(c, h, s.stop < 0 && s.iter < s.max_iters);
 }
 
 __global__ void k_after_bar(Ctl c) {
@@ -139,7 +144,7 @@ __global__ void k_ls_init(Ctl c, cudaGraphConditionalHandle ls_h) {
     } else {
         s.searching = s.mt.begin(c.ls, s.f_bar, s.slope) ? 1 : 0;
     }
-    cudaGraphSetConditional(ls_h, s.searching ? 1u : 0u);
+    set_cond(c, ls_h, s.searching != 0);
 }
 
 __global__ void k_trial(const DevState* s, const double* ub, const double* d, double* ut, int64_t n) {
@@ -162,11 +167,11 @@ __global__ void k_ls_update(Ctl c, cudaGraphConditionalHandle ls_h) {
             s.beta = s.mt.out_step;
         }
     }
-    cudaGraphSetConditional(ls_h, s.searching ? 1u : 0u);
+    set_cond(c, ls_h, s.searching != 0);
 }
 
 __global__ void k_accept_cond(Ctl c, cudaGraphConditionalHandle h) {
-    cudaGraphSetConditional(h, c.s->accepted ? 1u : 0u);
+    set_cond(c, h, c.s->accepted != 0);
 }
 
 __global__ void k_step_point(const DevState* s, const double* ub, const double* d, double* out, int64_t n) {
@@ -272,7 +277,7 @@ __global__ void k_commit(Ctl c, cudaGraphConditionalHandle loop_h) {
             s.stop = 0;
     }
     // the iteration budget is not a stored stop: a later run_loop() may extend it
-    cudaGraphSetConditional(loop_h, (s.stop < 0 && s.iter < s.max_iters) ? 1u : 0u);
+    set_cond(c, loop_h, s.stop < 0 && s.iter < s.max_iters);
 }
 
 // Vector part of the commit: u, g <- chosen pair; window slot; best iterate.
@@ -412,6 +417,7 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     CPFIT_CUDA(cudaMemset(sc_, 0, sizeof(EvalScalars) * 4));
     CPFIT_CUDA(cudaMalloc(&state_, sizeof(DevState)));
     CPFIT_CUDA(cudaMemset(state_, 0, sizeof(DevState)));
+    if (const char* e = std::getenv("CPFIT_EAGER"); e && e[0] == '1') eager_ = true;
     if (const char* e = std::getenv("CPFIT_PHASE_PROFILE"); e && e[0] == '1') {
         CPFIT_CUDA(cudaMalloc(&phase_, sizeof(unsigned long long) * (2 * kPhases + 1)));
         CPFIT_CUDA(cudaMemset(phase_, 0, sizeof(unsigned long long) * (2 * kPhases + 1)));
@@ -463,6 +469,8 @@ void Solver::build_graphs() {
     c.restart_on_ascent = opt_.restart_on_ascent;
     c.ls = LsParams{opt_.ftol, opt_.gtol, opt_.initial_step, opt_.max_evals, opt_.step_min, opt_.step_max};
     c.als_mode = (method_ == 1);
+    static_assert(sizeof(Ctl) <= sizeof(ctl_blob_), "ctl blob");
+    std::memcpy(ctl_blob_, &c, sizeof(Ctl));
     int* status = &s->status;
     const int vb = vec_blocks(n_);
     // phases: 0 ALS sweep, 1 eval(u_bar), 2 accelerate + LS init, 3 LS trial eval, 4 LS update,
@@ -593,8 +601,78 @@ void Solver::run_loop(int max_iters_total) {
     host_max_ = max_iters_total;
     DevState* s = reinterpret_cast<DevState*>(state_);
     CPFIT_CUDA(cudaMemcpyAsync(&s->max_iters, &host_max_, sizeof(int), cudaMemcpyHostToDevice, st_));
+    if (eager_) {
+        run_loop_eager();
+        return;
+    }
     CPFIT_CUDA(cudaGraphLaunch(x_loop_, st_));
     ++loop_launches_;
+}
+
+// The loop graph's iteration issued kernel by kernel on one stream with the control flow on the
+// host (one device-state read per decision). Same kernels, same order; for profilers that do
+// not see into graph conditional bodies (ncu launch lists). CPFIT_EAGER=1 at construction.
+void Solver::run_loop_eager() {
+    Ctl c;
+    std::memcpy(&c, ctl_blob_, sizeof(Ctl));
+    c.eager = 1;
+    DevState* s = reinterpret_cast<DevState*>(state_);
+    EvalScalars* sc_bar = reinterpret_cast<EvalScalars*>(sc_) + 1;
+    EvalScalars* sc_trial = reinterpret_cast<EvalScalars*>(sc_) + 2;
+    EvalScalars* sc_next = reinterpret_cast<EvalScalars*>(sc_) + 3;
+    int* status = &s->status;
+    const int vb = vec_blocks(n_);
+    const cudaGraphConditionalHandle none = 0;
+    auto state = [&] {
+        DevState hs;
+        CPFIT_CUDA(cudaMemcpyAsync(&hs, state_, sizeof(DevState), cudaMemcpyDeviceToHost, st_));
+        sync();
+        return hs;
+    };
+    for (;;) {
+        DevState hs = state();
+        if (!(hs.stop < 0 && hs.iter < hs.max_iters)) break;
+        if (method_ == 0) {
+            als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st_, m0_cur_);
+            eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st_, true, &s->resid);
+            if (m0_bar_)
+                CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
+            k_after_bar<<<1, 1, 0, st_>>>(c);
+            accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st_);
+            k_ls_init<<<1, 1, 0, st_>>>(c, none);
+            while (state().searching) {
+                k_trial<<<vb, 256, 0, st_>>>(s, ub_, d_, ut_, n_);
+                eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st_, true, &s->resid);
+                k_ls_update<<<1, 1, 0, st_>>>(c, none);
+                if (!opt_.reeval_accepted)
+                    k_keep_best<<<vb, 256, 0, st_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
+            }
+            k_accept_cond<<<1, 1, 0, st_>>>(c, none);
+            if (state().accepted) {
+                if (opt_.reeval_accepted) {
+                    k_step_point<<<vb, 256, 0, st_>>>(s, ub_, d_, ut_, n_);
+                    grams_device(*w_, ut_, st_);
+                    normalize_device(*w_, ut_, un_, st_);
+                    eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid);
+                    if (m0_cur_)
+                        CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
+                    k_after_next<<<1, 1, 0, st_>>>(c);
+                } else {
+                    k_select_accepted<<<vb, 256, 0, st_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
+                    grams_device(*w_, ut_, st_);
+                    const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st_, m0_sel_, m0_cur_);
+                    k_after_rescale<<<1, 1, 0, st_>>>(c, sc_next, red_, nb);
+                }
+            }
+        } else {
+            als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, t_->sparse ? nullptr : w_->m0);
+            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid);
+        }
+        k_commit<<<1, 1, 0, st_>>>(c, none);
+        k_commit_vec<<<vb, 256, 0, st_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,
+                                          m0_cur_, m0_n_);
+        CPFIT_CUDA(cudaGetLastError());
+    }
 }
 
 bool Solver::phase_times(double* out, int64_t* cnt) {

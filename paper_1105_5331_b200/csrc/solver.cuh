@@ -75,6 +75,9 @@ public:
 
 private:
     void build_graphs();
+    void run_loop_eager();
+    bool eager_ = false;
+    alignas(16) unsigned char ctl_blob_[512] = {};  // the control-kernel parameters (solver.cu Ctl)
     DevTensor* t_;
     int R_;
     SolverOptions opt_;
