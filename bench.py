@@ -257,11 +257,17 @@ def main():
             hbm_src = "measured"
         except (OSError, KeyError, ValueError):
             hbm_peak, hbm_src = 6650.0, "fallback"
+        try:  # DRAM bytes per launch of this kernel from the committed ncu capture (profiles/)
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["fused_fiber_pass_c2"]
+            traffic = tr["bytes_per_launch"] if tuple(dims) == (400, 400, 400) and R == 16 else None
+        except (OSError, KeyError, ValueError):
+            traffic = None
         tf = flops / (fused_ms * 1e-3) / 1e12
         gbs = bytes_alg / (fused_ms * 1e-3) / 1e9
         roof = {"bound": "tensor", "kernel": "fiber_ws_kernel<16,16> (fused S + M0 + per-fiber f, DMMA fp64)",
                 "achieved": round(tf, 3), "peak": round(dmma_peak, 3), "unit": "TFLOP/s",
-                "frac": round(tf / dmma_peak, 4), "traffic": None,
+                "frac": round(tf / dmma_peak, 4), "traffic": traffic,
+                "traffic_source": "profiles/traffic.json (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
                 "peak_source": "DMMA m8n8k4 f64 issue loop measured in-process (MEASURED_PEAKS.json has no fp64)",
                 "ms_per_launch": round(fused_ms, 5), "alg_flops_per_launch": flops, "alg_bytes_per_launch": bytes_alg,
                 "hbm": {"achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
