@@ -124,6 +124,14 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
                                        sizeof(double) * (size_t)(w.fiber_grid - grid) * w.RP * 32 * w.fiber_nchunk, st));
         if (do_f) CPFIT_CUDA(cudaMemsetAsync(w.f_part + grid, 0, sizeof(double) * (w.fiber_grid - grid), st));
     }
+    if (do_s && !do_m0 && !do_f) {  // S only: every warp on S
+        switch (w.RP) {
+            case 8: launch_spass<8>(p, grid, st); break;
+            case 16: launch_spass<16>(p, grid, st); break;
+            default: launch_spass<32>(p, grid, st); break;
+        }
+        return;
+    }
     switch (w.RP) {
         case 8: launch_fiber<8>(p, grid, w.fiber_smem, st); break;
         case 16: launch_fiber<16>(p, grid, w.fiber_smem, st); break;
@@ -587,7 +595,8 @@ EvalWork* work_create(const DevTensor& t, int R) {
         w->fiber_nchunk = (I0 + 31) / 32;
         if (w->fiber_nchunk > 13) throw std::invalid_argument("device dense path supports I_1 <= 416");
         w->fiber_smem = fiber_smem(w->RP, w->fiber_nchunk, I0);
-        if (w->fiber_smem > 227 * 1024) throw std::invalid_argument("fiber tile does not fit shared memory");
+        if (std::max(w->fiber_smem, spass_smem(w->RP, w->fiber_nchunk, I0)) > 227 * 1024)
+            throw std::invalid_argument("fiber tile does not fit shared memory");
         const int64_t ntiles = (t.J + w->fiber_F - 1) / w->fiber_F;
         const int per_sm = std::max(1, std::min(2048 / fiber_threads(w->RP),
                                                 (int)((228 * 1024) / (w->fiber_smem + 1024))));

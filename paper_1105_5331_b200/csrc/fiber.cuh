@@ -52,7 +52,7 @@ struct FiberRoles {
 static_assert(FiberRoles<32>::WARPS <= 16 && FiberRoles<16>::WARPS <= 16, "<= 512 threads (128 registers)");
 
 struct FiberSmem {
-    size_t tiles, a0, wbuf, gam, bars, total;
+    size_t tiles, a0, wbuf, gam, spart, bars, total;
 };
 
 // A0 rows staged in shared memory: every row an M0 warp's m-tiles touch (8 ceil(I0 / 8) >= ldT)
@@ -555,5 +555,175 @@ size_t fiber_smem(int RP, int nchunk, int64_t I0) {
         case 8: return fiber_layout<8, kFiberF>(nchunk, I0).total;
         case 16: return fiber_layout<16, kFiberF>(nchunk, I0).total;
         default: return fiber_layout<32, kFiberF>(nchunk, I0).total;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// S-only pass (the ALS S' = T x_1 A0' and the MTTKRP of modes >= 1): no W, no M0 — every
+// compute warp takes a K-part of one 8 x 8 sub-tile, so the whole SM issues DMMAs instead of
+// the fused kernel's four S warps; part 0 adds the other parts (in part order) and stores S.
+// ---------------------------------------------------------------------------------------
+template <int RP>
+struct SPassRoles {
+    static constexpr int NRT = RP / 8;
+    static constexpr int NQ = 2 * NRT;                       // 8x8 sub-tiles per tile
+    static constexpr int KSPLIT = RP == 8 ? 6 : (RP == 16 ? 3 : 1);
+    static constexpr int NCW = NQ * KSPLIT;                  // compute warps (12, 12, 8)
+    static constexpr int NPART = NQ * (KSPLIT - 1);
+    static constexpr int WARPS = 1 + NCW;
+};
+
+template <int RP, int F>
+__host__ __device__ FiberSmem spass_layout(int nchunk, int64_t I0) {
+    const int I0s = 32 * nchunk + 4;
+    FiberSmem s{};
+    size_t off = 0;
+    s.tiles = off;
+    off += sizeof(double) * (size_t)kFStages * F * I0s;
+    s.a0 = off;
+    if (FiberRoles<RP>::A0SMEM) off += sizeof(double) * (size_t)a0_rows(I0) * RP;
+    s.spart = off;
+    off += sizeof(double) * (size_t)kFStages * SPassRoles<RP>::NPART * 64;
+    s.wbuf = s.gam = off;
+    s.bars = off;
+    off += sizeof(uint64_t) * 64;
+    s.total = off;
+    return s;
+}
+
+template <int RP, int F>
+__global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(const FiberParams p) {
+    using Ro = SPassRoles<RP>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int NRT = Ro::NRT;
+    const FiberSmem L = spass_layout<RP, F>(p.nchunk, p.I0);
+    const int I0s = p.I0s;
+    const int KS = (int)(p.ldT / 4);
+    double* tiles = reinterpret_cast<double*>(smem_raw + L.tiles);
+    double* a0s = reinterpret_cast<double*>(smem_raw + L.a0);
+    double* spart = reinterpret_cast<double*>(smem_raw + L.spart);  // [stage][NPART][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
+    uint64_t* tfull = bars;       // [kFStages]
+    uint64_t* tempty = bars + 3;  // [kFStages] compute warps
+    uint64_t* pfull = bars + 6;   // [kFStages][NQ] the other K-parts of a sub-tile
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t t_begin = (int64_t)blockIdx.x * p.tiles_per_cta;
+    const int64_t t_end = imin64(p.ntiles, t_begin + p.tiles_per_cta);
+    const int64_t ntl = t_end > t_begin ? t_end - t_begin : 0;
+
+    for (int64_t e = tid; e < (int64_t)kFStages * F * I0s; e += blockDim.x) tiles[e] = 0.0;
+    if (FiberRoles<RP>::A0SMEM)
+        for (int64_t e = tid; e < a0_rows(p.I0) * RP; e += blockDim.x) {
+            const int i = (int)(e / RP), r = (int)(e % RP);
+            a0s[a0s_index<RP>(i, r)] = (i < p.I0 && r < p.R) ? p.A0[(int64_t)r * p.I0 + i] : 0.0;
+        }
+    if (tid == 0) {
+        for (int s = 0; s < kFStages; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], Ro::NCW);
+            for (int q = 0; q < Ro::NQ; ++q) mbar_init(&pfull[s * Ro::NQ + q], Ro::KSPLIT > 1 ? Ro::KSPLIT - 1 : 1);
+        }
+    }
+    mbar_fence_init();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    auto a0_at = [&](int i, int r) -> double {
+        if (FiberRoles<RP>::A0SMEM) return a0s[a0s_index<RP>(i, r)];
+        return (i < p.I0 && r < p.R) ? __ldg(p.A0 + (int64_t)r * p.I0 + i) : 0.0;
+    };
+
+    if (warp == 0) {
+        for (int64_t k = 0; k < ntl; ++k) {
+            const int s = (int)(k % kFStages);
+            const int64_t f0 = (t_begin + k) * F;
+            if (k >= kFStages) mbar_wait(&tempty[s], (uint32_t)(((k / kFStages) - 1) & 1));
+            const int nvalid = (int)imin64(F, p.J - f0);
+            double* st = tiles + (size_t)s * F * I0s;
+            if (nvalid < F)
+                for (int e = lane; e < (F - nvalid) * I0s; e += 32) st[(size_t)nvalid * I0s + e] = 0.0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
+            __syncwarp();
+            if (lane < nvalid)
+                bulk_g2s(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s]);
+        }
+        return;
+    }
+    const int c = warp - 1;
+    const int q = c % Ro::NQ, h = c / Ro::NQ;
+    const int ft = q / NRT, nt = q % NRT;
+    const int fl = ft * 8 + (lane >> 2);
+    const int rr = nt * 8 + (lane >> 2);
+    const int k_lo = (int)((int64_t)KS * h / Ro::KSPLIT), k_hi = (int)((int64_t)KS * (h + 1) / Ro::KSPLIT);
+    for (int64_t k = 0; k < ntl; ++k) {
+        const int s = (int)(k % kFStages);
+        const int64_t f0 = (t_begin + k) * F;
+        mbar_wait(&tfull[s], (uint32_t)((k / kFStages) & 1));
+        const double* ta = tiles + (size_t)s * F * I0s + fl * I0s + (lane & 3);
+        constexpr int U = 8;
+        double acc[U][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u][0] = acc[u][1] = 0.0;
+        int ks = k_lo;
+        for (; ks + U <= k_hi; ks += U) {
+            double a[U], bb[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                a[u] = ta[(ks + u) * 4];
+                bb[u] = a0_at((ks + u) * 4 + (lane & 3), rr);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) dmma_8x8x4(acc[u][0], acc[u][1], a[u], bb[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U - 1; ++u)
+            if (ks + u < k_hi)
+                dmma_8x8x4(acc[u][0], acc[u][1], ta[(ks + u) * 4], a0_at((ks + u) * 4 + (lane & 3), rr));
+        double sv0 = ((acc[0][0] + acc[4][0]) + (acc[1][0] + acc[5][0])) + ((acc[2][0] + acc[6][0]) + (acc[3][0] + acc[7][0]));
+        double sv1 = ((acc[0][1] + acc[4][1]) + (acc[1][1] + acc[5][1])) + ((acc[2][1] + acc[6][1]) + (acc[3][1] + acc[7][1]));
+        if (h > 0) {
+            // this stage's slot is refilled only after part 0 has read it (it releases the T
+            // stage after the read)
+            double* sp = spart + ((size_t)s * Ro::NPART + q * (Ro::KSPLIT - 1) + (h - 1)) * 64 + 2 * lane;
+            sp[0] = sv0;
+            sp[1] = sv1;
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&pfull[s * Ro::NQ + q]);
+                mbar_arrive(&tempty[s]);
+            }
+            continue;
+        }
+        if (Ro::KSPLIT > 1) {
+            mbar_wait(&pfull[s * Ro::NQ + q], (uint32_t)((k / kFStages) & 1));
+#pragma unroll
+            for (int hh = 1; hh < Ro::KSPLIT; ++hh) {
+                const double* sp = spart + ((size_t)s * Ro::NPART + q * (Ro::KSPLIT - 1) + (hh - 1)) * 64 + 2 * lane;
+                sv0 += sp[0];
+                sv1 += sp[1];
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[s]);
+        const int r = nt * 8 + 2 * (lane & 3);
+        if (f0 + fl < p.J) *reinterpret_cast<double2*>(p.S_out + (f0 + fl) * RP + r) = make_double2(sv0, sv1);
+    }
+}
+
+template <int RP>
+void launch_spass(const FiberParams& p, int grid, cudaStream_t st) {
+    const size_t smem = spass_layout<RP, kFiberF>(p.nchunk, p.I0).total;
+    auto k = spass_kernel<RP, kFiberF>;
+    CPFIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 32 * SPassRoles<RP>::WARPS, smem, st>>>(p);
+    CPFIT_CUDA(cudaGetLastError());
+}
+
+size_t spass_smem(int RP, int nchunk, int64_t I0) {
+    switch (RP) {
+        case 8: return spass_layout<8, kFiberF>(nchunk, I0).total;
+        case 16: return spass_layout<16, kFiberF>(nchunk, I0).total;
+        default: return spass_layout<32, kFiberF>(nchunk, I0).total;
     }
 }
