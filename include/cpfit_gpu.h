@@ -135,6 +135,11 @@ int cpfit_solver_destroy(cpfit_solver s);
 /* kernels of this library launched by the solver's loop graphs since cpfit_solver_init
  * (counted from the captured graph bodies x the device-side iteration / line-search counters) */
 int cpfit_solver_launches(cpfit_solver s, int64_t* launches);
+/* phi(a) = f(u_bar + a d) and phi'(a) = g(u_bar + a d).d at the n steps alphas[], evaluated from
+ * the degree-6 polynomial the device line search uses (dense order-3 tensors; the reference
+ * evaluates objective_and_gradient at each trial, ngmres.cpp:113-126). Parity / diagnostics. */
+int cpfit_line_polynomial(cpfit_tensor t, int64_t rank, const double* u_bar, const double* d, const double* alphas,
+                          int64_t n, double* phi, double* dphi);
 /* Diagnostic: fiber-pass barrier-wait cycles by role (12 counters; nonzero only in a library
  * built with -DCPFIT_FIBER_PROF, see tools/fiber_prof.py); reset != 0 clears them. */
 int cpfit_fiber_prof(uint64_t* out, int reset);

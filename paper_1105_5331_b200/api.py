@@ -106,6 +106,7 @@ _SIGS = {
     "cpfit_solver_best": (C.c_int, [C.c_void_p, _f64p]),
     "cpfit_solver_iterate": (C.c_int, [C.c_void_p, _f64p]),
     "cpfit_solver_launches": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "cpfit_line_polynomial": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p, _f64p, C.c_int64, _f64p, _f64p]),
     "cpfit_solver_phase_times": (C.c_int, [C.c_void_p, _f64p, C.POINTER(C.c_int64)]),
     "cpfit_measure_fp64_peak": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "cpfit_host_register": (C.c_int, [C.c_void_p, C.c_int64]),
@@ -275,6 +276,16 @@ def objective_and_gradient(t: DataTensor, u):
 
 def gradient(t, u):
     return objective_and_gradient(t, u)[1]
+
+
+def line_polynomial(t: DataTensor, u_bar, d, alphas):
+    """(phi, dphi) at alphas from the device line-search polynomial (dense order 3)."""
+    ub, r = t._rank(u_bar)
+    dv = _f64(d)
+    al = _f64(alphas)
+    phi, dphi = np.zeros(al.size), np.zeros(al.size)
+    _check(lib.cpfit_line_polynomial(t._h, r, ub, dv, al if al.size else np.zeros(1), al.size, phi, dphi))
+    return phi, dphi
 
 
 def fit_h(t: DataTensor, u) -> float:

@@ -518,6 +518,43 @@ int cpfit_solver_launches(cpfit_solver s, int64_t* launches) {
     return guard([&] { *launches = s->s->summary().launches; });
 }
 
+int cpfit_line_polynomial(cpfit_tensor t, int64_t rank, const double* u_bar, const double* d, const double* alphas,
+                          int64_t n, double* phi, double* dphi) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(t->mu);
+        check_rank(rank);
+        if (!cpfit_gpu::poly_supported(*t->t))
+            throw std::invalid_argument("line polynomial: dense order-3 tensors only");
+        if (n < 0) throw std::invalid_argument("line polynomial: n >= 0");
+        EvalWork& w = t->work((int)rank);
+        check_finite(u_bar, w.nu);
+        check_finite(d, w.nu);
+        DevBuf b(3 * (size_t)w.nu + 3 * (size_t)std::max<int64_t>(n, 1) + 16);
+        double* du = b.p;
+        double* dd_ = du + w.nu;
+        double* dg = dd_ + w.nu;
+        double* da = dg + w.nu;
+        double* dphi_d = da + std::max<int64_t>(n, 1);
+        double* dd2 = dphi_d + std::max<int64_t>(n, 1);
+        EvalScalars* sc = reinterpret_cast<EvalScalars*>(dd2 + std::max<int64_t>(n, 1));
+        int* status = reinterpret_cast<int*>(sc + 1);
+        CPFIT_CUDA(cudaMemcpyAsync(du, u_bar, sizeof(double) * w.nu, cudaMemcpyHostToDevice, t->st));
+        CPFIT_CUDA(cudaMemcpyAsync(dd_, d, sizeof(double) * w.nu, cudaMemcpyHostToDevice, t->st));
+        if (n > 0) CPFIT_CUDA(cudaMemcpyAsync(da, alphas, sizeof(double) * n, cudaMemcpyHostToDevice, t->st));
+        // the evaluation at u_bar leaves S(u_bar) in w.S
+        eval_device(*t->t, w, du, dg, sc, nullptr, status, t->st, true, t->one());
+        std::unique_ptr<cpfit_gpu::PolyWork, void (*)(cpfit_gpu::PolyWork*)> pw(cpfit_gpu::poly_create(*t->t, w),
+                                                                               cpfit_gpu::poly_destroy);
+        cpfit_gpu::poly_build_device(*t->t, w, *pw, du, dd_, t->st);
+        if (n > 0) {
+            cpfit_gpu::poly_eval_device(*pw, da, (int)n, dphi_d, dd2, t->st);
+            CPFIT_CUDA(cudaMemcpyAsync(phi, dphi_d, sizeof(double) * n, cudaMemcpyDeviceToHost, t->st));
+            CPFIT_CUDA(cudaMemcpyAsync(dphi, dd2, sizeof(double) * n, cudaMemcpyDeviceToHost, t->st));
+        }
+        CPFIT_CUDA(cudaStreamSynchronize(t->st));
+    });
+}
+
 int cpfit_fiber_prof(uint64_t* out, int reset) {
     return guard([&] {
         unsigned long long* b = cpfit_gpu::fiber_prof_buffer();

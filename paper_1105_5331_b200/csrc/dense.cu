@@ -86,7 +86,7 @@ void reduce_m0(EvalWork& w, cudaStream_t st) {
 }
 
 void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, bool do_f,
-               const double* gamma0, cudaStream_t st, const int* resid_flag = nullptr) {
+               const double* gamma0, cudaStream_t st, const int* resid_flag = nullptr, double* s_out = nullptr) {
     FiberParams p{};
     p.T = t.T;
     p.ldT = t.ldT;
@@ -108,7 +108,7 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
         p.dims[m] = t.dims[m];
         p.fac[m] = u + w.off[m];
     }
-    p.S_out = w.S;
+    p.S_out = s_out ? s_out : w.S;
     p.m0_part = w.m0_part;
     p.f_part = w.f_part;
     p.gamma0 = gamma0;
@@ -778,6 +778,23 @@ void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, d
             gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, w.lvl_m[mode], 1, 0, 1, out);
     }
     CPFIT_CUDA(cudaGetLastError());
+}
+
+// exported for poly.cu
+void dense_s_pass(const DevTensor& t, EvalWork& w, const double* u, double* S_out, cudaStream_t st) {
+    run_fiber(t, w, u, true, false, false, nullptr, st, nullptr, S_out);
+}
+void eval_given_s_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc,
+                         cudaStream_t st) {
+    grams_device(w, u, st);
+    run_fiber(t, w, u, false, true, false, nullptr, st);  // M0 only
+    reduce_m0(w, st);
+    const double* Sin = w.S;
+    for (int h = 1; h < t.order - 1; ++h) {
+        run_level(t, w, h, Sin, u, true, true, w.lvl_S[h], st);
+        Sin = w.lvl_S[h];
+    }
+    run_grad(t, w, u, g, nullptr, true, sc, st);
 }
 
 // exported for als.cu

@@ -24,7 +24,7 @@ struct DevTensor {
     int64_t dims[kMaxOrder] = {};
     int64_t K = 0;
     bool sparse = false;
-    double norm = 0.0, norm_sq = 0.0;
+    double norm = 0.0, norm_sq = 0.0, norm_sq_lo = 0.0;  // ||T||^2 = norm_sq + norm_sq_lo (dense)
     // dense
     double* T = nullptr;
     int64_t ldT = 0;  // padded fiber stride
@@ -125,6 +125,36 @@ int normalize_grad_device(EvalWork& w, const double* u, const double* g, double*
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
                          int* status, cudaStream_t st, const double* m0_given = nullptr);
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
+
+// Dense pieces for the exact line search (poly.cu): S = T x_1 A (first factor of u) into S_out;
+// and the evaluation at u when w.S already holds T x_1 A0(u) (order 3: M0 pass + level +
+// gradient; scalars->f is NOT the objective — the caller supplies it).
+void dense_s_pass(const DevTensor& t, EvalWork& w, const double* u, double* S_out, cudaStream_t st);
+void eval_given_s_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc,
+                         cudaStream_t st);
+
+// Exact line search along d for order-3 dense tensors (poly.cu): phi(a) = f(u_bar + a d) is a
+// degree-6 polynomial whose coefficients follow from S(u_bar) (in w.S), S_d = T x_1 D0, the
+// factor/direction Grams and ||T||^2; they are built in double-double.
+struct PolyWork {
+    int64_t nchunk_total = 0;
+    double* S_d = nullptr;    // J x RP
+    dd* gpart = nullptr;      // cross-Gram task partials
+    dd* grams = nullptr;      // [3 modes][3 kinds AA, AD, DD][RP*RP]
+    dd* s8part = nullptr;     // per-block partials of the 8 contractions
+    dd* s8 = nullptr;         // the 8 contractions <T, [[X0, X1, X2]]>
+    dd* coef = nullptr;       // phi coefficients [7]
+    unsigned int* counter = nullptr;
+    int s8_grid = 0;
+};
+bool poly_supported(const DevTensor& t);
+PolyWork* poly_create(const DevTensor& t, const EvalWork& w);
+void poly_destroy(PolyWork* p);
+// coefficients of phi from u_bar (its S in w.S) and d
+void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const double* ub, const double* d,
+                       cudaStream_t st);
+// phi(alphas[i]), phi'(alphas[i]) (device arrays)
+void poly_eval_device(const PolyWork& pw, const double* alphas, int n, double* phi, double* dphi, cudaStream_t st);
 
 // Accelerate (ngmres.cpp:27-63) on device.
 struct AccelWork {

@@ -105,6 +105,7 @@ DevTensor* tensor_create_dense(int order, const int64_t* dims, const double* hos
     dd s{0.0, 0.0};
     for (const dd& x : hp) s = dd_add(s, x);
     t->norm_sq = s.hi + s.lo;
+    t->norm_sq_lo = (s.hi - t->norm_sq) + s.lo;  // ||T||^2 = norm_sq + norm_sq_lo in double-double
     t->norm = std::sqrt(t->norm_sq);
     return t;
 }

@@ -277,3 +277,21 @@ def test_swamp_config_within_oracle_envelope(gpu, O, cfg):
     assert res.stop_reason == ref["stop"] == P.GRAD_TOL
     assert abs(res.f - ref["f"]) <= 1e-8 * ref["f"]
     assert 0.9 * min(counts) <= n <= 1.1 * max(counts)
+
+
+@pytest.mark.parametrize("dims,rank", [((20, 20, 20), 3), ((50, 50, 50), 5), ((33, 20, 17), 16), ((120, 100, 80), 16)])
+def test_line_polynomial_matches_direct_evaluations(gpu, dims, rank):
+    """phi(a) = f(u_bar + a d), phi'(a) = g.d from the exact line-search polynomial vs direct
+    objective_and_gradient evaluations (residual form) at the same points."""
+    P = gpu
+    rng = np.random.default_rng(sum(dims) + rank)
+    T, _, _ = P.dense_test_problem(dims, rank, 0.5, 1.0, 1.0, 3, noise_mode=1)
+    t = P.DataTensor.dense(T, dims)
+    ub = P.uniform_initial_guess(dims, rank, 5)
+    d = 0.3 * rng.standard_normal(ub.size)
+    alphas = np.array([0.0, 1e-3, 0.25, 1.0, 1.7, 4.0])
+    phi, dphi = P.line_polynomial(t, ub, d, alphas)
+    for a, f, g in zip(alphas, phi, dphi):
+        fd, gd = P.objective_and_gradient(t, ub + a * d)
+        assert abs(f - fd) <= 1e-12 * abs(fd) + 1e-14 * t.norm() ** 2, (a, f, fd)
+        assert abs(g - gd @ d) <= 1e-10 * (np.linalg.norm(gd) * np.linalg.norm(d) + 1e-300), (a, g, gd @ d)
