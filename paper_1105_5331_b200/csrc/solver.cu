@@ -11,6 +11,7 @@
 // device memory, executed by single-thread kernels between the streaming passes.
 #include "device.cuh"
 #include "linesearch.cuh"
+#include "poly.cuh"
 #include "solver.cuh"
 
 #include <cmath>
@@ -43,6 +44,10 @@ struct DevState {
     // objective form for every evaluation of this solve: 0 per-fiber three-term (4KR),
     // 1 residual (6KR, the reference's form); switched on (sticky) once f stagnates or h is small
     int resid;
+    // this iteration's line search runs on the exact polynomial phi (poly.cu) instead of trial
+    // evaluations; counters for the kernel-launch accounting
+    int poly;
+    long long total_poly, total_poly_acc;
     MoreThuente mt;
 };
 
@@ -62,6 +67,8 @@ struct Ctl {
     LsParams ls;
     int als_mode;  // 1: stand-alone ALS trace semantics
     int eager;     // 1: host-driven loop (no graph conditionals; profiling / launch lists)
+    int poly_ok;   // the polynomial line search applies to this tensor / options
+    const dd* coef;
 };
 
 __device__ __forceinline__ void set_cond(const Ctl& c, cudaGraphConditionalHandle h, bool v) {
@@ -84,6 +91,8 @@ __global__ void k_reset(Ctl c, int max_iters) {
     s.slot = 0;
     s.beta = 0.0;
     s.total_ls_evals = s.total_accepted = 0;
+    s.poly = 0;
+    s.total_poly = s.total_poly_acc = 0;
     s.resid = c.resid_always;
     s.t0 = globaltimer();
 }
@@ -170,8 +179,47 @@ __global__ void k_ls_update(Ctl c, cudaGraphConditionalHandle ls_h) {
     set_cond(c, ls_h, s.searching != 0);
 }
 
-__global__ void k_accept_cond(Ctl c, cudaGraphConditionalHandle h) {
-    set_cond(c, h, c.s->accepted != 0);
+// the line search of this iteration runs on the polynomial when it applies and the per-fiber
+// objective is in use (the residual phase keeps trial evaluations)
+__global__ void k_poly_gate(Ctl c, cudaGraphConditionalHandle poly_h, cudaGraphConditionalHandle ls_h) {
+    DevState& s = *c.s;
+    s.poly = (c.poly_ok && s.searching && !s.resid) ? 1 : 0;
+    if (s.poly) {
+        s.searching = 0;  // no trial-evaluation loop
+        s.total_poly += 1;
+    }
+    set_cond(c, poly_h, s.poly != 0);
+    set_cond(c, ls_h, s.searching != 0);
+}
+
+// Moré–Thuente (as started by k_ls_init) to termination on phi(a) = f(u_bar + a d) and phi'(a)
+// from the polynomial; the same bookkeeping as k_ls_update at termination
+__global__ void k_poly_ls(Ctl c) {
+    DevState& s = *c.s;
+    for (;;) {
+        double f, g;
+        poly_eval(c.coef, s.mt.stp, f, g);
+        if (s.mt.update(f, g)) break;
+    }
+    s.fevals += s.mt.evals;
+    s.gevals += s.mt.evals;
+    s.stalled = (s.mt.status == LS_STALL) ? 1 : 0;
+    if (!s.status && s.mt.out_step > 0.0 && s.mt.out_f <= s.f_bar) {
+        s.accepted = 1;
+        s.beta = s.mt.out_step;
+    }
+}
+
+__global__ void k_accept_cond(Ctl c, cudaGraphConditionalHandle h, cudaGraphConditionalHandle hp) {
+    set_cond(c, h, c.s->accepted != 0 && !c.s->poly);
+    if (hp) set_cond(c, hp, c.s->accepted != 0 && c.s->poly);
+}
+
+// S(u_bar + beta d) = S(u_bar) + beta S_d in place
+__global__ void k_axpy_s(const DevState* s, double* S, const double* Sd, int64_t n) {
+    const double b = s->beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        S[i] += b * Sd[i];
 }
 
 __global__ void k_step_point(const DevState* s, const double* ub, const double* d, double* out, int64_t n) {
@@ -236,6 +284,7 @@ __global__ void k_commit(Ctl c, cudaGraphConditionalHandle loop_h) {
         s.f = c.sc_next->f;
         s.gnorm2 = c.sc_next->gnorm2;
         s.total_accepted += 1;
+        if (s.poly) s.total_poly_acc += 1;
     } else {
         s.f = s.f_bar;
         s.gnorm2 = c.sc_bar->gnorm2;
@@ -418,6 +467,10 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     CPFIT_CUDA(cudaMalloc(&state_, sizeof(DevState)));
     CPFIT_CUDA(cudaMemset(state_, 0, sizeof(DevState)));
     if (const char* e = std::getenv("CPFIT_EAGER"); e && e[0] == '1') eager_ = true;
+    // exact polynomial line search: dense order 3, default objective handling, not disabled
+    const char* np = std::getenv("CPFIT_NO_POLY_LS");
+    if (method_ == 0 && poly_supported(*t) && !o.reeval_accepted && !o.residual_objective && !(np && np[0] == '1'))
+        pw_ = poly_create(*t, *w_);
     if (const char* e = std::getenv("CPFIT_PHASE_PROFILE"); e && e[0] == '1') {
         CPFIT_CUDA(cudaMalloc(&phase_, sizeof(unsigned long long) * (2 * kPhases + 1)));
         CPFIT_CUDA(cudaMemset(phase_, 0, sizeof(unsigned long long) * (2 * kPhases + 1)));
@@ -440,6 +493,7 @@ Solver::~Solver() {
     if (phase_) cudaFree(phase_);
     cudaFree(trace_);
     accel_destroy(a_);
+    poly_destroy(pw_);
     work_destroy(w_);
     cudaStreamDestroy(st_);
     cudaStreamDestroy(st2_);
@@ -469,6 +523,8 @@ void Solver::build_graphs() {
     c.restart_on_ascent = opt_.restart_on_ascent;
     c.ls = LsParams{opt_.ftol, opt_.gtol, opt_.initial_step, opt_.max_evals, opt_.step_min, opt_.step_max};
     c.als_mode = (method_ == 1);
+    c.poly_ok = pw_ ? 1 : 0;
+    c.coef = pw_ ? pw_->coef : nullptr;
     static_assert(sizeof(Ctl) <= sizeof(ctl_blob_), "ctl blob");
     std::memcpy(ctl_blob_, &c, sizeof(Ctl));
     int* status = &s->status;
@@ -504,7 +560,7 @@ void Solver::build_graphs() {
     cudaGraph_t body = append_conditional(st_, loop_h, cudaGraphCondTypeWhile);
     CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st2_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     stamp(st2_, 7);
-    cudaGraph_t lsb = nullptr, ab = nullptr;
+    cudaGraph_t lsb = nullptr, ab = nullptr, pb = nullptr, apb = nullptr;
     if (method_ == 0) {
         // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
         als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_, m0_cur_);
@@ -519,6 +575,17 @@ void Solver::build_graphs() {
         // Step III: restart test / Moré–Thuente line search                 (ngmres.cpp:111-147)
         const cudaGraphConditionalHandle ls_h = make_handle(st2_);
         k_ls_init<<<1, 1, 0, st2_>>>(c, ls_h);
+        if (pw_) {
+            // exact line search on phi(a) (poly.cu): one S_d pass + reductions, then Moré–Thuente
+            const cudaGraphConditionalHandle poly_h = make_handle(st2_);
+            k_poly_gate<<<1, 1, 0, st2_>>>(c, poly_h, ls_h);
+            pb = append_conditional(st2_, poly_h, cudaGraphCondTypeIf);
+            CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, pb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+            poly_build_device(*t_, *w_, *pw_, ub_, d_, st3_);
+            k_poly_ls<<<1, 1, 0, st3_>>>(c);
+            CPFIT_CUDA(cudaGetLastError());
+            CPFIT_CUDA(cudaStreamEndCapture(st3_, &pb));
+        }
         stamp(st2_, 2);
         lsb = append_conditional(st2_, ls_h, cudaGraphCondTypeWhile);
         CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
@@ -532,7 +599,17 @@ void Solver::build_graphs() {
         CPFIT_CUDA(cudaStreamEndCapture(st3_, &lsb));
         // accepted step: canonicalize u_bar + beta d and re-evaluate        (ngmres.cpp:137-142)
         const cudaGraphConditionalHandle acc_h = make_handle(st2_);
-        k_accept_cond<<<1, 1, 0, st2_>>>(c, acc_h);
+        const cudaGraphConditionalHandle accp_h = pw_ ? make_handle(st2_) : cudaGraphConditionalHandle{};
+        k_accept_cond<<<1, 1, 0, st2_>>>(c, acc_h, accp_h);
+        if (pw_) {
+            // accepted polynomial step: u* = u_bar + beta d, S(u*) by the axpy, M0 pass + levels +
+            // gradient at u*, then the canonical rescale as for an evaluated trial
+            apb = append_conditional(st2_, accp_h, cudaGraphCondTypeIf);
+            CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, apb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+            emit_poly_accept(st3_, &c);
+            CPFIT_CUDA(cudaGetLastError());
+            CPFIT_CUDA(cudaStreamEndCapture(st3_, &apb));
+        }
         ab = append_conditional(st2_, acc_h, cudaGraphCondTypeIf);
         CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, ab, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         if (opt_.reeval_accepted) {
@@ -573,7 +650,25 @@ void Solver::build_graphs() {
     n_body_ = count_kernels(body);
     n_ls_ = lsb ? count_kernels(lsb) : 0;
     n_acc_ = ab ? count_kernels(ab) : 0;
+    n_poly_ = pb ? count_kernels(pb) : 0;
+    n_accp_ = apb ? count_kernels(apb) : 0;
     CPFIT_CUDA(cudaGraphInstantiate(&x_loop_, g_loop_, 0));
+}
+
+// accepted step of a polynomial line search (see build_graphs)
+void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
+    const Ctl& c = *reinterpret_cast<const Ctl*>(ctl);
+    DevState* s = c.s;
+    EvalScalars* sc_trial = reinterpret_cast<EvalScalars*>(sc_) + 2;
+    EvalScalars* sc_next = reinterpret_cast<EvalScalars*>(sc_) + 3;
+    const int vb = vec_blocks(n_);
+    k_step_point<<<vb, 256, 0, st>>>(s, ub_, d_, ut_, n_);
+    const int64_t ns = t_->J * w_->RP;
+    k_axpy_s<<<(int)std::min<int64_t>(4 * 148, (ns + 255) / 256), 256, 0, st>>>(s, w_->S, pw_->S_d, ns);
+    eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st);
+    const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, w_->m0, m0_cur_);
+    k_after_rescale<<<1, 1, 0, st>>>(c, sc_next, red_, nb);
+    CPFIT_CUDA(cudaGetLastError());
 }
 
 void Solver::set_initial(const double* u0, bool host) {
@@ -593,7 +688,8 @@ long long Solver::pending_loop_launches() {
     DevState hs;
     CPFIT_CUDA(cudaMemcpyAsync(&hs, state_, sizeof(DevState), cudaMemcpyDeviceToHost, st_));
     sync();
-    return (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + hs.total_accepted * n_acc_;
+    return (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + (hs.total_accepted - hs.total_poly_acc) * n_acc_ +
+           hs.total_poly * n_poly_ + hs.total_poly_acc * n_accp_;
 }
 
 void Solver::run_loop(int max_iters_total) {
@@ -640,6 +736,13 @@ void Solver::run_loop_eager() {
             k_after_bar<<<1, 1, 0, st_>>>(c);
             accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st_);
             k_ls_init<<<1, 1, 0, st_>>>(c, none);
+            if (pw_) {
+                k_poly_gate<<<1, 1, 0, st_>>>(c, none, none);
+                if (state().poly) {
+                    poly_build_device(*t_, *w_, *pw_, ub_, d_, st_);
+                    k_poly_ls<<<1, 1, 0, st_>>>(c);
+                }
+            }
             while (state().searching) {
                 k_trial<<<vb, 256, 0, st_>>>(s, ub_, d_, ut_, n_);
                 eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st_, true, &s->resid);
@@ -647,8 +750,11 @@ void Solver::run_loop_eager() {
                 if (!opt_.reeval_accepted)
                     k_keep_best<<<vb, 256, 0, st_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
             }
-            k_accept_cond<<<1, 1, 0, st_>>>(c, none);
-            if (state().accepted) {
+            k_accept_cond<<<1, 1, 0, st_>>>(c, none, none);
+            const DevState ha = state();
+            if (ha.accepted && ha.poly) {
+                emit_poly_accept(st_, &c);
+            } else if (ha.accepted) {
                 if (opt_.reeval_accepted) {
                     k_step_point<<<vb, 256, 0, st_>>>(s, ub_, d_, ut_, n_);
                     grams_device(*w_, ut_, st_);
@@ -702,7 +808,8 @@ SolverSummary Solver::summary() {
     r.fevals = hs.fevals;
     r.gevals = hs.gevals;
     r.launches = launches_done_ + loop_launches_ * n_prelude_ + init_launches_ * n_init_ +
-                 (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + hs.total_accepted * n_acc_;
+                 (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + (hs.total_accepted - hs.total_poly_acc) * n_acc_ +
+                 hs.total_poly * n_poly_ + hs.total_poly_acc * n_accp_;
     return r;
 }
 

@@ -76,6 +76,9 @@ public:
 private:
     void build_graphs();
     void run_loop_eager();
+    void emit_poly_accept(cudaStream_t st, const void* ctl);
+    PolyWork* pw_ = nullptr;  // exact line search (poly.cu), when it applies
+    int n_poly_ = 0, n_accp_ = 0;
     bool eager_ = false;
     alignas(16) unsigned char ctl_blob_[512] = {};  // the control-kernel parameters (solver.cu Ctl)
     DevTensor* t_;
