@@ -265,6 +265,9 @@ struct NormParams {
     // summed from the partials here, and block 0 finalises it into gram_w
     GramPending pend;
     double* gram_w;
+    // optional: the permutation and the mode-0 scales of the normalisation (block 0 writes)
+    int* perm_out;
+    double* scale0_out;
 };
 
 // normalize_and_reorder: norms from the (double-double) Gram diagonals, lambda_r =
@@ -306,6 +309,10 @@ __global__ void normalize_kernel(const NormParams p) {
         const int src = perm[tid];
         const double l = lam[src];
         for (int n = 0; n < p.order; ++n) scale[n][tid] = (l == 0.0) ? 1.0 : pow(l, 1.0 / p.order) / nrm[n][src];
+        if (blockIdx.x == 0 && p.perm_out) {
+            p.perm_out[tid] = src;
+            p.scale0_out[tid] = scale[0][tid];
+        }
     }
     __syncthreads();
     const int64_t total = p.off[p.order];
@@ -388,10 +395,14 @@ void gram_hadamard_device(EvalWork& w, int skip, double* out, cudaStream_t st) {
     CPFIT_CUDA(cudaGetLastError());
 }
 
-void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st, int pending) {
+void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st, int pending, bool save_perm) {
     NormParams p{};
     p.pend = pending_of(w, pending);
     p.gram_w = w.gram;
+    if (save_perm) {
+        p.perm_out = w.nperm;
+        p.scale0_out = w.nscale0;
+    }
     p.order = w.order;
     p.R = w.R;
     p.RP = w.RP;
@@ -489,9 +500,29 @@ void fork_chol(EvalWork& w, int n, int* status, cudaStream_t st) {
 void join_chol(EvalWork& w, cudaStream_t st) { CPFIT_CUDA(cudaStreamWaitEvent(st, w.ev_join, 0)); }
 }  // namespace
 
+namespace {
+// S(u_bar)[j][r] = S'[j][perm r] * s_0(r): the sweep's S' = T x_1 A0' mapped to the normalised
+// iterate (its mode-0 factor is A0' permuted and scaled), for the evaluation that follows
+template <int RP>
+__global__ void s_rescale_kernel(double* S, int64_t J, int R, const int* perm, const double* sc) {
+    // one element per lane; a row (RP <= 32 lanes) lives in one warp, so the permutation is a
+    // shuffle after every lane has loaded its element
+    const int64_t n = J * RP;
+    const int lane = threadIdx.x & 31;
+    for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < n; e0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = e0 + threadIdx.x;
+        const int r = (int)(e % RP);
+        const double v = e < n ? S[e] : 0.0;
+        const int src = (lane & ~(RP - 1)) + (r < R ? perm[r] : 0);
+        const double o = __shfl_sync(0xffffffffu, v, src);
+        if (e < n) S[e] = r < R ? o * sc[r] : 0.0;
+    }
+}
+}  // namespace
+
 // work: n_u scratch (pre-normalisation iterate), mbuf: max(I_n)*R scratch
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
-                         int* status, cudaStream_t st, const double* m0_given) {
+                         int* status, cudaStream_t st, const double* m0_given, bool keep_s) {
     CPFIT_CUDA(cudaMemcpyAsync(work, u, sizeof(double) * w.nu, cudaMemcpyDeviceToDevice, st));
     grams_device(w, work, st);
     const int N = t.order;
@@ -529,7 +560,16 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
             }
         }
     }
-    normalize_device(w, work, out, st, N - 1);
+    normalize_device(w, work, out, st, N - 1, keep_s && !t.sparse);
+    if (keep_s && !t.sparse) {
+        const int blocks = (int)std::min<int64_t>(8 * 148, (t.J * w.RP + 255) / 256);
+        switch (w.RP) {
+            case 8: s_rescale_kernel<8><<<blocks, 256, 0, st>>>(w.S, t.J, w.R, w.nperm, w.nscale0); break;
+            case 16: s_rescale_kernel<16><<<blocks, 256, 0, st>>>(w.S, t.J, w.R, w.nperm, w.nscale0); break;
+            default: s_rescale_kernel<32><<<blocks, 256, 0, st>>>(w.S, t.J, w.R, w.nperm, w.nscale0); break;
+        }
+        CPFIT_CUDA(cudaGetLastError());
+    }
 }
 
 }  // namespace cpfit_gpu

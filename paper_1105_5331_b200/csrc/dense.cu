@@ -60,6 +60,7 @@ struct FiberParams {
     int64_t tiles_per_cta;
     int64_t ntiles;
     unsigned long long* prof;  // diagnostic build only (fiber.cuh FIBER_WAIT)
+    const double* S_in;        // S given (M0 + per-fiber objective pass): J x RP
 };
 
 #include "fiber.cuh"
@@ -86,7 +87,8 @@ void reduce_m0(EvalWork& w, cudaStream_t st) {
 }
 
 void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, bool do_f,
-               const double* gamma0, cudaStream_t st, const int* resid_flag = nullptr, double* s_out = nullptr) {
+               const double* gamma0, cudaStream_t st, const int* resid_flag = nullptr, double* s_out = nullptr,
+               const double* s_in = nullptr) {
     FiberParams p{};
     p.T = t.T;
     p.ldT = t.ldT;
@@ -109,6 +111,7 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
         p.fac[m] = u + w.off[m];
     }
     p.S_out = s_out ? s_out : w.S;
+    p.S_in = s_in;
     p.m0_part = w.m0_part;
     p.f_part = w.f_part;
     p.gamma0 = gamma0;
@@ -582,6 +585,8 @@ EvalWork* work_create(const DevTensor& t, int R) {
     // ALS solve Gram partials: <= 148 blocks per mode (als.cu solve_blocks)
     w->solve_part_stride = (int64_t)148 * (R * (R + 1) / 2);
     CPFIT_CUDA(cudaMalloc(&w->solve_part, sizeof(dd) * (size_t)t.order * w->solve_part_stride));
+    CPFIT_CUDA(cudaMalloc(&w->nperm, sizeof(int) * kMaxRank));
+    CPFIT_CUDA(cudaMalloc(&w->nscale0, sizeof(double) * kMaxRank));
     w->chol_stride = (int64_t)R * R + R + 1;
     CPFIT_CUDA(cudaMalloc(&w->chol, sizeof(double) * (size_t)t.order * w->chol_stride));
     CPFIT_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
@@ -648,6 +653,8 @@ void work_destroy(EvalWork* w) {
     cudaFree(w->counter);
     cudaFree(w->chol);
     cudaFree(w->solve_part);
+    cudaFree(w->nperm);
+    cudaFree(w->nscale0);
     if (w->ev_fork) cudaEventDestroy(w->ev_fork);
     if (w->ev_join) cudaEventDestroy(w->ev_join);
     if (w->side) cudaStreamDestroy(w->side);
@@ -712,12 +719,16 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
 }  // namespace
 
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
-                 int* status, cudaStream_t st, bool need_grad, const int* resid_flag) {
+                 int* status, cudaStream_t st, bool need_grad, const int* resid_flag, bool s_given) {
     (void)status;
     grams_device(w, u, st);
     if (!t.sparse) {
-        // fused pass: S, M0 partials and per-fiber objective
-        run_fiber(t, w, u, true, true, true, w.gram /* mode-0 Gram */, st, resid_flag);
+        // fused pass: S, M0 partials and per-fiber objective — or, when w.S already holds
+        // T x_1 A0(u), M0 and the objective only (no S contraction)
+        if (s_given)
+            run_fiber(t, w, u, false, true, true, w.gram, st, resid_flag, nullptr, w.S);
+        else
+            run_fiber(t, w, u, true, true, true, w.gram /* mode-0 Gram */, st, resid_flag);
         reduce_m0(w, st);
         // modes 1..N-1 from S
         const double* Sin = w.S;

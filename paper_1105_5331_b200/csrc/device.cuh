@@ -84,6 +84,8 @@ struct EvalWork {
     // factorisations run on, overlapping the streaming passes
     double* chol = nullptr;
     int64_t chol_stride = 0;
+    int* nperm = nullptr;            // last normalisation: permutation, mode-0 scales
+    double* nscale0 = nullptr;
     dd* solve_part = nullptr;        // per-mode Gram partials of the ALS solves
     int64_t solve_part_stride = 0;   // dd per mode ([blocks][npair])
     cudaStream_t side = nullptr;
@@ -105,7 +107,8 @@ struct EvalScalars {
 // scalars->f, ->gnorm2 and (if d != nullptr) ->gdotd.  Grams of u are computed first.
 // mode = 0 gradient+f; mode = 1 f only (objective()).
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
-                 int* status, cudaStream_t st, bool need_grad = true, const int* resid_flag = nullptr);
+                 int* status, cudaStream_t st, bool need_grad = true, const int* resid_flag = nullptr,
+                 bool s_given = false);
 
 // mttkrp(T, factors(u), mode) (tensor.cpp:206-259) -> out (I_mode x R col-major).
 void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st);
@@ -115,15 +118,17 @@ void grams_device(EvalWork& w, const double* u, cudaStream_t st);
 // gram_hadamard(factors(u), skip) (tensor.cpp:261-274) -> out (R x R col-major), from w.gram.
 void gram_hadamard_device(EvalWork& w, int skip, double* out, cudaStream_t st);
 // normalize_and_reorder (kruskal.cpp:156-193): u -> out, Grams in w.gram updated to match.
-void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st, int pending = -1);
+void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st, int pending = -1,
+                      bool save_perm = false);
 // normalize u -> uout and map the gradient g at u to the normalised point (G_n D_n^-1,
 // permuted) -> gout; writes per-block partial ||gout||^2 to red, returns the block count.
 int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
                           cudaStream_t st, const double* m0 = nullptr, double* m0out = nullptr);
 // One ALS sweep (als.cpp:38-48): u -> out (normalized); work: n_u scratch, mbuf: max I_n x R
 // scratch. status: bit0 singular normal matrix after the ridge retry, bit1 non-finite solve.
+// keep_s: leave S(out) = T x_1 A0(out) in w.S (dense; for an evaluation with s_given)
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
-                         int* status, cudaStream_t st, const double* m0_given = nullptr);
+                         int* status, cudaStream_t st, const double* m0_given = nullptr, bool keep_s = false);
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
 
 // Dense pieces for the exact line search (poly.cu): S = T x_1 A (first factor of u) into S_out;

@@ -329,7 +329,46 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
         }
     } else if (warp < Ro::M0W) {
         // ---------------- S warps ----------------
-        if (p.do_s) {
+        if (!p.do_s && epi_w && p.S_in) {
+            // S is given (the ALS sweep's S' rescaled to u_bar): only the per-fiber objective
+            const int sw = warp - Ro::S0;
+            for (int64_t k = 0; k < ntl; ++k) {
+                const int b = (int)(k & 1);
+                const int64_t f0 = (t_begin + k) * F;
+                double sv[Ro::SPW][2], fn[Ro::SPW];
+#pragma unroll
+                for (int j = 0; j < Ro::SPW; ++j) {
+                    const int q = sw * Ro::SPW + j, ft = q / NRT, nt = q % NRT;
+                    const int64_t f = f0 + ft * 8 + (lane >> 2);
+                    const int r = nt * 8 + 2 * (lane & 3);
+                    fn[j] = (nt == 0 && f < p.J) ? p.fnorm2[f] : 0.0;
+                    const double2 v = f < p.J ? *reinterpret_cast<const double2*>(p.S_in + f * RP + r) : make_double2(0.0, 0.0);
+                    sv[j][0] = v.x;
+                    sv[j][1] = v.y;
+                }
+                FIBER_WAIT(6, &wfull[b], (uint32_t)((k / 2) & 1));
+                const double* wv = wbuf + (size_t)b * F * WLD;
+#pragma unroll
+                for (int j = 0; j < Ro::SPW; ++j) {
+                    const int q = sw * Ro::SPW + j, ft = q / NRT, nt = q % NRT;
+                    const int fl = ft * 8 + (lane >> 2);
+                    const int r = nt * 8 + 2 * (lane & 3);
+                    double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+                    for (int kr = 0; kr < RP / 4; ++kr) {
+                        const double gb = gam[(kr * 4 + (lane & 3)) * RP + nt * 8 + (lane >> 2)];
+                        dmma_8x8x4(q0, q1, wv[fl * WLD + kr * 4 + (lane & 3)], gb);
+                    }
+                    const double2 wd = *reinterpret_cast<const double2*>(wv + fl * WLD + r);
+                    double term = wd.x * (q0 - 2.0 * sv[j][0]) + wd.y * (q1 - 2.0 * sv[j][1]);
+                    term += __shfl_xor_sync(0xffffffffu, term, 1);
+                    term += __shfl_xor_sync(0xffffffffu, term, 2);
+                    if ((lane & 3) == 0 && f0 + fl < p.J) facc += fn[j] + term;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&wempty[b]);
+            }
+        } else if (p.do_s) {
             const int sw = warp - Ro::S0;
             for (int64_t k = 0; k < ntl; ++k) {
                 const int s = (int)(k % kFStages);

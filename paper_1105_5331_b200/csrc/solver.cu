@@ -563,9 +563,9 @@ void Solver::build_graphs() {
     cudaGraph_t lsb = nullptr, ab = nullptr, pb = nullptr, apb = nullptr;
     if (method_ == 0) {
         // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
-        als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_, m0_cur_);
+        als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_, m0_cur_, true);
         stamp(st2_, 0);
-        eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_, true, &s->resid);
+        eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_, true, &s->resid, !t_->sparse);
         if (m0_bar_)
             CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st2_));
         k_after_bar<<<1, 1, 0, st2_>>>(c);
@@ -635,8 +635,8 @@ void Solver::build_graphs() {
     } else {
         // stand-alone ALS iteration (als.cpp:79-95)
         // the previous evaluation (of u) left M0(u) in w.m0 for dense tensors
-        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, t_->sparse ? nullptr : w_->m0);
-        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid);
+        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, t_->sparse ? nullptr : w_->m0, true);
+        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid, !t_->sparse);
     }
     k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
     k_commit_vec<<<vb, 256, 0, st2_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,
@@ -729,8 +729,8 @@ void Solver::run_loop_eager() {
         DevState hs = state();
         if (!(hs.stop < 0 && hs.iter < hs.max_iters)) break;
         if (method_ == 0) {
-            als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st_, m0_cur_);
-            eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st_, true, &s->resid);
+            als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st_, m0_cur_, true);
+            eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st_, true, &s->resid, !t_->sparse);
             if (m0_bar_)
                 CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
             k_after_bar<<<1, 1, 0, st_>>>(c);
@@ -771,8 +771,8 @@ void Solver::run_loop_eager() {
                 }
             }
         } else {
-            als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, t_->sparse ? nullptr : w_->m0);
-            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid);
+            als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, t_->sparse ? nullptr : w_->m0, true);
+            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid, !t_->sparse);
         }
         k_commit<<<1, 1, 0, st_>>>(c, none);
         k_commit_vec<<<vb, 256, 0, st_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,
