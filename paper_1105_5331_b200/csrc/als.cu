@@ -268,6 +268,9 @@ struct NormParams {
     // optional: the permutation and the mode-0 scales of the normalisation (block 0 writes)
     int* perm_out;
     double* scale0_out;
+    // optional: the last block rewrites gram_w as the Grams of the output,
+    // G'_n(q, r) = s_n(q) s_n(r) G_n(perm q, perm r)
+    unsigned int* counter;
 };
 
 // normalize_and_reorder: norms from the (double-double) Gram diagonals, lambda_r =
@@ -360,6 +363,23 @@ __global__ void normalize_kernel(const NormParams p) {
             p.red[blockIdx.x] = s;
         }
     }
+    if (p.counter) {
+        // every block has read the input Grams once the last one arrives: rewrite them as the
+        // Grams of the normalised output (the next evaluation / sweep then skips the Gram pass)
+        if (!last_block_arrives(p.counter)) return;
+        __shared__ double gin[kGramsOutMax];  // callers check order * RP * RP <= kGramsOutMax
+        const int RR = p.RP * p.RP;
+        {
+            for (int e = tid; e < p.order * RR; e += blockDim.x) gin[e] = p.gram_w[e];
+            __syncthreads();
+            for (int e = tid; e < p.order * RR; e += blockDim.x) {
+                const int n = e / RR, q = (e % RR) / p.RP, r = e % p.RP;
+                double v = 0.0;
+                if (q < p.R && r < p.R) v = scale[n][q] * scale[n][r] * gin[n * RR + perm[q] * p.RP + perm[r]];
+                p.gram_w[e] = v;
+            }
+        }
+    }
 }
 
 __global__ void gram_hadamard_kernel(const double* gram, int order, int R, int RP, int skip, double* out) {
@@ -395,10 +415,12 @@ void gram_hadamard_device(EvalWork& w, int skip, double* out, cudaStream_t st) {
     CPFIT_CUDA(cudaGetLastError());
 }
 
-void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st, int pending, bool save_perm) {
+void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st, int pending, bool save_perm,
+                      bool out_grams) {
     NormParams p{};
     p.pend = pending_of(w, pending);
     p.gram_w = w.gram;
+    if (out_grams) p.counter = w.counter + kCounterNorm;
     if (save_perm) {
         p.perm_out = w.nperm;
         p.scale0_out = w.nscale0;
@@ -420,9 +442,11 @@ void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st
 }
 
 int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
-                          cudaStream_t st, const double* m0, double* m0out) {
+                          cudaStream_t st, const double* m0, double* m0out, bool out_grams) {
     NormParams p{};
     p.pend.mode = -1;
+    p.gram_w = w.gram;
+    if (out_grams) p.counter = w.counter + kCounterNorm;
     p.order = w.order;
     p.R = w.R;
     p.RP = w.RP;
@@ -522,9 +546,9 @@ __global__ void s_rescale_kernel(double* S, int64_t J, int R, const int* perm, c
 
 // work: n_u scratch (pre-normalisation iterate), mbuf: max(I_n)*R scratch
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
-                         int* status, cudaStream_t st, const double* m0_given, bool keep_s) {
+                         int* status, cudaStream_t st, const double* m0_given, bool keep_s, bool grams_given) {
     CPFIT_CUDA(cudaMemcpyAsync(work, u, sizeof(double) * w.nu, cudaMemcpyDeviceToDevice, st));
-    grams_device(w, work, st);
+    if (!grams_given) grams_device(w, work, st);
     const int N = t.order;
     // Gamma_0 from the Grams of u; each later Gamma_n as soon as G_{n-1}' exists (side stream)
     chol_mode(w, 0, -1, status, st);
@@ -560,7 +584,7 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
             }
         }
     }
-    normalize_device(w, work, out, st, N - 1, keep_s && !t.sparse);
+    normalize_device(w, work, out, st, N - 1, keep_s && !t.sparse, grams_given);
     if (keep_s && !t.sparse) {
         const int blocks = (int)std::min<int64_t>(8 * 148, (t.J * w.RP + 255) / 256);
         switch (w.RP) {

@@ -719,9 +719,9 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
 }  // namespace
 
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
-                 int* status, cudaStream_t st, bool need_grad, const int* resid_flag, bool s_given) {
+                 int* status, cudaStream_t st, bool need_grad, const int* resid_flag, bool s_given, bool grams_given) {
     (void)status;
-    grams_device(w, u, st);
+    if (!grams_given) grams_device(w, u, st);
     if (!t.sparse) {
         // fused pass: S, M0 partials and per-fiber objective — or, when w.S already holds
         // T x_1 A0(u), M0 and the objective only (no S contraction)

@@ -46,7 +46,9 @@ DevTensor* tensor_create_coo(int order, const int64_t* dims, int64_t nnz, const 
 void tensor_destroy(DevTensor* t);
 
 // last-block-done counters (one per kernel family; each resets its own after use)
-constexpr int kCounterGrad = 0, kCounterGram = 1, kCounterSolve = 2, kCounters = 4;
+constexpr int kCounterGrad = 0, kCounterGram = 1, kCounterSolve = 2, kCounterNorm = 3, kCounters = 4;
+// normalisations can hand on the Grams of their output when order * RP^2 <= kGramsOutMax
+constexpr int kGramsOutMax = 4096;
 
 // Scratch for one evaluation context (sized from tensor + rank).
 struct EvalWork {
@@ -108,7 +110,7 @@ struct EvalScalars {
 // mode = 0 gradient+f; mode = 1 f only (objective()).
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
                  int* status, cudaStream_t st, bool need_grad = true, const int* resid_flag = nullptr,
-                 bool s_given = false);
+                 bool s_given = false, bool grams_given = false);
 
 // mttkrp(T, factors(u), mode) (tensor.cpp:206-259) -> out (I_mode x R col-major).
 void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st);
@@ -118,17 +120,20 @@ void grams_device(EvalWork& w, const double* u, cudaStream_t st);
 // gram_hadamard(factors(u), skip) (tensor.cpp:261-274) -> out (R x R col-major), from w.gram.
 void gram_hadamard_device(EvalWork& w, int skip, double* out, cudaStream_t st);
 // normalize_and_reorder (kruskal.cpp:156-193): u -> out, Grams in w.gram updated to match.
+// out_grams: leave the Grams of out in w.gram (rescaled/permuted input Grams)
 void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st, int pending = -1,
-                      bool save_perm = false);
+                      bool save_perm = false, bool out_grams = false);
 // normalize u -> uout and map the gradient g at u to the normalised point (G_n D_n^-1,
 // permuted) -> gout; writes per-block partial ||gout||^2 to red, returns the block count.
 int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
-                          cudaStream_t st, const double* m0 = nullptr, double* m0out = nullptr);
+                          cudaStream_t st, const double* m0 = nullptr, double* m0out = nullptr, bool out_grams = false);
 // One ALS sweep (als.cpp:38-48): u -> out (normalized); work: n_u scratch, mbuf: max I_n x R
 // scratch. status: bit0 singular normal matrix after the ridge retry, bit1 non-finite solve.
 // keep_s: leave S(out) = T x_1 A0(out) in w.S (dense; for an evaluation with s_given)
+// grams_given: w.gram already holds the Grams of u; then the Grams of out are left in w.gram
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
-                         int* status, cudaStream_t st, const double* m0_given = nullptr, bool keep_s = false);
+                         int* status, cudaStream_t st, const double* m0_given = nullptr, bool keep_s = false,
+                         bool grams_given = false);
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
 
 // Dense pieces for the exact line search (poly.cu): S = T x_1 A (first factor of u) into S_out;

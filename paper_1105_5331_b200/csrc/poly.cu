@@ -88,32 +88,60 @@ __device__ __forceinline__ dd dd_shfl_xor(dd v, int o) {
     return dd{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
 }
 
-// the eight <T, [[X0, X1, X2]]> (index 4 b0 + 2 b1 + b2, b_n = 1 selects D_n), double-double
+// the eight <T, [[X0, X1, X2]]> (index 4 b0 + 2 b1 + b2, b_n = 1 selects D_n): fp64 sums over
+// the R ranks of one fibre (FMA), folded into double-double accumulators per fibre — a fibre's
+// sum carries the same ~1e-15 relative error as the DMMA-computed S it is built from
+
+// Thread (i1, r) walks a chunk of i2 (fibre j = i1 + I1 i2): the S reads are coalesced over
+// (i1, r), X1 is loaded once, and X2[i2][r] comes from a shared-memory copy of the chunk's
+// rows of A2 and D2. fp64 FMA partial sums over kS8Run fibres are folded into double-double.
+constexpr int kS8Run = 16;
+constexpr int kS8I2 = 64;  // i2 per block chunk
+
 __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
     __shared__ dd red[8][8];
+    __shared__ double x2s[2][kS8I2][33];
     dd acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = dd{0.0, 0.0};
-    const int64_t total = p.J * p.RP;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(e % p.RP);
-        if (r >= p.R) continue;
-        const int64_t j = e / p.RP;
-        const int64_t i1 = j % p.I1, i2 = j / p.I1;
-        const double s[2] = {p.S[e], p.Sd[e]};
-        const int64_t o1 = (int64_t)r * p.I1 + i1;
-        const int64_t I2 = p.J / p.I1;
-        const int64_t o2 = (int64_t)r * I2 + i2;
-        const double x1[2] = {p.A1[o1], p.D1[o1]};
-        const double x2[2] = {p.A2[o2], p.D2[o2]};
+    const int I1 = (int)p.I1, I2 = (int)(p.J / p.I1);
+    const int npr = I1 * p.RP;                           // (i1, r) pairs
+    const int ngx = (npr + blockDim.x - 1) / blockDim.x;  // blocks over pairs
+    const int pr = (blockIdx.x % ngx) * blockDim.x + threadIdx.x;
+    const int i2a = (blockIdx.x / ngx) * kS8I2;
+    const int i2b = min(I2, i2a + kS8I2);
+    for (int e = threadIdx.x; e < (i2b - i2a) * p.RP; e += blockDim.x) {
+        const int ii = e / p.RP, r = e % p.RP;
+        const bool ok = r < p.R;
+        x2s[0][ii][r] = ok ? p.A2[(int64_t)r * I2 + i2a + ii] : 0.0;
+        x2s[1][ii][r] = ok ? p.D2[(int64_t)r * I2 + i2a + ii] : 0.0;
+    }
+    __syncthreads();
+    const int i1 = pr / p.RP, r = pr % p.RP;
+    if (pr < npr && r < p.R) {
+        const double x1a = p.A1[(int64_t)r * I1 + i1], x1d = p.D1[(int64_t)r * I1 + i1];
+        for (int i0 = i2a; i0 < i2b; i0 += kS8Run) {
+            double part[8];
 #pragma unroll
-        for (int b1 = 0; b1 < 2; ++b1)
-#pragma unroll
-            for (int b2 = 0; b2 < 2; ++b2) {
-                const dd x12 = dd_mul(dd{x1[b1], 0.0}, dd{x2[b2], 0.0});
-#pragma unroll
-                for (int b0 = 0; b0 < 2; ++b0) acc[4 * b0 + 2 * b1 + b2] = dd_add(acc[4 * b0 + 2 * b1 + b2], dd_mul(x12, dd{s[b0], 0.0}));
+            for (int k = 0; k < 8; ++k) part[k] = 0.0;
+            const int iend = min(i2b, i0 + kS8Run);
+            for (int i2 = i0; i2 < iend; ++i2) {
+                const int64_t e = ((int64_t)i2 * I1 + i1) * p.RP + r;
+                const double sa = p.S[e], sd = p.Sd[e];
+                const double x2a = x2s[0][i2 - i2a][r], x2d = x2s[1][i2 - i2a][r];
+                const double aa = x1a * x2a, ad = x1a * x2d, da = x1d * x2a, dd2 = x1d * x2d;
+                part[0] = fma(sa, aa, part[0]);
+                part[1] = fma(sa, ad, part[1]);
+                part[2] = fma(sa, da, part[2]);
+                part[3] = fma(sa, dd2, part[3]);
+                part[4] = fma(sd, aa, part[4]);
+                part[5] = fma(sd, ad, part[5]);
+                part[6] = fma(sd, da, part[6]);
+                part[7] = fma(sd, dd2, part[7]);
             }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[k] = dd_add(acc[k], dd{part[k], 0.0});
+        }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -129,10 +157,19 @@ __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
         p.part[(size_t)blockIdx.x * 8 + threadIdx.x] = s;
     }
     if (!last_block_arrives(p.counter)) return;
-    if (threadIdx.x < 8) {
+    // blocks' partials: thread t folds blocks t, t + 256, ... (fixed order), then a shared tree
+    __shared__ dd tr[256];
+    for (int k = 0; k < 8; ++k) {
         dd s{0.0, 0.0};
-        for (int b = 0; b < (int)gridDim.x; ++b) s = dd_add(s, p.part[(size_t)b * 8 + threadIdx.x]);
-        p.out[threadIdx.x] = s;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) s = dd_add(s, p.part[(size_t)b * 8 + k]);
+        tr[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if ((int)threadIdx.x < w) tr[threadIdx.x] = dd_add(tr[threadIdx.x], tr[threadIdx.x + w]);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) p.out[k] = tr[0];
+        __syncthreads();
     }
 }
 
@@ -224,7 +261,7 @@ PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {
     int64_t tasks = 0;
     for (int n = 0; n < 3; ++n) tasks += (int64_t)gram_chunks(t.dims[n]) * kKinds * w.R * w.R;
     p->nchunk_total = tasks;
-    p->s8_grid = 2 * sm_count();
+    p->s8_grid = (int)(((t.dims[1] * w.RP + 255) / 256) * ((t.dims[2] + kS8I2 - 1) / kS8I2));
     CPFIT_CUDA(cudaMalloc(&p->S_d, sizeof(double) * (size_t)t.J * w.RP));
     CPFIT_CUDA(cudaMalloc(&p->gpart, sizeof(dd) * (size_t)std::max<int64_t>(tasks, 1)));
     CPFIT_CUDA(cudaMalloc(&p->grams, sizeof(dd) * 3 * kKinds * (size_t)w.RP * w.RP));
@@ -285,7 +322,9 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     s.part = pw.s8part;
     s.out = pw.s8;
     s.counter = pw.counter + 1;
-    s8_kernel<<<pw.s8_grid, 256, 0, st>>>(s);
+    const int ngx = (int)((t.dims[0 + 1] * w.RP + 255) / 256);
+    const int ngy = (int)((t.dims[2] + kS8I2 - 1) / kS8I2);
+    s8_kernel<<<ngx * ngy, 256, 0, st>>>(s);
     CPFIT_CUDA(cudaGetLastError());
     CoefParams q{};
     q.R = w.R;

@@ -332,11 +332,14 @@ __global__ void k_commit(Ctl c, cudaGraphConditionalHandle loop_h) {
 // Vector part of the commit: u, g <- chosen pair; window slot; best iterate.
 __global__ void k_commit_vec(const DevState* s, int als_mode, const double* ub, const double* gb, const double* un,
                              const double* gn, double* u, double* g, double* wu, double* wg, double* ubest,
-                             int64_t n, const double* m0bar, double* m0cur, int64_t nm) {
+                             int64_t n, const double* m0bar, double* m0cur, int64_t nm, const double* gbar, double* gram,
+                             int64_t ng) {
     const bool acc = als_mode || s->accepted;
-    if (!acc)  // u <- u_bar: its M0 was kept after eval(u_bar)
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nm; i += (int64_t)gridDim.x * blockDim.x)
-            m0cur[i] = m0bar[i];
+    if (!acc)  // u <- u_bar: its M0 and Grams were kept after eval(u_bar)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nm + ng; i += (int64_t)gridDim.x * blockDim.x) {
+            if (i < nm) m0cur[i] = m0bar[i];
+            else gram[i - nm] = gbar[i - nm];
+        }
     const double* su = acc ? un : ub;
     const double* sg = acc ? gn : gb;
     double* wu_s = als_mode ? nullptr : wu + (int64_t)s->slot * n;
@@ -467,6 +470,9 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     CPFIT_CUDA(cudaMalloc(&state_, sizeof(DevState)));
     CPFIT_CUDA(cudaMemset(state_, 0, sizeof(DevState)));
     if (const char* e = std::getenv("CPFIT_EAGER"); e && e[0] == '1') eager_ = true;
+    // Grams handed on by the normalisations (no Gram pass at the sweep start / for u_bar)
+    gout_ = (int64_t)t->order * w_->RP * w_->RP <= kGramsOutMax;
+    if (gout_) alloc(&gram_bar_, gram_n());
     // exact polynomial line search: dense order 3, default objective handling, not disabled
     const char* np = std::getenv("CPFIT_NO_POLY_LS");
     if (method_ == 0 && poly_supported(*t) && !o.reeval_accepted && !o.residual_objective && !(np && np[0] == '1'))
@@ -486,7 +492,7 @@ Solver::~Solver() {
     if (g_init_) cudaGraphDestroy(g_init_);
     if (g_loop_) cudaGraphDestroy(g_loop_);
     for (double* p : {u_, g_, ub_, gb_, d_, ut_, gt_, un_, gn_, u0_, ubest_, work_, mbuf_, wu_, wg_, ubl_, gbl_, red_,
-                      m0_cur_, m0_bar_, m0_best_, m0_sel_})
+                      m0_cur_, m0_bar_, m0_best_, m0_sel_, gram_bar_})
         cudaFree(p);
     cudaFree(sc_);
     cudaFree(state_);
@@ -563,11 +569,12 @@ void Solver::build_graphs() {
     cudaGraph_t lsb = nullptr, ab = nullptr, pb = nullptr, apb = nullptr;
     if (method_ == 0) {
         // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
-        als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_, m0_cur_, true);
+        als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_, m0_cur_, true, gout_);
         stamp(st2_, 0);
-        eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_, true, &s->resid, !t_->sparse);
+        eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_, true, &s->resid, !t_->sparse, gout_);
         if (m0_bar_)
             CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st2_));
+        if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st2_));
         k_after_bar<<<1, 1, 0, st2_>>>(c);
         stamp(st2_, 1);
         // Step II: windowed recombination -> d, slope                        (ngmres.cpp:97-101)
@@ -626,7 +633,7 @@ void Solver::build_graphs() {
             // prod_n D_n = I, so f is unchanged and G_n -> G_n D_n^-1 (permuted)
             k_select_accepted<<<vb, 256, 0, st3_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
             grams_device(*w_, ut_, st3_);
-            const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st3_, m0_sel_, m0_cur_);
+            const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st3_, m0_sel_, m0_cur_, gout_);
             k_after_rescale<<<1, 1, 0, st3_>>>(c, sc_next, red_, nb);
         }
         stamp(st3_, 5);
@@ -635,12 +642,12 @@ void Solver::build_graphs() {
     } else {
         // stand-alone ALS iteration (als.cpp:79-95)
         // the previous evaluation (of u) left M0(u) in w.m0 for dense tensors
-        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, t_->sparse ? nullptr : w_->m0, true);
-        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid, !t_->sparse);
+        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, t_->sparse ? nullptr : w_->m0, true, gout_);
+        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid, !t_->sparse, gout_);
     }
     k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
     k_commit_vec<<<vb, 256, 0, st2_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,
-                                        m0_cur_, m0_n_);
+                                        m0_cur_, m0_n_, gram_bar_, w_->gram, gout_ ? gram_n() : 0);
     stamp(st2_, 6);
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaStreamEndCapture(st2_, &body));
@@ -666,7 +673,7 @@ void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
     const int64_t ns = t_->J * w_->RP;
     k_axpy_s<<<(int)std::min<int64_t>(4 * 148, (ns + 255) / 256), 256, 0, st>>>(s, w_->S, pw_->S_d, ns);
     eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st);
-    const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, w_->m0, m0_cur_);
+    const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, w_->m0, m0_cur_, gout_);
     k_after_rescale<<<1, 1, 0, st>>>(c, sc_next, red_, nb);
     CPFIT_CUDA(cudaGetLastError());
 }
@@ -729,10 +736,11 @@ void Solver::run_loop_eager() {
         DevState hs = state();
         if (!(hs.stop < 0 && hs.iter < hs.max_iters)) break;
         if (method_ == 0) {
-            als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st_, m0_cur_, true);
-            eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st_, true, &s->resid, !t_->sparse);
+            als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st_, m0_cur_, true, gout_);
+            eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st_, true, &s->resid, !t_->sparse, gout_);
             if (m0_bar_)
                 CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
+            if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st_));
             k_after_bar<<<1, 1, 0, st_>>>(c);
             accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st_);
             k_ls_init<<<1, 1, 0, st_>>>(c, none);
@@ -766,17 +774,17 @@ void Solver::run_loop_eager() {
                 } else {
                     k_select_accepted<<<vb, 256, 0, st_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
                     grams_device(*w_, ut_, st_);
-                    const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st_, m0_sel_, m0_cur_);
+                    const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st_, m0_sel_, m0_cur_, gout_);
                     k_after_rescale<<<1, 1, 0, st_>>>(c, sc_next, red_, nb);
                 }
             }
         } else {
-            als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, t_->sparse ? nullptr : w_->m0, true);
-            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid, !t_->sparse);
+            als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, t_->sparse ? nullptr : w_->m0, true, gout_);
+            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid, !t_->sparse, gout_);
         }
         k_commit<<<1, 1, 0, st_>>>(c, none);
         k_commit_vec<<<vb, 256, 0, st_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,
-                                          m0_cur_, m0_n_);
+                                          m0_cur_, m0_n_, gram_bar_, w_->gram, gout_ ? gram_n() : 0);
         CPFIT_CUDA(cudaGetLastError());
     }
 }

@@ -78,6 +78,10 @@ private:
     void run_loop_eager();
     void emit_poly_accept(cudaStream_t st, const void* ctl);
     PolyWork* pw_ = nullptr;  // exact line search (poly.cu), when it applies
+    bool gout_ = false;       // normalisations hand on their output's Grams
+    double* gram_bar_ = nullptr;
+    int64_t gram_n() const { return (int64_t)w_->order * w_->RP * w_->RP; }
+    size_t gram_bytes() const { return sizeof(double) * (size_t)gram_n(); }
     int n_poly_ = 0, n_accp_ = 0;
     bool eager_ = false;
     alignas(16) unsigned char ctl_blob_[512] = {};  // the control-kernel parameters (solver.cu Ctl)
