@@ -31,45 +31,27 @@ struct CrossParams {
     int64_t dims[3];
     const double* a[3];
     const double* d[3];
-    int nchunk[3];
-    int64_t base[3];  // first task of mode n
-    int64_t rows[3];
-    dd* part;         // [task]
     dd* out;          // [mode][kind][RP*RP]
-    unsigned int* counter;
 };
 
-// warp task t of mode n: (chunk c, kind k, q, r) -> part
+// one warp per (mode n, kind k, q, r) over all rows of the mode (lane-strided dd accumulation,
+// fixed xor tree); padded entries are written as zero by warps with q or r >= R
 __global__ void __launch_bounds__(256) cross_gram_kernel(const CrossParams p) {
-    const int RR = p.R * p.R;
-    const int64_t total = p.base[2] + (int64_t)p.nchunk[2] * kKinds * RR;
+    const int RR = p.RP * p.RP;
+    const int total = 3 * kKinds * RR;
     const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
-    for (int64_t t = warp; t < total; t += nwarps) {
-        const int n = t < p.base[1] ? 0 : (t < p.base[2] ? 1 : 2);
-        const int64_t tl = t - p.base[n];
-        const int c = (int)(tl / (kKinds * RR));
-        const int k = (int)((tl / RR) % kKinds);
-        const int e = (int)(tl % RR);
-        const int q = e / p.R, r = e % p.R;
-        const int64_t In = p.dims[n];
-        const double* x = (k == 2 ? p.d[n] : p.a[n]) + (int64_t)q * In;
-        const double* y = (k == 0 ? p.a[n] : p.d[n]) + (int64_t)r * In;
-        const int64_t i0 = (int64_t)c * p.rows[n];
-        const dd s = warp_dot_dd(x, y, i0, imin64(In, i0 + p.rows[n]));
-        if ((threadIdx.x & 31) == 0) p.part[t] = s;
-    }
-    if (!last_block_arrives(p.counter)) return;
-    for (int f = threadIdx.x; f < 3 * kKinds * p.RP * p.RP; f += blockDim.x) {
-        const int n = f / (kKinds * p.RP * p.RP);
-        const int k = (f / (p.RP * p.RP)) % kKinds;
-        const int e = f % (p.RP * p.RP);
+    for (int t = warp; t < total; t += nwarps) {
+        const int n = t / (kKinds * RR), k = (t / RR) % kKinds, e = t % RR;
         const int q = e / p.RP, r = e % p.RP;
         dd s{0.0, 0.0};
-        if (q < p.R && r < p.R)
-            for (int c = 0; c < p.nchunk[n]; ++c)
-                s = dd_add(s, p.part[p.base[n] + ((int64_t)c * kKinds + k) * RR + q * p.R + r]);
-        p.out[f] = s;
+        if (q < p.R && r < p.R) {
+            const int64_t In = p.dims[n];
+            const double* x = (k == 2 ? p.d[n] : p.a[n]) + (int64_t)q * In;
+            const double* y = (k == 0 ? p.a[n] : p.d[n]) + (int64_t)r * In;
+            s = warp_dot_dd(x, y, 0, In);
+        }
+        if ((threadIdx.x & 31) == 0) p.out[t] = s;
     }
 }
 
@@ -88,15 +70,24 @@ __device__ __forceinline__ dd dd_shfl_xor(dd v, int o) {
     return dd{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
 }
 
-// the eight <T, [[X0, X1, X2]]> (index 4 b0 + 2 b1 + b2, b_n = 1 selects D_n): fp64 sums over
-// the R ranks of one fibre (FMA), folded into double-double accumulators per fibre — a fibre's
-// sum carries the same ~1e-15 relative error as the DMMA-computed S it is built from
+// the eight <T, [[X0, X1, X2]]> (index 4 b0 + 2 b1 + b2, b_n = 1 selects D_n) as
+//   sum_{i1, r} X1[i1][r] sum_{i2} S_{b0}[i1 + I1 i2][r] X2[i2][r]:
+// thread (i1, r) walks a chunk of i2 (fibre j = i1 + I1 i2) accumulating the four inner sums
+// (S or S_d against A2 or D2); the X1 factors multiply in once per chunk, in double-double. The
+// S reads are coalesced over (i1, r) and X2[i2][r] comes from a shared-memory copy of the chunk's
+// rows of A2 and D2. fp64 FMA partial sums over kS8Run fibres are folded into double-double —
+// a run's sum carries the same ~1e-15 relative error as the DMMA-computed S it is built from.
+constexpr int kS8Run = 8;
+constexpr int kS8I2 = 32;  // i2 per block chunk
 
-// Thread (i1, r) walks a chunk of i2 (fibre j = i1 + I1 i2): the S reads are coalesced over
-// (i1, r), X1 is loaded once, and X2[i2][r] comes from a shared-memory copy of the chunk's
-// rows of A2 and D2. fp64 FMA partial sums over kS8Run fibres are folded into double-double.
-constexpr int kS8Run = 16;
-constexpr int kS8I2 = 64;  // i2 per block chunk
+// a += b for a double-double accumulator without renormalising (lo collects the rounding errors
+// of hi; dd_norm once at the end)
+__device__ __forceinline__ void dd_acc(dd& a, double b) {
+    const double s = a.hi + b;
+    const double bb = s - a.hi;
+    a.lo += (a.hi - (s - bb)) + (b - bb);
+    a.hi = s;
+}
 
 __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
     __shared__ dd red[8][8];
@@ -110,125 +101,191 @@ __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
     const int pr = (blockIdx.x % ngx) * blockDim.x + threadIdx.x;
     const int i2a = (blockIdx.x / ngx) * kS8I2;
     const int i2b = min(I2, i2a + kS8I2);
+    const int i1 = pr / p.RP, r = pr % p.RP;
+    const bool active = pr < npr && r < p.R;
+    // the first run's S loads and the X1 factors go out before the X2 staging barrier
+    double sav[kS8Run], sdv[kS8Run];
+    auto load_run = [&](int i0) {
+#pragma unroll
+        for (int u = 0; u < kS8Run; ++u) {
+            const int i2 = i0 + u;
+            const int64_t e = ((int64_t)i2 * I1 + i1) * p.RP + r;
+            sav[u] = active && i2 < i2b ? p.S[e] : 0.0;
+            sdv[u] = active && i2 < i2b ? p.Sd[e] : 0.0;
+        }
+    };
+    load_run(i2a);
+    const dd x1a{active ? p.A1[(int64_t)r * I1 + i1] : 0.0, 0.0};
+    const dd x1d{active ? p.D1[(int64_t)r * I1 + i1] : 0.0, 0.0};
     for (int e = threadIdx.x; e < (i2b - i2a) * p.RP; e += blockDim.x) {
-        const int ii = e / p.RP, r = e % p.RP;
-        const bool ok = r < p.R;
-        x2s[0][ii][r] = ok ? p.A2[(int64_t)r * I2 + i2a + ii] : 0.0;
-        x2s[1][ii][r] = ok ? p.D2[(int64_t)r * I2 + i2a + ii] : 0.0;
+        const int n = i2b - i2a, ii = e % n, rr = e / n;  // coalesced over i2
+        const bool ok = rr < p.R;
+        x2s[0][ii][rr] = ok ? p.A2[(int64_t)rr * I2 + i2a + ii] : 0.0;
+        x2s[1][ii][rr] = ok ? p.D2[(int64_t)rr * I2 + i2a + ii] : 0.0;
     }
     __syncthreads();
-    const int i1 = pr / p.RP, r = pr % p.RP;
-    if (pr < npr && r < p.R) {
-        const double x1a = p.A1[(int64_t)r * I1 + i1], x1d = p.D1[(int64_t)r * I1 + i1];
-        for (int i0 = i2a; i0 < i2b; i0 += kS8Run) {
-            double part[8];
+    if (active) {
+        dd q[4];  // S.A2, S.D2, S_d.A2, S_d.D2 over the chunk
 #pragma unroll
-            for (int k = 0; k < 8; ++k) part[k] = 0.0;
-            const int iend = min(i2b, i0 + kS8Run);
-            for (int i2 = i0; i2 < iend; ++i2) {
-                const int64_t e = ((int64_t)i2 * I1 + i1) * p.RP + r;
-                const double sa = p.S[e], sd = p.Sd[e];
+        for (int k = 0; k < 4; ++k) q[k] = dd{0.0, 0.0};
+        for (int i0 = i2a; i0 < i2b; i0 += kS8Run) {
+            if (i0 > i2a) load_run(i0);  // the run's loads issue together
+            double part[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int u = 0; u < kS8Run; ++u) {
+                const int i2 = i0 + u;
+                if (i2 >= i2b) break;
                 const double x2a = x2s[0][i2 - i2a][r], x2d = x2s[1][i2 - i2a][r];
-                const double aa = x1a * x2a, ad = x1a * x2d, da = x1d * x2a, dd2 = x1d * x2d;
-                part[0] = fma(sa, aa, part[0]);
-                part[1] = fma(sa, ad, part[1]);
-                part[2] = fma(sa, da, part[2]);
-                part[3] = fma(sa, dd2, part[3]);
-                part[4] = fma(sd, aa, part[4]);
-                part[5] = fma(sd, ad, part[5]);
-                part[6] = fma(sd, da, part[6]);
-                part[7] = fma(sd, dd2, part[7]);
+                part[0] = fma(sav[u], x2a, part[0]);
+                part[1] = fma(sav[u], x2d, part[1]);
+                part[2] = fma(sdv[u], x2a, part[2]);
+                part[3] = fma(sdv[u], x2d, part[3]);
             }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) acc[k] = dd_add(acc[k], dd{part[k], 0.0});
+            for (int k = 0; k < 4; ++k) dd_acc(q[k], part[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[k] = dd_two_sum(q[k].hi, q[k].lo);
+        // k = 4 b0 + 2 b1 + b2: q index 2 b0 + b2, X1 by b1
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = dd_mul(q[2 * (k >> 2) + (k & 1)], (k & 2) ? x1d : x1a);
+    }
+    // transposing warp reduction: each xor step halves the values a lane holds (4 + 2 + 1 + 1 + 1
+    // double-double adds per lane); contraction k ends in lane 4 k
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    {
+        const bool b = lane & 16;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const dd mine = b ? acc[j + 4] : acc[j], other = b ? acc[j] : acc[j + 4];
+            acc[j] = dd_add(mine, dd_shfl_xor(other, 16));
         }
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    {
+        const bool c = lane & 8;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[k] = dd_add(acc[k], dd_shfl_xor(acc[k], o));
-        if (lane == 0) red[warp][k] = acc[k];
+        for (int j = 0; j < 2; ++j) {
+            const dd mine = c ? acc[j + 2] : acc[j], other = c ? acc[j] : acc[j + 2];
+            acc[j] = dd_add(mine, dd_shfl_xor(other, 8));
+        }
     }
+    {
+        const bool d = lane & 4;
+        const dd mine = d ? acc[1] : acc[0], other = d ? acc[0] : acc[1];
+        acc[0] = dd_add(mine, dd_shfl_xor(other, 4));
+    }
+    acc[0] = dd_add(acc[0], dd_shfl_xor(acc[0], 2));
+    acc[0] = dd_add(acc[0], dd_shfl_xor(acc[0], 1));
+    if ((lane & 3) == 0) red[warp][lane >> 2] = acc[0];
     __syncthreads();
     if (threadIdx.x < 8) {
         dd s{0.0, 0.0};
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s = dd_add(s, red[w][threadIdx.x]);
         p.part[(size_t)blockIdx.x * 8 + threadIdx.x] = s;
     }
-    if (!last_block_arrives(p.counter)) return;
-    // blocks' partials: thread t folds blocks t, t + 256, ... (fixed order), then a shared tree
-    __shared__ dd tr[256];
-    for (int k = 0; k < 8; ++k) {
-        dd s{0.0, 0.0};
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) s = dd_add(s, p.part[(size_t)b * 8 + k]);
-        tr[threadIdx.x] = s;
-        __syncthreads();
-        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-            if ((int)threadIdx.x < w) tr[threadIdx.x] = dd_add(tr[threadIdx.x], tr[threadIdx.x + w]);
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) p.out[k] = tr[0];
-        __syncthreads();
-    }
 }
 
 struct CoefParams {
     int R, RP;
-    const dd* grams;  // [mode][kind][RP*RP]
-    const dd* s8;
+    const dd* grams;   // [mode][kind][RP*RP]
+    const dd* s8part;  // [block][8] partials of the eight contractions
+    int s8_blocks;
     dd half_norm_sq;
-    dd* coef;         // [kPolyDeg + 1]
+    dd* coef;          // [kPolyDeg + 1]
 };
 
 // phi coefficients: 1/2 ||T||^2 - sum_S a^|S| s8[S] + 1/2 sum_qr prod_n G_n(a)_qr
 __global__ void __launch_bounds__(256) coef_kernel(const CoefParams p) {
-    __shared__ dd red[256][kPolyDeg + 1];
-    dd c[kPolyDeg + 1];
+    dd c8[8];
 #pragma unroll
-    for (int k = 0; k <= kPolyDeg; ++k) c[k] = dd{0.0, 0.0};
+    for (int k = 0; k <= kPolyDeg; ++k) c8[k] = dd{0.0, 0.0};
     const int RR = p.RP * p.RP;
     for (int e = threadIdx.x; e < p.R * p.R; e += blockDim.x) {
         const int q = e / p.R, r = e % p.R;
-        dd prod[kPolyDeg + 1];
+        dd qc[3][3];
 #pragma unroll
-        for (int k = 0; k <= kPolyDeg; ++k) prod[k] = dd{k == 0 ? 1.0 : 0.0, 0.0};
-        int deg = 0;
         for (int n = 0; n < 3; ++n) {
             const dd* g = p.grams + (size_t)n * kKinds * RR;
-            const dd q0 = g[q * p.RP + r];
-            const dd q1 = dd_add(g[RR + q * p.RP + r], g[RR + r * p.RP + q]);
-            const dd q2 = g[2 * RR + q * p.RP + r];
-            dd nx[kPolyDeg + 1];
-#pragma unroll
-            for (int k = 0; k <= kPolyDeg; ++k) nx[k] = dd{0.0, 0.0};
-            for (int k = 0; k <= deg; ++k) {
-                nx[k] = dd_add(nx[k], dd_mul(prod[k], q0));
-                nx[k + 1] = dd_add(nx[k + 1], dd_mul(prod[k], q1));
-                nx[k + 2] = dd_add(nx[k + 2], dd_mul(prod[k], q2));
-            }
-            deg += 2;
-#pragma unroll
-            for (int k = 0; k <= kPolyDeg; ++k) prod[k] = nx[k];
+            qc[n][0] = g[q * p.RP + r];
+            qc[n][1] = dd_add(g[RR + q * p.RP + r], g[RR + r * p.RP + q]);
+            qc[n][2] = g[2 * RR + q * p.RP + r];
         }
+        // (q0 + q1 a + q2 a^2) for modes 0, 1, 2 multiplied out (degrees 4 then 6), unrolled
+        dd p4[5];
 #pragma unroll
-        for (int k = 0; k <= kPolyDeg; ++k) c[k] = dd_add(c[k], prod[k]);
+        for (int k = 0; k < 5; ++k) p4[k] = dd{0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) p4[i + j] = dd_add(p4[i + j], dd_mul(qc[0][i], qc[1][j]));
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) c8[i + j] = dd_add(c8[i + j], dd_mul(p4[i], qc[2][j]));
     }
+    // the eight contractions: s8_kernel's block partials, thread t folding blocks b = t / 8 mod 32
+    // of contraction t % 8 (loads issued together)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    dd v8{0.0, 0.0};
+    {
+        const int k = threadIdx.x & 7, g = threadIdx.x >> 3;
+        for (int b0 = g; b0 < p.s8_blocks; b0 += 32 * 16) {
+            dd x[16];
 #pragma unroll
-    for (int k = 0; k <= kPolyDeg; ++k) red[threadIdx.x][k] = c[k];
+            for (int u = 0; u < 16; ++u) {
+                const int b = b0 + 32 * u;
+                x[u] = b < p.s8_blocks ? p.s8part[(size_t)b * 8 + k] : dd{0.0, 0.0};
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v8 = dd_add(v8, x[u]);
+        }
+    }
+    // fixed-order trees: a transposing shuffle reduction of the seven coefficients (plus a zero)
+    // that ends with coefficient k in lane 4 k, the s8 sums over the warp's four groups, then the
+    // warps in order
+    c8[kPolyDeg + 1] = dd{0.0, 0.0};
+    {
+        const bool b = lane & 16;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const dd mine = b ? c8[j + 4] : c8[j], other = b ? c8[j] : c8[j + 4];
+            c8[j] = dd_add(mine, dd_shfl_xor(other, 16));
+        }
+    }
+    {
+        const bool cc = lane & 8;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const dd mine = cc ? c8[j + 2] : c8[j], other = cc ? c8[j] : c8[j + 2];
+            c8[j] = dd_add(mine, dd_shfl_xor(other, 8));
+        }
+    }
+    {
+        const bool d = lane & 4;
+        const dd mine = d ? c8[1] : c8[0], other = d ? c8[0] : c8[1];
+        c8[0] = dd_add(mine, dd_shfl_xor(other, 4));
+    }
+    c8[0] = dd_add(c8[0], dd_shfl_xor(c8[0], 2));
+    c8[0] = dd_add(c8[0], dd_shfl_xor(c8[0], 1));
+#pragma unroll
+    for (int o = 16; o >= 8; o >>= 1) v8 = dd_add(v8, dd_shfl_xor(v8, o));
+    __shared__ dd red[8][kPolyDeg + 1 + 8];
+    if ((lane & 3) == 0 && (lane >> 2) <= kPolyDeg) red[warp][lane >> 2] = c8[0];
+    if (lane < 8) red[warp][kPolyDeg + 1 + lane] = v8;
     __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {  // fixed-order tree
-        if ((int)threadIdx.x < w)
-#pragma unroll
-            for (int k = 0; k <= kPolyDeg; ++k) red[threadIdx.x][k] = dd_add(red[threadIdx.x][k], red[threadIdx.x + w][k]);
-        __syncthreads();
+    __shared__ dd tot[kPolyDeg + 1 + 8];
+    if (threadIdx.x < kPolyDeg + 1 + 8) {
+        dd v{0.0, 0.0};
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = dd_add(v, red[w][threadIdx.x]);
+        tot[threadIdx.x] = v;
     }
+    __syncthreads();
+    const dd* s8v = tot + kPolyDeg + 1;
     if (threadIdx.x == 0) {
         // <T, model(a)>: a^|S| s8[S]
-        dd a[4] = {p.s8[0], dd_add(dd_add(p.s8[4], p.s8[2]), p.s8[1]), dd_add(dd_add(p.s8[6], p.s8[5]), p.s8[3]),
-                   p.s8[7]};
+        dd a[4] = {s8v[0], dd_add(dd_add(s8v[4], s8v[2]), s8v[1]), dd_add(dd_add(s8v[6], s8v[5]), s8v[3]), s8v[7]};
         for (int k = 0; k <= kPolyDeg; ++k) {
-            dd v = dd_mul(dd{0.5, 0.0}, red[0][k]);
+            dd v = dd_mul(dd{0.5, 0.0}, tot[k]);
             if (k <= 3) v = dd_sub(v, a[k]);
             if (k == 0) v = dd_add(v, p.half_norm_sq);
             p.coef[k] = v;
@@ -292,21 +349,14 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     CrossParams c{};
     c.R = w.R;
     c.RP = w.RP;
-    int64_t base = 0;
     for (int n = 0; n < 3; ++n) {
         c.dims[n] = t.dims[n];
         c.a[n] = ub + w.off[n];
         c.d[n] = d + w.off[n];
-        c.nchunk[n] = gram_chunks(t.dims[n]);
-        c.rows[n] = gram_chunk_rows(t.dims[n]);
-        c.base[n] = base;
-        base += (int64_t)c.nchunk[n] * kKinds * w.R * w.R;
     }
-    c.part = pw.gpart;
     c.out = pw.grams;
-    c.counter = pw.counter;
-    const int cgrid = (int)std::max<int64_t>(1, std::min<int64_t>((base + 7) / 8, 4 * sm_count()));
-    cross_gram_kernel<<<cgrid, 256, 0, st>>>(c);
+    const int ctasks = 3 * kKinds * w.RP * w.RP;
+    cross_gram_kernel<<<(ctasks + 7) / 8, 256, 0, st>>>(c);
     CPFIT_CUDA(cudaGetLastError());
     S8Params s{};
     s.S = w.S;
@@ -320,17 +370,22 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     s.A2 = ub + w.off[2];
     s.D2 = d + w.off[2];
     s.part = pw.s8part;
-    s.out = pw.s8;
-    s.counter = pw.counter + 1;
+
     const int ngx = (int)((t.dims[0 + 1] * w.RP + 255) / 256);
     const int ngy = (int)((t.dims[2] + kS8I2 - 1) / kS8I2);
+    static bool carve = [] {  // several CTAs per SM need the shared-memory carveout
+        cudaFuncSetAttribute(s8_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        return true;
+    }();
+    (void)carve;
     s8_kernel<<<ngx * ngy, 256, 0, st>>>(s);
     CPFIT_CUDA(cudaGetLastError());
     CoefParams q{};
     q.R = w.R;
     q.RP = w.RP;
     q.grams = pw.grams;
-    q.s8 = pw.s8;
+    q.s8part = pw.s8part;
+    q.s8_blocks = ngx * ngy;
     q.half_norm_sq = dd{0.5 * t.norm_sq, 0.5 * t.norm_sq_lo};
     q.coef = pw.coef;
     coef_kernel<<<1, 256, 0, st>>>(q);
