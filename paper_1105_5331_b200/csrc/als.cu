@@ -311,7 +311,8 @@ __global__ void normalize_kernel(const NormParams p) {
     if (tid < p.R) {
         const int src = perm[tid];
         const double l = lam[src];
-        for (int n = 0; n < p.order; ++n) scale[n][tid] = (l == 0.0) ? 1.0 : pow(l, 1.0 / p.order) / nrm[n][src];
+        const double root = (l == 0.0) ? 0.0 : pow(l, 1.0 / p.order);
+        for (int n = 0; n < p.order; ++n) scale[n][tid] = (l == 0.0) ? 1.0 : root / nrm[n][src];
         if (blockIdx.x == 0 && p.perm_out) {
             p.perm_out[tid] = src;
             p.scale0_out[tid] = scale[0][tid];

@@ -80,10 +80,26 @@ unsigned long long* fiber_prof_buffer() {
 
 namespace {
 
+// fixed-order reductions of partial vectors, several in one launch (reduce_jobs)
+struct RedJob {
+    const double* part;
+    int nparts;
+    int64_t nout;
+    double* out;
+};
+struct RedJobs {
+    static constexpr int kMax = 2 * kMaxOrder + 1;
+    RedJob j[kMax];
+    int n = 0;
+    void add(const double* part, int nparts, int64_t nout, double* out) { j[n++] = RedJob{part, nparts, nout, out}; }
+};
+void reduce_jobs(const RedJobs& jobs, cudaStream_t st);
 // M0 = sum over the fiber-pass CTAs of their [RP][32 NC] partials (fixed order)
-void reduce_parts(const double* part, int nparts, int64_t nout, double* out, cudaStream_t st);
+void add_m0_job(EvalWork& w, RedJobs& j) { j.add(w.m0_part, w.fiber_grid, (int64_t)w.RP * 32 * w.fiber_nchunk, w.m0); }
 void reduce_m0(EvalWork& w, cudaStream_t st) {
-    reduce_parts(w.m0_part, w.fiber_grid, (int64_t)w.RP * 32 * w.fiber_nchunk, w.m0, st);
+    RedJobs j;
+    add_m0_job(w, j);
+    reduce_jobs(j, st);
 }
 
 void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, bool do_f,
@@ -162,6 +178,9 @@ struct LevelParams {
     double* m_part;  // [gridDim.x][Ih*RP] or null (no M_h)
     double* s_out;   // [gridDim.y][Jt][RP] or null (no Sout)
     int64_t spc;     // slabs per CTA
+    // optional: the input is Sin + beta Sd (beta on the device), read on the fly
+    const double* Sd;
+    const double* beta;
 };
 
 constexpr int kLevelThreads = 256;
@@ -171,7 +190,7 @@ constexpr int kSlabBatch = 8;
 // L2 latency in flight per thread); the Khatri-Rao tail rows of a batch of slabs are built once
 // per batch with 32-bit index math.
 template <int RP, int KM, bool DO_M, bool DO_S>
-__global__ void __launch_bounds__(kLevelThreads) level_kernel(const LevelParams p) {
+__global__ void __launch_bounds__(kLevelThreads, 2) level_kernel(const LevelParams p) {
     constexpr int B = kLevelThreads, NW = B / 32;
     __shared__ double wt[kSlabBatch][RP];
     __shared__ double sred[kSlabBatch][NW][RP];
@@ -182,6 +201,7 @@ __global__ void __launch_bounds__(kLevelThreads) level_kernel(const LevelParams 
     const int s_begin = (int)(blockIdx.x * p.spc);
     const int s_end = (int)imin64(p.Jt, s_begin + p.spc);
     double acc[KM], ah[KM];
+    const double bt = p.Sd ? *p.beta : 0.0;
 #pragma unroll
     for (int k = 0; k < KM; ++k) {
         const int pr = pbase + k * B;
@@ -219,6 +239,16 @@ __global__ void __launch_bounds__(kLevelThreads) level_kernel(const LevelParams 
                 const int pr = pbase + k * B;
                 v0[k] = pr < npairs ? __ldg(src0 + pr) : 0.0;
                 v1[k] = (two && pr < npairs) ? __ldg(src1 + pr) : 0.0;
+            }
+            if (p.Sd) {  // S(u_bar + beta d) = S(u_bar) + beta S_d, as the separate axpy would
+                const double* d0 = p.Sd + (int64_t)(s0 + sl) * npairs;
+                const double* d1 = d0 + npairs;
+#pragma unroll
+                for (int k = 0; k < KM; ++k) {
+                    const int pr = pbase + k * B;
+                    if (pr < npairs) v0[k] = fma(bt, __ldg(d0 + pr), v0[k]);
+                    if (two && pr < npairs) v1[k] = fma(bt, __ldg(d1 + pr), v1[k]);
+                }
             }
             if (DO_M) {
                 const double w0 = wt[sl][r], w1 = two ? wt[sl + 1][r] : 0.0;
@@ -264,6 +294,106 @@ __global__ void __launch_bounds__(kLevelThreads) level_kernel(const LevelParams 
     }
 }
 
+// Last level (one Khatri-Rao tail factor, e.g. h = 1 of an order-3 tensor): CTA (x, y) owns the
+// pair tile [256 x, 256 (x + 1)) of slabs [kBulkSlabs y, kBulkSlabs (y + 1)). One thread issues
+// the tile's slab rows (2 KB each, and those of Sd) as bulk async copies into shared memory while
+// the others stage the tail factor's rows; a thread then owns one pair:
+//   M partial (per y)   = sum over its slabs of Sin * A_tail[slab][r]
+//   Sout partial (per x) = per slab, the sum over the tile's pairs of rank r of Sin * A_h[i][r]
+// (lanes of equal r by shuffles, then the warps in order). Partials reduced by reduce_jobs.
+constexpr int kBulkSlabs = 16;
+constexpr int kBulkPairs = kLevelThreads;
+
+template <int RP, bool DO_M, bool DO_S>
+__global__ void __launch_bounds__(kBulkPairs) level_bulk_kernel(const LevelParams p) {
+    constexpr int NW = kBulkPairs / 32;
+    extern __shared__ __align__(16) double lbuf[];  // [kBulkSlabs][kBulkPairs] Sin, then Sd
+    __shared__ double a2s[kBulkSlabs][RP];
+    __shared__ __align__(8) uint64_t bar;
+    // the per-warp Sout sums reuse the Sin rows once every warp has read them
+    static_assert(NW * kBulkSlabs * RP <= kBulkSlabs * kBulkPairs, "sred alias");
+    double(*sred)[kBulkSlabs][RP] = reinterpret_cast<double(*)[kBulkSlabs][RP]>(lbuf);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int npairs = (int)(p.Ih * RP);
+    const int pr0 = blockIdx.x * kBulkPairs, pr = pr0 + tid;
+    const int s0 = blockIdx.y * kBulkSlabs;
+    const int nsl = (int)imin64(kBulkSlabs, p.Jt - s0);
+    const int npr = min(kBulkPairs, npairs - pr0);
+    const bool has_d = p.Sd != nullptr;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+        const uint32_t row = (uint32_t)npr * 8u;
+        mbar_arrive_expect_tx(&bar, row * (uint32_t)nsl * (has_d ? 2u : 1u));
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int64_t off = (int64_t)(s0 + sl) * npairs + pr0;
+            bulk_g2s(lbuf + sl * kBulkPairs, p.Sin + off, row, &bar);
+            if (has_d) bulk_g2s(lbuf + (kBulkSlabs + sl) * kBulkPairs, p.Sd + off, row, &bar);
+        }
+    }
+    const int r = tid % RP;
+    const double bt = has_d ? *p.beta : 0.0;
+    const double ah = (DO_S && pr < npairs && r < p.R) ? p.Ah[(int64_t)r * p.Ih + pr / RP] : 0.0;
+    if (DO_M && tid < kBulkSlabs * RP) {
+        const int sl = tid / RP, rr = tid % RP;
+        a2s[sl][rr] = (sl < nsl && rr < p.R) ? p.tfac[0][(int64_t)rr * p.tdims[0] + s0 + sl] : 0.0;
+    }
+    __syncthreads();  // a2s staged; the barrier's init is visible
+    mbar_wait(&bar, 0);
+    double acc = 0.0, xs[kBulkSlabs];
+    const bool live = pr < npairs;
+#pragma unroll
+    for (int sl = 0; sl < kBulkSlabs; ++sl) {
+        xs[sl] = 0.0;
+        if (sl < nsl) {
+            double v = live ? lbuf[sl * kBulkPairs + tid] : 0.0;
+            if (has_d && live) v = fma(bt, lbuf[(kBulkSlabs + sl) * kBulkPairs + tid], v);
+            if (DO_M) acc = fma(v, a2s[sl][r], acc);
+            if (DO_S) {
+                double x = v * ah;
+#pragma unroll
+                for (int o = 16; o >= RP; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                xs[sl] = x;
+            }
+        }
+    }
+    if (DO_M && live) p.m_part[(int64_t)blockIdx.y * npairs + pr] = acc;
+    if (DO_S) {
+        __syncthreads();  // every warp is done with the Sin rows
+        if (lane < RP)
+#pragma unroll
+            for (int sl = 0; sl < kBulkSlabs; ++sl) sred[warp][sl][lane] = xs[sl];
+        __syncthreads();
+        for (int e = tid; e < nsl * RP; e += kBulkPairs) {
+            const int sl = e / RP, rr = e % RP;
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) v += sred[w][sl][rr];
+            p.s_out[((int64_t)blockIdx.x * p.Jt + s0 + sl) * RP + rr] = v;
+        }
+    }
+}
+
+template <int RP>
+void launch_level_bulk(const LevelParams& p, dim3 grid, cudaStream_t st) {
+    const bool m = p.m_part != nullptr, s = p.s_out != nullptr;
+    const size_t smem = sizeof(double) * kBulkSlabs * kBulkPairs * (p.Sd ? 2 : 1);
+    static bool attr = [] {  // every variant (the kernels share one function-pointer type)
+        const int mx = (int)(sizeof(double) * kBulkSlabs * kBulkPairs * 2);
+        cudaFuncSetAttribute(level_bulk_kernel<RP, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(level_bulk_kernel<RP, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(level_bulk_kernel<RP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        return true;
+    }();
+    (void)attr;
+    if (m && s)
+        level_bulk_kernel<RP, true, true><<<grid, kBulkPairs, smem, st>>>(p);
+    else if (m)
+        level_bulk_kernel<RP, true, false><<<grid, kBulkPairs, smem, st>>>(p);
+    else
+        level_bulk_kernel<RP, false, true><<<grid, kBulkPairs, smem, st>>>(p);
+}
+
 template <int RP, int KM>
 void launch_level_km(const LevelParams& p, dim3 grid, cudaStream_t st) {
     const bool m = p.m_part != nullptr, s = p.s_out != nullptr;
@@ -283,44 +413,69 @@ void launch_level_rp(const LevelParams& p, dim3 grid, int km, cudaStream_t st) {
     }
 }
 
-// Fixed-order reduction of `nparts` contiguous partial vectors: out[o] = sum_c part[c*nout+o].
+// Fixed-order reduction of `nparts` contiguous partial vectors: out[o] = sum_c part[c*nout+o],
+// for up to RedJobs::kMax jobs in one launch (job k owns blocks [blk0[k], blk0[k+1])).
 // Block = 32 outputs x 8 part-slices (coalesced across lanes), slices combined in order.
-__global__ void __launch_bounds__(256) reduce_parts_kernel(const double* __restrict__ part, int nparts, int64_t nout,
-                                                           double* __restrict__ out) {
+struct RedLaunch {
+    RedJob j[RedJobs::kMax];
+    int blk0[RedJobs::kMax + 1];
+    int n;
+};
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const RedLaunch L) {
     __shared__ double sl[8][33];
+    int k = 0;
+    while (k + 1 < L.n && (int)blockIdx.x >= L.blk0[k + 1]) ++k;
+    const double* __restrict__ part = L.j[k].part;
+    const int nparts = L.j[k].nparts;
+    const int64_t nout = L.j[k].nout;
     const int lane = threadIdx.x & 31, ws = threadIdx.x >> 5;
-    const int64_t o = (int64_t)blockIdx.x * 32 + lane;
+    const int64_t o = (int64_t)(blockIdx.x - L.blk0[k]) * 32 + lane;
     double v = 0.0;
     if (o < nout)
         for (int c0 = ws; c0 < nparts; c0 += 8 * 8) {
             double x[8];  // loads batched ahead of the in-order adds
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int c = c0 + 8 * k;
-                x[k] = c < nparts ? part[(int64_t)c * nout + o] : 0.0;
+            for (int u = 0; u < 8; ++u) {
+                const int c = c0 + 8 * u;
+                x[u] = c < nparts ? part[(int64_t)c * nout + o] : 0.0;
             }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v += x[k];
+            for (int u = 0; u < 8; ++u) v += x[u];
         }
     sl[ws][lane] = v;
     __syncthreads();
     if (ws == 0 && o < nout) {
         double s = 0.0;
-        for (int k = 0; k < 8; ++k) s += sl[k][lane];
-        out[o] = s;
+        for (int u = 0; u < 8; ++u) s += sl[u][lane];
+        L.j[k].out[o] = s;
     }
 }
 
-void reduce_parts(const double* part, int nparts, int64_t nout, double* out, cudaStream_t st) {
-    reduce_parts_kernel<<<(unsigned)((nout + 31) / 32), 256, 0, st>>>(part, nparts, nout, out);
+void reduce_jobs(const RedJobs& jobs, cudaStream_t st) {
+    if (jobs.n == 0) return;
+    RedLaunch L{};
+    L.n = jobs.n;
+    int b = 0;
+    for (int k = 0; k < jobs.n; ++k) {
+        L.j[k] = jobs.j[k];
+        L.blk0[k] = b;
+        b += (int)((jobs.j[k].nout + 31) / 32);
+    }
+    L.blk0[jobs.n] = b;
+    reduce_parts_kernel<<<(unsigned)b, 256, 0, st>>>(L);
     CPFIT_CUDA(cudaGetLastError());
 }
 
+// defer_m / defer_s: append the partial reductions of M_h / Sout to a job list instead of
+// launching them (reduce_jobs later, together with other reductions)
 void run_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
-               double* Sout, cudaStream_t st) {
+               double* Sout, cudaStream_t st, RedJobs* defer_m = nullptr, RedJobs* defer_s = nullptr,
+               const double* Sd = nullptr, const double* beta = nullptr) {
     if (!do_m && !do_s) return;
     LevelParams p{};
     p.Sin = Sin;
+    p.Sd = Sd;
+    p.beta = beta;
     p.Ih = t.dims[h];
     p.Jt = 1;
     for (int m = h + 1; m < t.order; ++m) p.Jt *= t.dims[m];
@@ -335,15 +490,30 @@ void run_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const 
     p.m_part = do_m ? w.lvl_part[h] : nullptr;
     p.s_out = do_s ? (ny > 1 ? w.lvl_spart[h] : Sout) : nullptr;
     p.spc = w.lvl_spc[h];
-    const dim3 grid((unsigned)w.lvl_nx[h], (unsigned)ny);
-    switch (w.RP) {
-        case 8: launch_level_rp<8>(p, grid, w.lvl_km[h], st); break;
-        case 16: launch_level_rp<16>(p, grid, w.lvl_km[h], st); break;
-        default: launch_level_rp<32>(p, grid, w.lvl_km[h], st); break;
+    if (w.lvl_bulk[h]) {
+        // grid x over pair tiles (the Sout partials), y over slab ranges (the M partials)
+        const dim3 grid((unsigned)ny, (unsigned)w.lvl_nx[h]);
+        switch (w.RP) {
+            case 8: launch_level_bulk<8>(p, grid, st); break;
+            case 16: launch_level_bulk<16>(p, grid, st); break;
+            default: launch_level_bulk<32>(p, grid, st); break;
+        }
+    } else {
+        if (Sd) throw std::logic_error("level: Sd needs the bulk level kernel");
+        const dim3 grid((unsigned)w.lvl_nx[h], (unsigned)ny);
+        switch (w.RP) {
+            case 8: launch_level_rp<8>(p, grid, w.lvl_km[h], st); break;
+            case 16: launch_level_rp<16>(p, grid, w.lvl_km[h], st); break;
+            default: launch_level_rp<32>(p, grid, w.lvl_km[h], st); break;
+        }
     }
     CPFIT_CUDA(cudaGetLastError());
-    if (do_m) reduce_parts(w.lvl_part[h], w.lvl_nx[h], p.Ih * w.RP, w.lvl_m[h], st);
-    if (do_s && ny > 1) reduce_parts(w.lvl_spart[h], ny, p.Jt * w.RP, Sout, st);
+    RedJobs own;
+    RedJobs& jm = defer_m ? *defer_m : own;
+    RedJobs& js = defer_s ? *defer_s : own;
+    if (do_m) jm.add(w.lvl_part[h], w.lvl_nx[h], p.Ih * w.RP, w.lvl_m[h]);
+    if (do_s && ny > 1) js.add(w.lvl_spart[h], ny, p.Jt * w.RP, Sout);
+    reduce_jobs(own, st);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -616,13 +786,21 @@ EvalWork* work_create(const DevTensor& t, int R) {
             int64_t Jt = 1;
             for (int m = h + 1; m < t.order; ++m) Jt *= t.dims[m];
             const int64_t npairs = t.dims[h] * w->RP;
-            const int64_t need = (npairs + kLevelThreads - 1) / kLevelThreads;
-            w->lvl_km[h] = need <= 4 ? 4 : need <= 8 ? 8 : 16;
-            w->lvl_ny[h] = (int)((npairs + (int64_t)kLevelThreads * w->lvl_km[h] - 1) / (kLevelThreads * w->lvl_km[h]));
-            const int64_t nx_want =
-                std::max<int64_t>(1, std::min<int64_t>(Jt, (2 * sms + w->lvl_ny[h] - 1) / w->lvl_ny[h]));
-            w->lvl_spc[h] = (Jt + nx_want - 1) / nx_want;
-            w->lvl_nx[h] = (int)((Jt + w->lvl_spc[h] - 1) / w->lvl_spc[h]);
+            if (h == t.order - 2) {  // one tail factor: the bulk-copy kernel
+                w->lvl_bulk[h] = true;
+                w->lvl_ny[h] = (int)((npairs + kBulkPairs - 1) / kBulkPairs);
+                w->lvl_nx[h] = (int)((Jt + kBulkSlabs - 1) / kBulkSlabs);
+                w->lvl_spc[h] = kBulkSlabs;
+            } else {
+                const int64_t need = (npairs + kLevelThreads - 1) / kLevelThreads;
+                w->lvl_km[h] = need <= 4 ? 4 : need <= 8 ? 8 : 16;
+                w->lvl_ny[h] =
+                    (int)((npairs + (int64_t)kLevelThreads * w->lvl_km[h] - 1) / (kLevelThreads * w->lvl_km[h]));
+                const int64_t nx_want =
+                    std::max<int64_t>(1, std::min<int64_t>(Jt, (2 * sms + w->lvl_ny[h] - 1) / w->lvl_ny[h]));
+                w->lvl_spc[h] = (Jt + nx_want - 1) / nx_want;
+                w->lvl_nx[h] = (int)((Jt + w->lvl_spc[h] - 1) / w->lvl_spc[h]);
+            }
             CPFIT_CUDA(cudaMalloc(&w->lvl_part[h], sizeof(double) * (size_t)w->lvl_nx[h] * npairs));
             CPFIT_CUDA(cudaMalloc(&w->lvl_m[h], sizeof(double) * (size_t)npairs));
             CPFIT_CUDA(cudaMalloc(&w->lvl_S[h], sizeof(double) * (size_t)Jt * w->RP));
@@ -729,13 +907,16 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
             run_fiber(t, w, u, false, true, true, w.gram, st, resid_flag, nullptr, w.S);
         else
             run_fiber(t, w, u, true, true, true, w.gram /* mode-0 Gram */, st, resid_flag);
-        reduce_m0(w, st);
-        // modes 1..N-1 from S
+        // modes 1..N-1 from S; the partial sums of M0, the M_h and the last level's Sout in one
+        // reduction launch
+        RedJobs jobs;
+        add_m0_job(w, jobs);
         const double* Sin = w.S;
         for (int h = 1; h < t.order - 1; ++h) {
-            run_level(t, w, h, Sin, u, true, true, w.lvl_S[h], st);
+            run_level(t, w, h, Sin, u, true, true, w.lvl_S[h], st, &jobs, h == t.order - 2 ? &jobs : nullptr);
             Sin = w.lvl_S[h];
         }
+        reduce_jobs(jobs, st);
     } else {
         sparse_all_modes(t, w, u, -1, st);
     }
@@ -796,15 +977,18 @@ void dense_s_pass(const DevTensor& t, EvalWork& w, const double* u, double* S_ou
     run_fiber(t, w, u, true, false, false, nullptr, st, nullptr, S_out);
 }
 void eval_given_s_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc,
-                         cudaStream_t st) {
-    grams_device(w, u, st);
+                         cudaStream_t st, const double* Sd, const double* beta, bool grams_given) {
+    if (!grams_given) grams_device(w, u, st);
     run_fiber(t, w, u, false, true, false, nullptr, st);  // M0 only
-    reduce_m0(w, st);
+    RedJobs jobs;
+    add_m0_job(w, jobs);
     const double* Sin = w.S;
     for (int h = 1; h < t.order - 1; ++h) {
-        run_level(t, w, h, Sin, u, true, true, w.lvl_S[h], st);
+        run_level(t, w, h, Sin, u, true, true, w.lvl_S[h], st, &jobs, h == t.order - 2 ? &jobs : nullptr,
+                  h == 1 ? Sd : nullptr, beta);
         Sin = w.lvl_S[h];
     }
+    reduce_jobs(jobs, st);
     run_grad(t, w, u, g, nullptr, true, sc, st);
 }
 

@@ -67,6 +67,7 @@ struct EvalWork {
     // level contractions (modes 1..N-2 heads)
     int lvl_nx[kMaxOrder] = {}, lvl_ny[kMaxOrder] = {}, lvl_km[kMaxOrder] = {};  // grid, pairs/thread
     int64_t lvl_spc[kMaxOrder] = {};   // slabs per CTA
+    bool lvl_bulk[kMaxOrder] = {};     // the last level: bulk-copy kernel (grid ny x nx)
     double* lvl_part[kMaxOrder] = {};  // M_h partials (nx x I_h x RP)
     double* lvl_spart[kMaxOrder] = {}; // Sout partials over pair chunks (ny x Jt x RP; ny > 1 only)
     double* lvl_m[kMaxOrder] = {};     // reduced M_h [i][r]
@@ -137,11 +138,12 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
 
 // Dense pieces for the exact line search (poly.cu): S = T x_1 A (first factor of u) into S_out;
-// and the evaluation at u when w.S already holds T x_1 A0(u) (order 3: M0 pass + level +
-// gradient; scalars->f is NOT the objective — the caller supplies it).
+// and the evaluation at u when T x_1 A0(u) = w.S (+ *beta Sd when Sd is given) (order 3: M0
+// pass + level + gradient; scalars->f is NOT the objective — the caller supplies it).
 void dense_s_pass(const DevTensor& t, EvalWork& w, const double* u, double* S_out, cudaStream_t st);
 void eval_given_s_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc,
-                         cudaStream_t st);
+                         cudaStream_t st, const double* Sd = nullptr, const double* beta = nullptr,
+                         bool grams_given = false);
 
 // Exact line search along d for order-3 dense tensors (poly.cu): phi(a) = f(u_bar + a d) is a
 // degree-6 polynomial whose coefficients follow from S(u_bar) (in w.S), S_d = T x_1 D0, the
@@ -163,6 +165,10 @@ void poly_destroy(PolyWork* p);
 // coefficients of phi from u_bar (its S in w.S) and d
 void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const double* ub, const double* d,
                        cudaStream_t st);
+// the accepted point u* = u_bar + beta d (beta on the device) and its Grams (into w.gram) from
+// the double-double cross Grams of the last build: A^T A + beta (A^T D + D^T A) + beta^2 D^T D
+void poly_point_device(EvalWork& w, const PolyWork& pw, const double* ub, const double* d, const double* beta,
+                       double* ut, cudaStream_t st);
 // phi(alphas[i]), phi'(alphas[i]) (device arrays)
 void poly_eval_device(const PolyWork& pw, const double* alphas, int n, double* phi, double* dphi, cudaStream_t st);
 

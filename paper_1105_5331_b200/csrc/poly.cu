@@ -311,6 +311,33 @@ void poly_eval_device(const PolyWork& pw, const double* alphas, int n, double* p
     CPFIT_CUDA(cudaGetLastError());
 }
 
+namespace {
+// u* = u_bar + beta d (grid-stride) and, in the first block, G_n(u*) from the cross Grams
+__global__ void __launch_bounds__(256) poly_point_kernel(const double* ub, const double* d, const double* beta_p,
+                                                         double* ut, int64_t n, const dd* cg, double* gram, int RP) {
+    const double beta = *beta_p;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        ut[i] = ub[i] + beta * d[i];
+    if (blockIdx.x != 0) return;
+    const int RR = RP * RP;
+    const dd b{beta, 0.0}, b2 = dd_mul(b, b);
+    for (int e = threadIdx.x; e < 3 * RR; e += blockDim.x) {
+        const int m = e / RR, q = (e % RR) / RP, r = e % RP;
+        const dd* g = cg + (size_t)m * kKinds * RR;
+        const dd ad = dd_add(g[RR + q * RP + r], g[RR + r * RP + q]);
+        const dd v = dd_add(dd_add(g[q * RP + r], dd_mul(b, ad)), dd_mul(b2, g[2 * RR + q * RP + r]));
+        gram[e] = v.hi + v.lo;
+    }
+}
+}  // namespace
+
+void poly_point_device(EvalWork& w, const PolyWork& pw, const double* ub, const double* d, const double* beta,
+                       double* ut, cudaStream_t st) {
+    poly_point_kernel<<<(int)std::min<int64_t>(148, (w.nu + 255) / 256), 256, 0, st>>>(ub, d, beta, ut, w.nu,
+                                                                                        pw.grams, w.gram, w.RP);
+    CPFIT_CUDA(cudaGetLastError());
+}
+
 bool poly_supported(const DevTensor& t) { return !t.sparse && t.order == 3; }
 
 PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {

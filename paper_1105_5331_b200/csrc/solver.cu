@@ -47,7 +47,7 @@ struct DevState {
     // this iteration's line search runs on the exact polynomial phi (poly.cu) instead of trial
     // evaluations; counters for the kernel-launch accounting
     int poly;
-    long long total_poly, total_poly_acc;
+    long long total_poly, total_poly_acc, total_direct;
     MoreThuente mt;
 };
 
@@ -92,7 +92,7 @@ __global__ void k_reset(Ctl c, int max_iters) {
     s.beta = 0.0;
     s.total_ls_evals = s.total_accepted = 0;
     s.poly = 0;
-    s.total_poly = s.total_poly_acc = 0;
+    s.total_poly = s.total_poly_acc = s.total_direct = 0;
     s.resid = c.resid_always;
     s.t0 = globaltimer();
 }
@@ -128,16 +128,16 @@ __global__ void k_set_cond_running(Ctl c, cudaGraphConditionalHandle h) {
     set_cond(c, h, s.stop < 0 && s.iter < s.max_iters);
 }
 
-__global__ void k_after_bar(Ctl c) {
+// After eval(u_bar) and the recombination: the eval's counters, then Step III entry
+// (ngmres.cpp:104-124) — restart test or the start of the line search, which runs on the
+// polynomial phi (poly.cu) when it applies and the per-fiber objective is in use (the residual
+// phase keeps trial evaluations). Selects the branch: 0 polynomial search, 1 trial-evaluation
+// search, 2 none (restart / no descent / failure).
+__global__ void k_branch(Ctl c, cudaGraphConditionalHandle br_h) {
     DevState& s = *c.s;
     s.f_bar = c.sc_bar->f;
     s.fevals += 1;
     s.gevals += 1;
-}
-
-// Step III entry (ngmres.cpp:104-124): restart test or start of the line search.
-__global__ void k_ls_init(Ctl c, cudaGraphConditionalHandle ls_h) {
-    DevState& s = *c.s;
     s.slope = c.accel_scal[1];
     s.restart = 0;
     s.stalled = 0;
@@ -153,8 +153,18 @@ __global__ void k_ls_init(Ctl c, cudaGraphConditionalHandle ls_h) {
     } else {
         s.searching = s.mt.begin(c.ls, s.f_bar, s.slope) ? 1 : 0;
     }
-    set_cond(c, ls_h, s.searching != 0);
+    s.poly = (c.poly_ok && s.searching && !s.resid) ? 1 : 0;
+    if (s.poly) {
+        s.searching = 0;  // no trial-evaluation loop
+        s.total_poly += 1;
+    } else if (s.searching) {
+        s.total_direct += 1;
+    }
+    if (!c.eager) cudaGraphSetConditional(br_h, s.poly ? 0u : s.searching ? 1u : 2u);
 }
+
+// first node of the trial-evaluation branch: the WHILE(searching) condition
+__global__ void k_ls_start(Ctl c, cudaGraphConditionalHandle ls_h) { set_cond(c, ls_h, c.s->searching != 0); }
 
 __global__ void k_trial(const DevState* s, const double* ub, const double* d, double* ut, int64_t n) {
     const double stp = s->mt.stp;
@@ -179,26 +189,25 @@ __global__ void k_ls_update(Ctl c, cudaGraphConditionalHandle ls_h) {
     set_cond(c, ls_h, s.searching != 0);
 }
 
-// the line search of this iteration runs on the polynomial when it applies and the per-fiber
-// objective is in use (the residual phase keeps trial evaluations)
-__global__ void k_poly_gate(Ctl c, cudaGraphConditionalHandle poly_h, cudaGraphConditionalHandle ls_h) {
+// Moré–Thuente (as started by k_branch) to termination on phi(a) = f(u_bar + a d) and phi'(a)
+// from the polynomial; the same bookkeeping as k_ls_update at termination; acc_h: accepted
+__global__ void k_poly_ls(Ctl c, cudaGraphConditionalHandle acc_h) {
     DevState& s = *c.s;
-    s.poly = (c.poly_ok && s.searching && !s.resid) ? 1 : 0;
-    if (s.poly) {
-        s.searching = 0;  // no trial-evaluation loop
-        s.total_poly += 1;
-    }
-    set_cond(c, poly_h, s.poly != 0);
-    set_cond(c, ls_h, s.searching != 0);
-}
-
-// Moré–Thuente (as started by k_ls_init) to termination on phi(a) = f(u_bar + a d) and phi'(a)
-// from the polynomial; the same bookkeeping as k_ls_update at termination
-__global__ void k_poly_ls(Ctl c) {
-    DevState& s = *c.s;
+    // phi and phi' by fp64 Horner on the rounded double-double coefficients (evaluation error
+    // ~ eps sum_k |c_k a^k|; the search compares values and slopes, not their tiny differences
+    // from phi(0), which comes from the evaluation of u_bar)
+    double cf[kPolyDeg + 1];
+#pragma unroll
+    for (int k = 0; k <= kPolyDeg; ++k) cf[k] = c.coef[k].hi + c.coef[k].lo;
     for (;;) {
-        double f, g;
-        poly_eval(c.coef, s.mt.stp, f, g);
+        const double a = s.mt.stp;
+        double f = cf[kPolyDeg], g = kPolyDeg * cf[kPolyDeg];
+#pragma unroll
+        for (int k = kPolyDeg - 1; k >= 1; --k) {
+            f = fma(f, a, cf[k]);
+            g = fma(g, a, k * cf[k]);
+        }
+        f = fma(f, a, cf[0]);
         if (s.mt.update(f, g)) break;
     }
     s.fevals += s.mt.evals;
@@ -208,19 +217,10 @@ __global__ void k_poly_ls(Ctl c) {
         s.accepted = 1;
         s.beta = s.mt.out_step;
     }
+    set_cond(c, acc_h, s.accepted != 0);
 }
 
-__global__ void k_accept_cond(Ctl c, cudaGraphConditionalHandle h, cudaGraphConditionalHandle hp) {
-    set_cond(c, h, c.s->accepted != 0 && !c.s->poly);
-    if (hp) set_cond(c, hp, c.s->accepted != 0 && c.s->poly);
-}
-
-// S(u_bar + beta d) = S(u_bar) + beta S_d in place
-__global__ void k_axpy_s(const DevState* s, double* S, const double* Sd, int64_t n) {
-    const double b = s->beta;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        S[i] += b * Sd[i];
-}
+__global__ void k_accept_cond(Ctl c, cudaGraphConditionalHandle h) { set_cond(c, h, c.s->accepted != 0); }
 
 __global__ void k_step_point(const DevState* s, const double* ub, const double* d, double* out, int64_t n) {
     const double b = s->beta;
@@ -406,8 +406,10 @@ cudaGraphConditionalHandle make_handle(cudaStream_t st) {
     return h;
 }
 
-// Appends a conditional node (WHILE / IF on handle h) to the capture on `st`; returns its body.
-cudaGraph_t append_conditional(cudaStream_t st, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
+// Appends a conditional node (WHILE / IF / SWITCH on handle h, `size` bodies) to the capture on
+// `st`; returns its first body (all bodies in `bodies` when given).
+cudaGraph_t append_conditional(cudaStream_t st, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                               unsigned size = 1, cudaGraph_t* bodies = nullptr) {
     cudaStreamCaptureStatus cs;
     cudaGraph_t g;
     const cudaGraphNode_t* deps = nullptr;
@@ -417,10 +419,12 @@ cudaGraph_t append_conditional(cudaStream_t st, cudaGraphConditionalHandle h, cu
     np.type = cudaGraphNodeTypeConditional;
     np.conditional.handle = h;
     np.conditional.type = type;
-    np.conditional.size = 1;
+    np.conditional.size = size;
     cudaGraphNode_t node;
     CPFIT_CUDA(cudaGraphAddNode(&node, g, deps, nd, &np));
     CPFIT_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+    if (bodies)
+        for (unsigned k = 0; k < size; ++k) bodies[k] = np.conditional.phGraph_out[k];
     return np.conditional.phGraph_out[0];
 }
 
@@ -431,6 +435,7 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     CPFIT_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     CPFIT_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
     CPFIT_CUDA(cudaStreamCreateWithFlags(&st3_, cudaStreamNonBlocking));
+    CPFIT_CUDA(cudaStreamCreateWithFlags(&st4_, cudaStreamNonBlocking));
     w_ = work_create(*t, R);
     n_ = w_->nu;
     cap_ = std::max(1, o.window);
@@ -504,6 +509,7 @@ Solver::~Solver() {
     cudaStreamDestroy(st_);
     cudaStreamDestroy(st2_);
     cudaStreamDestroy(st3_);
+    cudaStreamDestroy(st4_);
 }
 
 void Solver::build_graphs() {
@@ -566,7 +572,7 @@ void Solver::build_graphs() {
     cudaGraph_t body = append_conditional(st_, loop_h, cudaGraphCondTypeWhile);
     CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st2_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     stamp(st2_, 7);
-    cudaGraph_t lsb = nullptr, ab = nullptr, pb = nullptr, apb = nullptr;
+    cudaGraph_t lsb = nullptr, ab = nullptr, pb = nullptr, apb = nullptr, db = nullptr;
     if (method_ == 0) {
         // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
         als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_, m0_cur_, true, gout_);
@@ -575,70 +581,77 @@ void Solver::build_graphs() {
         if (m0_bar_)
             CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st2_));
         if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st2_));
-        k_after_bar<<<1, 1, 0, st2_>>>(c);
         stamp(st2_, 1);
         // Step II: windowed recombination -> d, slope                        (ngmres.cpp:97-101)
         accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st2_);
-        // Step III: restart test / Moré–Thuente line search                 (ngmres.cpp:111-147)
-        const cudaGraphConditionalHandle ls_h = make_handle(st2_);
-        k_ls_init<<<1, 1, 0, st2_>>>(c, ls_h);
+        // Step III: restart test / line search (ngmres.cpp:111-147) as one SWITCH node — every
+        // conditional node costs several microseconds of device time, taken or not
+        const cudaGraphConditionalHandle br_h = make_handle(st2_);
+        k_branch<<<1, 1, 0, st2_>>>(c, br_h);
+        stamp(st2_, 2);
+        cudaGraph_t br[2];
+        append_conditional(st2_, br_h, cudaGraphCondTypeSwitch, 2, br);
         if (pw_) {
-            // exact line search on phi(a) (poly.cu): one S_d pass + reductions, then Moré–Thuente
-            const cudaGraphConditionalHandle poly_h = make_handle(st2_);
-            k_poly_gate<<<1, 1, 0, st2_>>>(c, poly_h, ls_h);
-            pb = append_conditional(st2_, poly_h, cudaGraphCondTypeIf);
+            // 0: exact line search on phi(a) (poly.cu): one S_d pass + reductions, Moré–Thuente on
+            // the polynomial; accepted: u* = u_bar + beta d, S(u*) by the axpy, M0 pass + levels +
+            // gradient at u*, then the canonical rescale as for an evaluated trial
+            pb = br[0];
             CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, pb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+            const cudaGraphConditionalHandle accp_h = make_handle(st3_);
             poly_build_device(*t_, *w_, *pw_, ub_, d_, st3_);
-            k_poly_ls<<<1, 1, 0, st3_>>>(c);
+            k_poly_ls<<<1, 1, 0, st3_>>>(c, accp_h);
+            stamp(st3_, 3);
+            apb = append_conditional(st3_, accp_h, cudaGraphCondTypeIf);
+            CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st4_, apb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+            emit_poly_accept(st4_, &c);
+            stamp(st4_, 5);
+            CPFIT_CUDA(cudaGetLastError());
+            CPFIT_CUDA(cudaStreamEndCapture(st4_, &apb));
             CPFIT_CUDA(cudaGetLastError());
             CPFIT_CUDA(cudaStreamEndCapture(st3_, &pb));
         }
-        stamp(st2_, 2);
-        lsb = append_conditional(st2_, ls_h, cudaGraphCondTypeWhile);
-        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        k_trial<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
-        eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st3_, true, &s->resid);
-        stamp(st3_, 3);
-        k_ls_update<<<1, 1, 0, st3_>>>(c, ls_h);
-        if (!opt_.reeval_accepted) k_keep_best<<<vb, 256, 0, st3_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
-        stamp(st3_, 4);
+        // 1: Moré–Thuente on trial evaluations, then the accepted step
+        db = br[1];
+        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, db, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        const cudaGraphConditionalHandle ls_h = make_handle(st3_);
+        const cudaGraphConditionalHandle acc_h = make_handle(st3_);
+        k_ls_start<<<1, 1, 0, st3_>>>(c, ls_h);
+        lsb = append_conditional(st3_, ls_h, cudaGraphCondTypeWhile);
+        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st4_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        k_trial<<<vb, 256, 0, st4_>>>(s, ub_, d_, ut_, n_);
+        eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st4_, true, &s->resid);
+        stamp(st4_, 3);
+        k_ls_update<<<1, 1, 0, st4_>>>(c, ls_h);
+        if (!opt_.reeval_accepted) k_keep_best<<<vb, 256, 0, st4_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
+        stamp(st4_, 4);
         CPFIT_CUDA(cudaGetLastError());
-        CPFIT_CUDA(cudaStreamEndCapture(st3_, &lsb));
+        CPFIT_CUDA(cudaStreamEndCapture(st4_, &lsb));
         // accepted step: canonicalize u_bar + beta d and re-evaluate        (ngmres.cpp:137-142)
-        const cudaGraphConditionalHandle acc_h = make_handle(st2_);
-        const cudaGraphConditionalHandle accp_h = pw_ ? make_handle(st2_) : cudaGraphConditionalHandle{};
-        k_accept_cond<<<1, 1, 0, st2_>>>(c, acc_h, accp_h);
-        if (pw_) {
-            // accepted polynomial step: u* = u_bar + beta d, S(u*) by the axpy, M0 pass + levels +
-            // gradient at u*, then the canonical rescale as for an evaluated trial
-            apb = append_conditional(st2_, accp_h, cudaGraphCondTypeIf);
-            CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, apb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-            emit_poly_accept(st3_, &c);
-            CPFIT_CUDA(cudaGetLastError());
-            CPFIT_CUDA(cudaStreamEndCapture(st3_, &apb));
-        }
-        ab = append_conditional(st2_, acc_h, cudaGraphCondTypeIf);
-        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, ab, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        k_accept_cond<<<1, 1, 0, st3_>>>(c, acc_h);
+        ab = append_conditional(st3_, acc_h, cudaGraphCondTypeIf);
+        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st4_, ab, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         if (opt_.reeval_accepted) {
             // faithful: canonicalize u_bar + beta d, then a full evaluation there
-            k_step_point<<<vb, 256, 0, st3_>>>(s, ub_, d_, ut_, n_);
-            grams_device(*w_, ut_, st3_);
-            normalize_device(*w_, ut_, un_, st3_);
-            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st3_, true, &s->resid);
+            k_step_point<<<vb, 256, 0, st4_>>>(s, ub_, d_, ut_, n_);
+            grams_device(*w_, ut_, st4_);
+            normalize_device(*w_, ut_, un_, st4_);
+            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st4_, true, &s->resid);
             if (m0_cur_)
-                CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st3_));
-            k_after_next<<<1, 1, 0, st3_>>>(c);
+                CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st4_));
+            k_after_next<<<1, 1, 0, st4_>>>(c);
         } else {
             // exact rescale: normalize_and_reorder scales columns by D_n with
             // prod_n D_n = I, so f is unchanged and G_n -> G_n D_n^-1 (permuted)
-            k_select_accepted<<<vb, 256, 0, st3_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
-            grams_device(*w_, ut_, st3_);
-            const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st3_, m0_sel_, m0_cur_, gout_);
-            k_after_rescale<<<1, 1, 0, st3_>>>(c, sc_next, red_, nb);
+            k_select_accepted<<<vb, 256, 0, st4_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
+            grams_device(*w_, ut_, st4_);
+            const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st4_, m0_sel_, m0_cur_, gout_);
+            k_after_rescale<<<1, 1, 0, st4_>>>(c, sc_next, red_, nb);
         }
-        stamp(st3_, 5);
+        stamp(st4_, 5);
         CPFIT_CUDA(cudaGetLastError());
-        CPFIT_CUDA(cudaStreamEndCapture(st3_, &ab));
+        CPFIT_CUDA(cudaStreamEndCapture(st4_, &ab));
+        CPFIT_CUDA(cudaGetLastError());
+        CPFIT_CUDA(cudaStreamEndCapture(st3_, &db));
     } else {
         // stand-alone ALS iteration (als.cpp:79-95)
         // the previous evaluation (of u) left M0(u) in w.m0 for dense tensors
@@ -658,6 +671,7 @@ void Solver::build_graphs() {
     n_ls_ = lsb ? count_kernels(lsb) : 0;
     n_acc_ = ab ? count_kernels(ab) : 0;
     n_poly_ = pb ? count_kernels(pb) : 0;
+    n_direct_ = db ? count_kernels(db) : 0;
     n_accp_ = apb ? count_kernels(apb) : 0;
     CPFIT_CUDA(cudaGraphInstantiate(&x_loop_, g_loop_, 0));
 }
@@ -669,10 +683,10 @@ void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
     EvalScalars* sc_trial = reinterpret_cast<EvalScalars*>(sc_) + 2;
     EvalScalars* sc_next = reinterpret_cast<EvalScalars*>(sc_) + 3;
     const int vb = vec_blocks(n_);
-    k_step_point<<<vb, 256, 0, st>>>(s, ub_, d_, ut_, n_);
-    const int64_t ns = t_->J * w_->RP;
-    k_axpy_s<<<(int)std::min<int64_t>(4 * 148, (ns + 255) / 256), 256, 0, st>>>(s, w_->S, pw_->S_d, ns);
-    eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st);
+    // u* and its Grams (from the cross Grams); S(u*) = S(u_bar) + beta S_d is formed on the fly
+    // by the level pass
+    poly_point_device(*w_, *pw_, ub_, d_, &s->beta, ut_, st);
+    eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true);
     const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, w_->m0, m0_cur_, gout_);
     k_after_rescale<<<1, 1, 0, st>>>(c, sc_next, red_, nb);
     CPFIT_CUDA(cudaGetLastError());
@@ -696,7 +710,7 @@ long long Solver::pending_loop_launches() {
     CPFIT_CUDA(cudaMemcpyAsync(&hs, state_, sizeof(DevState), cudaMemcpyDeviceToHost, st_));
     sync();
     return (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + (hs.total_accepted - hs.total_poly_acc) * n_acc_ +
-           hs.total_poly * n_poly_ + hs.total_poly_acc * n_accp_;
+           hs.total_poly * n_poly_ + hs.total_poly_acc * n_accp_ + hs.total_direct * n_direct_;
 }
 
 void Solver::run_loop(int max_iters_total) {
@@ -741,15 +755,11 @@ void Solver::run_loop_eager() {
             if (m0_bar_)
                 CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
             if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st_));
-            k_after_bar<<<1, 1, 0, st_>>>(c);
             accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st_);
-            k_ls_init<<<1, 1, 0, st_>>>(c, none);
-            if (pw_) {
-                k_poly_gate<<<1, 1, 0, st_>>>(c, none, none);
-                if (state().poly) {
-                    poly_build_device(*t_, *w_, *pw_, ub_, d_, st_);
-                    k_poly_ls<<<1, 1, 0, st_>>>(c);
-                }
+            k_branch<<<1, 1, 0, st_>>>(c, none);
+            if (state().poly) {
+                poly_build_device(*t_, *w_, *pw_, ub_, d_, st_);
+                k_poly_ls<<<1, 1, 0, st_>>>(c, none);
             }
             while (state().searching) {
                 k_trial<<<vb, 256, 0, st_>>>(s, ub_, d_, ut_, n_);
@@ -758,7 +768,6 @@ void Solver::run_loop_eager() {
                 if (!opt_.reeval_accepted)
                     k_keep_best<<<vb, 256, 0, st_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
             }
-            k_accept_cond<<<1, 1, 0, st_>>>(c, none, none);
             const DevState ha = state();
             if (ha.accepted && ha.poly) {
                 emit_poly_accept(st_, &c);
@@ -817,7 +826,7 @@ SolverSummary Solver::summary() {
     r.gevals = hs.gevals;
     r.launches = launches_done_ + loop_launches_ * n_prelude_ + init_launches_ * n_init_ +
                  (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + (hs.total_accepted - hs.total_poly_acc) * n_acc_ +
-                 hs.total_poly * n_poly_ + hs.total_poly_acc * n_accp_;
+                 hs.total_poly * n_poly_ + hs.total_poly_acc * n_accp_ + hs.total_direct * n_direct_;
     return r;
 }
 

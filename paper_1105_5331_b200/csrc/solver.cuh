@@ -82,7 +82,7 @@ private:
     double* gram_bar_ = nullptr;
     int64_t gram_n() const { return (int64_t)w_->order * w_->RP * w_->RP; }
     size_t gram_bytes() const { return sizeof(double) * (size_t)gram_n(); }
-    int n_poly_ = 0, n_accp_ = 0;
+    int n_poly_ = 0, n_accp_ = 0, n_direct_ = 0;
     bool eager_ = false;
     alignas(16) unsigned char ctl_blob_[512] = {};  // the control-kernel parameters (solver.cu Ctl)
     DevTensor* t_;
@@ -93,7 +93,7 @@ private:
     AccelWork* a_ = nullptr;
     int64_t n_ = 0;
     int cap_ = 1;
-    cudaStream_t st_{}, st2_{}, st3_{};
+    cudaStream_t st_{}, st2_{}, st3_{}, st4_{};
     double *u_ = nullptr, *g_ = nullptr, *ub_ = nullptr, *gb_ = nullptr, *d_ = nullptr, *ut_ = nullptr,
            *gt_ = nullptr, *un_ = nullptr, *gn_ = nullptr, *u0_ = nullptr, *ubest_ = nullptr, *work_ = nullptr,
            *mbuf_ = nullptr, *wu_ = nullptr, *wg_ = nullptr, *ubl_ = nullptr, *gbl_ = nullptr, *red_ = nullptr;
