@@ -27,6 +27,11 @@
 
 constexpr int kFStages = 3;
 constexpr int kFiberF = 16;
+constexpr int kMaxKSteps = 104;  // ldT / 4 for I_0 <= 416 (work_create checks)
+#ifndef CPFIT_SREG_CHAINS
+#define CPFIT_SREG_CHAINS 1
+#endif
+constexpr int kSRegChains = CPFIT_SREG_CHAINS;
 
 template <int RP>
 __host__ __device__ constexpr int w_ld() {
@@ -750,8 +755,196 @@ __global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(co
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// S-only pass for RP <= 16 with the A0 operand in registers. With both DMMA operands read from
+// shared memory (spass_kernel) the pass is bound by shared-memory bandwidth and the DMMA pipe
+// together (~63% of each: two 256-byte fragment loads per 8x8x4 DMMA). Here compute warp c owns
+// column group nt = c % NRT over K part h = c / NRT for BOTH 8-fibre groups of the tile: its B
+// fragments (A0 rows of its K range, one column group) stay in registers for the whole pass, so
+// each DMMA needs one shared-memory fragment load (of T). Parts h > 0 leave their sums in shared
+// memory for part 0, which writes the S rows.
+// ---------------------------------------------------------------------------------------
+#ifndef CPFIT_SREG_WARPS
+#define CPFIT_SREG_WARPS 12
+#endif
+#ifndef CPFIT_SREG_STAGES
+#define CPFIT_SREG_STAGES 3
+#endif
+template <int RP>
+struct SRegRoles {
+    static constexpr int NRT = RP / 8;             // column groups
+    static constexpr int KSPLIT = CPFIT_SREG_WARPS / NRT;  // K parts
+    static constexpr int NCW = NRT * KSPLIT;       // compute warps
+    static constexpr int NST = CPFIT_SREG_STAGES;  // T ring stages
+    static constexpr int WARPS = 1 + NCW;          // + the T producer
+    static constexpr int KMAX = (kMaxKSteps + KSPLIT - 1) / KSPLIT;  // k-steps per warp (9, 18)
+    static constexpr int CH = kSRegChains;         // accumulator chains per fibre group
+    static constexpr int NPART = NRT * (KSPLIT - 1);
+};
+
+// T rows at a pitch of ldT + 4 rounded to 4 mod 16 doubles (conflict-free fragment loads)
+__host__ __device__ inline int sreg_pitch(int64_t ldT) { return (int)(((ldT + 15) / 16) * 16 + 4); }
+
+template <int RP, int F>
+__host__ __device__ FiberSmem sreg_layout(int64_t ldT) {
+    using Ro = SRegRoles<RP>;
+    const int I0s = sreg_pitch(ldT);
+    FiberSmem s{};
+    size_t off = 0;
+    s.tiles = off;
+    off += sizeof(double) * (size_t)Ro::NST * F * I0s;
+    s.spart = off;  // [stage][NPART][2 fibre groups][64]
+    off += sizeof(double) * (size_t)Ro::NST * Ro::NPART * 128;
+    s.a0 = s.wbuf = s.gam = off;
+    s.bars = off;
+    off += sizeof(uint64_t) * (2 * Ro::NST + Ro::NST * Ro::NRT);
+    s.total = off;
+    return s;
+}
+
+template <int RP, int F>
+__global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(const FiberParams p) {
+    static_assert(F == 16, "two 8-fibre groups per tile");
+    using Ro = SRegRoles<RP>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int NS = Ro::NST;
+    const FiberSmem L = sreg_layout<RP, F>(p.ldT);
+    const int I0s = sreg_pitch(p.ldT);
+    const int KS = (int)(p.ldT / 4);
+    double* tiles = reinterpret_cast<double*>(smem_raw + L.tiles);
+    double* spart = reinterpret_cast<double*>(smem_raw + L.spart);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
+    uint64_t* tfull = bars;           // [NS] tx bytes
+    uint64_t* tempty = bars + NS;     // [NS] compute warps
+    uint64_t* pfull = bars + 2 * NS;  // [NS][NRT] the other K parts of a column group
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t t_begin = (int64_t)blockIdx.x * p.tiles_per_cta;
+    const int64_t t_end = imin64(p.ntiles, t_begin + p.tiles_per_cta);
+    const int64_t ntl = t_end > t_begin ? t_end - t_begin : 0;
+
+    for (int64_t e = tid; e < (int64_t)NS * F * I0s; e += blockDim.x) tiles[e] = 0.0;
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], Ro::NCW);
+            for (int q = 0; q < Ro::NRT; ++q) mbar_init(&pfull[s * Ro::NRT + q], Ro::KSPLIT - 1);
+        }
+    }
+    mbar_fence_init();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+
+    if (warp == 0) {  // T producer
+        for (int64_t k = 0; k < ntl; ++k) {
+            const int s = (int)(k % NS);
+            const int64_t f0 = (t_begin + k) * F;
+            if (k >= NS) mbar_wait(&tempty[s], (uint32_t)(((k / NS) - 1) & 1));
+            const int nvalid = (int)imin64(F, p.J - f0);
+            double* st = tiles + (size_t)s * F * I0s;
+            if (nvalid < F)
+                for (int e = lane; e < (F - nvalid) * I0s; e += 32) st[(size_t)nvalid * I0s + e] = 0.0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
+            __syncwarp();
+            if (lane < nvalid)
+                bulk_g2s(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s]);
+        }
+        return;
+    }
+    const int c = warp - 1;
+    const int nt = c % Ro::NRT, h = c / Ro::NRT;
+    const int rr = nt * 8 + (lane >> 2);
+    const int k_lo = (int)((int64_t)KS * h / Ro::KSPLIT), k_hi = (int)((int64_t)KS * (h + 1) / Ro::KSPLIT);
+    double bq[Ro::KMAX];  // B fragments A0[4 ks + lane % 4][rr], ks in [k_lo, k_hi)
+#pragma unroll
+    for (int u = 0; u < Ro::KMAX; ++u) {
+        const int i = (k_lo + u) * 4 + (lane & 3);
+        bq[u] = (k_lo + u < k_hi && i < p.I0 && rr < p.R) ? __ldg(p.A0 + (int64_t)rr * p.I0 + i) : 0.0;
+    }
+    for (int64_t k = 0; k < ntl; ++k) {
+        const int s = (int)(k % NS);
+        const int64_t f0 = (t_begin + k) * F;
+        mbar_wait(&tfull[s], (uint32_t)((k / NS) & 1));
+        // fibre group g's A fragments: T[g * 8 + lane / 4][4 ks + lane % 4]
+        const double* ta0 = tiles + (size_t)s * F * I0s + (lane >> 2) * I0s + (lane & 3);
+        const double* ta1 = ta0 + 8 * I0s;
+        double acc[2][Ro::CH][2];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int j = 0; j < Ro::CH; ++j) acc[g][j][0] = acc[g][j][1] = 0.0;
+#pragma unroll
+        for (int u0 = 0; u0 < Ro::KMAX; u0 += Ro::CH) {
+            double a0[Ro::CH], a1[Ro::CH];
+#pragma unroll
+            for (int j = 0; j < Ro::CH; ++j) {
+                const int ks = k_lo + u0 + j;
+                const bool ok = u0 + j < Ro::KMAX && ks < k_hi;
+                a0[j] = ok ? ta0[ks * 4] : 0.0;
+                a1[j] = ok ? ta1[ks * 4] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < Ro::CH; ++j)
+                if (u0 + j < Ro::KMAX && k_lo + u0 + j < k_hi) {
+                    dmma_8x8x4(acc[0][j][0], acc[0][j][1], a0[j], bq[u0 + j]);
+                    dmma_8x8x4(acc[1][j][0], acc[1][j][1], a1[j], bq[u0 + j]);
+                }
+        }
+        double sv[2][2];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                // chain sums: scalar fp64 shares the DMMA pipe, so few chains
+                double v = acc[g][0][e];
+#pragma unroll
+                for (int j = 1; j < Ro::CH; ++j) v += acc[g][j][e];
+                sv[g][e] = v;
+            }
+        if (h > 0) {
+            double* sp = spart + ((size_t)s * Ro::NPART + nt * (Ro::KSPLIT - 1) + (h - 1)) * 128 + 2 * lane;
+            sp[0] = sv[0][0];
+            sp[1] = sv[0][1];
+            sp[64] = sv[1][0];
+            sp[65] = sv[1][1];
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&pfull[s * Ro::NRT + nt]);
+                mbar_arrive(&tempty[s]);
+            }
+            continue;
+        }
+        mbar_wait(&pfull[s * Ro::NRT + nt], (uint32_t)((k / NS) & 1));
+#pragma unroll
+        for (int hh = 1; hh < Ro::KSPLIT; ++hh) {
+            const double* sp = spart + ((size_t)s * Ro::NPART + nt * (Ro::KSPLIT - 1) + (hh - 1)) * 128 + 2 * lane;
+            sv[0][0] += sp[0];
+            sv[0][1] += sp[1];
+            sv[1][0] += sp[64];
+            sv[1][1] += sp[65];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[s]);
+        const int r = nt * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const int64_t f = f0 + g * 8 + (lane >> 2);
+            if (f < p.J) *reinterpret_cast<double2*>(p.S_out + f * RP + r) = make_double2(sv[g][0], sv[g][1]);
+        }
+    }
+}
+
 template <int RP>
 void launch_spass(const FiberParams& p, int grid, cudaStream_t st) {
+    if constexpr (RP <= 16) {
+        const size_t smem = sreg_layout<RP, kFiberF>(p.ldT).total;
+        auto k = sreg_kernel<RP, kFiberF>;
+        CPFIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k<<<grid, 32 * SRegRoles<RP>::WARPS, smem, st>>>(p);
+        CPFIT_CUDA(cudaGetLastError());
+        return;
+    }
     const size_t smem = spass_layout<RP, kFiberF>(p.nchunk, p.I0).total;
     auto k = spass_kernel<RP, kFiberF>;
     CPFIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -761,8 +954,8 @@ void launch_spass(const FiberParams& p, int grid, cudaStream_t st) {
 
 size_t spass_smem(int RP, int nchunk, int64_t I0) {
     switch (RP) {
-        case 8: return spass_layout<8, kFiberF>(nchunk, I0).total;
-        case 16: return spass_layout<16, kFiberF>(nchunk, I0).total;
+        case 8: return sreg_layout<8, kFiberF>(4 * ((I0 + 3) / 4)).total;
+        case 16: return sreg_layout<16, kFiberF>(4 * ((I0 + 3) / 4)).total;
         default: return spass_layout<32, kFiberF>(nchunk, I0).total;
     }
 }
