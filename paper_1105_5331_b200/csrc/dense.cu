@@ -86,16 +86,28 @@ struct RedJob {
     int nparts;
     int64_t nout;
     double* out;
+    // gradient epilogue (reduce_grad): the reduced vector is M_mode, laid out [r][ld] (layout 0,
+    // M0) or [i][RP] (layout 1, the levels)
+    int mode, layout, ld;
 };
 struct RedJobs {
     static constexpr int kMax = 2 * kMaxOrder + 1;
     RedJob j[kMax];
     int n = 0;
-    void add(const double* part, int nparts, int64_t nout, double* out) { j[n++] = RedJob{part, nparts, nout, out}; }
+    void add(const double* part, int nparts, int64_t nout, double* out, int mode = -1, int layout = 1, int ld = 0) {
+        j[n++] = RedJob{part, nparts, nout, out, mode, layout, ld};
+    }
+    int64_t blocks() const {
+        int64_t b = 0;
+        for (int k = 0; k < n; ++k) b += (j[k].nout + 31) / 32;
+        return b;
+    }
 };
 void reduce_jobs(const RedJobs& jobs, cudaStream_t st);
 // M0 = sum over the fiber-pass CTAs of their [RP][32 NC] partials (fixed order)
-void add_m0_job(EvalWork& w, RedJobs& j) { j.add(w.m0_part, w.fiber_grid, (int64_t)w.RP * 32 * w.fiber_nchunk, w.m0); }
+void add_m0_job(EvalWork& w, RedJobs& j) {
+    j.add(w.m0_part, w.fiber_grid, (int64_t)w.RP * 32 * w.fiber_nchunk, w.m0, 0, 0, 32 * w.fiber_nchunk);
+}
 void reduce_m0(EvalWork& w, cudaStream_t st) {
     RedJobs j;
     add_m0_job(w, j);
@@ -320,22 +332,28 @@ __global__ void __launch_bounds__(kBulkPairs) level_bulk_kernel(const LevelParam
     const int nsl = (int)imin64(kBulkSlabs, p.Jt - s0);
     const int npr = min(kBulkPairs, npairs - pr0);
     const bool has_d = p.Sd != nullptr;
-    if (tid == 0) {
-        mbar_init(&bar, 1);
-        mbar_fence_init();
+    if (warp == 0) {  // lane l < nsl copies slab row l (and lane 16 + l its Sd row)
         const uint32_t row = (uint32_t)npr * 8u;
-        mbar_arrive_expect_tx(&bar, row * (uint32_t)nsl * (has_d ? 2u : 1u));
-        for (int sl = 0; sl < nsl; ++sl) {
+        if (lane == 0) {
+            mbar_init(&bar, 1);
+            mbar_fence_init();
+            mbar_arrive_expect_tx(&bar, row * (uint32_t)nsl * (has_d ? 2u : 1u));
+        }
+        __syncwarp();
+        const int sl = lane & 15;
+        if (sl < nsl && (lane < 16 || has_d)) {
             const int64_t off = (int64_t)(s0 + sl) * npairs + pr0;
-            bulk_g2s(lbuf + sl * kBulkPairs, p.Sin + off, row, &bar);
-            if (has_d) bulk_g2s(lbuf + (kBulkSlabs + sl) * kBulkPairs, p.Sd + off, row, &bar);
+            if (lane < 16)
+                bulk_g2s(lbuf + sl * kBulkPairs, p.Sin + off, row, &bar);
+            else
+                bulk_g2s(lbuf + (kBulkSlabs + sl) * kBulkPairs, p.Sd + off, row, &bar);
         }
     }
     const int r = tid % RP;
     const double bt = has_d ? *p.beta : 0.0;
     const double ah = (DO_S && pr < npairs && r < p.R) ? p.Ah[(int64_t)r * p.Ih + pr / RP] : 0.0;
     if (DO_M && tid < kBulkSlabs * RP) {
-        const int sl = tid / RP, rr = tid % RP;
+        const int sl = tid % kBulkSlabs, rr = tid / kBulkSlabs;  // consecutive slabs of a column
         a2s[sl][rr] = (sl < nsl && rr < p.R) ? p.tfac[0][(int64_t)rr * p.tdims[0] + s0 + sl] : 0.0;
     }
     __syncthreads();  // a2s staged; the barrier's init is visible
@@ -416,13 +434,34 @@ void launch_level_rp(const LevelParams& p, dim3 grid, int km, cudaStream_t st) {
 // Fixed-order reduction of `nparts` contiguous partial vectors: out[o] = sum_c part[c*nout+o],
 // for up to RedJobs::kMax jobs in one launch (job k owns blocks [blk0[k], blk0[k+1])).
 // Block = 32 outputs x 8 part-slices (coalesced across lanes), slices combined in order.
+// With a gradient epilogue (dense evaluation; the jobs then hold M_0 .. M_{N-1}) each reduced
+// M_n(i, r) also gives g_n(i, r) = (A_n Gamma_n)(i, r) - M_n(i, r), Gamma_n = Hadamard of the
+// other Grams (kruskal.cpp:127-149), and the last block to finish forms ||g||^2, g.d, <M0, A0>
+// and the per-fiber objective sum (as grad_kernel does).
+struct GradEpi {
+    int order, R, RP, need_grad;
+    int64_t dims[kMaxOrder];
+    int64_t off[kMaxOrder + 1];
+    const double* u;
+    double* g;
+    const double* d;
+    const double* gram;  // [mode][RP*RP]
+    const double* f_part;
+    int f_grid;
+    EvalScalars* sc;
+    double* red;  // [block][3]
+    unsigned int* counter;
+};
 struct RedLaunch {
     RedJob j[RedJobs::kMax];
     int blk0[RedJobs::kMax + 1];
     int n;
+    int grad;  // gradient epilogue on
+    GradEpi ge;
 };
 __global__ void __launch_bounds__(256) reduce_parts_kernel(const RedLaunch L) {
     __shared__ double sl[8][33];
+    extern __shared__ double gam[];  // grad: Gamma_n [RP][RP]
     int k = 0;
     while (k + 1 < L.n && (int)blockIdx.x >= L.blk0[k + 1]) ++k;
     const double* __restrict__ part = L.j[k].part;
@@ -430,6 +469,17 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const RedLaunch L) {
     const int64_t nout = L.j[k].nout;
     const int lane = threadIdx.x & 31, ws = threadIdx.x >> 5;
     const int64_t o = (int64_t)(blockIdx.x - L.blk0[k]) * 32 + lane;
+    const GradEpi& G = L.ge;
+    const int n = L.j[k].mode;
+    if (L.grad && n >= 0) {  // Gamma_n, alongside the partial loads
+        const int RR = G.RP * G.RP;
+        for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+            double v = 1.0;
+            for (int m = 0; m < G.order; ++m)
+                if (m != n) v *= G.gram[(size_t)m * RR + e];
+            gam[e] = v;
+        }
+    }
     double v = 0.0;
     if (o < nout)
         for (int c0 = ws; c0 < nparts; c0 += 8 * 8) {
@@ -444,16 +494,90 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const RedLaunch L) {
         }
     sl[ws][lane] = v;
     __syncthreads();
-    if (ws == 0 && o < nout) {
+    if (ws != 0) {
+        if (!L.grad) return;
+    } else {
         double s = 0.0;
-        for (int u = 0; u < 8; ++u) s += sl[u][lane];
-        L.j[k].out[o] = s;
+        if (o < nout) {
+            for (int u = 0; u < 8; ++u) s += sl[u][lane];
+            L.j[k].out[o] = s;
+        }
+        if (L.grad) {
+            double g2 = 0.0, gd = 0.0, inner = 0.0;
+            if (n >= 0 && o < nout) {
+                int64_t i;
+                int r;
+                if (L.j[k].layout == 0) {
+                    r = (int)(o / L.j[k].ld);
+                    i = o % L.j[k].ld;
+                } else {
+                    r = (int)(o % G.RP);
+                    i = o / G.RP;
+                }
+                const int64_t In = G.dims[n];
+                if (r < G.R && i < In) {
+                    const int64_t e = G.off[n] + (int64_t)r * In + i;
+                    if (n == 0) inner = s * G.u[e];
+                    if (G.need_grad) {
+                        const double* a = G.u + G.off[n];
+                        double av[kMaxRank];  // row i of A_n, loaded before the in-order dot product
+#pragma unroll
+                        for (int q = 0; q < kMaxRank; ++q) av[q] = q < G.R ? a[(int64_t)q * In + i] : 0.0;
+                        double ag = 0.0;
+#pragma unroll
+                        for (int q = 0; q < kMaxRank; ++q)
+                            if (q < G.R) ag += av[q] * gam[q * G.RP + r];
+                        const double gv = -s + ag;
+                        G.g[e] = gv;
+                        g2 = gv * gv;
+                        if (G.d) gd = gv * G.d[e];
+                    }
+                }
+            }
+            g2 = warp_sum(g2);
+            gd = warp_sum(gd);
+            inner = warp_sum(inner);
+            if (lane == 0) {
+                G.red[blockIdx.x * 3 + 0] = g2;
+                G.red[blockIdx.x * 3 + 1] = gd;
+                G.red[blockIdx.x * 3 + 2] = inner;
+            }
+        }
+    }
+    if (!L.grad) return;
+    if (!last_block_arrives(G.counter)) return;
+    if (ws != 0) return;
+    // last block, one warp: lane-strided partial sums (loads batched) then a fixed shuffle tree
+    double a = 0.0, b = 0.0, c = 0.0, fs = 0.0;
+    for (int q0 = lane; q0 < (int)gridDim.x; q0 += 32 * 4) {
+        double x[4][3];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int q = q0 + 32 * u;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) x[u][t] = q < (int)gridDim.x ? G.red[q * 3 + t] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a += x[u][0];
+            b += x[u][1];
+            c += x[u][2];
+        }
+    }
+    for (int q = lane; q < G.f_grid; q += 32) fs += G.f_part[q];
+    a = warp_sum(a);
+    b = warp_sum(b);
+    c = warp_sum(c);
+    fs = warp_sum(fs);
+    if (lane == 0) {
+        G.sc->f = 0.5 * fs;
+        G.sc->gnorm2 = a;
+        G.sc->inner = c;
+        if (G.d) G.sc->gdotd = b;
     }
 }
 
-void reduce_jobs(const RedJobs& jobs, cudaStream_t st) {
-    if (jobs.n == 0) return;
-    RedLaunch L{};
+void reduce_launch(RedLaunch& L, const RedJobs& jobs, size_t smem, cudaStream_t st) {
     L.n = jobs.n;
     int b = 0;
     for (int k = 0; k < jobs.n; ++k) {
@@ -462,8 +586,13 @@ void reduce_jobs(const RedJobs& jobs, cudaStream_t st) {
         b += (int)((jobs.j[k].nout + 31) / 32);
     }
     L.blk0[jobs.n] = b;
-    reduce_parts_kernel<<<(unsigned)b, 256, 0, st>>>(L);
+    reduce_parts_kernel<<<(unsigned)b, 256, smem, st>>>(L);
     CPFIT_CUDA(cudaGetLastError());
+}
+void reduce_jobs(const RedJobs& jobs, cudaStream_t st) {
+    if (jobs.n == 0) return;
+    RedLaunch L{};
+    reduce_launch(L, jobs, 0, st);
 }
 
 // defer_m / defer_s: append the partial reductions of M_h / Sout to a job list instead of
@@ -511,8 +640,11 @@ void run_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const 
     RedJobs own;
     RedJobs& jm = defer_m ? *defer_m : own;
     RedJobs& js = defer_s ? *defer_s : own;
-    if (do_m) jm.add(w.lvl_part[h], w.lvl_nx[h], p.Ih * w.RP, w.lvl_m[h]);
-    if (do_s && ny > 1) js.add(w.lvl_spart[h], ny, p.Jt * w.RP, Sout);
+    // job modes for the gradient epilogue: M_h is mode h; the last level's Sout is mode N-1
+    const int smode = (h == t.order - 2) ? t.order - 1 : -1;
+    if (do_m) jm.add(w.lvl_part[h], w.lvl_nx[h], p.Ih * w.RP, w.lvl_m[h], h);
+    if (do_s && ny > 1) js.add(w.lvl_spart[h], ny, p.Jt * w.RP, Sout, smode);
+    if (do_s && ny == 1 && defer_s) js.add(Sout, 1, p.Jt * w.RP, Sout, smode);  // in place: reads it once
     reduce_jobs(own, st);
 }
 
@@ -752,6 +884,12 @@ EvalWork* work_create(const DevTensor& t, int R) {
     CPFIT_CUDA(cudaMalloc(&w->gram, sizeof(double) * (size_t)t.order * w->RP * w->RP));
     w->red_grid = sms * 2;
     CPFIT_CUDA(cudaMalloc(&w->red, sizeof(double) * 3 * (size_t)w->red_grid));
+    if (!t.sparse) {  // reduce_grad: one block per 32 outputs of M_0 .. M_{N-1}
+        int64_t b = (w->RP * 32 * (int64_t)((t.dims[0] + 31) / 32) + 31) / 32;
+        for (int n = 1; n < t.order; ++n) b += (t.dims[n] * w->RP + 31) / 32;
+        w->rg_blocks = b;
+        CPFIT_CUDA(cudaMalloc(&w->rg_red, sizeof(double) * 3 * (size_t)b));
+    }
     // ALS solve Gram partials: <= 148 blocks per mode (als.cu solve_blocks)
     w->solve_part_stride = (int64_t)148 * (R * (R + 1) / 2);
     CPFIT_CUDA(cudaMalloc(&w->solve_part, sizeof(dd) * (size_t)t.order * w->solve_part_stride));
@@ -822,6 +960,7 @@ void work_destroy(EvalWork* w) {
     cudaFree(w->gram_part);
     cudaFree(w->gram);
     cudaFree(w->red);
+    cudaFree(w->rg_red);
     cudaFree(w->S);
     cudaFree(w->m0_part);
     cudaFree(w->m0);
@@ -896,6 +1035,36 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
 }
 }  // namespace
 
+namespace {
+// the deferred reductions of a dense evaluation (M_0 .. M_{N-1}) with the gradient epilogue
+void reduce_grad(const DevTensor& t, EvalWork& w, const RedJobs& jobs, const double* u, double* g,
+                 const double* d, bool need_grad, EvalScalars* sc, cudaStream_t st) {
+    if (jobs.blocks() > w.rg_blocks) throw std::logic_error("reduce_grad: block partial buffer too small");
+    RedLaunch L{};
+    L.grad = 1;
+    GradEpi& G = L.ge;
+    G.order = t.order;
+    G.R = w.R;
+    G.RP = w.RP;
+    G.need_grad = need_grad ? 1 : 0;
+    for (int n = 0; n < t.order; ++n) {
+        G.dims[n] = t.dims[n];
+        G.off[n] = w.off[n];
+    }
+    G.off[t.order] = w.off[t.order];
+    G.u = u;
+    G.g = g;
+    G.d = d;
+    G.gram = w.gram;
+    G.f_part = w.f_part;
+    G.f_grid = w.fiber_grid;
+    G.sc = sc;
+    G.red = w.rg_red;
+    G.counter = w.counter + kCounterGrad;
+    reduce_launch(L, jobs, sizeof(double) * w.RP * w.RP, st);
+}
+}  // namespace
+
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
                  int* status, cudaStream_t st, bool need_grad, const int* resid_flag, bool s_given, bool grams_given) {
     (void)status;
@@ -915,6 +1084,10 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
         for (int h = 1; h < t.order - 1; ++h) {
             run_level(t, w, h, Sin, u, true, true, w.lvl_S[h], st, &jobs, h == t.order - 2 ? &jobs : nullptr);
             Sin = w.lvl_S[h];
+        }
+        if (t.order >= 3) {
+            reduce_grad(t, w, jobs, u, g, d, need_grad, sc, st);
+            return;
         }
         reduce_jobs(jobs, st);
     } else {
@@ -988,8 +1161,7 @@ void eval_given_s_device(const DevTensor& t, EvalWork& w, const double* u, doubl
                   h == 1 ? Sd : nullptr, beta);
         Sin = w.lvl_S[h];
     }
-    reduce_jobs(jobs, st);
-    run_grad(t, w, u, g, nullptr, true, sc, st);
+    reduce_grad(t, w, jobs, u, g, nullptr, true, sc, st);
 }
 
 // exported for als.cu

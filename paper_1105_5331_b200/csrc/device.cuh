@@ -82,6 +82,8 @@ struct EvalWork {
     double* frows = nullptr;    // row-major RP-padded factor copies (sum I_n x RP)
     // reductions
     double* red = nullptr;      // per-CTA partials for norms/dots
+    double* rg_red = nullptr;   // reduce_grad block partials [rg_blocks][3] (dense)
+    int64_t rg_blocks = 0;
     int red_grid = 0;
     // ALS: Cholesky factors of Gamma_n per mode (als.cu chol_kernel) and the side stream the
     // factorisations run on, overlapping the streaming passes

@@ -27,6 +27,7 @@
 
 constexpr int kFStages = 3;
 constexpr int kFiberF = 16;
+constexpr int kWStages = 4;  // W (Khatri-Rao row) ring: the gathers of a tile take about a tile's time
 constexpr int kMaxKSteps = 104;  // ldT / 4 for I_0 <= 416 (work_create checks)
 #ifndef CPFIT_SREG_CHAINS
 #define CPFIT_SREG_CHAINS 1
@@ -73,11 +74,11 @@ __host__ __device__ FiberSmem fiber_layout(int nchunk, int64_t I0) {
     s.a0 = off;
     if (FiberRoles<RP>::A0SMEM) off += sizeof(double) * (size_t)a0_rows(I0) * RP;
     s.wbuf = off;
-    off += sizeof(double) * 2 * (size_t)F * w_ld<RP>();
+    off += sizeof(double) * kWStages * (size_t)F * w_ld<RP>();
     s.gam = off;
     off += sizeof(double) * (size_t)RP * RP;
     s.bars = off;
-    off += sizeof(uint64_t) * 16;
+    off += sizeof(uint64_t) * (2 * kFStages + 2 * kWStages);
     s.total = off;
     return s;
 }
@@ -224,13 +225,13 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     const int KS = (int)(p.ldT / 4);  // k-steps of 4 rows (ldT = I0 rounded up to 4; pad rows are 0)
     double* tiles = reinterpret_cast<double*>(smem_raw + L.tiles);
     double* a0s = reinterpret_cast<double*>(smem_raw + L.a0);    // [a0_rows][RP] swizzled
-    double* wbuf = reinterpret_cast<double*>(smem_raw + L.wbuf);  // [2][F][WLD]
+    double* wbuf = reinterpret_cast<double*>(smem_raw + L.wbuf);  // [kWStages][F][WLD]
     double* gam = reinterpret_cast<double*>(smem_raw + L.gam);    // [RP][RP]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
     uint64_t* tfull = bars;       // [kFStages] tx bytes
     uint64_t* tempty = bars + 3;  // [kFStages] T consumers
-    uint64_t* wfull = bars + 6;   // [2] W producer
-    uint64_t* wempty = bars + 8;  // [2] W consumers
+    uint64_t* wfull = bars + 2 * kFStages;               // [kWStages] W producer
+    uint64_t* wempty = bars + 2 * kFStages + kWStages;   // [kWStages] W consumers
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef CPFIT_FIBER_PROF
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], t_cons);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kWStages; ++b) {
             mbar_init(&wfull[b], NW);
             mbar_init(&wempty[b], w_cons);
         }
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     // (independent), then the buffer
     auto w_producer = [&](int64_t k, FiberIndex<ORD>& xw, int fw, int hw) {
         constexpr int RS = RP * F / (32 * NW);
-        const int b = (int)(k & 1);
+        const int b = (int)(k % kWStages);
         const int64_t f0 = (t_begin + k) * F;
         if (k > 0) xw = advance_fiber<ORD>(p, xw, F, f0 + fw);
         double w[RS];
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                 if (ok && mode_active<ORD>(p, m)) v *= __ldg(p.fac[m] + (int64_t)r * p.dims[m] + xw.j[m]);
             w[j] = v;
         }
-        if (k >= 2) FIBER_WAIT(1, &wempty[b], (uint32_t)(((k / 2) - 1) & 1));
+        if (k >= kWStages) FIBER_WAIT(1, &wempty[b], (uint32_t)(((k / kWStages) - 1) & 1));
         double* wv = wbuf + (size_t)b * F * WLD;
 #pragma unroll
         for (int j = 0; j < RS; ++j) wv[fw * WLD + hw * RS + j] = w[j];
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
             // S is given (the ALS sweep's S' rescaled to u_bar): only the per-fiber objective
             const int sw = warp - Ro::S0;
             for (int64_t k = 0; k < ntl; ++k) {
-                const int b = (int)(k & 1);
+                const int b = (int)(k % kWStages);
                 const int64_t f0 = (t_begin + k) * F;
                 double sv[Ro::SPW][2], fn[Ro::SPW];
 #pragma unroll
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                     sv[j][0] = v.x;
                     sv[j][1] = v.y;
                 }
-                FIBER_WAIT(6, &wfull[b], (uint32_t)((k / 2) & 1));
+                FIBER_WAIT(6, &wfull[b], (uint32_t)((k / kWStages) & 1));
                 const double* wv = wbuf + (size_t)b * F * WLD;
 #pragma unroll
                 for (int j = 0; j < Ro::SPW; ++j) {
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
             const int sw = warp - Ro::S0;
             for (int64_t k = 0; k < ntl; ++k) {
                 const int s = (int)(k % kFStages);
-                const int b = (int)(k & 1);
+                const int b = (int)(k % kWStages);
                 const int64_t f0 = (t_begin + k) * F;
                 double fn[Ro::SPW];  // ||t_f||^2 of this lane's fiber, prefetched (r-tile 0 only)
 #pragma unroll
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                 // r = 8 nt + 2 (lane%4) + {0, 1}
                 // epilogue of the sub-tile(s): lane holds D fragment items f = 8 ft + lane/4,
                 // r = 8 nt + 2 (lane%4) + {0, 1}
-                if (epi_w) FIBER_WAIT(6, &wfull[b], (uint32_t)((k / 2) & 1));
+                if (epi_w) FIBER_WAIT(6, &wfull[b], (uint32_t)((k / kWStages) & 1));
                 const double* wv = wbuf + (size_t)b * F * WLD;
 #pragma unroll
                 for (int j = 0; j < Ro::SPW; ++j) {
@@ -480,9 +481,9 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
         if (m0w_on) {
             for (int64_t k = 0; k < ntl; ++k) {
                 const int s = (int)(k % kFStages);
-                const int b = (int)(k & 1);
+                const int b = (int)(k % kWStages);
                 FIBER_WAIT(3, &tfull[s], (uint32_t)((k / kFStages) & 1));
-                FIBER_WAIT(4, &wfull[b], (uint32_t)((k / 2) & 1));
+                FIBER_WAIT(4, &wfull[b], (uint32_t)((k / kWStages) & 1));
                 const double* tt = tiles + (size_t)s * F * I0s;
                 const double* wv = wbuf + (size_t)b * F * WLD;
                 if (p.do_m0) {
