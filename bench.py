@@ -245,35 +245,36 @@ def main():
     extras = {}
     roof = None
     if not args.no_extras:
-        # dominant kernel: the fused fiber pass, timed alone (same stream, CUDA events)
+        # dominant kernel of the step: the S pass S = T x1 A0 (sreg_kernel; 1.5 launches per
+        # iteration: the ALS sweep's S' and the line search's S_d), timed alone on its stream with
+        # CUDA events; HBM-bound (it streams T once). The M0 pass (fiber_ws_kernel) runs as often.
         k_elems = int(np.prod(dims))
-        fused_ms = P.bench_kernel(t, u0, kind=3, reps=20, flush_l2=False)
-        resid_ms = P.bench_kernel(t, u0, kind=6, reps=10, flush_l2=False)
-        flops = 4.0 * k_elems * R  # S = T x1 A0 (2KR) + M0 = T W (2KR) on DMMA
-        bytes_alg = 8.0 * k_elems + 8.0 * R * 2 * sum(dims)
+        s_ms = P.bench_kernel(t, u0, kind=5, reps=20, flush_l2=False)
+        fused_ms = P.bench_kernel(t, u0, kind=3, reps=10, flush_l2=False)
+        s_bytes = 8.0 * k_elems + 8.0 * R * dims[0] + 8.0 * R * (k_elems // dims[0])  # T + A0 in, S out
+        s_flops = 2.0 * k_elems * R
         dmma_peak, dfma_peak = P.measure_fp64_peak()
         try:
             hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-            hbm_src = "measured"
+            hbm_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
         except (OSError, KeyError, ValueError):
-            hbm_peak, hbm_src = 6650.0, "fallback"
+            hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
         try:  # DRAM bytes per launch of this kernel from the committed ncu capture (profiles/)
-            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["fused_fiber_pass_c2"]
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["s_pass_c2"]
             traffic = tr["bytes_per_launch"] if tuple(dims) == (400, 400, 400) and R == 16 else None
         except (OSError, KeyError, ValueError):
             traffic = None
-        tf = flops / (fused_ms * 1e-3) / 1e12
-        gbs = bytes_alg / (fused_ms * 1e-3) / 1e9
-        roof = {"bound": "tensor", "kernel": "fiber_ws_kernel<16,16> (fused S + M0 + per-fiber f, DMMA fp64)",
-                "achieved": round(tf, 3), "peak": round(dmma_peak, 3), "unit": "TFLOP/s",
-                "frac": round(tf / dmma_peak, 4), "traffic": traffic,
+        gbs = s_bytes / (s_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "sreg_kernel<16,16> (S = T x1 A0, DMMA fp64 with A0 fragments in registers)",
+                "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
+                "traffic": traffic,
                 "traffic_source": "profiles/traffic.json (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
-                "peak_source": "DMMA m8n8k4 f64 issue loop measured in-process (MEASURED_PEAKS.json has no fp64)",
-                "ms_per_launch": round(fused_ms, 5), "alg_flops_per_launch": flops, "alg_bytes_per_launch": bytes_alg,
-                "hbm": {"achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
-                        "peak_source": hbm_src},
-                "residual_form": {"ms_per_launch": round(resid_ms, 5),
-                                  "TFLOP/s": round(6.0 * k_elems * R / (resid_ms * 1e-3) / 1e12, 3)},
+                "peak_source": hbm_src, "ms_per_launch": round(s_ms, 5), "alg_bytes_per_launch": s_bytes,
+                "dmma": {"achieved_tflops": round(s_flops / (s_ms * 1e-3) / 1e12, 3), "peak_tflops": round(dmma_peak, 3),
+                         "peak_source": "DMMA m8n8k4 f64 issue loop measured in-process"},
+                "fused_pass": {"kernel": "fiber_ws_kernel<16,16> S + M0 + per-fiber f (init / residual phase)",
+                               "ms_per_launch": round(fused_ms, 5),
+                               "TFLOP/s": round(4.0 * k_elems * R / (fused_ms * 1e-3) / 1e12, 3)},
                 "dfma_peak_tflops": round(dfma_peak, 3)}
         kern = {}
         for mode in range(len(dims)):
@@ -286,7 +287,7 @@ def main():
             b = 8.0 * k_elems + 8.0 * R * 2 * sum(dims)
             kern[name] = {"ms": round(gms, 5), "GB/s": round(b / (gms * 1e-3) / 1e9, 1),
                           "hbm_frac": round(b / (gms * 1e-3) / 1e9 / hbm_peak, 4)}
-        for kind, name in ((4, "fiber_m0_only"), (5, "fiber_s_only")):
+        for kind, name in ((4, "fiber_m0_pass_plus_reduce"), (5, "fiber_s_only")):
             fm = P.bench_kernel(t, u0, kind=kind, reps=10, flush_l2=False)
             kern[name] = {"ms": round(fm, 5), "GB/s": round(8.0 * k_elems / (fm * 1e-3) / 1e9, 1),
                           "hbm_frac": round(8.0 * k_elems / (fm * 1e-3) / 1e9 / hbm_peak, 4)}
