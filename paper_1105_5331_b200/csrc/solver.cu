@@ -191,7 +191,7 @@ __global__ void k_ls_update(Ctl c, cudaGraphConditionalHandle ls_h) {
 
 // Moré–Thuente (as started by k_branch) to termination on phi(a) = f(u_bar + a d) and phi'(a)
 // from the polynomial; the same bookkeeping as k_ls_update at termination; acc_h: accepted
-__global__ void k_poly_ls(Ctl c, cudaGraphConditionalHandle acc_h) {
+__global__ void k_poly_ls(Ctl c) {
     DevState& s = *c.s;
     // phi and phi' by fp64 Horner on the rounded double-double coefficients (evaluation error
     // ~ eps sum_k |c_k a^k|; the search compares values and slopes, not their tiny differences
@@ -217,7 +217,6 @@ __global__ void k_poly_ls(Ctl c, cudaGraphConditionalHandle acc_h) {
         s.accepted = 1;
         s.beta = s.mt.out_step;
     }
-    set_cond(c, acc_h, s.accepted != 0);
 }
 
 __global__ void k_accept_cond(Ctl c, cudaGraphConditionalHandle h) { set_cond(c, h, c.s->accepted != 0); }
@@ -261,14 +260,20 @@ __global__ void k_select_accepted(const DevState* s, const double* ubl, const do
 
 // f at the canonical point equals f at the accepted trial (normalisation preserves full(K));
 // the gradient was mapped by the exact column rescale; counters as if re-evaluated
+// (one warp; the polynomial branch runs the accepted-step body unconditionally — its results
+// are dropped by the commit when the search did not accept, and nothing is counted then)
 __global__ void k_after_rescale(Ctl c, EvalScalars* scn, const double* red, int nblk) {
-    DevState& s = *c.s;
     double g2 = 0.0;
-    for (int b = 0; b < nblk; ++b) g2 += red[b];
+    for (int b = threadIdx.x; b < nblk; b += 32) g2 += red[b];
+    g2 = warp_sum(g2);
+    if (threadIdx.x != 0) return;
+    DevState& s = *c.s;
     scn->f = s.mt.out_f;
     scn->gnorm2 = g2;
-    s.fevals += 1;
-    s.gevals += 1;
+    if (s.accepted) {
+        s.fevals += 1;
+        s.gevals += 1;
+    }
 }
 
 // Scalar part of the commit (ngmres.cpp:150-157, 182-197).
@@ -595,18 +600,15 @@ void Solver::build_graphs() {
             // 0: exact line search on phi(a) (poly.cu): one S_d pass + reductions, Moré–Thuente on
             // the polynomial; accepted: u* = u_bar + beta d, S(u*) by the axpy, M0 pass + levels +
             // gradient at u*, then the canonical rescale as for an evaluated trial
+            // (no IF node around the accepted step: a conditional node costs ~6 us whether taken or
+            // not, the search almost always accepts, and the commit keeps u_bar otherwise)
             pb = br[0];
             CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, pb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-            const cudaGraphConditionalHandle accp_h = make_handle(st3_);
             poly_build_device(*t_, *w_, *pw_, ub_, d_, st3_);
-            k_poly_ls<<<1, 1, 0, st3_>>>(c, accp_h);
+            k_poly_ls<<<1, 1, 0, st3_>>>(c);
             stamp(st3_, 3);
-            apb = append_conditional(st3_, accp_h, cudaGraphCondTypeIf);
-            CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st4_, apb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-            emit_poly_accept(st4_, &c);
-            stamp(st4_, 5);
-            CPFIT_CUDA(cudaGetLastError());
-            CPFIT_CUDA(cudaStreamEndCapture(st4_, &apb));
+            emit_poly_accept(st3_, &c);
+            stamp(st3_, 5);
             CPFIT_CUDA(cudaGetLastError());
             CPFIT_CUDA(cudaStreamEndCapture(st3_, &pb));
         }
@@ -645,7 +647,7 @@ void Solver::build_graphs() {
             k_select_accepted<<<vb, 256, 0, st4_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
             grams_device(*w_, ut_, st4_);
             const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st4_, m0_sel_, m0_cur_, gout_);
-            k_after_rescale<<<1, 1, 0, st4_>>>(c, sc_next, red_, nb);
+            k_after_rescale<<<1, 32, 0, st4_>>>(c, sc_next, red_, nb);
         }
         stamp(st4_, 5);
         CPFIT_CUDA(cudaGetLastError());
@@ -688,7 +690,7 @@ void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
     poly_point_device(*w_, *pw_, ub_, d_, &s->beta, ut_, st);
     eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true);
     const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, w_->m0, m0_cur_, gout_);
-    k_after_rescale<<<1, 1, 0, st>>>(c, sc_next, red_, nb);
+    k_after_rescale<<<1, 32, 0, st>>>(c, sc_next, red_, nb);
     CPFIT_CUDA(cudaGetLastError());
 }
 
@@ -759,7 +761,7 @@ void Solver::run_loop_eager() {
             k_branch<<<1, 1, 0, st_>>>(c, none);
             if (state().poly) {
                 poly_build_device(*t_, *w_, *pw_, ub_, d_, st_);
-                k_poly_ls<<<1, 1, 0, st_>>>(c, none);
+                k_poly_ls<<<1, 1, 0, st_>>>(c);
             }
             while (state().searching) {
                 k_trial<<<vb, 256, 0, st_>>>(s, ub_, d_, ut_, n_);
@@ -769,7 +771,7 @@ void Solver::run_loop_eager() {
                     k_keep_best<<<vb, 256, 0, st_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
             }
             const DevState ha = state();
-            if (ha.accepted && ha.poly) {
+            if (ha.poly) {
                 emit_poly_accept(st_, &c);
             } else if (ha.accepted) {
                 if (opt_.reeval_accepted) {
@@ -784,7 +786,7 @@ void Solver::run_loop_eager() {
                     k_select_accepted<<<vb, 256, 0, st_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
                     grams_device(*w_, ut_, st_);
                     const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st_, m0_sel_, m0_cur_, gout_);
-                    k_after_rescale<<<1, 1, 0, st_>>>(c, sc_next, red_, nb);
+                    k_after_rescale<<<1, 32, 0, st_>>>(c, sc_next, red_, nb);
                 }
             }
         } else {
