@@ -529,7 +529,7 @@ void accel_destroy(AccelWork* a) {
 }
 
 void accelerate_device(AccelWork& a, const double* wu, const double* wg, const int* ring, const double* ub,
-                       const double* gb, double eps, double* uhat, double* d, cudaStream_t st) {
+                       const double* gb, double eps, double* uhat, double* d, cudaStream_t st, bool slope_by_caller) {
     const int C = a.cap + 1;  // smem sized for the full window
     TsqrParams p{};
     p.n = a.n;
@@ -580,9 +580,9 @@ void accelerate_device(AccelWork& a, const double* wu, const double* wg, const i
     u.uhat = uhat;
     u.d = d;
     u.red = a.red;
-    const int nb = (int)std::min<int64_t>(1024, (a.n + 255) / 256);
+    const int nb = accel_update_blocks(a);
     accel_update_kernel<<<nb, 256, 0, st>>>(u);
-    accel_slope_kernel<<<1, 32, 0, st>>>(a.red, nb, a.scal);
+    if (!slope_by_caller) accel_slope_kernel<<<1, 32, 0, st>>>(a.red, nb, a.scal);
     CPFIT_CUDA(cudaGetLastError());
 }
 

@@ -21,7 +21,7 @@ namespace cpfit_gpu {
 
 void dense_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, cudaStream_t st);
 void dense_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
-                 double* Sout, cudaStream_t st);
+                 double* Sout, cudaStream_t st, bool defer);
 void gather_m(int64_t In, EvalWork& w, const double* part, int grid, int ld, int layout, double* out,
               cudaStream_t st);
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
@@ -167,6 +167,8 @@ struct SolveGramParams {
     const double* M;     // layout 0: M[r * ld + i]; layout 1: M[i * RP + r]
     int layout;
     int64_t ld;
+    int nparts;          // M = sum of nparts partial vectors M + c * pstride (fixed order)
+    int64_t pstride;
     double* out;         // col-major In x R (block of the packed iterate)
     int* status;
     dd* part;            // this mode's Gram partials [gridDim.x][npair]
@@ -207,7 +209,17 @@ __global__ void __launch_bounds__(kSolveThreads) solve_gram_kernel(const SolveGr
     for (int64_t i0 = (int64_t)blockIdx.x * RPB; i0 < p.In; i0 += (int64_t)gridDim.x * RPB) {
         const int64_t i = i0 + rl;
         const bool live = i < p.In && r < R;
-        double s = live ? (p.layout == 0 ? p.M[(int64_t)r * p.ld + i] : p.M[i * RP + r]) : 0.0;
+        double s = 0.0;
+        if (live) {
+            const double* m = p.M + (p.layout == 0 ? (int64_t)r * p.ld + i : i * RP + r);
+            for (int c0 = 0; c0 < p.nparts; c0 += 32) {  // one round of loads for <= 32 partials
+                double x[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) x[u] = c0 + u < p.nparts ? m[(int64_t)(c0 + u) * p.pstride] : 0.0;
+#pragma unroll
+                for (int u = 0; u < 32; ++u) s += x[u];
+            }
+        }
         double y = 0.0;
 #pragma unroll
         for (int j = 0; j < RP; ++j) {
@@ -493,8 +505,10 @@ void chol_mode(EvalWork& w, int n, int pending, int* status, cudaStream_t st) {
 
 // A_n <- M_n Gamma_n^-1 (factor from chol_mode); G_n left as block partials (pending)
 void solve_gram(EvalWork& w, int n, const double* M, int layout, int64_t ld, double* ublock, int* status,
-                cudaStream_t st) {
+                cudaStream_t st, int nparts = 1, int64_t pstride = 0) {
     SolveGramParams p{};
+    p.nparts = nparts;
+    p.pstride = pstride;
     p.R = w.R;
     p.mode = n;
     p.In = w.dims[n];
@@ -572,13 +586,21 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
         dense_fiber(t, w, work, true, false, st);
         const double* Sin = w.S;
         for (int n = 1; n < N; ++n) {
+            // the solves sum the level partials themselves (no reduction launches)
             if (n < N - 1) {
-                dense_level(t, w, n, Sin, work, true, false, nullptr, st);
+                dense_level(t, w, n, Sin, work, true, false, nullptr, st, true);
                 join_chol(w, st);
-                solve_gram(w, n, w.lvl_m[n], 1, 0, work + w.off[n], status, st);
+                solve_gram(w, n, w.lvl_part[n], 1, 0, work + w.off[n], status, st, w.lvl_nx[n], t.dims[n] * w.RP);
                 fork_chol(w, n + 1, status, st);
-                dense_level(t, w, n, Sin, work, false, true, w.lvl_S[n], st);
+                const bool last_level = (n == N - 2);
+                dense_level(t, w, n, Sin, work, false, true, w.lvl_S[n], st, last_level);
                 Sin = w.lvl_S[n];
+                if (last_level && w.lvl_ny[n] > 1) {
+                    join_chol(w, st);
+                    solve_gram(w, N - 1, w.lvl_spart[n], 1, 0, work + w.off[N - 1], status, st, w.lvl_ny[n],
+                               t.dims[N - 1] * w.RP);
+                    break;
+                }
             } else {
                 join_chol(w, st);
                 solve_gram(w, n, Sin, 1, 0, work + w.off[n], status, st);

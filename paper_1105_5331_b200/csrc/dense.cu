@@ -1173,9 +1173,11 @@ void dense_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bo
 void dense_fiber_fused(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st, const int* resid_flag) {
     run_fiber(t, w, u, true, true, true, w.gram, st, resid_flag);
 }
+// defer: leave the partial sums to the caller (the ALS solves read them directly)
 void dense_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
-                 double* Sout, cudaStream_t st) {
-    run_level(t, w, h, Sin, u, do_m, do_s, Sout, st);
+                 double* Sout, cudaStream_t st, bool defer) {
+    RedJobs discard;
+    run_level(t, w, h, Sin, u, do_m, do_s, Sout, st, defer ? &discard : nullptr, defer ? &discard : nullptr);
 }
 void gather_m(int64_t In, EvalWork& w, const double* part, int grid, int ld, int layout, double* out,
               cudaStream_t st) {

@@ -189,7 +189,10 @@ AccelWork* accel_create(int64_t n, int cap);
 void accel_destroy(AccelWork* a);
 // Window as ring slots: wu/wg base pointers with slot stride n; order[j] = slot of j-th
 // oldest entry; m entries (device int). Produces uhat and d = uhat - ubar, slope = gbar.d.
+// slope_by_caller: leave slope = sum of a.red[0 .. accel_update_blocks(a)) to the caller
 void accelerate_device(AccelWork& a, const double* wu, const double* wg, const int* ring, const double* ub,
-                       const double* gb, double eps, double* uhat, double* d, cudaStream_t st);
+                       const double* gb, double eps, double* uhat, double* d, cudaStream_t st,
+                       bool slope_by_caller = false);
+inline int accel_update_blocks(const AccelWork& a) { return (int)std::min<int64_t>(1024, (a.n + 255) / 256); }
 
 }  // namespace cpfit_gpu

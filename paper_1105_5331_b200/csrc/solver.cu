@@ -58,6 +58,8 @@ struct Ctl {
     const EvalScalars* sc_trial;
     const EvalScalars* sc_next;
     const double* accel_scal;
+    const double* accel_red;  // accel_update_kernel's per-block g_bar.d partials
+    int accel_nb;
     TraceRow* trace;
     int trace_cap;
     double gradient_scale, hscale, tol_grad;
@@ -133,12 +135,17 @@ __global__ void k_set_cond_running(Ctl c, cudaGraphConditionalHandle h) {
 // polynomial phi (poly.cu) when it applies and the per-fiber objective is in use (the residual
 // phase keeps trial evaluations). Selects the branch: 0 polynomial search, 1 trial-evaluation
 // search, 2 none (restart / no descent / failure).
+// (one warp: the slope g_bar.d is summed here from the recombination's block partials)
 __global__ void k_branch(Ctl c, cudaGraphConditionalHandle br_h) {
+    double sl = 0.0;
+    for (int b = threadIdx.x; b < c.accel_nb; b += 32) sl += c.accel_red[b];
+    sl = warp_sum(sl);
+    if (threadIdx.x != 0) return;
     DevState& s = *c.s;
     s.f_bar = c.sc_bar->f;
     s.fevals += 1;
     s.gevals += 1;
-    s.slope = c.accel_scal[1];
+    s.slope = sl;
     s.restart = 0;
     s.stalled = 0;
     s.accepted = 0;
@@ -530,6 +537,8 @@ void Solver::build_graphs() {
     c.sc_trial = sc_trial;
     c.sc_next = sc_next;
     c.accel_scal = a_ ? a_->scal : nullptr;
+    c.accel_red = a_ ? a_->red : nullptr;
+    c.accel_nb = a_ ? accel_update_blocks(*a_) : 0;
     c.trace = trace_;
     c.trace_cap = trace_cap_;
     c.gradient_scale = opt_.gradient_scale;
@@ -588,11 +597,11 @@ void Solver::build_graphs() {
         if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st2_));
         stamp(st2_, 1);
         // Step II: windowed recombination -> d, slope                        (ngmres.cpp:97-101)
-        accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st2_);
+        accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st2_, true);
         // Step III: restart test / line search (ngmres.cpp:111-147) as one SWITCH node — every
         // conditional node costs several microseconds of device time, taken or not
         const cudaGraphConditionalHandle br_h = make_handle(st2_);
-        k_branch<<<1, 1, 0, st2_>>>(c, br_h);
+        k_branch<<<1, 32, 0, st2_>>>(c, br_h);
         stamp(st2_, 2);
         cudaGraph_t br[2];
         append_conditional(st2_, br_h, cudaGraphCondTypeSwitch, 2, br);
@@ -757,8 +766,8 @@ void Solver::run_loop_eager() {
             if (m0_bar_)
                 CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
             if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st_));
-            accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st_);
-            k_branch<<<1, 1, 0, st_>>>(c, none);
+            accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st_, true);
+            k_branch<<<1, 32, 0, st_>>>(c, none);
             if (state().poly) {
                 poly_build_device(*t_, *w_, *pw_, ub_, d_, st_);
                 k_poly_ls<<<1, 1, 0, st_>>>(c);
