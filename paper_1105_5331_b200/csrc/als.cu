@@ -169,6 +169,10 @@ struct SolveGramParams {
     int64_t ld;
     int nparts;          // M = sum of nparts partial vectors M + c * pstride (fixed order)
     int64_t pstride;
+    // optional: the last block to finish sums the Gram partials into gram (this mode's slot)
+    unsigned int* fin_counter;
+    double* gram;
+    int RP;
     double* out;         // col-major In x R (block of the packed iterate)
     int* status;
     dd* part;            // this mode's Gram partials [gridDim.x][npair]
@@ -254,6 +258,13 @@ __global__ void __launch_bounds__(kSolveThreads) solve_gram_kernel(const SolveGr
 #pragma unroll
     for (int k = 0; k < NPT; ++k)
         if (pa[k] >= 0) p.part[(size_t)blockIdx.x * npair + tid + k * kSolveThreads] = acc[k];
+    if (p.fin_counter && last_block_arrives(p.fin_counter)) {
+        GramPending g{};
+        g.mode = p.mode;
+        g.part = p.part;
+        g.nblk = (int)gridDim.x;
+        finalize_pending(g, R, p.RP, p.gram);
+    }
 }
 
 struct NormParams {
@@ -281,8 +292,9 @@ struct NormParams {
     int* perm_out;
     double* scale0_out;
     // optional: the last block rewrites gram_w as the Grams of the output,
-    // G'_n(q, r) = s_n(q) s_n(r) G_n(perm q, perm r)
+    // G'_n(q, r) = s_n(q) s_n(r) G_n(perm q, perm r) (and into gram_copy when given)
     unsigned int* counter;
+    double* gram_copy;
 };
 
 // normalize_and_reorder: norms from the (double-double) Gram diagonals, lambda_r =
@@ -390,6 +402,7 @@ __global__ void normalize_kernel(const NormParams p) {
                 double v = 0.0;
                 if (q < p.R && r < p.R) v = scale[n][q] * scale[n][r] * gin[n * RR + perm[q] * p.RP + perm[r]];
                 p.gram_w[e] = v;
+                if (p.gram_copy) p.gram_copy[e] = v;
             }
         }
     }
@@ -455,11 +468,17 @@ void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st
 }
 
 int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
-                          cudaStream_t st, const double* m0, double* m0out, bool out_grams) {
+                          cudaStream_t st, const double* m0, double* m0out, bool out_grams, bool save_perm,
+                          double* gram_copy) {
     NormParams p{};
     p.pend.mode = -1;
     p.gram_w = w.gram;
     if (out_grams) p.counter = w.counter + kCounterNorm;
+    p.gram_copy = gram_copy;
+    if (save_perm) {
+        p.perm_out = w.nperm;
+        p.scale0_out = w.nscale0;
+    }
     p.order = w.order;
     p.R = w.R;
     p.RP = w.RP;
@@ -505,10 +524,15 @@ void chol_mode(EvalWork& w, int n, int pending, int* status, cudaStream_t st) {
 
 // A_n <- M_n Gamma_n^-1 (factor from chol_mode); G_n left as block partials (pending)
 void solve_gram(EvalWork& w, int n, const double* M, int layout, int64_t ld, double* ublock, int* status,
-                cudaStream_t st, int nparts = 1, int64_t pstride = 0) {
+                cudaStream_t st, int nparts = 1, int64_t pstride = 0, bool finalize = false) {
     SolveGramParams p{};
     p.nparts = nparts;
     p.pstride = pstride;
+    p.RP = w.RP;
+    if (finalize) {
+        p.fin_counter = w.counter + kCounterSolve;
+        p.gram = w.gram;
+    }
     p.R = w.R;
     p.mode = n;
     p.In = w.dims[n];
@@ -526,6 +550,10 @@ void solve_gram(EvalWork& w, int n, const double* M, int layout, int64_t ld, dou
         default: solve_gram_kernel<32><<<grid, kSolveThreads, 0, st>>>(p); break;
     }
     CPFIT_CUDA(cudaGetLastError());
+}
+
+__global__ void finalize_gram_kernel(const GramPending g, int R, int RP, double* gram) {
+    finalize_pending(g, R, RP, gram);
 }
 
 // chol_mode(n) on the side stream once everything queued on st so far is done; the next
@@ -561,7 +589,9 @@ __global__ void s_rescale_kernel(double* S, int64_t J, int R, const int* perm, c
 
 // work: n_u scratch (pre-normalisation iterate), mbuf: max(I_n)*R scratch
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
-                         int* status, cudaStream_t st, const double* m0_given, bool keep_s, bool grams_given) {
+                         int* status, cudaStream_t st, const double* m0_given, bool keep_s, bool grams_given,
+                         bool defer_norm) {
+    if (defer_norm && t.sparse) throw std::logic_error("als sweep: deferred normalisation needs a dense tensor");
     CPFIT_CUDA(cudaMemcpyAsync(work, u, sizeof(double) * w.nu, cudaMemcpyDeviceToDevice, st));
     if (!grams_given) grams_device(w, work, st);
     const int N = t.order;
@@ -607,6 +637,10 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
             }
         }
     }
+    // deferred: the caller evaluates the sweep's own point (work, S' in w.S; the last mode's
+    // Gram still in solve partials: finalize_gram_side) and normalises afterwards
+    // (normalize_grad), so S never needs the rescale below
+    if (defer_norm) return;
     normalize_device(w, work, out, st, N - 1, keep_s && !t.sparse, grams_given);
     if (keep_s && !t.sparse) {
         const int blocks = (int)std::min<int64_t>(8 * 148, (t.J * w.RP + 255) / 256);
@@ -617,6 +651,16 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
         }
         CPFIT_CUDA(cudaGetLastError());
     }
+}
+
+// G_mode <- the sum of its pending solve partials, as one block on the side stream (forked
+// after everything queued on st); `done` is recorded on the side stream when it has finished
+void finalize_gram_side(EvalWork& w, int mode, cudaStream_t st, cudaEvent_t done) {
+    CPFIT_CUDA(cudaEventRecord(w.ev_fork, st));
+    CPFIT_CUDA(cudaStreamWaitEvent(w.side, w.ev_fork, 0));
+    finalize_gram_kernel<<<1, 256, 0, w.side>>>(pending_of(w, mode), w.R, w.RP, w.gram);
+    CPFIT_CUDA(cudaGetLastError());
+    CPFIT_CUDA(cudaEventRecord(done, w.side));
 }
 
 }  // namespace cpfit_gpu

@@ -190,9 +190,12 @@ struct LevelParams {
     double* m_part;  // [gridDim.x][Ih*RP] or null (no M_h)
     double* s_out;   // [gridDim.y][Jt][RP] or null (no Sout)
     int64_t spc;     // slabs per CTA
-    // optional: the input is Sin + beta Sd (beta on the device), read on the fly
+    // optional: the input is Sin + beta Sd (beta on the device), read on the fly, where Sin
+    // itself is given as S' with Sin[s][i][r] = S'[s][i][perm r] sc0[r] when perm is set
     const double* Sd;
     const double* beta;
+    const int* perm;
+    const double* sc0;
 };
 
 constexpr int kLevelThreads = 256;
@@ -351,6 +354,10 @@ __global__ void __launch_bounds__(kBulkPairs) level_bulk_kernel(const LevelParam
     }
     const int r = tid % RP;
     const double bt = has_d ? *p.beta : 0.0;
+    // Sin column permutation / scale (the normalised iterate's S from the sweep's S')
+    const bool pm = p.perm != nullptr && r < p.R;
+    const int src = pm ? tid - r + p.perm[r] : tid;
+    const double scl = pm ? p.sc0[r] : 1.0;
     const double ah = (DO_S && pr < npairs && r < p.R) ? p.Ah[(int64_t)r * p.Ih + pr / RP] : 0.0;
     if (DO_M && tid < kBulkSlabs * RP) {
         const int sl = tid % kBulkSlabs, rr = tid / kBulkSlabs;  // consecutive slabs of a column
@@ -364,7 +371,8 @@ __global__ void __launch_bounds__(kBulkPairs) level_bulk_kernel(const LevelParam
     for (int sl = 0; sl < kBulkSlabs; ++sl) {
         xs[sl] = 0.0;
         if (sl < nsl) {
-            double v = live ? lbuf[sl * kBulkPairs + tid] : 0.0;
+            double v = live ? lbuf[sl * kBulkPairs + src] : 0.0;
+            if (pm) v *= scl;
             if (has_d && live) v = fma(bt, lbuf[(kBulkSlabs + sl) * kBulkPairs + tid], v);
             if (DO_M) acc = fma(v, a2s[sl][r], acc);
             if (DO_S) {
@@ -599,12 +607,15 @@ void reduce_jobs(const RedJobs& jobs, cudaStream_t st) {
 // launching them (reduce_jobs later, together with other reductions)
 void run_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
                double* Sout, cudaStream_t st, RedJobs* defer_m = nullptr, RedJobs* defer_s = nullptr,
-               const double* Sd = nullptr, const double* beta = nullptr) {
+               const double* Sd = nullptr, const double* beta = nullptr, const int* perm = nullptr,
+               const double* sc0 = nullptr) {
     if (!do_m && !do_s) return;
     LevelParams p{};
     p.Sin = Sin;
     p.Sd = Sd;
     p.beta = beta;
+    p.perm = perm;
+    p.sc0 = sc0;
     p.Ih = t.dims[h];
     p.Jt = 1;
     for (int m = h + 1; m < t.order; ++m) p.Jt *= t.dims[m];
@@ -628,7 +639,7 @@ void run_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const 
             default: launch_level_bulk<32>(p, grid, st); break;
         }
     } else {
-        if (Sd) throw std::logic_error("level: Sd needs the bulk level kernel");
+        if (Sd || perm) throw std::logic_error("level: Sd / perm need the bulk level kernel");
         const dim3 grid((unsigned)w.lvl_nx[h], (unsigned)ny);
         switch (w.RP) {
             case 8: launch_level_rp<8>(p, grid, w.lvl_km[h], st); break;
@@ -900,6 +911,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
     CPFIT_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
     CPFIT_CUDA(cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming));
     CPFIT_CUDA(cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming));
+    CPFIT_CUDA(cudaEventCreateWithFlags(&w->ev_gram, cudaEventDisableTiming));
     CPFIT_CUDA(cudaMalloc(&w->counter, sizeof(unsigned int) * kCounters));
     CPFIT_CUDA(cudaMemset(w->counter, 0, sizeof(unsigned int) * kCounters));
     if (!t.sparse) {
@@ -914,7 +926,10 @@ EvalWork* work_create(const DevTensor& t, int R) {
         const int per_sm = std::max(1, std::min(2048 / fiber_threads(w->RP),
                                                 (int)((228 * 1024) / (w->fiber_smem + 1024))));
         w->fiber_grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
-        CPFIT_CUDA(cudaMalloc(&w->S, sizeof(double) * (size_t)t.J * w->RP));
+        // order 3: room for S_d right after S (one L2 persistence window covers both)
+        const size_t sn = (size_t)t.J * w->RP;
+        CPFIT_CUDA(cudaMalloc(&w->S, sizeof(double) * sn * (t.order == 3 ? 2 : 1)));
+        if (t.order == 3) w->S2 = w->S + sn;
         CPFIT_CUDA(cudaMalloc(&w->m0_part, sizeof(double) * (size_t)w->fiber_grid * w->RP * 32 * w->fiber_nchunk));
         // rows >= 8 ceil(I0 / 8) of the partials are never written: keep them zero
         CPFIT_CUDA(cudaMemset(w->m0_part, 0, sizeof(double) * (size_t)w->fiber_grid * w->RP * 32 * w->fiber_nchunk));
@@ -974,6 +989,7 @@ void work_destroy(EvalWork* w) {
     cudaFree(w->nscale0);
     if (w->ev_fork) cudaEventDestroy(w->ev_fork);
     if (w->ev_join) cudaEventDestroy(w->ev_join);
+    if (w->ev_gram) cudaEventDestroy(w->ev_gram);
     if (w->side) cudaStreamDestroy(w->side);
     for (int h = 0; h < kMaxOrder; ++h) {
         cudaFree(w->lvl_part[h]);
@@ -1066,7 +1082,8 @@ void reduce_grad(const DevTensor& t, EvalWork& w, const RedJobs& jobs, const dou
 }  // namespace
 
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
-                 int* status, cudaStream_t st, bool need_grad, const int* resid_flag, bool s_given, bool grams_given) {
+                 int* status, cudaStream_t st, bool need_grad, const int* resid_flag, bool s_given, bool grams_given,
+                 cudaEvent_t grad_dep) {
     (void)status;
     if (!grams_given) grams_device(w, u, st);
     if (!t.sparse) {
@@ -1086,6 +1103,7 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
             Sin = w.lvl_S[h];
         }
         if (t.order >= 3) {
+            if (grad_dep) CPFIT_CUDA(cudaStreamWaitEvent(st, grad_dep, 0));
             reduce_grad(t, w, jobs, u, g, d, need_grad, sc, st);
             return;
         }
@@ -1150,7 +1168,8 @@ void dense_s_pass(const DevTensor& t, EvalWork& w, const double* u, double* S_ou
     run_fiber(t, w, u, true, false, false, nullptr, st, nullptr, S_out);
 }
 void eval_given_s_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc,
-                         cudaStream_t st, const double* Sd, const double* beta, bool grams_given) {
+                         cudaStream_t st, const double* Sd, const double* beta, bool grams_given, const int* perm,
+                         const double* sc0) {
     if (!grams_given) grams_device(w, u, st);
     run_fiber(t, w, u, false, true, false, nullptr, st);  // M0 only
     RedJobs jobs;
@@ -1158,7 +1177,7 @@ void eval_given_s_device(const DevTensor& t, EvalWork& w, const double* u, doubl
     const double* Sin = w.S;
     for (int h = 1; h < t.order - 1; ++h) {
         run_level(t, w, h, Sin, u, true, true, w.lvl_S[h], st, &jobs, h == t.order - 2 ? &jobs : nullptr,
-                  h == 1 ? Sd : nullptr, beta);
+                  h == 1 ? Sd : nullptr, beta, h == 1 ? perm : nullptr, sc0);
         Sin = w.lvl_S[h];
     }
     reduce_grad(t, w, jobs, u, g, nullptr, true, sc, st);

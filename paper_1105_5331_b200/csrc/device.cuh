@@ -61,6 +61,7 @@ struct EvalWork {
     int fiber_grid = 0, fiber_F = 16, fiber_nchunk = 0;
     size_t fiber_smem = 0;
     double* S = nullptr;        // J x RP
+    double* S2 = nullptr;       // (dense order 3) a second J x RP right after S: the line search's S_d
     double* m0_part = nullptr;  // fiber_grid x RP x (32*nchunk)
     double* f_part = nullptr;   // fiber_grid (+ sparse/other scalars)
     double* m0 = nullptr;       // reduced M0 [RP][32*nchunk]
@@ -94,6 +95,7 @@ struct EvalWork {
     dd* solve_part = nullptr;        // per-mode Gram partials of the ALS solves
     int64_t solve_part_stride = 0;   // dd per mode ([blocks][npair])
     cudaStream_t side = nullptr;
+    cudaEvent_t ev_gram = nullptr;  // finalize_gram_side done
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
@@ -111,9 +113,11 @@ struct EvalScalars {
 // objective_and_gradient (kruskal.cpp:127-149) at device iterate u; writes g (packed),
 // scalars->f, ->gnorm2 and (if d != nullptr) ->gdotd.  Grams of u are computed first.
 // mode = 0 gradient+f; mode = 1 f only (objective()).
+// grad_dep (dense, order >= 3): an event the gradient step waits for (a Gram finalised beside
+// the T pass)
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
                  int* status, cudaStream_t st, bool need_grad = true, const int* resid_flag = nullptr,
-                 bool s_given = false, bool grams_given = false);
+                 bool s_given = false, bool grams_given = false, cudaEvent_t grad_dep = nullptr);
 
 // mttkrp(T, factors(u), mode) (tensor.cpp:206-259) -> out (I_mode x R col-major).
 void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st);
@@ -128,24 +132,35 @@ void normalize_device(EvalWork& w, const double* u, double* out, cudaStream_t st
                       bool save_perm = false, bool out_grams = false);
 // normalize u -> uout and map the gradient g at u to the normalised point (G_n D_n^-1,
 // permuted) -> gout; writes per-block partial ||gout||^2 to red, returns the block count.
+// save_perm: the permutation and mode-0 scales into w.nperm / w.nscale0; gram_copy: a second
+// copy of the output Grams (with out_grams)
 int normalize_grad_device(EvalWork& w, const double* u, const double* g, double* uout, double* gout, double* red,
-                          cudaStream_t st, const double* m0 = nullptr, double* m0out = nullptr, bool out_grams = false);
+                          cudaStream_t st, const double* m0 = nullptr, double* m0out = nullptr, bool out_grams = false,
+                          bool save_perm = false, double* gram_copy = nullptr);
 // One ALS sweep (als.cpp:38-48): u -> out (normalized); work: n_u scratch, mbuf: max I_n x R
 // scratch. status: bit0 singular normal matrix after the ridge retry, bit1 non-finite solve.
 // keep_s: leave S(out) = T x_1 A0(out) in w.S (dense; for an evaluation with s_given)
 // grams_given: w.gram already holds the Grams of u; then the Grams of out are left in w.gram
+// defer_norm (dense): stop before the normalisation — the unnormalised sweep result stays in
+// work with S' = T x_1 A0' in w.S and its Grams in w.gram except the last mode's, still in
+// solve partials (finalize_gram_side); out is not written.
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
                          int* status, cudaStream_t st, const double* m0_given = nullptr, bool keep_s = false,
-                         bool grams_given = false);
+                         bool grams_given = false, bool defer_norm = false);
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
+// G_mode <- its pending ALS-solve partials, one block on w.side after the work queued on st;
+// records `done` on w.side
+void finalize_gram_side(EvalWork& w, int mode, cudaStream_t st, cudaEvent_t done);
 
 // Dense pieces for the exact line search (poly.cu): S = T x_1 A (first factor of u) into S_out;
 // and the evaluation at u when T x_1 A0(u) = w.S (+ *beta Sd when Sd is given) (order 3: M0
 // pass + level + gradient; scalars->f is NOT the objective — the caller supplies it).
 void dense_s_pass(const DevTensor& t, EvalWork& w, const double* u, double* S_out, cudaStream_t st);
+// perm / sc0: w.S holds S' with S(u_bar)[j][r] = S'[j][perm r] sc0[r] (the iterate's
+// normalisation after the evaluation; null: w.S is S(u_bar) itself)
 void eval_given_s_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc,
                          cudaStream_t st, const double* Sd = nullptr, const double* beta = nullptr,
-                         bool grams_given = false);
+                         bool grams_given = false, const int* perm = nullptr, const double* sc0 = nullptr);
 
 // Exact line search along d for order-3 dense tensors (poly.cu): phi(a) = f(u_bar + a d) is a
 // degree-6 polynomial whose coefficients follow from S(u_bar) (in w.S), S_d = T x_1 D0, the
@@ -165,8 +180,9 @@ bool poly_supported(const DevTensor& t);
 PolyWork* poly_create(const DevTensor& t, const EvalWork& w);
 void poly_destroy(PolyWork* p);
 // coefficients of phi from u_bar (its S in w.S) and d
+// (perm / sc0 as for eval_given_s_device)
 void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const double* ub, const double* d,
-                       cudaStream_t st);
+                       cudaStream_t st, const int* perm = nullptr, const double* sc0 = nullptr);
 // the accepted point u* = u_bar + beta d (beta on the device) and its Grams (into w.gram) from
 // the double-double cross Grams of the last build: A^T A + beta (A^T D + D^T A) + beta^2 D^T D
 void poly_point_device(EvalWork& w, const PolyWork& pw, const double* ub, const double* d, const double* beta,

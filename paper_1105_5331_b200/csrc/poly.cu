@@ -64,6 +64,8 @@ struct S8Params {
     dd* part;          // [block][8]
     dd* out;           // [8]
     unsigned int* counter;
+    const int* perm;   // S(u_bar)[j][r] = S[j][perm r] sc0[r] when set
+    const double* sc0;
 };
 
 __device__ __forceinline__ dd dd_shfl_xor(dd v, int o) {
@@ -103,15 +105,20 @@ __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
     const int i2b = min(I2, i2a + kS8I2);
     const int i1 = pr / p.RP, r = pr % p.RP;
     const bool active = pr < npr && r < p.R;
+    // S(u_bar) column r = sc0[r] x S column perm[r]: coalesced loads, then a shuffle from the
+    // lane holding column perm[r] of the same row (a row of RP pairs lies in one warp)
+    const int lane0 = threadIdx.x & 31;
+    const int src = (lane0 & ~(p.RP - 1)) + ((p.perm && r < p.R) ? p.perm[r] : r);
+    const double scl = (active && p.perm) ? p.sc0[r] : 1.0;
     // the first run's S loads and the X1 factors go out before the X2 staging barrier
     double sav[kS8Run], sdv[kS8Run];
     auto load_run = [&](int i0) {
 #pragma unroll
         for (int u = 0; u < kS8Run; ++u) {
             const int i2 = i0 + u;
-            const int64_t e = ((int64_t)i2 * I1 + i1) * p.RP + r;
-            sav[u] = active && i2 < i2b ? p.S[e] : 0.0;
-            sdv[u] = active && i2 < i2b ? p.Sd[e] : 0.0;
+            const int64_t e = ((int64_t)i2 * I1 + i1) * p.RP;
+            sav[u] = active && i2 < i2b ? p.S[e + r] : 0.0;
+            sdv[u] = active && i2 < i2b ? p.Sd[e + r] : 0.0;
         }
     };
     load_run(i2a);
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
         x2s[1][ii][rr] = ok ? p.D2[(int64_t)rr * I2 + i2a + ii] : 0.0;
     }
     __syncthreads();
-    if (active) {
+    {  // every lane (the shuffles); inactive lanes hold zeros
         dd q[4];  // S.A2, S.D2, S_d.A2, S_d.D2 over the chunk
 #pragma unroll
         for (int k = 0; k < 4; ++k) q[k] = dd{0.0, 0.0};
@@ -136,8 +143,9 @@ __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
                 const int i2 = i0 + u;
                 if (i2 >= i2b) break;
                 const double x2a = x2s[0][i2 - i2a][r], x2d = x2s[1][i2 - i2a][r];
-                part[0] = fma(sav[u], x2a, part[0]);
-                part[1] = fma(sav[u], x2d, part[1]);
+                const double sa = p.perm ? __shfl_sync(0xffffffffu, sav[u], src) : sav[u];
+                part[0] = fma(sa, x2a, part[0]);
+                part[1] = fma(sa, x2d, part[1]);
                 part[2] = fma(sdv[u], x2a, part[2]);
                 part[3] = fma(sdv[u], x2d, part[3]);
             }
@@ -146,6 +154,11 @@ __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) q[k] = dd_two_sum(q[k].hi, q[k].lo);
+        // S(u_bar) column r = sc0[r] x S column perm[r]: the scale applies to the S sums
+        if (p.perm) {
+            q[0] = dd_mul(q[0], dd{scl, 0.0});
+            q[1] = dd_mul(q[1], dd{scl, 0.0});
+        }
         // k = 4 b0 + 2 b1 + b2: q index 2 b0 + b2, X1 by b1
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc[k] = dd_mul(q[2 * (k >> 2) + (k & 1)], (k & 2) ? x1d : x1a);
@@ -346,7 +359,7 @@ PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {
     for (int n = 0; n < 3; ++n) tasks += (int64_t)gram_chunks(t.dims[n]) * kKinds * w.R * w.R;
     p->nchunk_total = tasks;
     p->s8_grid = (int)(((t.dims[1] * w.RP + 255) / 256) * ((t.dims[2] + kS8I2 - 1) / kS8I2));
-    CPFIT_CUDA(cudaMalloc(&p->S_d, sizeof(double) * (size_t)t.J * w.RP));
+    p->S_d = w.S2;  // owned by the evaluation workspace (next to S)
     CPFIT_CUDA(cudaMalloc(&p->gpart, sizeof(dd) * (size_t)std::max<int64_t>(tasks, 1)));
     CPFIT_CUDA(cudaMalloc(&p->grams, sizeof(dd) * 3 * kKinds * (size_t)w.RP * w.RP));
     CPFIT_CUDA(cudaMalloc(&p->s8part, sizeof(dd) * 8 * (size_t)p->s8_grid));
@@ -359,7 +372,6 @@ PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {
 
 void poly_destroy(PolyWork* p) {
     if (!p) return;
-    cudaFree(p->S_d);
     cudaFree(p->gpart);
     cudaFree(p->grams);
     cudaFree(p->s8part);
@@ -370,7 +382,7 @@ void poly_destroy(PolyWork* p) {
 }
 
 void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const double* ub, const double* d,
-                       cudaStream_t st) {
+                       cudaStream_t st, const int* perm, const double* sc0) {
     // S_d = T x_1 D_0 (the direction's first block)
     dense_s_pass(t, w, d, pw.S_d, st);
     CrossParams c{};
@@ -397,6 +409,8 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     s.A2 = ub + w.off[2];
     s.D2 = d + w.off[2];
     s.part = pw.s8part;
+    s.perm = perm;
+    s.sc0 = sc0;
 
     const int ngx = (int)((t.dims[0 + 1] * w.RP + 255) / 256);
     const int ngy = (int)((t.dims[2] + kS8I2 - 1) / kS8I2);

@@ -60,6 +60,8 @@ struct Ctl {
     const double* accel_scal;
     const double* accel_red;  // accel_update_kernel's per-block g_bar.d partials
     int accel_nb;
+    const double* bar_red;    // deferred normalisation: per-block ||g_bar||^2 partials (else null)
+    int bar_nb;
     TraceRow* trace;
     int trace_cap;
     double gradient_scale, hscale, tol_grad;
@@ -137,10 +139,14 @@ __global__ void k_set_cond_running(Ctl c, cudaGraphConditionalHandle h) {
 // search, 2 none (restart / no descent / failure).
 // (one warp: the slope g_bar.d is summed here from the recombination's block partials)
 __global__ void k_branch(Ctl c, cudaGraphConditionalHandle br_h) {
-    double sl = 0.0;
+    double sl = 0.0, g2 = 0.0;
     for (int b = threadIdx.x; b < c.accel_nb; b += 32) sl += c.accel_red[b];
+    if (c.bar_red)  // ||g_bar||^2 of the normalised point (deferred normalisation)
+        for (int b = threadIdx.x; b < c.bar_nb; b += 32) g2 += c.bar_red[b];
     sl = warp_sum(sl);
+    g2 = warp_sum(g2);
     if (threadIdx.x != 0) return;
+    if (c.bar_red) const_cast<EvalScalars*>(c.sc_bar)->gnorm2 = g2;
     DevState& s = *c.s;
     s.f_bar = c.sc_bar->f;
     s.fevals += 1;
@@ -490,10 +496,34 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     // Grams handed on by the normalisations (no Gram pass at the sweep start / for u_bar)
     gout_ = (int64_t)t->order * w_->RP * w_->RP <= kGramsOutMax;
     if (gout_) alloc(&gram_bar_, gram_n());
+    defer_ = method_ == 0 && !t->sparse && gout_;
+    norm_nb_ = (int)std::min<int64_t>(296, (n_ + 255) / 256);
     // exact polynomial line search: dense order 3, default objective handling, not disabled
     const char* np = std::getenv("CPFIT_NO_POLY_LS");
     if (method_ == 0 && poly_supported(*t) && !o.reeval_accepted && !o.residual_objective && !(np && np[0] == '1'))
         pw_ = poly_create(*t, *w_);
+    // S (and S_d next to it) persist in L2 across the T passes: every consumer (the M0 +
+    // objective pass, the level contractions, the line-search contractions) then reads them
+    // from L2 instead of HBM; T streams through the rest of L2
+    if (const char* e = std::getenv("CPFIT_NO_L2_WINDOW"); !(e && e[0] == '1') && !t->sparse && w_->S) {
+        int dev = 0, max_persist = 0, max_win = 0;
+        CPFIT_CUDA(cudaGetDevice(&dev));
+        CPFIT_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+        CPFIT_CUDA(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+        const size_t bytes = std::min<size_t>(sizeof(double) * (size_t)t->J * w_->RP * (w_->S2 ? 2 : 1), (size_t)max_win);
+        const size_t persist = std::min<size_t>(bytes, (size_t)max_persist);
+        if (persist > 0) {
+            CPFIT_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+            cudaStreamAttrValue v{};
+            v.accessPolicyWindow.base_ptr = w_->S;
+            v.accessPolicyWindow.num_bytes = bytes;
+            v.accessPolicyWindow.hitRatio = (float)((double)persist / (double)bytes);
+            v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            for (cudaStream_t sx : {st_, st2_, st3_, st4_, w_->side})
+                CPFIT_CUDA(cudaStreamSetAttribute(sx, cudaStreamAttributeAccessPolicyWindow, &v));
+        }
+    }
     if (const char* e = std::getenv("CPFIT_PHASE_PROFILE"); e && e[0] == '1') {
         CPFIT_CUDA(cudaMalloc(&phase_, sizeof(unsigned long long) * (2 * kPhases + 1)));
         CPFIT_CUDA(cudaMemset(phase_, 0, sizeof(unsigned long long) * (2 * kPhases + 1)));
@@ -539,6 +569,8 @@ void Solver::build_graphs() {
     c.accel_scal = a_ ? a_->scal : nullptr;
     c.accel_red = a_ ? a_->red : nullptr;
     c.accel_nb = a_ ? accel_update_blocks(*a_) : 0;
+    c.bar_red = defer_ ? red_ : nullptr;
+    c.bar_nb = norm_nb_;
     c.trace = trace_;
     c.trace_cap = trace_cap_;
     c.gradient_scale = opt_.gradient_scale;
@@ -589,13 +621,8 @@ void Solver::build_graphs() {
     cudaGraph_t lsb = nullptr, ab = nullptr, pb = nullptr, apb = nullptr, db = nullptr;
     if (method_ == 0) {
         // Step I: u_bar = M(u) (canonical), g_bar = g(u_bar)                (ngmres.cpp:90-94)
-        als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st2_, m0_cur_, true, gout_);
-        stamp(st2_, 0);
-        eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st2_, true, &s->resid, !t_->sparse, gout_);
-        if (m0_bar_)
-            CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st2_));
-        if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st2_));
-        stamp(st2_, 1);
+        emit_bar(st2_, &c);
+        stamp(st2_, 1);  // (phase 1 = ALS sweep + evaluation of u_bar)
         // Step II: windowed recombination -> d, slope                        (ngmres.cpp:97-101)
         accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st2_, true);
         // Step III: restart test / line search (ngmres.cpp:111-147) as one SWITCH node — every
@@ -613,7 +640,8 @@ void Solver::build_graphs() {
             // not, the search almost always accepts, and the commit keeps u_bar otherwise)
             pb = br[0];
             CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, pb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-            poly_build_device(*t_, *w_, *pw_, ub_, d_, st3_);
+            poly_build_device(*t_, *w_, *pw_, ub_, d_, st3_, defer_ ? w_->nperm : nullptr,
+                              defer_ ? w_->nscale0 : nullptr);
             k_poly_ls<<<1, 1, 0, st3_>>>(c);
             stamp(st3_, 3);
             emit_poly_accept(st3_, &c);
@@ -687,6 +715,31 @@ void Solver::build_graphs() {
     CPFIT_CUDA(cudaGraphInstantiate(&x_loop_, g_loop_, 0));
 }
 
+// Step I (ngmres.cpp:90-94): u_bar = M(u) (canonical), g_bar = g(u_bar). Deferred form (dense):
+// the sweep stops before its normalisation, the evaluation runs at the sweep's own point u'
+// (S' = T x_1 A0' is its S: no rescale pass), and normalize_grad maps (u', g', M0') to the
+// canonical point — exact, as for an accepted step (f is invariant, G -> G D^-1 permuted) —
+// leaving the permutation / mode-0 scales for the users of S(u_bar) (line-search polynomial,
+// accepted-step level pass) and the Grams of u_bar in w.gram and gram_bar_.
+void Solver::emit_bar(cudaStream_t st, const void* ctl) {
+    const Ctl& c = *reinterpret_cast<const Ctl*>(ctl);
+    DevState* s = c.s;
+    EvalScalars* sc_bar = reinterpret_cast<EvalScalars*>(sc_) + 1;
+    int* status = &s->status;
+    if (defer_) {
+        als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st, m0_cur_, true, gout_, true);
+        // the last mode's Gram is summed beside the M0 + objective pass (only the gradient needs it)
+        finalize_gram_side(*w_, t_->order - 1, st, w_->ev_gram);
+        eval_device(*t_, *w_, work_, gt_, sc_bar, nullptr, status, st, true, &s->resid, true, true, w_->ev_gram);
+        normalize_grad_device(*w_, work_, gt_, ub_, gb_, red_, st, w_->m0, m0_bar_, true, true, gram_bar_);
+        return;
+    }
+    als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st, m0_cur_, true, gout_);
+    eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st, true, &s->resid, !t_->sparse, gout_);
+    if (m0_bar_) CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st));
+    if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st));
+}
+
 // accepted step of a polynomial line search (see build_graphs)
 void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
     const Ctl& c = *reinterpret_cast<const Ctl*>(ctl);
@@ -697,7 +750,8 @@ void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
     // u* and its Grams (from the cross Grams); S(u*) = S(u_bar) + beta S_d is formed on the fly
     // by the level pass
     poly_point_device(*w_, *pw_, ub_, d_, &s->beta, ut_, st);
-    eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true);
+    eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true, defer_ ? w_->nperm : nullptr,
+                        defer_ ? w_->nscale0 : nullptr);
     const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, w_->m0, m0_cur_, gout_);
     k_after_rescale<<<1, 32, 0, st>>>(c, sc_next, red_, nb);
     CPFIT_CUDA(cudaGetLastError());
@@ -745,7 +799,6 @@ void Solver::run_loop_eager() {
     std::memcpy(&c, ctl_blob_, sizeof(Ctl));
     c.eager = 1;
     DevState* s = reinterpret_cast<DevState*>(state_);
-    EvalScalars* sc_bar = reinterpret_cast<EvalScalars*>(sc_) + 1;
     EvalScalars* sc_trial = reinterpret_cast<EvalScalars*>(sc_) + 2;
     EvalScalars* sc_next = reinterpret_cast<EvalScalars*>(sc_) + 3;
     int* status = &s->status;
@@ -761,15 +814,12 @@ void Solver::run_loop_eager() {
         DevState hs = state();
         if (!(hs.stop < 0 && hs.iter < hs.max_iters)) break;
         if (method_ == 0) {
-            als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st_, m0_cur_, true, gout_);
-            eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st_, true, &s->resid, !t_->sparse, gout_);
-            if (m0_bar_)
-                CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
-            if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st_));
+            emit_bar(st_, &c);
             accelerate_device(*a_, wu_, wg_, s->ring, ub_, gb_, opt_.epsilon_reg, nullptr, d_, st_, true);
             k_branch<<<1, 32, 0, st_>>>(c, none);
             if (state().poly) {
-                poly_build_device(*t_, *w_, *pw_, ub_, d_, st_);
+                poly_build_device(*t_, *w_, *pw_, ub_, d_, st_, defer_ ? w_->nperm : nullptr,
+                                  defer_ ? w_->nscale0 : nullptr);
                 k_poly_ls<<<1, 1, 0, st_>>>(c);
             }
             while (state().searching) {

@@ -77,8 +77,11 @@ private:
     void build_graphs();
     void run_loop_eager();
     void emit_poly_accept(cudaStream_t st, const void* ctl);
+    void emit_bar(cudaStream_t st, const void* ctl);
     PolyWork* pw_ = nullptr;  // exact line search (poly.cu), when it applies
     bool gout_ = false;       // normalisations hand on their output's Grams
+    bool defer_ = false;      // eval at the sweep's own point, then normalise (no S rescale)
+    int norm_nb_ = 0;         // normalize_grad blocks (partials of ||g_bar||^2 in red_)
     double* gram_bar_ = nullptr;
     int64_t gram_n() const { return (int64_t)w_->order * w_->RP * w_->RP; }
     size_t gram_bytes() const { return sizeof(double) * (size_t)gram_n(); }
