@@ -554,14 +554,14 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const RedLaunch L) {
     }
     if (!L.grad) return;
     if (!last_block_arrives(G.counter)) return;
-    if (ws != 0) return;
-    // last block, one warp: lane-strided partial sums (loads batched) then a fixed shuffle tree
+    // last block, all warps: thread-strided partial sums (loads batched), a fixed shuffle tree
+    // per warp, then the warps in order
     double a = 0.0, b = 0.0, c = 0.0, fs = 0.0;
-    for (int q0 = lane; q0 < (int)gridDim.x; q0 += 32 * 4) {
+    for (int q0 = threadIdx.x; q0 < (int)gridDim.x; q0 += 256 * 4) {
         double x[4][3];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int q = q0 + 32 * u;
+            const int q = q0 + 256 * u;
 #pragma unroll
             for (int t = 0; t < 3; ++t) x[u][t] = q < (int)gridDim.x ? G.red[q * 3 + t] : 0.0;
         }
@@ -572,12 +572,27 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const RedLaunch L) {
             c += x[u][2];
         }
     }
-    for (int q = lane; q < G.f_grid; q += 32) fs += G.f_part[q];
+    for (int q = threadIdx.x; q < G.f_grid; q += 256) fs += G.f_part[q];
     a = warp_sum(a);
     b = warp_sum(b);
     c = warp_sum(c);
     fs = warp_sum(fs);
+    __shared__ double wr[4][8];
     if (lane == 0) {
+        wr[0][ws] = a;
+        wr[1][ws] = b;
+        wr[2][ws] = c;
+        wr[3][ws] = fs;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a = b = c = fs = 0.0;
+        for (int w8 = 0; w8 < 8; ++w8) {
+            a += wr[0][w8];
+            b += wr[1][w8];
+            c += wr[2][w8];
+            fs += wr[3][w8];
+        }
         G.sc->f = 0.5 * fs;
         G.sc->gnorm2 = a;
         G.sc->inner = c;
