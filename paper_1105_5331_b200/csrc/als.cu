@@ -16,6 +16,36 @@
 
 #include <algorithm>
 
+#ifdef CPFIT_NORM_STAMPS
+__device__ unsigned long long g_norm_stamps[32];
+#define NSTAMP(k)                                                                              \
+    do {                                                                                       \
+        if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) {            \
+            unsigned long long t_;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+            g_norm_stamps[(blockIdx.x == 0 ? 0 : 16) + (k)] = t_;                              \
+        }                                                                                      \
+    } while (0)
+#define NSTAMPL(k)                                                                             \
+    do {                                                                                       \
+        if (threadIdx.x == 0) {                                                                \
+            unsigned long long t_;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+            g_norm_stamps[k] = t_;                                                             \
+        }                                                                                      \
+    } while (0)
+extern "C" int cpfit_debug_norm_stamps(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_norm_stamps, sizeof(unsigned long long) * 32);
+}
+#else
+#define NSTAMP(k) \
+    do {          \
+    } while (0)
+#define NSTAMPL(k) \
+    do {           \
+    } while (0)
+#endif
+
 namespace cpfit_gpu {
 
 
@@ -307,6 +337,7 @@ __global__ void normalize_kernel(const NormParams p) {
     __shared__ double scale[kMaxOrder][kMaxRank];
     __shared__ double diag[kMaxOrder][kMaxRank];
     const int tid = threadIdx.x;
+    NSTAMP(0);
     for (int e = tid; e < p.order * p.R; e += blockDim.x) {  // Gram diagonals, independent loads
         const int n = e / p.R, r = e % p.R;
         diag[n][r] = (n == p.pend.mode) ? pending_pair(p.pend, p.R * (p.R + 1) / 2, r * p.R - r * (r - 1) / 2)
@@ -314,58 +345,47 @@ __global__ void normalize_kernel(const NormParams p) {
     }
     if (blockIdx.x == 0) finalize_pending(p.pend, p.R, p.RP, p.gram_w);
     __syncthreads();
-    if (tid < p.R) {
+    NSTAMP(1);
+    if (tid < 32) {
+        // warp 0, lane r: rank r's norms (shared memory) and lambda, the stable sort by shuffles
+        const int r = tid;
+        const bool on = r < p.R;
         double l = 1.0;
-        for (int n = 0; n < p.order; ++n) {
-            const double v = sqrt(diag[n][tid]);
-            nrm[n][tid] = v;
-            l *= v;
-        }
-        lam[tid] = l;
-    }
-    __syncthreads();
-    if (tid < p.R) {
+        if (on)
+            for (int n = 0; n < p.order; ++n) {
+                const double v = sqrt(diag[n][r]);
+                nrm[n][r] = v;
+                l *= v;
+            }
+        if (on) lam[r] = l;
         // stable descending rank: count entries that must precede this one
         int pos = 0;
-        for (int q = 0; q < p.R; ++q)
-            if (lam[q] > lam[tid] || (q < tid && !(lam[tid] > lam[q]) && !(lam[q] > lam[tid]))) ++pos;
-        perm[pos] = tid;
-    }
-    __syncthreads();
-    if (tid < p.R) {
-        const int src = perm[tid];
-        const double l = lam[src];
-        const double root = (l == 0.0) ? 0.0 : pow(l, 1.0 / p.order);
-        for (int n = 0; n < p.order; ++n) scale[n][tid] = (l == 0.0) ? 1.0 : root / nrm[n][src];
-        if (blockIdx.x == 0 && p.perm_out) {
-            p.perm_out[tid] = src;
-            p.scale0_out[tid] = scale[0][tid];
+        for (int q = 0; q < p.R; ++q) {
+            const double lq = __shfl_sync(0xffffffffu, l, q);
+            if (lq > l || (q < r && !(l > lq) && !(lq > l))) ++pos;
+        }
+        if (on) perm[pos] = r;
+        __syncwarp();
+        const int src = on ? perm[r] : 0;
+        const double ls = __shfl_sync(0xffffffffu, l, src);
+        if (on) {
+            // lambda^(1/N): cbrt for N = 3 (one root instead of pow's log / exp)
+            const double root = (ls == 0.0) ? 0.0 : (p.order == 3 ? cbrt(ls) : pow(ls, 1.0 / p.order));
+            for (int n = 0; n < p.order; ++n) scale[n][r] = (ls == 0.0) ? 1.0 : root / nrm[n][src];
+            if (blockIdx.x == 0 && p.perm_out) {
+                p.perm_out[r] = src;
+                p.scale0_out[r] = scale[0][r];
+            }
         }
     }
     __syncthreads();
+    NSTAMP(4);
     const int64_t total = p.off[p.order];
+    const int64_t tm = p.m0 ? (int64_t)p.RP * p.m0_ld : 0;
     double g2 = 0.0;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + tid; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        int n = 0;
-        while (e >= p.off[n + 1]) ++n;
-        const int64_t loc = e - p.off[n];
-        const int64_t In = p.dims[n];
-        const int r = (int)(loc / In);
-        const int64_t i = loc % In;
-        const int src = perm[r];
-        const int64_t at = p.off[n] + (int64_t)src * In + i;
-        const double v = p.u[at];
-        const bool keep = (lam[src] == 0.0);
-        p.out[e] = keep ? v : v * scale[n][r];
-        if (p.g) {
-            const double gv = keep ? p.g[at] : p.g[at] / scale[n][r];
-            p.gout[e] = gv;
-            g2 += gv * gv;
-        }
-    }
-    if (p.m0) {
-        const int64_t tm = (int64_t)p.RP * p.m0_ld;
-        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + tid; e < tm; e += (int64_t)gridDim.x * blockDim.x) {
+    // the iterate / gradient element and the M0 element of one index together (their loads overlap)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + tid; e < total || e < tm; e += (int64_t)gridDim.x * blockDim.x) {
+        if (e < tm) {
             const int r = (int)(e / p.m0_ld);
             const int64_t i = e % p.m0_ld;
             double v = 0.0;
@@ -376,12 +396,31 @@ __global__ void normalize_kernel(const NormParams p) {
             }
             p.m0out[e] = v;
         }
+        if (e < total) {
+            int n = 0;
+            while (e >= p.off[n + 1]) ++n;
+            const int64_t loc = e - p.off[n];
+            const int64_t In = p.dims[n];
+            const int r = (int)(loc / In);
+            const int64_t i = loc % In;
+            const int src = perm[r];
+            const int64_t at = p.off[n] + (int64_t)src * In + i;
+            const double v = p.u[at];
+            const bool keep = (lam[src] == 0.0);
+            p.out[e] = keep ? v : v * scale[n][r];
+            if (p.g) {
+                const double gv = keep ? p.g[at] : p.g[at] / scale[n][r];
+                p.gout[e] = gv;
+                g2 += gv * gv;
+            }
+        }
     }
     if (p.g) {
         __shared__ double red[32];
         g2 = warp_sum(g2);
         if ((tid & 31) == 0) red[tid >> 5] = g2;
         __syncthreads();
+        NSTAMP(5);
         if (tid == 0) {
             double s = 0.0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
@@ -391,12 +430,15 @@ __global__ void normalize_kernel(const NormParams p) {
     if (p.counter) {
         // every block has read the input Grams once the last one arrives: rewrite them as the
         // Grams of the normalised output (the next evaluation / sweep then skips the Gram pass)
+        NSTAMP(10);
         if (!last_block_arrives(p.counter)) return;
+        NSTAMPL(27);
         __shared__ double gin[kGramsOutMax];  // callers check order * RP * RP <= kGramsOutMax
         const int RR = p.RP * p.RP;
         {
             for (int e = tid; e < p.order * RR; e += blockDim.x) gin[e] = p.gram_w[e];
             __syncthreads();
+            NSTAMPL(28);
             for (int e = tid; e < p.order * RR; e += blockDim.x) {
                 const int n = e / RR, q = (e % RR) / p.RP, r = e % p.RP;
                 double v = 0.0;
@@ -406,6 +448,8 @@ __global__ void normalize_kernel(const NormParams p) {
             }
         }
     }
+    NSTAMP(12);
+    if (p.counter) NSTAMPL(29);
 }
 
 __global__ void gram_hadamard_kernel(const double* gram, int order, int R, int RP, int skip, double* out) {
