@@ -941,7 +941,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
         const int per_sm = std::max(1, std::min(2048 / fiber_threads(w->RP),
                                                 (int)((228 * 1024) / (w->fiber_smem + 1024))));
         w->fiber_grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
-        // order 3: room for S_d right after S (one L2 persistence window covers both)
+        // order 3: room for the line search's S_d right after S
         const size_t sn = (size_t)t.J * w->RP;
         CPFIT_CUDA(cudaMalloc(&w->S, sizeof(double) * sn * (t.order == 3 ? 2 : 1)));
         if (t.order == 3) w->S2 = w->S + sn;

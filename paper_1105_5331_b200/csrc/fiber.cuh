@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
             if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
             __syncwarp();
             if (lane < nvalid)
-                bulk_g2s(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s]);
+                bulk_g2s_hint(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s], l2_evict_first());
             if (!Ro::SEPW && need_w) w_producer(k, xw, fw, hw);
         }
     } else if (Ro::SEPW && warp <= Ro::NWP) {
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(co
             if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
             __syncwarp();
             if (lane < nvalid)
-                bulk_g2s(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s]);
+                bulk_g2s_hint(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s], l2_evict_first());
         }
         return;
     }
@@ -849,7 +849,7 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
             if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
             __syncwarp();
             if (lane < nvalid)
-                bulk_g2s(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s]);
+                bulk_g2s_hint(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s], l2_evict_first());
         }
         return;
     }

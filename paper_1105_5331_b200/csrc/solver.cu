@@ -502,28 +502,6 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     const char* np = std::getenv("CPFIT_NO_POLY_LS");
     if (method_ == 0 && poly_supported(*t) && !o.reeval_accepted && !o.residual_objective && !(np && np[0] == '1'))
         pw_ = poly_create(*t, *w_);
-    // S (and S_d next to it) persist in L2 across the T passes: every consumer (the M0 +
-    // objective pass, the level contractions, the line-search contractions) then reads them
-    // from L2 instead of HBM; T streams through the rest of L2
-    if (const char* e = std::getenv("CPFIT_NO_L2_WINDOW"); !(e && e[0] == '1') && !t->sparse && w_->S) {
-        int dev = 0, max_persist = 0, max_win = 0;
-        CPFIT_CUDA(cudaGetDevice(&dev));
-        CPFIT_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
-        CPFIT_CUDA(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev));
-        const size_t bytes = std::min<size_t>(sizeof(double) * (size_t)t->J * w_->RP * (w_->S2 ? 2 : 1), (size_t)max_win);
-        const size_t persist = std::min<size_t>(bytes, (size_t)max_persist);
-        if (persist > 0) {
-            CPFIT_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
-            cudaStreamAttrValue v{};
-            v.accessPolicyWindow.base_ptr = w_->S;
-            v.accessPolicyWindow.num_bytes = bytes;
-            v.accessPolicyWindow.hitRatio = (float)((double)persist / (double)bytes);
-            v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            for (cudaStream_t sx : {st_, st2_, st3_, st4_, w_->side})
-                CPFIT_CUDA(cudaStreamSetAttribute(sx, cudaStreamAttributeAccessPolicyWindow, &v));
-        }
-    }
     if (const char* e = std::getenv("CPFIT_PHASE_PROFILE"); e && e[0] == '1') {
         CPFIT_CUDA(cudaMalloc(&phase_, sizeof(unsigned long long) * (2 * kPhases + 1)));
         CPFIT_CUDA(cudaMemset(phase_, 0, sizeof(unsigned long long) * (2 * kPhases + 1)));
