@@ -115,8 +115,16 @@ int cpfit_ngmres_solve(cpfit_tensor t, int64_t rank, const double* u0, const cpf
 int cpfit_als_solve(cpfit_tensor t, int64_t rank, const double* u0, double tol_grad, int max_iters, double* u_best,
                     double* f_best, cpfit_trace_row* trace, int64_t cap, int64_t* rows, int* stop_reason);
 
+/* ncg_solve(t, initial, opts) — ncg.hpp:29 (NcgOptions ncg.hpp:14-18: tol_grad, max_iters,
+ * line_search; ls may be NULL for the defaults). Device-resident like cpfit_ngmres_solve;
+ * u_best is the best-f iterate, normalised once (ncg.cpp:122). Stalled iterations write no
+ * trace row (ncg.cpp:60-67), so *rows can be below iterations + 1. */
+int cpfit_ncg_solve(cpfit_tensor t, int64_t rank, const double* u0, double tol_grad, int max_iters,
+                    const cpfit_line_search_params* ls, double* u_best, double* f_best, cpfit_trace_row* trace,
+                    int64_t cap, int64_t* rows, int* stop_reason);
+
 /* Persistent solver handle for measurement (the same device loop as cpfit_ngmres_solve,
- * split into init + timed loop launches). method 0: N-GMRES, 1: ALS. */
+ * split into init + timed loop launches). method 0: N-GMRES, 1: ALS, 2: N-CG. */
 int cpfit_solver_create(cpfit_tensor t, int64_t rank, const cpfit_ngmres_options* o, int method, cpfit_solver* out);
 int cpfit_solver_set_initial(cpfit_solver s, const double* u0);
 int cpfit_solver_init(cpfit_solver s);

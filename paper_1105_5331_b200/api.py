@@ -4,7 +4,8 @@ Names, argument meaning and error behaviour follow proj/core/include/cpfit/*.hpp
 ``DataTensor`` (tensor.hpp:129-148), ``mttkrp`` (tensor.hpp:119-120), ``gram_hadamard``
 (tensor.hpp:124), ``objective`` / ``objective_and_gradient`` / ``normalize_and_reorder`` /
 ``pack`` / ``unpack`` (kruskal.hpp:29-58), ``als_sweep`` / ``als_solve`` (als.hpp:14,23),
-``accelerate`` / ``ngmres_solve`` (ngmres.hpp:44-127), ``more_thuente`` (line_search.hpp:41).
+``accelerate`` / ``ngmres_solve`` (ngmres.hpp:44-127), ``ncg_solve`` (ncg.hpp:29),
+``more_thuente`` (line_search.hpp:41).
 std::invalid_argument -> ValueError, cpfit::numerical_error -> NumericalError.
 
 All compute goes through libcpfit_gpu.so (sm_100a kernels). There is no CPU fallback: if the
@@ -94,6 +95,9 @@ _SIGS = {
                                      C.POINTER(C.c_int)]),
     "cpfit_als_solve": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_double, C.c_int, _f64p, C.POINTER(C.c_double),
                                   C.POINTER(TraceRow), C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
+    "cpfit_ncg_solve": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_double, C.c_int, C.POINTER(LsParamsC), _f64p,
+                                  C.POINTER(C.c_double), C.POINTER(TraceRow), C.c_int64, C.POINTER(C.c_int64),
+                                  C.POINTER(C.c_int)]),
     "cpfit_solver_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(NgmresOptionsC), C.c_int,
                                       C.POINTER(C.c_void_p)]),
     "cpfit_solver_set_initial": (C.c_int, [C.c_void_p, _f64p]),
@@ -448,6 +452,32 @@ def als_solve(t: DataTensor, u0, tol_grad=1e-9, max_iters=2000) -> SolveResult:
     stop = C.c_int()
     _check(lib.cpfit_als_solve(t._h, r, u0, tol_grad, max_iters, ub, C.byref(fb), trace, cap, C.byref(rows),
                                C.byref(stop)))
+    return SolveResult(ub, fb.value, _trace_list(trace, rows.value), stop.value)
+
+
+@dataclass
+class NcgOptions:
+    """ncg.hpp:14-18"""
+    tol_grad: float = 1e-9
+    max_iters: int = 2000
+    line_search: LineSearchParams = field(default_factory=LineSearchParams)
+
+
+def ncg_solve(t: DataTensor, u0, opts: NcgOptions = None) -> SolveResult:
+    """ncg_solve (ncg.hpp:29, ncg.cpp:111-122): N-CG on the CP objective, device resident.
+    Stalled iterations write no trace row (ncg.cpp:60-67)."""
+    o = opts or NcgOptions()
+    u0, r = t._rank(u0)
+    cap = o.max_iters + 1
+    trace = (TraceRow * cap)()
+    ub = np.empty_like(u0)
+    fb = C.c_double()
+    rows = C.c_int64()
+    stop = C.c_int()
+    ls = o.line_search
+    cp = LsParamsC(ls.ftol, ls.gtol, ls.initial_step, ls.max_evals, ls.step_min, ls.step_max)
+    _check(lib.cpfit_ncg_solve(t._h, r, u0, o.tol_grad, o.max_iters, C.byref(cp), ub, C.byref(fb), trace, cap,
+                               C.byref(rows), C.byref(stop)))
     return SolveResult(ub, fb.value, _trace_list(trace, rows.value), stop.value)
 
 

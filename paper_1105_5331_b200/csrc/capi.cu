@@ -37,7 +37,7 @@ struct cpfit_tensor_s {
     }
     // solvers of the one-shot solve calls, kept between calls (graph capture and instantiation
     // cost milliseconds): one per method, reused while rank and graph-baked options match
-    std::unique_ptr<Solver> solvers[2];
+    std::unique_ptr<Solver> solvers[3];
     Solver& solver(int R, const SolverOptions& o, int method) {
         std::unique_ptr<Solver>& s = solvers[method];
         if (!s || s->rank() != R || !s->options().serves(o)) {
@@ -47,8 +47,7 @@ struct cpfit_tensor_s {
         return *s;
     }
     ~cpfit_tensor_s() {
-        solvers[0].reset();
-        solvers[1].reset();
+        for (auto& sv : solvers) sv.reset();
         for (auto& kv : works) work_destroy(kv.second);
         cudaFree(one_);
         cudaFree(scratch);
@@ -183,7 +182,7 @@ void finish_solve(Solver& sv, double* u_best, double* f_best, cpfit_trace_row* t
                 "als_sweep: normal matrix is singular after regularization (structurally rank-deficient iterate)");
         throw cpfit_gpu::numerical_error("als_sweep: non-finite solution of the normal equations");
     }
-    const int nrows = sm.iters + 1;
+    const int nrows = sm.rows;
     if (rows) *rows = nrows;
     if (trace && cap > 0) {
         std::vector<TraceRow> tr((size_t)nrows);
@@ -435,9 +434,40 @@ int cpfit_als_solve(cpfit_tensor t, int64_t rank, const double* u0, double tol_g
     });
 }
 
+int cpfit_ncg_solve(cpfit_tensor t, int64_t rank, const double* u0, double tol_grad, int max_iters,
+                    const cpfit_line_search_params* ls, double* u_best, double* f_best, cpfit_trace_row* trace,
+                    int64_t cap, int64_t* rows, int* stop_reason) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(t->mu);
+        check_rank(rank);
+        if (!(tol_grad > 0.0)) throw std::invalid_argument("ncg: tol_grad must be > 0");  // ncg.cpp:12
+        cpfit_ngmres_options o;
+        cpfit_default_ngmres_options(&o);
+        o.tol_grad = tol_grad;
+        o.max_iters = max_iters;
+        o.gradient_scale = t->t->norm;  // ncg_solve passes ||T|| (ncg.cpp:119)
+        if (ls) {
+            o.ftol = ls->ftol;
+            o.gtol = ls->gtol;
+            o.initial_step = ls->initial_step;
+            o.max_evals = ls->max_evals;
+            o.step_min = ls->step_min;
+            o.step_max = ls->step_max;
+        }
+        const SolverOptions so = to_opts(&o, t->t->norm);
+        Solver& sv = t->solver((int)rank, so, 2);
+        check_finite(u0, sv.n());
+        sv.set_initial(u0, true);
+        sv.run_init();
+        sv.run_loop(so.max_iters);
+        finish_solve(sv, u_best, f_best, trace, cap, rows, stop_reason);
+    });
+}
+
 int cpfit_solver_create(cpfit_tensor t, int64_t rank, const cpfit_ngmres_options* o, int method, cpfit_solver* out) {
     return guard([&] {
         check_rank(rank);
+        if (method < 0 || method > 2) throw std::invalid_argument("solver: method must be 0 (N-GMRES), 1 (ALS) or 2 (N-CG)");
         SolverOptions so = to_opts(o, t->t->norm);
         if (method == 1) so.gradient_scale = (o->gradient_scale > 0.0) ? o->gradient_scale : t->t->norm;
         auto h = std::make_unique<cpfit_solver_s>();

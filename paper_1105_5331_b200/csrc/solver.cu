@@ -48,6 +48,11 @@ struct DevState {
     // evaluations; counters for the kernel-launch accounting
     int poly;
     long long total_poly, total_poly_acc, total_direct;
+    // N-CG (ncg.cpp:9-110): trace rows written (stalled iterations write none), the clamped
+    // Polak–Ribière coefficient, and whether the accepted step is the line search's last trial
+    int rows;
+    double pr_plus;
+    int last_trial;
     MoreThuente mt;
 };
 
@@ -70,6 +75,7 @@ struct Ctl {
     int restart_on_ascent;
     LsParams ls;
     int als_mode;  // 1: stand-alone ALS trace semantics
+    int ncg;       // 1: N-CG (ncg.cpp) control flow
     int eager;     // 1: host-driven loop (no graph conditionals; profiling / launch lists)
     int poly_ok;   // the polynomial line search applies to this tensor / options
     const dd* coef;
@@ -98,6 +104,9 @@ __global__ void k_reset(Ctl c, int max_iters) {
     s.poly = 0;
     s.total_poly = s.total_poly_acc = s.total_direct = 0;
     s.resid = c.resid_always;
+    s.rows = 1;
+    s.pr_plus = 0.0;
+    s.last_trial = 1;
     s.t0 = globaltimer();
 }
 
@@ -123,7 +132,7 @@ __global__ void k_after_init(Ctl c) {
     c.trace[0] = TraceRow{0, 0, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, c.hscale), gn / c.gradient_scale,
                           0.0, s.fevals, s.gevals, 0};
     if (s.status) s.stop = 100 + s.status;
-    if (c.als_mode && gn / c.gradient_scale <= c.tol_grad) s.stop = 0;  // als.cpp:74-77
+    if ((c.als_mode || c.ncg) && gn / c.gradient_scale <= c.tol_grad) s.stop = 0;  // als.cpp:74-77, ncg.cpp:34-37
     if (2.0 * s.f < 1e-6 * c.hscale * c.hscale) s.resid = 1;
 }
 
@@ -194,7 +203,9 @@ __global__ void k_ls_update(Ctl c, cudaGraphConditionalHandle ls_h) {
         s.gevals += s.mt.evals;
         s.total_ls_evals += s.mt.evals;
         s.stalled = (s.mt.status == LS_STALL) ? 1 : 0;
-        if (!s.status && s.mt.out_step > 0.0 && s.mt.out_f <= s.f_bar) {
+        // N-GMRES keeps a step that does not increase f (ngmres.cpp:131); N-CG needs a strict
+        // decrease (ncg.cpp:60)
+        if (!s.status && s.mt.out_step > 0.0 && (c.ncg ? s.mt.out_f < s.f_bar : s.mt.out_f <= s.f_bar)) {
             s.accepted = 1;
             s.beta = s.mt.out_step;
         }
@@ -383,6 +394,164 @@ __global__ void k_seed_window(const double* u, const double* g, double* wu, doub
     }
 }
 
+
+// ---- N-CG (ncg.cpp:9-110) ------------------------------------------------------------------
+// per-block partial sums of a.b (one double per block in red)
+__global__ void k_dot_part(const double* a, const double* b, double* red, int64_t n) {
+    double v = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v += a[i] * b[i];
+    v = warp_sum(v);
+    __shared__ double ws[8];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) red[blockIdx.x] = v;
+    }
+}
+
+// iteration start (ncg.cpp:44-58): slope = d.g, steepest-descent reset when d is not a descent
+// direction, then the Moré–Thuente start at u (one warp)
+__global__ void k_ncg_begin(Ctl c, const double* red, int nb, cudaGraphConditionalHandle ls_h) {
+    double sl = 0.0;
+    for (int b = threadIdx.x; b < nb; b += 32) sl += red[b];
+    sl = warp_sum(sl);
+    if (threadIdx.x != 0) return;
+    DevState& s = *c.s;
+    s.restart = 0;
+    if (sl >= 0.0) {
+        s.restart = 1;
+        sl = -s.gnorm2;
+    }
+    s.slope = sl;
+    s.f_bar = s.f;
+    s.accepted = 0;
+    s.beta = 0.0;
+    s.searching = s.mt.begin(c.ls, s.f, sl) ? 1 : 0;
+    if (!s.searching) {  // no evaluation (NotDescent): step 0, a stall (ncg.cpp:60)
+        s.stalled = 1;
+    } else {
+        s.total_direct += 1;
+    }
+    set_cond(c, ls_h, s.searching != 0);
+}
+
+__global__ void k_ncg_reset_dir(const DevState* s, const double* g, double* d, int64_t n) {
+    if (!s->restart) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = -g[i];
+}
+
+// partial sums of g_next.(g_next - g) -> red[0, nb) and ||g_next||^2 -> red[512, 512 + nb); g_next
+// is the last trial's gradient when the search converged on it, else the kept best trial's (the
+// reference re-evaluates there, ncg.cpp:72-79: the same point, so the same gradient)
+__global__ void k_ncg_part(const DevState* s, const double* g, const double* gt, const double* gbl, double* red,
+                           int64_t n) {
+    const bool last = s->mt.status == LS_CONVERGED;
+    const double* gn = last ? gt : gbl;
+    double v = 0.0, q = 0.0;
+    if (s->accepted)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+            const double a = gn[i];
+            v += a * (a - g[i]);
+            q += a * a;
+        }
+    v = warp_sum(v);
+    q = warp_sum(q);
+    __shared__ double ws[2][8];
+    if ((threadIdx.x & 31) == 0) {
+        ws[0][threadIdx.x >> 5] = v;
+        ws[1][threadIdx.x >> 5] = q;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const bool in = threadIdx.x < (blockDim.x >> 5);
+        v = warp_sum(in ? ws[0][threadIdx.x] : 0.0);
+        q = warp_sum(in ? ws[1][threadIdx.x] : 0.0);
+        if (threadIdx.x == 0) {
+            red[blockIdx.x] = v;
+            red[512 + blockIdx.x] = q;
+        }
+    }
+}
+
+// scalar end of an N-CG iteration (ncg.cpp:60-108): stall handling, Polak–Ribière+, trace row,
+// best f, stop tests (one warp)
+__global__ void k_ncg_commit(Ctl c, const double* red, int nb, cudaGraphConditionalHandle loop_h) {
+    double v = 0.0, q = 0.0;
+    for (int b = threadIdx.x; b < nb; b += 32) {
+        v += red[b];
+        q += red[512 + b];
+    }
+    v = warp_sum(v);
+    q = warp_sum(q);
+    if (threadIdx.x != 0) return;
+    DevState& s = *c.s;
+    const double f_old = s.f;
+    s.iter += 1;
+    s.is_best = 0;
+    if (s.status) {
+        s.stop = 100 + s.status;
+    } else if (!s.accepted) {
+        // no usable step: retry once from steepest descent, then stop (ncg.cpp:60-67)
+        if (++s.stalls >= 2) s.stop = 2;
+    } else {
+        s.stalls = 0;
+        // the accepted step is not the last trial: the reference re-evaluates it (ncg.cpp:72-79)
+        s.last_trial = (s.mt.stp == s.mt.out_step) ? 1 : 0;
+        if (!s.last_trial) {
+            s.fevals += 1;
+            s.gevals += 1;
+        }
+        const double pr = v / s.gnorm2;
+        s.pr_plus = fmax(0.0, pr);
+        s.f = s.mt.out_f;
+        s.gnorm2 = q;
+        const double gn = sqrt(q);
+        if (s.rows < c.trace_cap)
+            c.trace[s.rows] = TraceRow{s.iter, s.restart, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, c.hscale),
+                                       gn / c.gradient_scale, s.beta, s.fevals, s.gevals, 0};
+        s.rows += 1;
+        s.is_best = (s.f < s.best_f) ? 1 : 0;
+        if (s.is_best) s.best_f = s.f;
+        update_objective_form(c, s, f_old);
+        if (gn / c.gradient_scale <= c.tol_grad) s.stop = 0;
+    }
+    set_cond(c, loop_h, s.stop < 0 && s.iter < s.max_iters);
+}
+
+// vector end: u <- u + beta d, g <- g_next, d <- -g_next + pr+ d (ncg.cpp:71-89); after a stall,
+// d <- -g
+__global__ void k_ncg_vec(const DevState* s, double* u, double* g, double* d, const double* ut, const double* gt,
+                          const double* ubl, const double* gbl, double* ubest, int64_t n) {
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+    if (!s->accepted) {
+        for (int64_t i = i0; i < n; i += step) d[i] = -g[i];
+        return;
+    }
+    const bool last = s->mt.status == LS_CONVERGED;
+    const double* un = last ? ut : ubl;
+    const double* gn = last ? gt : gbl;
+    const double pr = s->pr_plus;
+    const bool best = s->is_best;
+    for (int64_t i = i0; i < n; i += step) {
+        const double a = un[i], b = gn[i];
+        d[i] = -b + pr * d[i];
+        u[i] = a;
+        g[i] = b;
+        if (best) ubest[i] = a;
+    }
+}
+
+__global__ void k_ncg_seed(const double* u, const double* g, double* d, double* ubest, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        d[i] = -g[i];
+        ubest[i] = u[i];
+    }
+}
+
 // phase profiler: time since the previous stamp is charged to `phase`
 __global__ void k_stamp(unsigned long long* ph, int phase) {
     const unsigned long long t = globaltimer();
@@ -559,6 +728,7 @@ void Solver::build_graphs() {
     c.restart_on_ascent = opt_.restart_on_ascent;
     c.ls = LsParams{opt_.ftol, opt_.gtol, opt_.initial_step, opt_.max_evals, opt_.step_min, opt_.step_max};
     c.als_mode = (method_ == 1);
+    c.ncg = (method_ == 2);
     c.poly_ok = pw_ ? 1 : 0;
     c.coef = pw_ ? pw_->coef : nullptr;
     static_assert(sizeof(Ctl) <= sizeof(ctl_blob_), "ctl blob");
@@ -581,6 +751,8 @@ void Solver::build_graphs() {
     k_after_init<<<1, 1, 0, st_>>>(c);
     if (method_ == 0)
         k_seed_window<<<vb, 256, 0, st_>>>(u_, g_, wu_, wg_, ubest_, n_);
+    else if (method_ == 2)
+        k_ncg_seed<<<vb, 256, 0, st_>>>(u_, g_, d_, ubest_, n_);
     else
         k_seed_window<<<vb, 256, 0, st_>>>(u_, g_, ut_, gt_, ubest_, n_);
     CPFIT_CUDA(cudaGetLastError());
@@ -669,15 +841,36 @@ void Solver::build_graphs() {
         CPFIT_CUDA(cudaStreamEndCapture(st4_, &ab));
         CPFIT_CUDA(cudaGetLastError());
         CPFIT_CUDA(cudaStreamEndCapture(st3_, &db));
+    } else if (method_ == 2) {
+        // N-CG iteration (ncg.cpp:42-108): slope / reset, Moré–Thuente on trial evaluations at
+        // u + stp d, Polak–Ribière+ direction update
+        k_dot_part<<<norm_nb_, 256, 0, st2_>>>(d_, g_, red_, n_);
+        const cudaGraphConditionalHandle ls_h = make_handle(st2_);
+        k_ncg_begin<<<1, 32, 0, st2_>>>(c, red_, norm_nb_, ls_h);
+        k_ncg_reset_dir<<<vb, 256, 0, st2_>>>(s, g_, d_, n_);
+        stamp(st2_, 2);
+        lsb = append_conditional(st2_, ls_h, cudaGraphCondTypeWhile);
+        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        k_trial<<<vb, 256, 0, st3_>>>(s, u_, d_, ut_, n_);
+        eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st3_, true, &s->resid);
+        stamp(st3_, 3);
+        k_ls_update<<<1, 1, 0, st3_>>>(c, ls_h);
+        k_keep_best<<<vb, 256, 0, st3_>>>(s, ut_, gt_, ubl_, gbl_, n_, nullptr, nullptr, 0);
+        stamp(st3_, 4);
+        CPFIT_CUDA(cudaGetLastError());
+        CPFIT_CUDA(cudaStreamEndCapture(st3_, &lsb));
+        emit_ncg_end(st2_, &c, loop_h);
     } else {
         // stand-alone ALS iteration (als.cpp:79-95)
         // the previous evaluation (of u) left M0(u) in w.m0 for dense tensors
         als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, t_->sparse ? nullptr : w_->m0, true, gout_);
         eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid, !t_->sparse, gout_);
     }
-    k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
-    k_commit_vec<<<vb, 256, 0, st2_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,
-                                        m0_cur_, m0_n_, gram_bar_, w_->gram, gout_ ? gram_n() : 0);
+    if (method_ != 2) {
+        k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
+        k_commit_vec<<<vb, 256, 0, st2_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,
+                                            m0_cur_, m0_n_, gram_bar_, w_->gram, gout_ ? gram_n() : 0);
+    }
     stamp(st2_, 6);
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaStreamEndCapture(st2_, &body));
@@ -691,6 +884,17 @@ void Solver::build_graphs() {
     n_direct_ = db ? count_kernels(db) : 0;
     n_accp_ = apb ? count_kernels(apb) : 0;
     CPFIT_CUDA(cudaGraphInstantiate(&x_loop_, g_loop_, 0));
+}
+
+// end of an N-CG iteration: Polak–Ribière+ partials, the scalar commit, the vector update
+void Solver::emit_ncg_end(cudaStream_t st, const void* ctl, unsigned long long loop_h) {
+    const Ctl& c = *reinterpret_cast<const Ctl*>(ctl);
+    DevState* s = c.s;
+    const int vb = vec_blocks(n_);
+    k_ncg_part<<<norm_nb_, 256, 0, st>>>(s, g_, gt_, gbl_, red_, n_);
+    k_ncg_commit<<<1, 32, 0, st>>>(c, red_, norm_nb_, (cudaGraphConditionalHandle)loop_h);
+    k_ncg_vec<<<vb, 256, 0, st>>>(s, u_, g_, d_, ut_, gt_, ubl_, gbl_, ubest_, n_);
+    CPFIT_CUDA(cudaGetLastError());
 }
 
 // Step I (ngmres.cpp:90-94): u_bar = M(u) (canonical), g_bar = g(u_bar). Deferred form (dense):
@@ -826,6 +1030,18 @@ void Solver::run_loop_eager() {
                     k_after_rescale<<<1, 32, 0, st_>>>(c, sc_next, red_, nb);
                 }
             }
+        } else if (method_ == 2) {
+            k_dot_part<<<norm_nb_, 256, 0, st_>>>(d_, g_, red_, n_);
+            k_ncg_begin<<<1, 32, 0, st_>>>(c, red_, norm_nb_, none);
+            k_ncg_reset_dir<<<vb, 256, 0, st_>>>(s, g_, d_, n_);
+            while (state().searching) {
+                k_trial<<<vb, 256, 0, st_>>>(s, u_, d_, ut_, n_);
+                eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st_, true, &s->resid);
+                k_ls_update<<<1, 1, 0, st_>>>(c, none);
+                k_keep_best<<<vb, 256, 0, st_>>>(s, ut_, gt_, ubl_, gbl_, n_, nullptr, nullptr, 0);
+            }
+            emit_ncg_end(st_, &c, none);
+            continue;
         } else {
             als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, t_->sparse ? nullptr : w_->m0, true, gout_);
             eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid, !t_->sparse, gout_);
@@ -863,6 +1079,7 @@ SolverSummary Solver::summary() {
     r.status = hs.status;
     r.fevals = hs.fevals;
     r.gevals = hs.gevals;
+    r.rows = (method_ == 2) ? hs.rows : hs.iter + 1;
     r.launches = launches_done_ + loop_launches_ * n_prelude_ + init_launches_ * n_init_ +
                  (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + (hs.total_accepted - hs.total_poly_acc) * n_acc_ +
                  hs.total_poly * n_poly_ + hs.total_poly_acc * n_accp_ + hs.total_direct * n_direct_;
@@ -875,7 +1092,13 @@ void Solver::copy_trace(TraceRow* out, int rows) {
 }
 
 void Solver::copy_best(double* out, bool host) {
-    CPFIT_CUDA(cudaMemcpyAsync(out, ubest_, sizeof(double) * n_, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+    const double* src = ubest_;
+    if (method_ == 2) {  // N-CG does not renormalise between iterations; its result is (ncg.cpp:122)
+        grams_device(*w_, ubest_, st_);
+        normalize_device(*w_, ubest_, work_, st_);
+        src = work_;
+    }
+    CPFIT_CUDA(cudaMemcpyAsync(out, src, sizeof(double) * n_, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
                                st_));
 }
 

@@ -48,11 +48,12 @@ struct SolverSummary {
     double f, best_f;
     long long fevals, gevals;
     long long launches;  // kernels launched by the loop graphs since init
+    int rows;            // trace rows written (N-CG writes none for stalled iterations)
 };
 
 class Solver {
 public:
-    // method 0: ALS-preconditioned N-GMRES, 1: stand-alone ALS
+    // method 0: ALS-preconditioned N-GMRES, 1: stand-alone ALS, 2: N-CG (ncg.cpp)
     Solver(DevTensor* t, int R, const SolverOptions& o, int method);
     ~Solver();
     void set_initial(const double* u0, bool host);
@@ -78,6 +79,7 @@ private:
     void run_loop_eager();
     void emit_poly_accept(cudaStream_t st, const void* ctl);
     void emit_bar(cudaStream_t st, const void* ctl);
+    void emit_ncg_end(cudaStream_t st, const void* ctl, unsigned long long loop_h);
     PolyWork* pw_ = nullptr;  // exact line search (poly.cu), when it applies
     bool gout_ = false;       // normalisations hand on their output's Grams
     bool defer_ = false;      // eval at the sweep's own point, then normalise (no S rescale)
