@@ -282,16 +282,34 @@ def main():
             b = 8.0 * k_elems + 8.0 * R * sum(dims)
             kern[f"mttkrp_mode{mode}"] = {"ms": round(mms, 5), "GB/s": round(b / (mms * 1e-3) / 1e9, 1),
                                           "hbm_frac": round(b / (mms * 1e-3) / 1e9 / hbm_peak, 4)}
-        for kind, name in ((7, "objective_and_gradient_perfiber_f"), (1, "objective_and_gradient_residual_f")):
+        # the fused gradient reads T once but contracts it twice (S = T x1 A0 and M0 = T_(0) KR):
+        # 4KR flops (+2KR for the residual form) on the fp64 tensor pipe take longer than the
+        # 8K bytes take on HBM at R = 16, so it is bounded by the DMMA peak, not by HBM
+        for kind, name, fl in ((7, "objective_and_gradient_perfiber_f", 4.0),
+                               (1, "objective_and_gradient_residual_f", 6.0)):
             gms = P.bench_kernel(t, u0, kind=kind, reps=10, flush_l2=True)
             b = 8.0 * k_elems + 8.0 * R * 2 * sum(dims)
+            flops = fl * k_elems * R
+            tf = flops / (gms * 1e-3) / 1e12
             kern[name] = {"ms": round(gms, 5), "GB/s": round(b / (gms * 1e-3) / 1e9, 1),
-                          "hbm_frac": round(b / (gms * 1e-3) / 1e9 / hbm_peak, 4)}
+                          "hbm_frac": round(b / (gms * 1e-3) / 1e9 / hbm_peak, 4),
+                          "bound": "fp64 tensor" if flops / (dmma_peak * 1e12) > b / (hbm_peak * 1e9) else "hbm",
+                          "TFLOP/s": round(tf, 3), "dmma_frac": round(tf / dmma_peak, 4),
+                          "floor_ms": round(max(flops / (dmma_peak * 1e12), b / (hbm_peak * 1e9)) * 1e3, 5)}
         for kind, name in ((4, "fiber_m0_pass_plus_reduce"), (5, "fiber_s_only")):
             fm = P.bench_kernel(t, u0, kind=kind, reps=10, flush_l2=False)
             kern[name] = {"ms": round(fm, 5), "GB/s": round(8.0 * k_elems / (fm * 1e-3) / 1e9, 1),
                           "hbm_frac": round(8.0 * k_elems / (fm * 1e-3) / 1e9 / hbm_peak, 4)}
         extras["kernels"] = kern
+        # N-CG (ncg.cpp) through the same device loop machinery: 100 iterations from the first
+        # start (restart() includes the init's canonicalisation + evaluation)
+        ncg = P.Solver(t, R, P.NgmresOptions(max_iters=400, tol_grad=tol, gradient_scale=float(nu)), method=2)
+        ncg.restart(u0, 20)
+        n_ms = ncg.restart(u0, 100)
+        nst = ncg.state()
+        extras["ncg"] = {"iters/s": round(nst["iters"] / (n_ms * 1e-3), 1), "iters": nst["iters"],
+                         "fevals": nst["fevals"], "ms": round(n_ms, 3),
+                         "note": "device N-CG (Polak-Ribiere+, More-Thuente on trial evaluations), init included"}
 
     # end to end through the public C-ABI from pinned host buffers: tensor upload + solves
     T_pin = np.ascontiguousarray(T)

@@ -1147,6 +1147,54 @@ __global__ void gather_m_kernel(int64_t In, int R, int RP, const double* part, i
 }
 }  // namespace
 
+namespace {
+// Order-3 MTTKRP of the last mode from S = T x_1 A0 ([J][RP] row-major, fibre f = j + I1 k):
+//   M2[k][r] = sum_j S[j + I1 k][r] A1[j][r]: one CTA per k (its slab of S is contiguous), the
+//     256 / RP j-lanes of each r combined in order, written straight to the col-major output
+//     (one kernel instead of the bulk level kernel + gather; mode 1 keeps the level kernel,
+//     whose bulk copies hide the S latency better than a second kernel of this form did)
+template <int RP>
+__global__ void __launch_bounds__(256) mttkrp3_last_kernel(const double* __restrict__ S, const double* __restrict__ A1,
+                                                           int64_t I1, int64_t I2, int R, double* out) {
+    constexpr int JL = 256 / RP;
+    __shared__ double red[256];
+    const int tid = threadIdx.x, r = tid % RP, jl = tid / RP;
+    const int64_t k = blockIdx.x;
+    const double* Sk = S + k * I1 * RP;
+    const double* a = A1 + (int64_t)(r < R ? r : 0) * I1;
+    // batches of 8 independent loads (latency bound: S is 20 MB at 400^3)
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int64_t j0 = jl; j0 < I1; j0 += 8 * JL) {
+        double x[8], y[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t j = j0 + q * JL;
+            x[q] = j < I1 ? Sk[j * RP + r] : 0.0;
+            y[q] = j < I1 ? __ldg(a + j) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+            acc0 = fma(x[q], y[q], acc0);
+            acc1 = fma(x[q + 1], y[q + 1], acc1);
+        }
+    }
+    red[tid] = acc0 + acc1;
+    __syncthreads();
+    if (tid < R) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < JL; ++q) v += red[q * RP + tid];
+        out[(int64_t)tid * I2 + k] = v;
+    }
+}
+
+template <int RP>
+void launch_mttkrp3_last(const EvalWork& w, const double* u, double* out, cudaStream_t st) {
+    mttkrp3_last_kernel<RP><<<(unsigned)w.dims[2], 256, 0, st>>>(w.S, u + w.off[1], w.dims[1], w.dims[2], w.R, out);
+    CPFIT_CUDA(cudaGetLastError());
+}
+}  // namespace
+
 void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st) {
     const int64_t In = t.dims[mode];
     const int blocks = (int)std::min<int64_t>(1024, (In * w.R + 255) / 256);
@@ -1164,16 +1212,37 @@ void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, d
         gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, w.m0, 1, 32 * w.fiber_nchunk, 0, out);
     } else {
         run_fiber(t, w, u, true, false, false, nullptr, st);
+        if (t.order == 3 && mode == 2) {
+            switch (w.RP) {
+                case 8: launch_mttkrp3_last<8>(w, u, out, st); break;
+                case 16: launch_mttkrp3_last<16>(w, u, out, st); break;
+                default: launch_mttkrp3_last<32>(w, u, out, st); break;
+            }
+            return;
+        }
         const double* Sin = w.S;
+        // the level that produces M_mode leaves its per-CTA partials to the gather (one launch
+        // fewer): M_h partials [slab range][i][r] at h = mode < N-1, the last level's Sout
+        // partials [pair tile][slab][r] for mode N-1
+        RedJobs skip;
+        const double* part = w.S;  // order 2: M_1 = S
+        int nparts = 1;
         for (int h = 1; h <= mode && h < t.order - 1; ++h) {
             const bool last = (h == mode);
-            run_level(t, w, h, Sin, u, last, !last, w.lvl_S[h], st);
+            const bool final = last || h == t.order - 2;
+            run_level(t, w, h, Sin, u, last, !last, w.lvl_S[h], st, final ? &skip : nullptr, final ? &skip : nullptr);
             Sin = w.lvl_S[h];
+            if (final) {
+                if (last) {
+                    part = w.lvl_part[h];
+                    nparts = w.lvl_nx[h];
+                } else {
+                    part = w.lvl_ny[h] > 1 ? w.lvl_spart[h] : w.lvl_S[h];
+                    nparts = w.lvl_ny[h];
+                }
+            }
         }
-        if (mode == t.order - 1)
-            gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, Sin, 1, 0, 1, out);
-        else
-            gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, w.lvl_m[mode], 1, 0, 1, out);
+        gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, part, nparts, 0, 1, out);
     }
     CPFIT_CUDA(cudaGetLastError());
 }

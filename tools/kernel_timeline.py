@@ -17,11 +17,12 @@ T = rng.random(int(np.prod(dims)))
 u = rng.random(sum(dims) * R)
 t = P.DataTensor.dense(T, dims)
 kinds = [int(k) for k in os.environ.get("KINDS", "2,7").split(",")]
+mode = int(os.environ.get("MODE", "0"))
 torch.cuda.init()
 for kind in kinds:
-    P.bench_kernel(t, u, kind=kind, mode=0, reps=2, flush_l2=False)
+    P.bench_kernel(t, u, kind=kind, mode=mode, reps=2, flush_l2=False)
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        P.bench_kernel(t, u, kind=kind, mode=0, reps=3, flush_l2=False)
+        P.bench_kernel(t, u, kind=kind, mode=mode, reps=3, flush_l2=False)
     ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     ev.sort(key=lambda e: e.time_range.start)
     # bench_kernel runs 3 warm-up calls + reps (3) calls: the last call is the last sixth
