@@ -662,6 +662,7 @@ int cpfit_bench_kernel(cpfit_tensor t, int64_t rank, const double* u, int kind, 
                 case 6: dense_fiber_fused(*t->t, w, du, t->st, t->one()); break;  // S + M0 + residual f
                 case 4: dense_fiber(*t->t, w, du, false, true, t->st); break;   // M0 only
                 case 5: dense_fiber(*t->t, w, du, true, false, t->st); break;   // S only
+                case 8: mttkrp3_last_only(w, du, dout, t->st); break;           // last-mode contraction of S
                 default: throw std::invalid_argument("bench kind");
             }
         };

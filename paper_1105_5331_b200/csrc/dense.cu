@@ -1153,47 +1153,85 @@ namespace {
 //     256 / RP j-lanes of each r combined in order, written straight to the col-major output
 //     (one kernel instead of the bulk level kernel + gather; mode 1 keeps the level kernel,
 //     whose bulk copies hide the S latency better than a second kernel of this form did)
+constexpr int kM3Threads = 512, kM3Batch = 16;
+// A1 is staged in shared memory as [j][RP + 1] from a coalesced read of the col-major factor: a
+// direct load of A1[j][r] by lane (r, j) touches RP separate 128-byte lines per instruction and
+// the L1 wavefronts, not the bytes, then bound the kernel
 template <int RP>
-__global__ void __launch_bounds__(256) mttkrp3_last_kernel(const double* __restrict__ S, const double* __restrict__ A1,
-                                                           int64_t I1, int64_t I2, int R, double* out) {
-    constexpr int JL = 256 / RP;
-    __shared__ double red[256];
+__global__ void __launch_bounds__(kM3Threads) mttkrp3_last_kernel(const double* __restrict__ S,
+                                                                  const double* __restrict__ A1, int I1, int I2, int R,
+                                                                  double* out) {
+    constexpr int JL = kM3Threads / RP, LD = RP + 1;
+    extern __shared__ double a_s[];
+    __shared__ double red[kM3Threads];
     const int tid = threadIdx.x, r = tid % RP, jl = tid / RP;
-    const int64_t k = blockIdx.x;
-    const double* Sk = S + k * I1 * RP;
-    const double* a = A1 + (int64_t)(r < R ? r : 0) * I1;
-    // batches of 8 independent loads (latency bound: S is 20 MB at 400^3)
+    const int k = blockIdx.x;
+    const double* Sk = S + (int64_t)k * I1 * RP;
+    // the slab's first batch of S loads goes out before the staging
+    double x[kM3Batch];
+#pragma unroll
+    for (int q = 0; q < kM3Batch; ++q) {
+        const int j = jl + q * JL;
+        x[q] = j < I1 ? Sk[j * RP + r] : 0.0;
+    }
+    for (int e = tid; e < I1 * RP; e += kM3Threads) {
+        const int rr = e / I1, j = e - rr * I1;
+        a_s[j * LD + rr] = rr < R ? A1[e] : 0.0;
+    }
+    __syncthreads();
     double acc0 = 0.0, acc1 = 0.0;
-    for (int64_t j0 = jl; j0 < I1; j0 += 8 * JL) {
-        double x[8], y[8];
+    for (int j0 = jl;;) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int64_t j = j0 + q * JL;
-            x[q] = j < I1 ? Sk[j * RP + r] : 0.0;
-            y[q] = j < I1 ? __ldg(a + j) : 0.0;
+        for (int q = 0; q < kM3Batch; q += 2) {
+            const int j = j0 + q * JL;
+            if (j < I1) acc0 = fma(x[q], a_s[j * LD + r], acc0);
+            if (j + JL < I1) acc1 = fma(x[q + 1], a_s[(j + JL) * LD + r], acc1);
         }
+        j0 += kM3Batch * JL;
+        if (j0 >= I1) break;
 #pragma unroll
-        for (int q = 0; q < 8; q += 2) {
-            acc0 = fma(x[q], y[q], acc0);
-            acc1 = fma(x[q + 1], y[q + 1], acc1);
+        for (int q = 0; q < kM3Batch; ++q) {
+            const int j = j0 + q * JL;
+            x[q] = j < I1 ? Sk[j * RP + r] : 0.0;
         }
     }
     red[tid] = acc0 + acc1;
     __syncthreads();
     if (tid < R) {
         double v = 0.0;
-#pragma unroll
+#pragma unroll 8
         for (int q = 0; q < JL; ++q) v += red[q * RP + tid];
         out[(int64_t)tid * I2 + k] = v;
     }
 }
 
+// the kernel's A1 copy fits shared memory (and the slab index math 32 bits)
+inline bool mttkrp3_fits(int64_t I1, int64_t I2, int RP) {
+    return (size_t)I1 * (RP + 1) * sizeof(double) <= 160 * 1024 && I1 * I2 * RP < (int64_t)1 << 31;
+}
+
 template <int RP>
 void launch_mttkrp3_last(const EvalWork& w, const double* u, double* out, cudaStream_t st) {
-    mttkrp3_last_kernel<RP><<<(unsigned)w.dims[2], 256, 0, st>>>(w.S, u + w.off[1], w.dims[1], w.dims[2], w.R, out);
+    static bool attr = [] {
+        cudaFuncSetAttribute(mttkrp3_last_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        return true;
+    }();
+    (void)attr;
+    const size_t smem = sizeof(double) * (size_t)w.dims[1] * (RP + 1);
+    mttkrp3_last_kernel<RP><<<(unsigned)w.dims[2], kM3Threads, smem, st>>>(w.S, u + w.off[1], (int)w.dims[1],
+                                                                           (int)w.dims[2], w.R, out);
     CPFIT_CUDA(cudaGetLastError());
 }
 }  // namespace
+
+// measurement hook: the last-mode contraction alone, from the S left by the previous pass
+void mttkrp3_last_only(EvalWork& w, const double* u, double* out, cudaStream_t st) {
+    switch (w.RP) {
+        case 8: launch_mttkrp3_last<8>(w, u, out, st); break;
+        case 16: launch_mttkrp3_last<16>(w, u, out, st); break;
+        default: launch_mttkrp3_last<32>(w, u, out, st); break;
+    }
+}
 
 void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st) {
     const int64_t In = t.dims[mode];
@@ -1212,7 +1250,7 @@ void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, d
         gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, w.m0, 1, 32 * w.fiber_nchunk, 0, out);
     } else {
         run_fiber(t, w, u, true, false, false, nullptr, st);
-        if (t.order == 3 && mode == 2) {
+        if (t.order == 3 && mode == 2 && mttkrp3_fits(t.dims[1], t.dims[2], w.RP)) {
             switch (w.RP) {
                 case 8: launch_mttkrp3_last<8>(w, u, out, st); break;
                 case 16: launch_mttkrp3_last<16>(w, u, out, st); break;

@@ -120,6 +120,7 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
                  bool s_given = false, bool grams_given = false, cudaEvent_t grad_dep = nullptr);
 
 // mttkrp(T, factors(u), mode) (tensor.cpp:206-259) -> out (I_mode x R col-major).
+void mttkrp3_last_only(EvalWork& w, const double* u, double* out, cudaStream_t st);
 void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st);
 
 // Grams G_n = A_n^T A_n for all modes (double-double accumulation) -> w.gram.

@@ -14,7 +14,7 @@ T = rng.random(int(np.prod(dims)))
 u = rng.random(sum(dims) * R)
 t = P.DataTensor.dense(T, dims)
 reps = int(os.environ.get("REPS", "3"))
-names = {2: "als_sweep", 3: "fused", 4: "m0", 5: "s", 0: "mttkrp0", 1: "eval_resid", 6: "fused_resid", 7: "eval_perfiber"}
+names = {8: "mttkrp3_last_only", 2: "als_sweep", 3: "fused", 4: "m0", 5: "s", 0: "mttkrp0", 1: "eval_resid", 6: "fused_resid", 7: "eval_perfiber"}
 kinds = [int(k) for k in os.environ.get("KINDS", "3,4,5,6,0,7,1").split(",")]
 for kind in kinds:
     ms = P.bench_kernel(t, u, kind=kind, mode=0, reps=reps, flush_l2=False)
