@@ -123,6 +123,15 @@ int cpfit_ncg_solve(cpfit_tensor t, int64_t rank, const double* u0, double tol_g
                     const cpfit_line_search_params* ls, double* u_best, double* f_best, cpfit_trace_row* trace,
                     int64_t cap, int64_t* rows, int* stop_reason);
 
+/* Batched solves (bench.cpp:80-158 runs seeds on a thread pool): nsolves independent solves of
+ * the same tensor from the starts u0s (nsolves x n, pack layout), `concurrency` of them in
+ * flight at once (<= 0: 16), each on its own stream and workspace. method 0 N-GMRES, 1 ALS,
+ * 2 N-CG (gradient_scale <= 0 means ||T|| as in the single-solve calls). Per solve: best
+ * iterate (u_best, may be NULL), best f, iterations, stop reason, f evaluations. */
+int cpfit_solve_batch(cpfit_tensor t, int64_t rank, int method, int64_t nsolves, const double* u0s,
+                      const cpfit_ngmres_options* o, int concurrency, double* u_best, double* f_best, int* iters,
+                      int* stop_reason, int64_t* fevals);
+
 /* Persistent solver handle for measurement (the same device loop as cpfit_ngmres_solve,
  * split into init + timed loop launches). method 0: N-GMRES, 1: ALS, 2: N-CG. */
 int cpfit_solver_create(cpfit_tensor t, int64_t rank, const cpfit_ngmres_options* o, int method, cpfit_solver* out);

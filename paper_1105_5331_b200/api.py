@@ -98,6 +98,8 @@ _SIGS = {
     "cpfit_ncg_solve": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_double, C.c_int, C.POINTER(LsParamsC), _f64p,
                                   C.POINTER(C.c_double), C.POINTER(TraceRow), C.c_int64, C.POINTER(C.c_int64),
                                   C.POINTER(C.c_int)]),
+    "cpfit_solve_batch": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int64, _f64p, C.POINTER(NgmresOptionsC), C.c_int,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cpfit_solver_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(NgmresOptionsC), C.c_int,
                                       C.POINTER(C.c_void_p)]),
     "cpfit_solver_set_initial": (C.c_int, [C.c_void_p, _f64p]),
@@ -479,6 +481,33 @@ def ncg_solve(t: DataTensor, u0, opts: NcgOptions = None) -> SolveResult:
     _check(lib.cpfit_ncg_solve(t._h, r, u0, o.tol_grad, o.max_iters, C.byref(cp), ub, C.byref(fb), trace, cap,
                                C.byref(rows), C.byref(stop)))
     return SolveResult(ub, fb.value, _trace_list(trace, rows.value), stop.value)
+
+
+@dataclass
+class BatchResult:
+    solutions: np.ndarray  # nsolves x n best iterates
+    f: np.ndarray
+    iters: np.ndarray
+    stop_reason: np.ndarray
+    fevals: np.ndarray
+
+
+def solve_batch(t: DataTensor, u0s, opts: NgmresOptions = None, method: int = 0, concurrency: int = 16) -> BatchResult:
+    """Independent solves of t from each row of u0s, `concurrency` at a time on their own streams
+    (the reference's seed sweeps, bench.cpp:80-158). method 0 N-GMRES, 1 ALS, 2 N-CG."""
+    o = opts or NgmresOptions()
+    u0s = np.ascontiguousarray(np.atleast_2d(np.asarray(u0s, dtype=np.float64)))
+    ns, n = u0s.shape
+    _, r = t._rank(u0s[0])
+    ub = np.empty((ns, n))
+    fb = np.empty(ns)
+    it = np.empty(ns, dtype=np.int32)
+    st = np.empty(ns, dtype=np.int32)
+    fe = np.empty(ns, dtype=np.int64)
+    oc = o.c()
+    _check(lib.cpfit_solve_batch(t._h, r, method, ns, u0s.reshape(-1), C.byref(oc), concurrency,
+                                 ub.ctypes.data, fb.ctypes.data, it.ctypes.data, st.ctypes.data, fe.ctypes.data))
+    return BatchResult(ub, fb, it, st, fe)
 
 
 class Solver:

@@ -46,7 +46,21 @@ struct cpfit_tensor_s {
         }
         return *s;
     }
+    // concurrent solvers of the batched solve calls (own streams and workspaces each), kept
+    // while rank, method and graph-baked options match
+    std::vector<std::unique_ptr<Solver>> pool;
+    int pool_method = -1;
+    std::vector<Solver*> batch(int R, const SolverOptions& o, int method, int n) {
+        if (!pool.empty() && (pool_method != method || pool[0]->rank() != R || !pool[0]->options().serves(o)))
+            pool.clear();
+        pool_method = method;
+        while ((int)pool.size() < n) pool.push_back(std::make_unique<Solver>(t, R, o, method));
+        std::vector<Solver*> v;
+        for (int k = 0; k < n; ++k) v.push_back(pool[(size_t)k].get());
+        return v;
+    }
     ~cpfit_tensor_s() {
+        pool.clear();
         for (auto& sv : solvers) sv.reset();
         for (auto& kv : works) work_destroy(kv.second);
         cudaFree(one_);
@@ -461,6 +475,46 @@ int cpfit_ncg_solve(cpfit_tensor t, int64_t rank, const double* u0, double tol_g
         sv.run_init();
         sv.run_loop(so.max_iters);
         finish_solve(sv, u_best, f_best, trace, cap, rows, stop_reason);
+    });
+}
+
+int cpfit_solve_batch(cpfit_tensor t, int64_t rank, int method, int64_t nsolves, const double* u0s,
+                      const cpfit_ngmres_options* o, int concurrency, double* u_best, double* f_best, int* iters,
+                      int* stop_reason, int64_t* fevals) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(t->mu);
+        check_rank(rank);
+        if (method < 0 || method > 2) throw std::invalid_argument("solve_batch: method must be 0, 1 or 2");
+        if (nsolves < 0) throw std::invalid_argument("solve_batch: nsolves must be >= 0");
+        if (nsolves == 0) return;
+        SolverOptions so = to_opts(o, t->t->norm);
+        if (method == 2 && !(o->gradient_scale > 0.0)) so.gradient_scale = t->t->norm;
+        const int conc = (int)std::max<int64_t>(1, std::min<int64_t>(nsolves, concurrency > 0 ? concurrency : 16));
+        std::vector<Solver*> sv = t->batch((int)rank, so, method, conc);
+        const int64_t n = sv[0]->n();
+        check_finite(u0s, n * nsolves);
+        // waves of `conc` solves: every solver's init + loop graphs are queued on its own stream
+        // before any result is read back, so the solves of a wave run concurrently
+        for (int64_t w0 = 0; w0 < nsolves; w0 += conc) {
+            const int64_t w1 = std::min<int64_t>(nsolves, w0 + conc);
+            for (int64_t i = w0; i < w1; ++i) {
+                Solver& s = *sv[(size_t)(i - w0)];
+                s.set_initial(u0s + i * n, true);
+                s.run_init();
+                s.run_loop(so.max_iters);
+            }
+            for (int64_t i = w0; i < w1; ++i) {
+                Solver& s = *sv[(size_t)(i - w0)];
+                const SolverSummary sm = s.summary();
+                if (sm.status) throw cpfit_gpu::numerical_error("solve_batch: numerical failure in the ALS normal equations");
+                if (u_best) s.copy_best(u_best + i * n, true);
+                if (f_best) f_best[i] = sm.best_f;
+                if (iters) iters[i] = sm.iters;
+                if (stop_reason) stop_reason[i] = (sm.stop < 0) ? 1 : sm.stop;
+                if (fevals) fevals[i] = sm.fevals;
+            }
+            for (Solver* s : sv) s->sync();
+        }
     });
 }
 

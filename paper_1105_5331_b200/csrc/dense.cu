@@ -61,6 +61,7 @@ struct FiberParams {
     int64_t ntiles;
     unsigned long long* prof;  // diagnostic build only (fiber.cuh FIBER_WAIT)
     const double* S_in;        // S given (M0 + per-fiber objective pass): J x RP
+    int nst;                   // T ring stages (EvalWork::fiber_nst: kFStages or kDeepFStages)
 };
 
 #include "fiber.cuh"
@@ -124,6 +125,7 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
     p.J = t.J;
     p.nchunk = w.fiber_nchunk;
     p.I0s = 32 * w.fiber_nchunk + 4;
+    p.nst = w.fiber_nst;
     fiber_schedule(w.RP, p.I0, do_s, p);
 #ifdef CPFIT_FIBER_PROF
     p.prof = fiber_prof_buffer();
@@ -934,12 +936,20 @@ EvalWork* work_create(const DevTensor& t, int R) {
         const int I0 = (int)t.dims[0];
         w->fiber_nchunk = (I0 + 31) / 32;
         if (w->fiber_nchunk > 13) throw std::invalid_argument("device dense path supports I_1 <= 416");
-        w->fiber_smem = fiber_smem(w->RP, w->fiber_nchunk, I0);
-        if (std::max(w->fiber_smem, spass_smem(w->RP, w->fiber_nchunk, I0)) > 227 * 1024)
+        // short fibres: a deep T ring (a 16-fibre tile of I0 <= 128 is <= 17 KB; three of them do
+        // not cover the HBM latency at one CTA per SM)
+        w->fiber_nst = kFStages;
+        if (w->fiber_nchunk <= 4 &&
+            std::max(fiber_smem(w->RP, w->fiber_nchunk, I0, kDeepFStages),
+                     spass_smem(w->RP, w->fiber_nchunk, I0, kDeepFStages)) <= 220 * 1024)
+            w->fiber_nst = kDeepFStages;
+        w->fiber_smem = fiber_smem(w->RP, w->fiber_nchunk, I0, w->fiber_nst);
+        if (std::max(w->fiber_smem, spass_smem(w->RP, w->fiber_nchunk, I0, w->fiber_nst)) > 227 * 1024)
             throw std::invalid_argument("fiber tile does not fit shared memory");
         const int64_t ntiles = (t.J + w->fiber_F - 1) / w->fiber_F;
-        const int per_sm = std::max(1, std::min(2048 / fiber_threads(w->RP),
-                                                (int)((228 * 1024) / (w->fiber_smem + 1024))));
+        // resident CTAs per SM: threads, shared memory and registers (128 per thread)
+        const int per_sm = std::max(1, std::min({2048 / fiber_threads(w->RP), 65536 / (128 * fiber_threads(w->RP)),
+                                                 (int)((228 * 1024) / (w->fiber_smem + 1024))}));
         w->fiber_grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
         // order 3: room for the line search's S_d right after S
         const size_t sn = (size_t)t.J * w->RP;

@@ -58,7 +58,7 @@ struct EvalWork {
     int64_t dims[kMaxOrder] = {};
     int64_t off[kMaxOrder + 1] = {};  // packed offsets (R * prefix sum)
     // dense fiber pass
-    int fiber_grid = 0, fiber_F = 16, fiber_nchunk = 0;
+    int fiber_grid = 0, fiber_F = 16, fiber_nchunk = 0, fiber_nst = 3;
     size_t fiber_smem = 0;
     double* S = nullptr;        // J x RP
     double* S2 = nullptr;       // (dense order 3) a second J x RP right after S: the line search's S_d

@@ -1,7 +1,7 @@
 // Warp-specialized fiber pass (included by dense.cu inside cpfit_gpu::(anonymous)).
 //
 // One CTA per SM streams a contiguous range of F = 16-fiber tiles of T (mode-0 fibers, padded
-// to ldT doubles) through a kFStages-deep shared-memory ring. Roles:
+// to ldT doubles) through a kFStages-deep (short fibres: kDeepFStages) shared-memory ring. Roles:
 //   T producer (warp 0)    one bulk async copy per fiber into the ring, issued by 16 lanes at
 //                          once (mbarrier complete_tx);
 //   W producers (warps 1-2) the W tile — Khatri-Rao rows of modes >= 1, never materialised in
@@ -25,7 +25,8 @@
 // fragment load is conflict free (two wavefronts per 32 doubles).
 #pragma once
 
-constexpr int kFStages = 3;
+constexpr int kFStages = 3;      // T ring depth for long fibres (a tile is ~54 KB at I0 = 400)
+constexpr int kDeepFStages = 8;  // short fibres (I0 <= 128): ~70 KB of T in flight per SM
 constexpr int kFiberF = 16;
 constexpr int kWStages = 4;  // W (Khatri-Rao row) ring: the gathers of a tile take about a tile's time
 constexpr int kMaxKSteps = 104;  // ldT / 4 for I_0 <= 416 (work_create checks)
@@ -65,12 +66,12 @@ struct FiberSmem {
 __host__ __device__ inline int64_t a0_rows(int64_t I0) { return (I0 + 7) / 8 * 8; }
 
 template <int RP, int F>
-__host__ __device__ FiberSmem fiber_layout(int nchunk, int64_t I0) {
+__host__ __device__ FiberSmem fiber_layout(int nchunk, int64_t I0, int nst) {
     const int I0s = 32 * nchunk + 4;
     FiberSmem s{};
     size_t off = 0;
     s.tiles = off;
-    off += sizeof(double) * (size_t)kFStages * F * I0s;
+    off += sizeof(double) * (size_t)nst * F * I0s;
     s.a0 = off;
     if (FiberRoles<RP>::A0SMEM) off += sizeof(double) * (size_t)a0_rows(I0) * RP;
     s.wbuf = off;
@@ -78,7 +79,7 @@ __host__ __device__ FiberSmem fiber_layout(int nchunk, int64_t I0) {
     s.gam = off;
     off += sizeof(double) * (size_t)RP * RP;
     s.bars = off;
-    off += sizeof(uint64_t) * (2 * kFStages + 2 * kWStages);
+    off += sizeof(uint64_t) * (2 * nst + 2 * kWStages);
     s.total = off;
     return s;
 }
@@ -212,7 +213,7 @@ __device__ __forceinline__ int a0s_index(int i, int r) {
     return i * RP + r;
 }
 
-template <int RP, int F, int ORD>
+template <int RP, int F, int ORD, int NST>
 __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel(const FiberParams p) {
     using Ro = FiberRoles<RP>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     constexpr int WLD = w_ld<RP>();
     constexpr int NW = Ro::NWP > 0 ? Ro::NWP : 1;  // warps building W
     static_assert(F == 16, "two 8-fiber m-tiles per tile");
-    const FiberSmem L = fiber_layout<RP, F>(p.nchunk, p.I0);
+    const FiberSmem L = fiber_layout<RP, F>(p.nchunk, p.I0, NST);
     const int I0s = p.I0s;
     const int KS = (int)(p.ldT / 4);  // k-steps of 4 rows (ldT = I0 rounded up to 4; pad rows are 0)
     double* tiles = reinterpret_cast<double*>(smem_raw + L.tiles);
@@ -228,10 +229,10 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     double* wbuf = reinterpret_cast<double*>(smem_raw + L.wbuf);  // [kWStages][F][WLD]
     double* gam = reinterpret_cast<double*>(smem_raw + L.gam);    // [RP][RP]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
-    uint64_t* tfull = bars;       // [kFStages] tx bytes
-    uint64_t* tempty = bars + 3;  // [kFStages] T consumers
-    uint64_t* wfull = bars + 2 * kFStages;               // [kWStages] W producer
-    uint64_t* wempty = bars + 2 * kFStages + kWStages;   // [kWStages] W consumers
+    uint64_t* tfull = bars;          // [NST] tx bytes
+    uint64_t* tempty = bars + NST;   // [NST] T consumers
+    uint64_t* wfull = bars + 2 * NST;               // [kWStages] W producer
+    uint64_t* wempty = bars + 2 * NST + kWStages;   // [kWStages] W consumers
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef CPFIT_FIBER_PROF
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     const bool need_a0 = p.do_s || resid;
     dd racc{0.0, 0.0};
 
-    for (int64_t e = tid; e < (int64_t)kFStages * F * I0s; e += blockDim.x) tiles[e] = 0.0;
+    for (int64_t e = tid; e < (int64_t)NST * F * I0s; e += blockDim.x) tiles[e] = 0.0;
     if (Ro::A0SMEM && need_a0)
         for (int64_t e = tid; e < a0_rows(p.I0) * RP; e += blockDim.x) {
             const int i = (int)(e / RP), r = (int)(e % RP);
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     if (tid == 0) {
         const int t_cons = (p.do_s ? Ro::NS : 0) + (m0w_on ? Ro::NM : 0);
         const int w_cons = (m0w_on ? Ro::NM : 0) + (epi_w ? Ro::NS : 0);
-        for (int s = 0; s < kFStages; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], t_cons);
         }
@@ -312,9 +313,9 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
         FiberIndex<ORD> xw;
         if (!Ro::SEPW && need_w) xw = decode_fiber<ORD>(p, t_begin * F + fw);
         for (int64_t k = 0; k < ntl; ++k) {
-            const int s = (int)(k % kFStages);
+            const int s = (int)(k % NST);
             const int64_t f0 = (t_begin + k) * F;
-            if (k >= kFStages) FIBER_WAIT(0, &tempty[s], (uint32_t)(((k / kFStages) - 1) & 1));
+            if (k >= NST) FIBER_WAIT(0, &tempty[s], (uint32_t)(((k / NST) - 1) & 1));
             const int nvalid = (int)imin64(F, p.J - f0);
             double* st = tiles + (size_t)s * F * I0s;
             if (nvalid < F)
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
         } else if (p.do_s) {
             const int sw = warp - Ro::S0;
             for (int64_t k = 0; k < ntl; ++k) {
-                const int s = (int)(k % kFStages);
+                const int s = (int)(k % NST);
                 const int b = (int)(k % kWStages);
                 const int64_t f0 = (t_begin + k) * F;
                 double fn[Ro::SPW];  // ||t_f||^2 of this lane's fiber, prefetched (r-tile 0 only)
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                     const int64_t f = f0 + ft * 8 + (lane >> 2);
                     fn[j] = (epi_w && nt == 0 && f < p.J) ? p.fnorm2[f] : 0.0;
                 }
-                FIBER_WAIT(2, &tfull[s], (uint32_t)((k / kFStages) & 1));
+                FIBER_WAIT(2, &tfull[s], (uint32_t)((k / NST) & 1));
                 const double* tt = tiles + (size_t)s * F * I0s;
                 double sv[Ro::SPW][2];
 #pragma unroll
@@ -480,9 +481,9 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
             for (int nt = 0; nt < Ro::MAXMT; ++nt) macc[rt][nt][0] = macc[rt][nt][1] = 0.0;
         if (m0w_on) {
             for (int64_t k = 0; k < ntl; ++k) {
-                const int s = (int)(k % kFStages);
+                const int s = (int)(k % NST);
                 const int b = (int)(k % kWStages);
-                FIBER_WAIT(3, &tfull[s], (uint32_t)((k / kFStages) & 1));
+                FIBER_WAIT(3, &tfull[s], (uint32_t)((k / NST) & 1));
                 FIBER_WAIT(4, &wfull[b], (uint32_t)((k / kWStages) & 1));
                 const double* tt = tiles + (size_t)s * F * I0s;
                 const double* wv = wbuf + (size_t)b * F * WLD;
@@ -495,7 +496,8 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                         for (int rt = 0; rt < NRT; ++rt) wa[rt] = wv[f * WLD + rt * 8 + (lane >> 2)];
 #pragma unroll
                         for (int nt = 0; nt < Ro::MAXMT; ++nt) {
-                            if (nt < cnt) {
+                            if (nt >= cnt) break;  // warp-uniform: no predicated-off DMMAs
+                            {
                                 const double bb = tt[f * I0s + rb + nt * 8 + (lane >> 2)];
 #pragma unroll
                                 for (int rt = 0; rt < NRT; ++rt)
@@ -510,7 +512,8 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                     double tsum = 0.0;
 #pragma unroll
                     for (int mt = 0; mt < Ro::MAXMT; ++mt) {
-                        if (mt < cnt) {
+                        if (mt >= cnt) break;
+                        {
                             const int i = rb + mt * 8 + (lane >> 2);
                             double a0r[RP / 4];
 #pragma unroll
@@ -579,7 +582,8 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
 
 template <int RP, int ORD>
 void launch_fiber_ord(const FiberParams& p, int grid, size_t smem, cudaStream_t st) {
-    auto k = fiber_ws_kernel<RP, kFiberF, ORD>;
+    auto k = p.nst == kDeepFStages ? fiber_ws_kernel<RP, kFiberF, ORD, kDeepFStages>
+                                   : fiber_ws_kernel<RP, kFiberF, ORD, kFStages>;
     CPFIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, 32 * FiberRoles<RP>::WARPS, smem, st>>>(p);
 }
@@ -595,11 +599,11 @@ void launch_fiber(const FiberParams& p, int grid, size_t smem, cudaStream_t st) 
     CPFIT_CUDA(cudaGetLastError());
 }
 
-size_t fiber_smem(int RP, int nchunk, int64_t I0) {
+size_t fiber_smem(int RP, int nchunk, int64_t I0, int nst) {
     switch (RP) {
-        case 8: return fiber_layout<8, kFiberF>(nchunk, I0).total;
-        case 16: return fiber_layout<16, kFiberF>(nchunk, I0).total;
-        default: return fiber_layout<32, kFiberF>(nchunk, I0).total;
+        case 8: return fiber_layout<8, kFiberF>(nchunk, I0, nst).total;
+        case 16: return fiber_layout<16, kFiberF>(nchunk, I0, nst).total;
+        default: return fiber_layout<32, kFiberF>(nchunk, I0, nst).total;
     }
 }
 
@@ -619,52 +623,52 @@ struct SPassRoles {
 };
 
 template <int RP, int F>
-__host__ __device__ FiberSmem spass_layout(int nchunk, int64_t I0) {
+__host__ __device__ FiberSmem spass_layout(int nchunk, int64_t I0, int nst) {
     const int I0s = 32 * nchunk + 4;
     FiberSmem s{};
     size_t off = 0;
     s.tiles = off;
-    off += sizeof(double) * (size_t)kFStages * F * I0s;
+    off += sizeof(double) * (size_t)nst * F * I0s;
     s.a0 = off;
     if (FiberRoles<RP>::A0SMEM) off += sizeof(double) * (size_t)a0_rows(I0) * RP;
     s.spart = off;
-    off += sizeof(double) * (size_t)kFStages * SPassRoles<RP>::NPART * 64;
+    off += sizeof(double) * (size_t)nst * SPassRoles<RP>::NPART * 64;
     s.wbuf = s.gam = off;
     s.bars = off;
-    off += sizeof(uint64_t) * 64;
+    off += sizeof(uint64_t) * (2 + SPassRoles<RP>::NQ) * nst;
     s.total = off;
     return s;
 }
 
-template <int RP, int F>
+template <int RP, int F, int NST>
 __global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(const FiberParams p) {
     using Ro = SPassRoles<RP>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int NRT = Ro::NRT;
-    const FiberSmem L = spass_layout<RP, F>(p.nchunk, p.I0);
+    const FiberSmem L = spass_layout<RP, F>(p.nchunk, p.I0, NST);
     const int I0s = p.I0s;
     const int KS = (int)(p.ldT / 4);
     double* tiles = reinterpret_cast<double*>(smem_raw + L.tiles);
     double* a0s = reinterpret_cast<double*>(smem_raw + L.a0);
     double* spart = reinterpret_cast<double*>(smem_raw + L.spart);  // [stage][NPART][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
-    uint64_t* tfull = bars;       // [kFStages]
-    uint64_t* tempty = bars + 3;  // [kFStages] compute warps
-    uint64_t* pfull = bars + 6;   // [kFStages][NQ] the other K-parts of a sub-tile
+    uint64_t* tfull = bars;            // [NST]
+    uint64_t* tempty = bars + NST;     // [NST] compute warps
+    uint64_t* pfull = bars + 2 * NST;  // [NST][NQ] the other K-parts of a sub-tile
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t t_begin = (int64_t)blockIdx.x * p.tiles_per_cta;
     const int64_t t_end = imin64(p.ntiles, t_begin + p.tiles_per_cta);
     const int64_t ntl = t_end > t_begin ? t_end - t_begin : 0;
 
-    for (int64_t e = tid; e < (int64_t)kFStages * F * I0s; e += blockDim.x) tiles[e] = 0.0;
+    for (int64_t e = tid; e < (int64_t)NST * F * I0s; e += blockDim.x) tiles[e] = 0.0;
     if (FiberRoles<RP>::A0SMEM)
         for (int64_t e = tid; e < a0_rows(p.I0) * RP; e += blockDim.x) {
             const int i = (int)(e / RP), r = (int)(e % RP);
             a0s[a0s_index<RP>(i, r)] = (i < p.I0 && r < p.R) ? p.A0[(int64_t)r * p.I0 + i] : 0.0;
         }
     if (tid == 0) {
-        for (int s = 0; s < kFStages; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], Ro::NCW);
             for (int q = 0; q < Ro::NQ; ++q) mbar_init(&pfull[s * Ro::NQ + q], Ro::KSPLIT > 1 ? Ro::KSPLIT - 1 : 1);
@@ -680,9 +684,9 @@ __global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(co
 
     if (warp == 0) {
         for (int64_t k = 0; k < ntl; ++k) {
-            const int s = (int)(k % kFStages);
+            const int s = (int)(k % NST);
             const int64_t f0 = (t_begin + k) * F;
-            if (k >= kFStages) mbar_wait(&tempty[s], (uint32_t)(((k / kFStages) - 1) & 1));
+            if (k >= NST) mbar_wait(&tempty[s], (uint32_t)(((k / NST) - 1) & 1));
             const int nvalid = (int)imin64(F, p.J - f0);
             double* st = tiles + (size_t)s * F * I0s;
             if (nvalid < F)
@@ -702,9 +706,9 @@ __global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(co
     const int rr = nt * 8 + (lane >> 2);
     const int k_lo = (int)((int64_t)KS * h / Ro::KSPLIT), k_hi = (int)((int64_t)KS * (h + 1) / Ro::KSPLIT);
     for (int64_t k = 0; k < ntl; ++k) {
-        const int s = (int)(k % kFStages);
+        const int s = (int)(k % NST);
         const int64_t f0 = (t_begin + k) * F;
-        mbar_wait(&tfull[s], (uint32_t)((k / kFStages) & 1));
+        mbar_wait(&tfull[s], (uint32_t)((k / NST) & 1));
         const double* ta = tiles + (size_t)s * F * I0s + fl * I0s + (lane & 3);
         constexpr int U = 8;
         double acc[U][2];
@@ -741,7 +745,7 @@ __global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(co
             continue;
         }
         if (Ro::KSPLIT > 1) {
-            mbar_wait(&pfull[s * Ro::NQ + q], (uint32_t)((k / kFStages) & 1));
+            mbar_wait(&pfull[s * Ro::NQ + q], (uint32_t)((k / NST) & 1));
 #pragma unroll
             for (int hh = 1; hh < Ro::KSPLIT; ++hh) {
                 const double* sp = spart + ((size_t)s * Ro::NPART + q * (Ro::KSPLIT - 1) + (hh - 1)) * 64 + 2 * lane;
@@ -768,15 +772,11 @@ __global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(co
 #ifndef CPFIT_SREG_WARPS
 #define CPFIT_SREG_WARPS 12
 #endif
-#ifndef CPFIT_SREG_STAGES
-#define CPFIT_SREG_STAGES 3
-#endif
 template <int RP>
 struct SRegRoles {
     static constexpr int NRT = RP / 8;             // column groups
     static constexpr int KSPLIT = CPFIT_SREG_WARPS / NRT;  // K parts
     static constexpr int NCW = NRT * KSPLIT;       // compute warps
-    static constexpr int NST = CPFIT_SREG_STAGES;  // T ring stages
     static constexpr int WARPS = 1 + NCW;          // + the T producer
     static constexpr int KMAX = (kMaxKSteps + KSPLIT - 1) / KSPLIT;  // k-steps per warp (9, 18)
     static constexpr int CH = kSRegChains;         // accumulator chains per fibre group
@@ -787,29 +787,29 @@ struct SRegRoles {
 __host__ __device__ inline int sreg_pitch(int64_t ldT) { return (int)(((ldT + 15) / 16) * 16 + 4); }
 
 template <int RP, int F>
-__host__ __device__ FiberSmem sreg_layout(int64_t ldT) {
+__host__ __device__ FiberSmem sreg_layout(int64_t ldT, int nst) {
     using Ro = SRegRoles<RP>;
     const int I0s = sreg_pitch(ldT);
     FiberSmem s{};
     size_t off = 0;
     s.tiles = off;
-    off += sizeof(double) * (size_t)Ro::NST * F * I0s;
+    off += sizeof(double) * (size_t)nst * F * I0s;
     s.spart = off;  // [stage][NPART][2 fibre groups][64]
-    off += sizeof(double) * (size_t)Ro::NST * Ro::NPART * 128;
+    off += sizeof(double) * (size_t)nst * Ro::NPART * 128;
     s.a0 = s.wbuf = s.gam = off;
     s.bars = off;
-    off += sizeof(uint64_t) * (2 * Ro::NST + Ro::NST * Ro::NRT);
+    off += sizeof(uint64_t) * (2 * nst + nst * Ro::NRT);
     s.total = off;
     return s;
 }
 
-template <int RP, int F>
+template <int RP, int F, int NSTG>
 __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(const FiberParams p) {
     static_assert(F == 16, "two 8-fibre groups per tile");
     using Ro = SRegRoles<RP>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int NS = Ro::NST;
-    const FiberSmem L = sreg_layout<RP, F>(p.ldT);
+    constexpr int NS = NSTG;
+    const FiberSmem L = sreg_layout<RP, F>(p.ldT, NS);
     const int I0s = sreg_pitch(p.ldT);
     const int KS = (int)(p.ldT / 4);
     double* tiles = reinterpret_cast<double*>(smem_raw + L.tiles);
@@ -877,6 +877,9 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
             for (int j = 0; j < Ro::CH; ++j) acc[g][j][0] = acc[g][j][1] = 0.0;
 #pragma unroll
         for (int u0 = 0; u0 < Ro::KMAX; u0 += Ro::CH) {
+            // warp-uniform exit: short fibres (k_hi - k_lo << KMAX) must not issue the
+            // predicated-off DMMAs of the remaining unrolled steps
+            if (u0 >= k_hi - k_lo) break;
             double a0[Ro::CH], a1[Ro::CH];
 #pragma unroll
             for (int j = 0; j < Ro::CH; ++j) {
@@ -938,25 +941,26 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
 
 template <int RP>
 void launch_spass(const FiberParams& p, int grid, cudaStream_t st) {
+    const bool deep = p.nst == kDeepFStages;
     if constexpr (RP <= 16) {
-        const size_t smem = sreg_layout<RP, kFiberF>(p.ldT).total;
-        auto k = sreg_kernel<RP, kFiberF>;
+        const size_t smem = sreg_layout<RP, kFiberF>(p.ldT, p.nst).total;
+        auto k = deep ? sreg_kernel<RP, kFiberF, kDeepFStages> : sreg_kernel<RP, kFiberF, kFStages>;
         CPFIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k<<<grid, 32 * SRegRoles<RP>::WARPS, smem, st>>>(p);
         CPFIT_CUDA(cudaGetLastError());
         return;
     }
-    const size_t smem = spass_layout<RP, kFiberF>(p.nchunk, p.I0).total;
-    auto k = spass_kernel<RP, kFiberF>;
+    const size_t smem = spass_layout<RP, kFiberF>(p.nchunk, p.I0, p.nst).total;
+    auto k = deep ? spass_kernel<RP, kFiberF, kDeepFStages> : spass_kernel<RP, kFiberF, kFStages>;
     CPFIT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, 32 * SPassRoles<RP>::WARPS, smem, st>>>(p);
     CPFIT_CUDA(cudaGetLastError());
 }
 
-size_t spass_smem(int RP, int nchunk, int64_t I0) {
+size_t spass_smem(int RP, int nchunk, int64_t I0, int nst) {
     switch (RP) {
-        case 8: return sreg_layout<8, kFiberF>(4 * ((I0 + 3) / 4)).total;
-        case 16: return sreg_layout<16, kFiberF>(4 * ((I0 + 3) / 4)).total;
-        default: return spass_layout<32, kFiberF>(nchunk, I0).total;
+        case 8: return sreg_layout<8, kFiberF>(4 * ((I0 + 3) / 4), nst).total;
+        case 16: return sreg_layout<16, kFiberF>(4 * ((I0 + 3) / 4), nst).total;
+        default: return spass_layout<32, kFiberF>(nchunk, I0, nst).total;
     }
 }

@@ -18,6 +18,7 @@ out = {}
 
 
 def dense_case(name, tol, oracle_full):
+    # (wall clock for the batched sweeps: host sync per wave is part of the cost)
     cfg = bench.CONFIGS[name]
     dims, R = cfg["dims"], cfg["rank"]
     nu = float(sum(dims) * R)
@@ -42,6 +43,17 @@ def dense_case(name, tol, oracle_full):
                          "iters_per_s": n_ref / cpu_s}
         rec["parity"] = {"f_rel": abs(st["best_f"] - ref["f"]) / ref["f"],
                          "iters_rel": abs(st["iters"] - n_ref) / max(n_ref, 1)}
+    if name in ("c0", "c1"):
+        # seed sweep (bench.cpp:80-158) as concurrent device solves: 64 starts, aggregate iters/s
+        starts = np.stack([P.uniform_initial_guess(dims, R, 1000 + i) for i in range(64)])
+        for conc in (1, 8, 32):
+            P.solve_batch(t, starts[:conc], opts, 0, conc)  # solver pool + graphs built
+            t0 = time.perf_counter()
+            b = P.solve_batch(t, starts, opts, 0, conc)
+            dt = time.perf_counter() - t0
+            rec[f"batch64_conc{conc}"] = {"iters": int(b.iters.sum()), "seconds": dt,
+                                          "iters_per_s": float(b.iters.sum()) / dt,
+                                          "solves_per_s": 64 / dt, "all_grad_tol": bool((b.stop_reason == 0).all())}
     kk = int(np.prod(dims))
     for kind, nm in ((3, "fused_pass_ms"), (4, "m0_pass_ms"), (5, "s_pass_ms"), (7, "eval_ms")):
         rec[nm] = P.bench_kernel(t, u0, kind=kind, reps=10, flush_l2=True)

@@ -8,7 +8,8 @@ import numpy as np
 
 import paper_1105_5331_b200 as P
 
-dims, R = (400, 400, 400), 16
+dims = tuple(int(x) for x in os.environ.get("DIMS", "400,400,400").split(","))
+R = int(os.environ.get("RANK", "16"))
 rng = np.random.default_rng(0)
 T = rng.random(int(np.prod(dims)))
 u = rng.random(sum(dims) * R)
