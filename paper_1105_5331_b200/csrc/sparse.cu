@@ -22,6 +22,7 @@ struct SpParams {
     const int32_t* oidx;
     const double* vals;
     int nother;
+    int R;  // lanes r >= R skip their (zero) factor loads: a row of R < RP doubles touches fewer sectors
     const double* frow[kMaxOrder];
     double* out;  // In x RP
 };
@@ -37,20 +38,52 @@ __global__ void __launch_bounds__(256) sp_mttkrp_kernel(const SpParams p) {
     const int lane = threadIdx.x & 31;
     const int r = lane % RP, g = lane / RP;
     const int nother = NO > 0 ? NO : p.nother;
+    const bool live = r < p.R;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = gw; i < p.In; i += nw) {
         double acc = 0.0;
         const int64_t j0 = p.rowptr[i], j1 = p.rowptr[i + 1];
-        for (int64_t jb = j0; jb < j1; jb += 32) {
+        // the next chunk's values and indices are loaded while this chunk's gathers run
+        constexpr int NK = NO > 0 ? NO : kMaxOrder;
+        double vn = 0.0;
+        int cn[NK];
+        auto load_chunk = [&](int64_t jb) {
             const int64_t jl = jb + lane;
             const bool okl = jl < j1;
-            const double vl = okl ? __ldg(p.vals + jl) : 0.0;
-            int cl[NO > 0 ? NO : kMaxOrder];
+            vn = okl ? __ldg(p.vals + jl) : 0.0;
 #pragma unroll
-            for (int k = 0; k < (NO > 0 ? NO : kMaxOrder); ++k)
-                cl[k] = (okl && k < nother) ? __ldg(p.oidx + (int64_t)k * p.nnz + jl) : 0;
+            for (int k = 0; k < NK; ++k) cn[k] = (okl && k < nother) ? __ldg(p.oidx + (int64_t)k * p.nnz + jl) : 0;
+        };
+        if (j0 < j1) load_chunk(j0);
+        for (int64_t jb = j0; jb < j1; jb += 32) {
+            const double vl = vn;
+            int cl[NK];
+#pragma unroll
+            for (int k = 0; k < NK; ++k) cl[k] = cn[k];
+            if (jb + 32 < j1) load_chunk(jb + 32);
             const int cnt = (int)imin64(32, j1 - jb);
+            if (cnt == 32) {
+                // full chunk: every gather of the 32 nonzeros in flight before the products
+                // (the loop is L2-latency bound otherwise)
+                double pr[32 / G];
+#pragma unroll
+                for (int t = 0; t < 32 / G; ++t) {
+                    const int q = t * G + g;
+                    double prod = __shfl_sync(0xffffffffu, vl, q);
+#pragma unroll
+                    for (int k = 0; k < (NO > 0 ? NO : kMaxOrder); ++k) {
+                        if (k < nother) {
+                            const int c = __shfl_sync(0xffffffffu, cl[k], q);
+                            prod *= live ? __ldg(p.frow[k] + (int64_t)c * RP + r) : 0.0;
+                        }
+                    }
+                    pr[t] = prod;
+                }
+#pragma unroll
+                for (int t = 0; t < 32 / G; ++t) acc += pr[t];
+                continue;
+            }
             for (int q0 = 0; q0 < cnt; q0 += G) {
                 const int q = q0 + g;
                 double prod = __shfl_sync(0xffffffffu, vl, q & 31);
@@ -58,7 +91,7 @@ __global__ void __launch_bounds__(256) sp_mttkrp_kernel(const SpParams p) {
                 for (int k = 0; k < (NO > 0 ? NO : kMaxOrder); ++k) {
                     if (k < nother) {
                         const int c = __shfl_sync(0xffffffffu, cl[k], q & 31);
-                        prod *= __ldg(p.frow[k] + (int64_t)c * RP + r);
+                        prod *= live ? __ldg(p.frow[k] + (int64_t)c * RP + r) : 0.0;
                     }
                 }
                 if (q < cnt) acc += prod;
@@ -174,6 +207,7 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
         for (int m = 0; m < N; ++m)
             if (m != n) p.frow[k++] = w.frows + off[m];
         p.nother = k;
+        p.R = w.R;
         p.out = w.sp_part + off[n];
         const int blocks = (int)std::min<int64_t>(148 * 8, (p.In * 32 + 255) / 256);
         switch (w.RP) {
