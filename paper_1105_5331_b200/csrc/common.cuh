@@ -2,6 +2,7 @@
 // and the sm_100a PTX wrappers (fp64 tensor-core DMMA, mbarrier, bulk async copy).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -139,6 +140,17 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// 2D tensor-map copy (TMA): box at (x = column, y = row) of the map into shared memory,
+// completing tx bytes on bar; out-of-bounds elements of the box arrive as zeros
+__device__ __forceinline__ void tma_2d_g2s_hint(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                                uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], "
+        "[%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 

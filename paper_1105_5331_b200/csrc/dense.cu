@@ -34,7 +34,9 @@ namespace {
 // ---------------------------------------------------------------------------------------
 constexpr int kMaxM0W = 16;  // M0 warps per fiber CTA (fiber.cuh FiberRoles)
 
-struct FiberParams {
+struct alignas(64) FiberParams {
+    CUtensorMap tmap;  // T as [J][ldT] with a 16 x pitch box (use_tmap)
+    int use_tmap;
     const double* T;
     int64_t ldT;
     int I0;
@@ -126,6 +128,10 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
     p.nchunk = w.fiber_nchunk;
     p.I0s = 32 * w.fiber_nchunk + 4;
     p.nst = w.fiber_nst;
+    // the S-only pass (sreg_kernel, RP <= 16) has its own row pitch
+    const bool sreg = do_s && !do_m0 && !do_f && w.RP <= 16;
+    p.use_tmap = w.fiber_tmap ? 1 : 0;
+    if (w.fiber_tmap) p.tmap = sreg ? w.tmap_sreg : w.tmap_fws;
     fiber_schedule(w.RP, p.I0, do_s, p);
 #ifdef CPFIT_FIBER_PROF
     p.prof = fiber_prof_buffer();
@@ -944,6 +950,33 @@ EvalWork* work_create(const DevTensor& t, int R) {
                      spass_smem(w->RP, w->fiber_nchunk, I0, kDeepFStages)) <= 220 * 1024)
             w->fiber_nst = kDeepFStages;
         w->fiber_smem = fiber_smem(w->RP, w->fiber_nchunk, I0, w->fiber_nst);
+        {
+            const int pitch_fws = 32 * w->fiber_nchunk + 4, pitch_sreg = sreg_pitch(t.ldT);
+            if (pitch_fws <= 256 && pitch_sreg <= 256 && t.J < ((int64_t)1 << 31)) {
+                using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                              CUtensorMapFloatOOBfill);
+                void* fn = nullptr;
+                cudaDriverEntryPointQueryResult q{};
+                if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                    q == cudaDriverEntryPointSuccess && fn) {
+                    auto encode = reinterpret_cast<EncodeFn>(fn);
+                    const cuuint64_t gdim[2] = {(cuuint64_t)t.ldT, (cuuint64_t)t.J};
+                    const cuuint64_t gstride[1] = {(cuuint64_t)t.ldT * sizeof(double)};
+                    const cuuint32_t estride[2] = {1, 1};
+                    auto make = [&](CUtensorMap* m, int pitch) {
+                        const cuuint32_t box[2] = {(cuuint32_t)pitch, (cuuint32_t)w->fiber_F};
+                        return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)t.T, gdim, gstride, box, estride,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                    };
+                    w->fiber_tmap = make(&w->tmap_fws, pitch_fws) && make(&w->tmap_sreg, pitch_sreg);
+                } else {
+                    (void)cudaGetLastError();
+                }
+            }
+        }
         if (std::max(w->fiber_smem, spass_smem(w->RP, w->fiber_nchunk, I0, w->fiber_nst)) > 227 * 1024)
             throw std::invalid_argument("fiber tile does not fit shared memory");
         const int64_t ntiles = (t.J + w->fiber_F - 1) / w->fiber_F;

@@ -59,6 +59,10 @@ struct EvalWork {
     int64_t off[kMaxOrder + 1] = {};  // packed offsets (R * prefix sum)
     // dense fiber pass
     int fiber_grid = 0, fiber_F = 16, fiber_nchunk = 0, fiber_nst = 3;
+    // short fibres (row pitch <= 256 doubles): one TMA box of 16 fibres per tile instead of 16
+    // bulk copies, for the fused/M0 kernel's pitch and the S pass's pitch
+    bool fiber_tmap = false;
+    CUtensorMap tmap_fws{}, tmap_sreg{};
     size_t fiber_smem = 0;
     double* S = nullptr;        // J x RP
     double* S2 = nullptr;       // (dense order 3) a second J x RP right after S: the line search's S_d

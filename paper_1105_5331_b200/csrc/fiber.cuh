@@ -214,7 +214,7 @@ __device__ __forceinline__ int a0s_index(int i, int r) {
 }
 
 template <int RP, int F, int ORD, int NST>
-__global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel(const FiberParams p) {
+__global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel(const __grid_constant__ FiberParams p) {
     using Ro = FiberRoles<RP>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int NRT = Ro::NRT;
@@ -318,13 +318,21 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
             if (k >= NST) FIBER_WAIT(0, &tempty[s], (uint32_t)(((k / NST) - 1) & 1));
             const int nvalid = (int)imin64(F, p.J - f0);
             double* st = tiles + (size_t)s * F * I0s;
-            if (nvalid < F)
-                for (int e = lane; e < (F - nvalid) * I0s; e += 32) st[(size_t)nvalid * I0s + e] = 0.0;
-            __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
-            __syncwarp();
-            if (lane < nvalid)
-                bulk_g2s_hint(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s], l2_evict_first());
+            if (p.use_tmap) {  // one box of F rows x pitch (pad columns / rows past J arrive as 0)
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&tfull[s], (uint32_t)(F * I0s * 8));
+                    tma_2d_g2s_hint(st, &p.tmap, 0, (int)f0, &tfull[s], l2_evict_first());
+                }
+            } else {
+                if (nvalid < F)
+                    for (int e = lane; e < (F - nvalid) * I0s; e += 32) st[(size_t)nvalid * I0s + e] = 0.0;
+                __syncwarp();
+                if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
+                __syncwarp();
+                if (lane < nvalid)
+                    bulk_g2s_hint(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s],
+                                  l2_evict_first());
+            }
             if (!Ro::SEPW && need_w) w_producer(k, xw, fw, hw);
         }
     } else if (Ro::SEPW && warp <= Ro::NWP) {
@@ -641,7 +649,7 @@ __host__ __device__ FiberSmem spass_layout(int nchunk, int64_t I0, int nst) {
 }
 
 template <int RP, int F, int NST>
-__global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(const FiberParams p) {
+__global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(const __grid_constant__ FiberParams p) {
     using Ro = SPassRoles<RP>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int NRT = Ro::NRT;
@@ -689,13 +697,21 @@ __global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(co
             if (k >= NST) mbar_wait(&tempty[s], (uint32_t)(((k / NST) - 1) & 1));
             const int nvalid = (int)imin64(F, p.J - f0);
             double* st = tiles + (size_t)s * F * I0s;
-            if (nvalid < F)
-                for (int e = lane; e < (F - nvalid) * I0s; e += 32) st[(size_t)nvalid * I0s + e] = 0.0;
-            __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
-            __syncwarp();
-            if (lane < nvalid)
-                bulk_g2s_hint(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s], l2_evict_first());
+            if (p.use_tmap) {  // one box of F rows x pitch (pad columns / rows past J arrive as 0)
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&tfull[s], (uint32_t)(F * I0s * 8));
+                    tma_2d_g2s_hint(st, &p.tmap, 0, (int)f0, &tfull[s], l2_evict_first());
+                }
+            } else {
+                if (nvalid < F)
+                    for (int e = lane; e < (F - nvalid) * I0s; e += 32) st[(size_t)nvalid * I0s + e] = 0.0;
+                __syncwarp();
+                if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
+                __syncwarp();
+                if (lane < nvalid)
+                    bulk_g2s_hint(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s],
+                                  l2_evict_first());
+            }
         }
         return;
     }
@@ -804,7 +820,7 @@ __host__ __device__ FiberSmem sreg_layout(int64_t ldT, int nst) {
 }
 
 template <int RP, int F, int NSTG>
-__global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(const FiberParams p) {
+__global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(const __grid_constant__ FiberParams p) {
     static_assert(F == 16, "two 8-fibre groups per tile");
     using Ro = SRegRoles<RP>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -843,13 +859,21 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
             if (k >= NS) mbar_wait(&tempty[s], (uint32_t)(((k / NS) - 1) & 1));
             const int nvalid = (int)imin64(F, p.J - f0);
             double* st = tiles + (size_t)s * F * I0s;
-            if (nvalid < F)
-                for (int e = lane; e < (F - nvalid) * I0s; e += 32) st[(size_t)nvalid * I0s + e] = 0.0;
-            __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
-            __syncwarp();
-            if (lane < nvalid)
-                bulk_g2s_hint(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s], l2_evict_first());
+            if (p.use_tmap) {  // one box of F rows x pitch (pad columns / rows past J arrive as 0)
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&tfull[s], (uint32_t)(F * I0s * 8));
+                    tma_2d_g2s_hint(st, &p.tmap, 0, (int)f0, &tfull[s], l2_evict_first());
+                }
+            } else {
+                if (nvalid < F)
+                    for (int e = lane; e < (F - nvalid) * I0s; e += 32) st[(size_t)nvalid * I0s + e] = 0.0;
+                __syncwarp();
+                if (lane == 0) mbar_arrive_expect_tx(&tfull[s], (uint32_t)(nvalid * p.ldT * 8));
+                __syncwarp();
+                if (lane < nvalid)
+                    bulk_g2s_hint(st + (size_t)lane * I0s, p.T + (f0 + lane) * p.ldT, (uint32_t)(p.ldT * 8), &tfull[s],
+                                  l2_evict_first());
+            }
         }
         return;
     }
