@@ -64,6 +64,7 @@ struct alignas(64) FiberParams {
     unsigned long long* prof;  // diagnostic build only (fiber.cuh FIBER_WAIT)
     const double* S_in;        // S given (M0 + per-fiber objective pass): J x RP
     int nst;                   // T ring stages (EvalWork::fiber_nst: kFStages or kDeepFStages)
+    int sreg_groups;           // S pass without K split: tile groups (0: K-split mode)
 };
 
 #include "fiber.cuh"
@@ -131,6 +132,7 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
     // the S-only pass (sreg_kernel, RP <= 16) has its own row pitch
     const bool sreg = do_s && !do_m0 && !do_f && w.RP <= 16;
     p.use_tmap = w.fiber_tmap ? 1 : 0;
+    p.sreg_groups = w.sreg_groups;
     if (w.fiber_tmap) p.tmap = sreg ? w.tmap_sreg : w.tmap_fws;
     fiber_schedule(w.RP, p.I0, do_s, p);
 #ifdef CPFIT_FIBER_PROF
@@ -950,6 +952,16 @@ EvalWork* work_create(const DevTensor& t, int R) {
                      spass_smem(w->RP, w->fiber_nchunk, I0, kDeepFStages)) <= 220 * 1024)
             w->fiber_nst = kDeepFStages;
         w->fiber_smem = fiber_smem(w->RP, w->fiber_nchunk, I0, w->fiber_nst);
+        {  // S pass without K split when a warp's register-held A0 fragments cover the whole fibre
+            const int nrt = w->RP / 8, kmax = w->RP == 8 ? SRegRoles<8>::KMAX : SRegRoles<16>::KMAX;
+            w->sreg_groups = 0;
+            if (w->RP <= 16 && t.ldT / 4 <= kmax)
+                for (int ng = CPFIT_SREG_WARPS / nrt; ng >= 2; --ng)
+                    if (w->fiber_nst % ng == 0) {
+                        w->sreg_groups = ng;
+                        break;
+                    }
+        }
         {
             const int pitch_fws = 32 * w->fiber_nchunk + 4, pitch_sreg = sreg_pitch(t.ldT);
             if (pitch_fws <= 256 && pitch_sreg <= 256 && t.J < ((int64_t)1 << 31)) {

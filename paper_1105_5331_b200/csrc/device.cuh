@@ -62,6 +62,7 @@ struct EvalWork {
     // short fibres (row pitch <= 256 doubles): one TMA box of 16 fibres per tile instead of 16
     // bulk copies, for the fused/M0 kernel's pitch and the S pass's pitch
     bool fiber_tmap = false;
+    int sreg_groups = 0;  // S pass tile groups for short fibres (0: K split)
     CUtensorMap tmap_fws{}, tmap_sreg{};
     size_t fiber_smem = 0;
     double* S = nullptr;        // J x RP

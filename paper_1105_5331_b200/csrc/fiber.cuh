@@ -844,7 +844,7 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], Ro::NCW);
+            mbar_init(&tempty[s], p.sreg_groups ? Ro::NRT : Ro::NCW);
             for (int q = 0; q < Ro::NRT; ++q) mbar_init(&pfull[s * Ro::NRT + q], Ro::KSPLIT - 1);
         }
     }
@@ -878,16 +878,21 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
         return;
     }
     const int c = warp - 1;
-    const int nt = c % Ro::NRT, h = c / Ro::NRT;
+    // short fibres (KS <= KMAX, p.sreg_groups = NG > 0): no K split — NG groups of NRT warps take
+    // whole tiles in turn (NG divides the ring depth, so every stage has one consumer group)
+    const int NG = p.sreg_groups;
+    const int nt = c % Ro::NRT, h = NG ? 0 : c / Ro::NRT, grp = NG ? c / Ro::NRT : 0;
+    if (NG && grp >= NG) return;
     const int rr = nt * 8 + (lane >> 2);
-    const int k_lo = (int)((int64_t)KS * h / Ro::KSPLIT), k_hi = (int)((int64_t)KS * (h + 1) / Ro::KSPLIT);
+    const int k_lo = NG ? 0 : (int)((int64_t)KS * h / Ro::KSPLIT);
+    const int k_hi = NG ? KS : (int)((int64_t)KS * (h + 1) / Ro::KSPLIT);
     double bq[Ro::KMAX];  // B fragments A0[4 ks + lane % 4][rr], ks in [k_lo, k_hi)
 #pragma unroll
     for (int u = 0; u < Ro::KMAX; ++u) {
         const int i = (k_lo + u) * 4 + (lane & 3);
         bq[u] = (k_lo + u < k_hi && i < p.I0 && rr < p.R) ? __ldg(p.A0 + (int64_t)rr * p.I0 + i) : 0.0;
     }
-    for (int64_t k = 0; k < ntl; ++k) {
+    for (int64_t k = grp; k < ntl; k += (NG ? NG : 1)) {
         const int s = (int)(k % NS);
         const int64_t f0 = (t_begin + k) * F;
         mbar_wait(&tfull[s], (uint32_t)((k / NS) & 1));
@@ -943,9 +948,10 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
             }
             continue;
         }
-        mbar_wait(&pfull[s * Ro::NRT + nt], (uint32_t)((k / NS) & 1));
+        if (!NG) mbar_wait(&pfull[s * Ro::NRT + nt], (uint32_t)((k / NS) & 1));
 #pragma unroll
         for (int hh = 1; hh < Ro::KSPLIT; ++hh) {
+            if (NG) break;
             const double* sp = spart + ((size_t)s * Ro::NPART + nt * (Ro::KSPLIT - 1) + (hh - 1)) * 128 + 2 * lane;
             sv[0][0] += sp[0];
             sv[0][1] += sp[1];
