@@ -955,7 +955,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
         {  // S pass without K split when a warp's register-held A0 fragments cover the whole fibre
             const int nrt = w->RP / 8, kmax = w->RP == 8 ? SRegRoles<8>::KMAX : SRegRoles<16>::KMAX;
             w->sreg_groups = 0;
-            if (w->RP <= 16 && t.ldT / 4 <= kmax)
+            if (w->RP <= 16 && t.ldT / 4 <= kmax && w->fiber_nst == kDeepFStages)
                 for (int ng = CPFIT_SREG_WARPS / nrt; ng >= 2; --ng)
                     if (w->fiber_nst % ng == 0) {
                         w->sreg_groups = ng;
@@ -964,7 +964,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
         }
         {
             const int pitch_fws = 32 * w->fiber_nchunk + 4, pitch_sreg = sreg_pitch(t.ldT);
-            if (pitch_fws <= 256 && pitch_sreg <= 256 && t.J < ((int64_t)1 << 31)) {
+            if (w->fiber_nst == kDeepFStages && pitch_fws <= 256 && pitch_sreg <= 256 && t.J < ((int64_t)1 << 31)) {
                 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                               CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,

@@ -25,6 +25,8 @@
 // fragment load is conflict free (two wavefronts per 32 doubles).
 #pragma once
 
+#include <type_traits>
+
 constexpr int kFStages = 3;      // T ring depth for long fibres (a tile is ~54 KB at I0 = 400)
 constexpr int kDeepFStages = 8;  // short fibres (I0 <= 128): ~70 KB of T in flight per SM
 constexpr int kFiberF = 16;
@@ -283,12 +285,10 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     double facc = 0.0;
     // W tile k: lane = (fiber fw, r-slice hw) of one of the NW producer warps; gathers first
     // (independent), then the buffer
-    auto w_producer = [&](int64_t k, FiberIndex<ORD>& xw, int fw, int hw) {
-        constexpr int RS = RP * F / (32 * NW);
-        const int b = (int)(k % kWStages);
+    constexpr int RS = RP * F / (32 * NW);
+    auto w_gather = [&](int64_t k, FiberIndex<ORD>& xw, int fw, int hw, double (&w)[RS]) {
         const int64_t f0 = (t_begin + k) * F;
         if (k > 0) xw = advance_fiber<ORD>(p, xw, F, f0 + fw);
-        double w[RS];
 #pragma unroll
         for (int j = 0; j < RS; ++j) {
             const int r = hw * RS + j;
@@ -299,12 +299,20 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                 if (ok && mode_active<ORD>(p, m)) v *= __ldg(p.fac[m] + (int64_t)r * p.dims[m] + xw.j[m]);
             w[j] = v;
         }
+    };
+    auto w_store = [&](int64_t k, int fw, int hw, const double (&w)[RS]) {
+        const int b = (int)(k % kWStages);
         if (k >= kWStages) FIBER_WAIT(1, &wempty[b], (uint32_t)(((k / kWStages) - 1) & 1));
         double* wv = wbuf + (size_t)b * F * WLD;
 #pragma unroll
         for (int j = 0; j < RS; ++j) wv[fw * WLD + hw * RS + j] = w[j];
         __syncwarp();
         if (lane == 0) mbar_arrive(&wfull[b]);
+    };
+    auto w_producer = [&](int64_t k, FiberIndex<ORD>& xw, int fw, int hw) {
+        double w[RS];
+        w_gather(k, xw, fw, hw, w);
+        w_store(k, fw, hw, w);
     };
 
     if (warp == 0) {
@@ -318,7 +326,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
             if (k >= NST) FIBER_WAIT(0, &tempty[s], (uint32_t)(((k / NST) - 1) & 1));
             const int nvalid = (int)imin64(F, p.J - f0);
             double* st = tiles + (size_t)s * F * I0s;
-            if (p.use_tmap) {  // one box of F rows x pitch (pad columns / rows past J arrive as 0)
+            if (NST == kDeepFStages && p.use_tmap) {  // one box of F rows x pitch (pads / rows past J arrive as 0)
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&tfull[s], (uint32_t)(F * I0s * 8));
                     tma_2d_g2s_hint(st, &p.tmap, 0, (int)f0, &tfull[s], l2_evict_first());
@@ -340,7 +348,16 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
         if (need_w) {
             const int fw = lane % F, hw = (warp - 1) * (32 / F) + lane / F;
             FiberIndex<ORD> xw = decode_fiber<ORD>(p, t_begin * F + fw);
-            for (int64_t k = 0; k < ntl; ++k) w_producer(k, xw, fw, hw);
+            // one tile ahead: the next tile's gathers are in flight while this one waits for its
+            // ring slot (the producers are latency bound for short fibres)
+            double wc[RS], wn[RS];
+            if (ntl > 0) w_gather(0, xw, fw, hw, wc);
+            for (int64_t k = 0; k < ntl; ++k) {
+                if (k + 1 < ntl) w_gather(k + 1, xw, fw, hw, wn);
+                w_store(k, fw, hw, wc);
+#pragma unroll
+                for (int j = 0; j < RS; ++j) wc[j] = wn[j];
+            }
         }
     } else if (warp < Ro::M0W) {
         // ---------------- S warps ----------------
@@ -496,20 +513,33 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                 const double* tt = tiles + (size_t)s * F * I0s;
                 const double* wv = wbuf + (size_t)b * F * WLD;
                 if (p.do_m0) {
+                    // few m-tiles per warp (short fibres): warp-uniform exit, no predicated-off
+                    // DMMAs; otherwise the predicated form, which schedules better
+                    const bool few = NST == kDeepFStages && 2 * cnt <= Ro::MAXMT;
 #pragma unroll
                     for (int kf = 0; kf < F / 4; ++kf) {
                         const int f = kf * 4 + (lane & 3);
                         double wa[NRT];
 #pragma unroll
                         for (int rt = 0; rt < NRT; ++rt) wa[rt] = wv[f * WLD + rt * 8 + (lane >> 2)];
+                        if (few) {
 #pragma unroll
-                        for (int nt = 0; nt < Ro::MAXMT; ++nt) {
-                            if (nt >= cnt) break;  // warp-uniform: no predicated-off DMMAs
-                            {
+                            for (int nt = 0; nt < Ro::MAXMT; ++nt) {
+                                if (nt >= cnt) break;
                                 const double bb = tt[f * I0s + rb + nt * 8 + (lane >> 2)];
 #pragma unroll
                                 for (int rt = 0; rt < NRT; ++rt)
                                     dmma_8x8x4(macc[rt][nt][0], macc[rt][nt][1], wa[rt], bb);
+                            }
+                        } else {
+#pragma unroll
+                            for (int nt = 0; nt < Ro::MAXMT; ++nt) {
+                                if (nt < cnt) {
+                                    const double bb = tt[f * I0s + rb + nt * 8 + (lane >> 2)];
+#pragma unroll
+                                    for (int rt = 0; rt < NRT; ++rt)
+                                        dmma_8x8x4(macc[rt][nt][0], macc[rt][nt][1], wa[rt], bb);
+                                }
                             }
                         }
                     }
@@ -697,7 +727,7 @@ __global__ void __launch_bounds__(32 * SPassRoles<RP>::WARPS, 1) spass_kernel(co
             if (k >= NST) mbar_wait(&tempty[s], (uint32_t)(((k / NST) - 1) & 1));
             const int nvalid = (int)imin64(F, p.J - f0);
             double* st = tiles + (size_t)s * F * I0s;
-            if (p.use_tmap) {  // one box of F rows x pitch (pad columns / rows past J arrive as 0)
+            if (NST == kDeepFStages && p.use_tmap) {  // one box of F rows x pitch (pads / rows past J arrive as 0)
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&tfull[s], (uint32_t)(F * I0s * 8));
                     tma_2d_g2s_hint(st, &p.tmap, 0, (int)f0, &tfull[s], l2_evict_first());
@@ -859,7 +889,7 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
             if (k >= NS) mbar_wait(&tempty[s], (uint32_t)(((k / NS) - 1) & 1));
             const int nvalid = (int)imin64(F, p.J - f0);
             double* st = tiles + (size_t)s * F * I0s;
-            if (p.use_tmap) {  // one box of F rows x pitch (pad columns / rows past J arrive as 0)
+            if (NS == kDeepFStages && p.use_tmap) {  // one box of F rows x pitch (pads / rows past J arrive as 0)
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&tfull[s], (uint32_t)(F * I0s * 8));
                     tma_2d_g2s_hint(st, &p.tmap, 0, (int)f0, &tfull[s], l2_evict_first());
@@ -880,7 +910,8 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
     const int c = warp - 1;
     // short fibres (KS <= KMAX, p.sreg_groups = NG > 0): no K split — NG groups of NRT warps take
     // whole tiles in turn (NG divides the ring depth, so every stage has one consumer group)
-    const int NG = p.sreg_groups;
+    constexpr bool SHORT = NSTG == kDeepFStages;  // short-fibre features compiled in
+    const int NG = SHORT ? p.sreg_groups : 0;
     const int nt = c % Ro::NRT, h = NG ? 0 : c / Ro::NRT, grp = NG ? c / Ro::NRT : 0;
     if (NG && grp >= NG) return;
     const int rr = nt * 8 + (lane >> 2);
@@ -904,26 +935,34 @@ __global__ void __launch_bounds__(32 * SRegRoles<RP>::WARPS, 1) sreg_kernel(cons
         for (int g = 0; g < 2; ++g)
 #pragma unroll
             for (int j = 0; j < Ro::CH; ++j) acc[g][j][0] = acc[g][j][1] = 0.0;
+        // short K ranges (short fibres: k_hi - k_lo << KMAX) take a warp-uniform exit so the
+        // predicated-off DMMAs of the remaining unrolled steps are not issued; long ones keep the
+        // predicated form, which schedules better
+        auto kloop = [&](auto few_tag) {
+            constexpr bool FEW = decltype(few_tag)::value;
 #pragma unroll
-        for (int u0 = 0; u0 < Ro::KMAX; u0 += Ro::CH) {
-            // warp-uniform exit: short fibres (k_hi - k_lo << KMAX) must not issue the
-            // predicated-off DMMAs of the remaining unrolled steps
-            if (u0 >= k_hi - k_lo) break;
-            double a0[Ro::CH], a1[Ro::CH];
+            for (int u0 = 0; u0 < Ro::KMAX; u0 += Ro::CH) {
+                if (FEW && u0 >= k_hi - k_lo) break;
+                double a0[Ro::CH], a1[Ro::CH];
 #pragma unroll
-            for (int j = 0; j < Ro::CH; ++j) {
-                const int ks = k_lo + u0 + j;
-                const bool ok = u0 + j < Ro::KMAX && ks < k_hi;
-                a0[j] = ok ? ta0[ks * 4] : 0.0;
-                a1[j] = ok ? ta1[ks * 4] : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < Ro::CH; ++j)
-                if (u0 + j < Ro::KMAX && k_lo + u0 + j < k_hi) {
-                    dmma_8x8x4(acc[0][j][0], acc[0][j][1], a0[j], bq[u0 + j]);
-                    dmma_8x8x4(acc[1][j][0], acc[1][j][1], a1[j], bq[u0 + j]);
+                for (int j = 0; j < Ro::CH; ++j) {
+                    const int ks = k_lo + u0 + j;
+                    const bool ok = u0 + j < Ro::KMAX && ks < k_hi;
+                    a0[j] = ok ? ta0[ks * 4] : 0.0;
+                    a1[j] = ok ? ta1[ks * 4] : 0.0;
                 }
-        }
+#pragma unroll
+                for (int j = 0; j < Ro::CH; ++j)
+                    if (u0 + j < Ro::KMAX && k_lo + u0 + j < k_hi) {
+                        dmma_8x8x4(acc[0][j][0], acc[0][j][1], a0[j], bq[u0 + j]);
+                        dmma_8x8x4(acc[1][j][0], acc[1][j][1], a1[j], bq[u0 + j]);
+                    }
+            }
+        };
+        if (SHORT && 2 * (k_hi - k_lo) <= Ro::KMAX)
+            kloop(std::true_type{});
+        else
+            kloop(std::false_type{});
         double sv[2][2];
 #pragma unroll
         for (int g = 0; g < 2; ++g)
