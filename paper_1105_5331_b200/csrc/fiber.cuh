@@ -348,15 +348,19 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
         if (need_w) {
             const int fw = lane % F, hw = (warp - 1) * (32 / F) + lane / F;
             FiberIndex<ORD> xw = decode_fiber<ORD>(p, t_begin * F + fw);
-            // one tile ahead: the next tile's gathers are in flight while this one waits for its
-            // ring slot (the producers are latency bound for short fibres)
-            double wc[RS], wn[RS];
-            if (ntl > 0) w_gather(0, xw, fw, hw, wc);
-            for (int64_t k = 0; k < ntl; ++k) {
-                if (k + 1 < ntl) w_gather(k + 1, xw, fw, hw, wn);
-                w_store(k, fw, hw, wc);
+            // short fibres: one tile ahead — the next tile's gathers are in flight while this one
+            // waits for its ring slot (the producers are latency bound there)
+            if (NST == kDeepFStages) {
+                double wc[RS], wn[RS];
+                if (ntl > 0) w_gather(0, xw, fw, hw, wc);
+                for (int64_t k = 0; k < ntl; ++k) {
+                    if (k + 1 < ntl) w_gather(k + 1, xw, fw, hw, wn);
+                    w_store(k, fw, hw, wc);
 #pragma unroll
-                for (int j = 0; j < RS; ++j) wc[j] = wn[j];
+                    for (int j = 0; j < RS; ++j) wc[j] = wn[j];
+                }
+            } else {
+                for (int64_t k = 0; k < ntl; ++k) w_producer(k, xw, fw, hw);
             }
         }
     } else if (warp < Ro::M0W) {
