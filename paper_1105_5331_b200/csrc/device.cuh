@@ -181,6 +181,9 @@ struct PolyWork {
     dd* coef = nullptr;       // phi coefficients [7]
     unsigned int* counter = nullptr;
     int s8_grid = 0;
+    // the cross Grams run beside the S_d pass on their own stream (graph branch)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 bool poly_supported(const DevTensor& t);
 PolyWork* poly_create(const DevTensor& t, const EvalWork& w);

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(256) cross_gram_kernel(const CrossParams p) {
 }
 
 struct S8Params {
+    int i2c;           // i2 per block (<= kS8I2)
     const double* S;   // S(u_bar), J x RP
     const double* Sd;  // S_d
     int64_t J, I1;
@@ -80,7 +81,7 @@ __device__ __forceinline__ dd dd_shfl_xor(dd v, int o) {
 // rows of A2 and D2. fp64 FMA partial sums over kS8Run fibres are folded into double-double —
 // a run's sum carries the same ~1e-15 relative error as the DMMA-computed S it is built from.
 constexpr int kS8Run = 8;
-constexpr int kS8I2 = 32;  // i2 per block chunk
+constexpr int kS8I2 = 48;  // max i2 per block chunk (the chunk is sized so the grid is one wave)
 
 // a += b for a double-double accumulator without renormalising (lo collects the rounding errors
 // of hi; dd_norm once at the end)
@@ -101,8 +102,8 @@ __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
     const int npr = I1 * p.RP;                           // (i1, r) pairs
     const int ngx = (npr + blockDim.x - 1) / blockDim.x;  // blocks over pairs
     const int pr = (blockIdx.x % ngx) * blockDim.x + threadIdx.x;
-    const int i2a = (blockIdx.x / ngx) * kS8I2;
-    const int i2b = min(I2, i2a + kS8I2);
+    const int i2a = (blockIdx.x / ngx) * p.i2c;
+    const int i2b = min(I2, i2a + p.i2c);
     const int i1 = pr / p.RP, r = pr % p.RP;
     const bool active = pr < npr && r < p.R;
     // S(u_bar) column r = sc0[r] x S column perm[r]: coalesced loads, then a shuffle from the
@@ -196,6 +197,30 @@ __global__ void __launch_bounds__(256) s8_kernel(const S8Params p) {
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s = dd_add(s, red[w][threadIdx.x]);
         p.part[(size_t)blockIdx.x * 8 + threadIdx.x] = s;
     }
+}
+
+// s8 grid: (i1, r) pair blocks x i2 chunks, the chunk sized so all blocks are resident at once
+// (a second, mostly empty wave doubled the kernel time); returns (blocks, pair blocks, chunk)
+int3 s8_grid_dims(const DevTensor& t, const EvalWork& w) {
+    static int per_sm = [] {
+        int b = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, s8_kernel, 256, 0) != cudaSuccess || b < 1) {
+            (void)cudaGetLastError();
+            b = 1;
+        }
+        return b;
+    }();
+    int sms = 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) {
+        (void)cudaGetLastError();
+        sms = 148;
+    }
+    const int64_t I2 = t.dims[2];
+    const int ngx = (int)((t.dims[1] * w.RP + 255) / 256);
+    int64_t ngy = std::max<int64_t>(1, (int64_t)sms * per_sm / ngx);
+    int64_t i2c = std::min<int64_t>(kS8I2, (I2 + ngy - 1) / ngy);
+    ngy = (I2 + i2c - 1) / i2c;
+    return make_int3((int)(ngx * ngy), ngx, (int)i2c);
 }
 
 struct CoefParams {
@@ -358,8 +383,11 @@ PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {
     int64_t tasks = 0;
     for (int n = 0; n < 3; ++n) tasks += (int64_t)gram_chunks(t.dims[n]) * kKinds * w.R * w.R;
     p->nchunk_total = tasks;
-    p->s8_grid = (int)(((t.dims[1] * w.RP + 255) / 256) * ((t.dims[2] + kS8I2 - 1) / kS8I2));
+    p->s8_grid = s8_grid_dims(t, w).x;
     p->S_d = w.S2;  // owned by the evaluation workspace (next to S)
+    CPFIT_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    CPFIT_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+    CPFIT_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
     CPFIT_CUDA(cudaMalloc(&p->gpart, sizeof(dd) * (size_t)std::max<int64_t>(tasks, 1)));
     CPFIT_CUDA(cudaMalloc(&p->grams, sizeof(dd) * 3 * kKinds * (size_t)w.RP * w.RP));
     CPFIT_CUDA(cudaMalloc(&p->s8part, sizeof(dd) * 8 * (size_t)p->s8_grid));
@@ -378,13 +406,18 @@ void poly_destroy(PolyWork* p) {
     cudaFree(p->coef);
     cudaFree(p->s8);
     cudaFree(p->counter);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
+    if (p->side) cudaStreamDestroy(p->side);
     delete p;
 }
 
 void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const double* ub, const double* d,
                        cudaStream_t st, const int* perm, const double* sc0) {
-    // S_d = T x_1 D_0 (the direction's first block)
-    dense_s_pass(t, w, d, pw.S_d, st);
+    // the cross Grams need only u_bar and d: on the side stream, beside the S_d pass (38
+    // registers per thread: they fit next to the pass's one CTA per SM)
+    CPFIT_CUDA(cudaEventRecord(pw.ev_fork, st));
+    CPFIT_CUDA(cudaStreamWaitEvent(pw.side, pw.ev_fork, 0));
     CrossParams c{};
     c.R = w.R;
     c.RP = w.RP;
@@ -395,8 +428,11 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     }
     c.out = pw.grams;
     const int ctasks = 3 * kKinds * w.RP * w.RP;
-    cross_gram_kernel<<<(ctasks + 7) / 8, 256, 0, st>>>(c);
+    cross_gram_kernel<<<(ctasks + 7) / 8, 256, 0, pw.side>>>(c);
     CPFIT_CUDA(cudaGetLastError());
+    CPFIT_CUDA(cudaEventRecord(pw.ev_join, pw.side));
+    // S_d = T x_1 D_0 (the direction's first block)
+    dense_s_pass(t, w, d, pw.S_d, st);
     S8Params s{};
     s.S = w.S;
     s.Sd = pw.S_d;
@@ -412,21 +448,22 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     s.perm = perm;
     s.sc0 = sc0;
 
-    const int ngx = (int)((t.dims[0 + 1] * w.RP + 255) / 256);
-    const int ngy = (int)((t.dims[2] + kS8I2 - 1) / kS8I2);
+    const int3 sg = s8_grid_dims(t, w);
+    s.i2c = sg.z;
     static bool carve = [] {  // several CTAs per SM need the shared-memory carveout
         cudaFuncSetAttribute(s8_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         return true;
     }();
     (void)carve;
-    s8_kernel<<<ngx * ngy, 256, 0, st>>>(s);
+    s8_kernel<<<sg.x, 256, 0, st>>>(s);
     CPFIT_CUDA(cudaGetLastError());
+    CPFIT_CUDA(cudaStreamWaitEvent(st, pw.ev_join, 0));  // cross Grams done
     CoefParams q{};
     q.R = w.R;
     q.RP = w.RP;
     q.grams = pw.grams;
     q.s8part = pw.s8part;
-    q.s8_blocks = ngx * ngy;
+    q.s8_blocks = sg.x;
     q.half_norm_sq = dd{0.5 * t.norm_sq, 0.5 * t.norm_sq_lo};
     q.coef = pw.coef;
     coef_kernel<<<1, 256, 0, st>>>(q);
