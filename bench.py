@@ -309,7 +309,7 @@ def main():
         nst = ncg.state()
         extras["ncg"] = {"iters/s": round(nst["iters"] / (n_ms * 1e-3), 1), "iters": nst["iters"],
                          "fevals": nst["fevals"], "ms": round(n_ms, 3),
-                         "note": "device N-CG (Polak-Ribiere+, More-Thuente on trial evaluations), init included"}
+                         "note": "device N-CG (Polak-Ribiere+, More-Thuente on the exact line polynomial for dense order 3, trial evaluations otherwise), init included"}
 
     # end to end through the public C-ABI from pinned host buffers: tensor upload + solves
     T_pin = np.ascontiguousarray(T)

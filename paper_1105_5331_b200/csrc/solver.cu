@@ -14,6 +14,7 @@
 #include "poly.cuh"
 #include "solver.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -237,10 +238,18 @@ __global__ void k_poly_ls(Ctl c) {
     s.fevals += s.mt.evals;
     s.gevals += s.mt.evals;
     s.stalled = (s.mt.status == LS_STALL) ? 1 : 0;
-    if (!s.status && s.mt.out_step > 0.0 && s.mt.out_f <= s.f_bar) {
+    if (!s.status && s.mt.out_step > 0.0 && (c.ncg ? s.mt.out_f < s.f_bar : s.mt.out_f <= s.f_bar)) {
         s.accepted = 1;
         s.beta = s.mt.out_step;
     }
+}
+
+// N-CG accepted polynomial step: S(u*) = S(u) + beta S_d for the next iteration's polynomial
+__global__ void k_s_axpy(const DevState* s, double* S, const double* Sd, int64_t n) {
+    if (!s->accepted) return;
+    const double b = s->beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        S[i] = fma(b, Sd[i], S[i]);
 }
 
 __global__ void k_accept_cond(Ctl c, cudaGraphConditionalHandle h) { set_cond(c, h, c.s->accepted != 0); }
@@ -414,7 +423,7 @@ __global__ void k_dot_part(const double* a, const double* b, double* red, int64_
 
 // iteration start (ncg.cpp:44-58): slope = d.g, steepest-descent reset when d is not a descent
 // direction, then the Moré–Thuente start at u (one warp)
-__global__ void k_ncg_begin(Ctl c, const double* red, int nb, cudaGraphConditionalHandle ls_h) {
+__global__ void k_ncg_begin(Ctl c, const double* red, int nb, cudaGraphConditionalHandle br_h) {
     double sl = 0.0;
     for (int b = threadIdx.x; b < nb; b += 32) sl += red[b];
     sl = warp_sum(sl);
@@ -430,12 +439,18 @@ __global__ void k_ncg_begin(Ctl c, const double* red, int nb, cudaGraphCondition
     s.accepted = 0;
     s.beta = 0.0;
     s.searching = s.mt.begin(c.ls, s.f, sl) ? 1 : 0;
-    if (!s.searching) {  // no evaluation (NotDescent): step 0, a stall (ncg.cpp:60)
-        s.stalled = 1;
-    } else {
+    // branch: 0 Moré–Thuente on the exact polynomial phi (dense order 3, per-fibre objective
+    // phase), 1 on trial evaluations, 2 none (NotDescent: step 0, a stall, ncg.cpp:60)
+    s.poly = (c.poly_ok && s.searching && !s.resid) ? 1 : 0;
+    if (s.poly) {
+        s.searching = 0;
+        s.total_poly += 1;
+    } else if (s.searching) {
         s.total_direct += 1;
+    } else {
+        s.stalled = 1;
     }
-    set_cond(c, ls_h, s.searching != 0);
+    if (!c.eager) cudaGraphSetConditional(br_h, s.poly ? 0u : s.searching ? 1u : 2u);
 }
 
 __global__ void k_ncg_reset_dir(const DevState* s, const double* g, double* d, int64_t n) {
@@ -449,7 +464,7 @@ __global__ void k_ncg_reset_dir(const DevState* s, const double* g, double* d, i
 // reference re-evaluates there, ncg.cpp:72-79: the same point, so the same gradient)
 __global__ void k_ncg_part(const DevState* s, const double* g, const double* gt, const double* gbl, double* red,
                            int64_t n) {
-    const bool last = s->mt.status == LS_CONVERGED;
+    const bool last = s->poly || s->mt.status == LS_CONVERGED;  // poly: (u*, g*) in (ut, gt)
     const double* gn = last ? gt : gbl;
     double v = 0.0, q = 0.0;
     if (s->accepted)
@@ -531,7 +546,7 @@ __global__ void k_ncg_vec(const DevState* s, double* u, double* g, double* d, co
         for (int64_t i = i0; i < n; i += step) d[i] = -g[i];
         return;
     }
-    const bool last = s->mt.status == LS_CONVERGED;
+    const bool last = s->poly || s->mt.status == LS_CONVERGED;
     const double* un = last ? ut : ubl;
     const double* gn = last ? gt : gbl;
     const double pr = s->pr_plus;
@@ -669,7 +684,8 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     norm_nb_ = (int)std::min<int64_t>(296, (n_ + 255) / 256);
     // exact polynomial line search: dense order 3, default objective handling, not disabled
     const char* np = std::getenv("CPFIT_NO_POLY_LS");
-    if (method_ == 0 && poly_supported(*t) && !o.reeval_accepted && !o.residual_objective && !(np && np[0] == '1'))
+    if ((method_ == 0 || method_ == 2) && poly_supported(*t) && !o.reeval_accepted && !o.residual_objective &&
+        !(np && np[0] == '1'))
         pw_ = poly_create(*t, *w_);
     if (const char* e = std::getenv("CPFIT_PHASE_PROFILE"); e && e[0] == '1') {
         CPFIT_CUDA(cudaMalloc(&phase_, sizeof(unsigned long long) * (2 * kPhases + 1)));
@@ -845,20 +861,40 @@ void Solver::build_graphs() {
         // N-CG iteration (ncg.cpp:42-108): slope / reset, Moré–Thuente on trial evaluations at
         // u + stp d, Polak–Ribière+ direction update
         k_dot_part<<<norm_nb_, 256, 0, st2_>>>(d_, g_, red_, n_);
-        const cudaGraphConditionalHandle ls_h = make_handle(st2_);
-        k_ncg_begin<<<1, 32, 0, st2_>>>(c, red_, norm_nb_, ls_h);
+        const cudaGraphConditionalHandle br_h = make_handle(st2_);
+        k_ncg_begin<<<1, 32, 0, st2_>>>(c, red_, norm_nb_, br_h);
         k_ncg_reset_dir<<<vb, 256, 0, st2_>>>(s, g_, d_, n_);
         stamp(st2_, 2);
-        lsb = append_conditional(st2_, ls_h, cudaGraphCondTypeWhile);
-        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        k_trial<<<vb, 256, 0, st3_>>>(s, u_, d_, ut_, n_);
-        eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st3_, true, &s->resid);
-        stamp(st3_, 3);
-        k_ls_update<<<1, 1, 0, st3_>>>(c, ls_h);
-        k_keep_best<<<vb, 256, 0, st3_>>>(s, ut_, gt_, ubl_, gbl_, n_, nullptr, nullptr, 0);
-        stamp(st3_, 4);
+        cudaGraph_t br[2];
+        append_conditional(st2_, br_h, cudaGraphCondTypeSwitch, 2, br);
+        if (pw_) {
+            // 0: exact line search on phi(a) = f(u + a d): S_d pass, coefficients, Moré–Thuente on
+            // phi; then u* = u + beta d with its Grams, M0 pass + levels + gradient at u* from
+            // S(u*) = S(u) + beta S_d, and S(u*) kept for the next iteration
+            pb = br[0];
+            CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, pb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+            emit_ncg_poly(st3_, &c);
+            stamp(st3_, 3);
+            CPFIT_CUDA(cudaGetLastError());
+            CPFIT_CUDA(cudaStreamEndCapture(st3_, &pb));
+        }
+        // 1: Moré–Thuente on trial evaluations at u + stp d
+        db = br[1];
+        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st3_, db, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        const cudaGraphConditionalHandle ls_h = make_handle(st3_);
+        k_ls_start<<<1, 1, 0, st3_>>>(c, ls_h);
+        lsb = append_conditional(st3_, ls_h, cudaGraphCondTypeWhile);
+        CPFIT_CUDA(cudaStreamBeginCaptureToGraph(st4_, lsb, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        k_trial<<<vb, 256, 0, st4_>>>(s, u_, d_, ut_, n_);
+        eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st4_, true, &s->resid);
+        stamp(st4_, 3);
+        k_ls_update<<<1, 1, 0, st4_>>>(c, ls_h);
+        k_keep_best<<<vb, 256, 0, st4_>>>(s, ut_, gt_, ubl_, gbl_, n_, nullptr, nullptr, 0);
+        stamp(st4_, 4);
         CPFIT_CUDA(cudaGetLastError());
-        CPFIT_CUDA(cudaStreamEndCapture(st3_, &lsb));
+        CPFIT_CUDA(cudaStreamEndCapture(st4_, &lsb));
+        CPFIT_CUDA(cudaGetLastError());
+        CPFIT_CUDA(cudaStreamEndCapture(st3_, &db));
         emit_ncg_end(st2_, &c, loop_h);
     } else {
         // stand-alone ALS iteration (als.cpp:79-95)
@@ -884,6 +920,20 @@ void Solver::build_graphs() {
     n_direct_ = db ? count_kernels(db) : 0;
     n_accp_ = apb ? count_kernels(apb) : 0;
     CPFIT_CUDA(cudaGraphInstantiate(&x_loop_, g_loop_, 0));
+}
+
+// N-CG polynomial line search and the evaluation of its accepted point (see build_graphs)
+void Solver::emit_ncg_poly(cudaStream_t st, const void* ctl) {
+    const Ctl& c = *reinterpret_cast<const Ctl*>(ctl);
+    DevState* s = c.s;
+    EvalScalars* sc_trial = reinterpret_cast<EvalScalars*>(sc_) + 2;
+    poly_build_device(*t_, *w_, *pw_, u_, d_, st, nullptr, nullptr);
+    k_poly_ls<<<1, 1, 0, st>>>(c);
+    poly_point_device(*w_, *pw_, u_, d_, &s->beta, ut_, st);
+    eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true, nullptr, nullptr);
+    const int64_t ns = t_->J * (int64_t)w_->RP;
+    k_s_axpy<<<(int)std::min<int64_t>(1184, (ns + 255) / 256), 256, 0, st>>>(s, w_->S, pw_->S_d, ns);
+    CPFIT_CUDA(cudaGetLastError());
 }
 
 // end of an N-CG iteration: Polak–Ribière+ partials, the scalar commit, the vector update
@@ -1034,6 +1084,7 @@ void Solver::run_loop_eager() {
             k_dot_part<<<norm_nb_, 256, 0, st_>>>(d_, g_, red_, n_);
             k_ncg_begin<<<1, 32, 0, st_>>>(c, red_, norm_nb_, none);
             k_ncg_reset_dir<<<vb, 256, 0, st_>>>(s, g_, d_, n_);
+            if (state().poly) emit_ncg_poly(st_, &c);
             while (state().searching) {
                 k_trial<<<vb, 256, 0, st_>>>(s, u_, d_, ut_, n_);
                 eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st_, true, &s->resid);

@@ -80,6 +80,7 @@ private:
     void emit_poly_accept(cudaStream_t st, const void* ctl);
     void emit_bar(cudaStream_t st, const void* ctl);
     void emit_ncg_end(cudaStream_t st, const void* ctl, unsigned long long loop_h);
+    void emit_ncg_poly(cudaStream_t st, const void* ctl);
     PolyWork* pw_ = nullptr;  // exact line search (poly.cu), when it applies
     bool gout_ = false;       // normalisations hand on their output's Grams
     bool defer_ = false;      // eval at the sweep's own point, then normalise (no S rescale)
