@@ -369,10 +369,11 @@ __global__ void __launch_bounds__(kBulkPairs) level_bulk_kernel(const LevelParam
     const int src = pm ? tid - r + p.perm[r] : tid;
     const double scl = pm ? p.sc0[r] : 1.0;
     const double ah = (DO_S && pr < npairs && r < p.R) ? p.Ah[(int64_t)r * p.Ih + pr / RP] : 0.0;
-    if (DO_M && tid < kBulkSlabs * RP) {
-        const int sl = tid % kBulkSlabs, rr = tid / kBulkSlabs;  // consecutive slabs of a column
-        a2s[sl][rr] = (sl < nsl && rr < p.R) ? p.tfac[0][(int64_t)rr * p.tdims[0] + s0 + sl] : 0.0;
-    }
+    if (DO_M)  // kBulkSlabs x RP entries (512 at RP = 32: more than the block's threads)
+        for (int e = tid; e < kBulkSlabs * RP; e += kBulkPairs) {
+            const int sl = e % kBulkSlabs, rr = e / kBulkSlabs;  // consecutive slabs of a column
+            a2s[sl][rr] = (sl < nsl && rr < p.R) ? p.tfac[0][(int64_t)rr * p.tdims[0] + s0 + sl] : 0.0;
+        }
     __syncthreads();  // a2s staged; the barrier's init is visible
     mbar_wait(&bar, 0);
     double acc = 0.0, xs[kBulkSlabs];

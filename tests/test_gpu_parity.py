@@ -9,7 +9,12 @@ from conftest import random_factors, random_sparse, rel
 pytestmark = pytest.mark.gpu
 
 SHAPES = [((3, 4, 2), 3), ((4, 3, 5), 2), ((5, 5, 5, 5), 3), ((20, 20, 20), 3), ((50, 50, 50), 5),
-          ((64, 64, 64, 64), 10), ((7, 1, 9), 4), ((33, 6, 5), 16), ((2, 3), 2), ((40, 30), 17), ((8, 3, 4, 2, 3), 5)]
+          ((64, 64, 64, 64), 10), ((7, 1, 9), 4), ((33, 6, 5), 16), ((2, 3), 2), ((40, 30), 17), ((8, 3, 4, 2, 3), 5),
+          # short-fibre kernel variants: deep T ring + TMA box with the K-split S pass (I0 = 100),
+          # RP = 32 (spass_kernel), RP = 8 tile groups, the last J tile partial (J % 16 != 0)
+          ((100, 30, 20), 16), ((128, 9, 11), 20), ((36, 40, 7), 5), ((20, 7, 3, 5), 9),
+          # RP = 32 level contractions (the factor staging once covered only 16 of 32 columns)
+          ((200, 30, 20), 20), ((40, 30, 20, 6), 24)]
 
 
 def _dense(P, O, dims, seed=0):
@@ -85,7 +90,7 @@ def test_gram_and_normalize(gpu, O, dims, rank):
 
 
 @pytest.mark.parametrize("dims,rank", [((5, 4, 6), 3), ((20, 20, 20), 3), ((50, 50, 50), 5), ((12, 10, 8, 6), 4),
-                                       ((30, 25), 6)])
+                                       ((30, 25), 6), ((100, 30, 20), 16), ((128, 9, 11), 20)])
 def test_als_sweep(gpu, O, dims, rank):
     P = gpu
     t, o, rng = _dense(P, O, dims, seed=7)
@@ -279,7 +284,8 @@ def test_swamp_config_within_oracle_envelope(gpu, O, cfg):
     assert 0.9 * min(counts) <= n <= 1.1 * max(counts)
 
 
-@pytest.mark.parametrize("dims,rank", [((20, 20, 20), 3), ((50, 50, 50), 5), ((33, 20, 17), 16), ((120, 100, 80), 16)])
+@pytest.mark.parametrize("dims,rank", [((20, 20, 20), 3), ((50, 50, 50), 5), ((33, 20, 17), 16), ((120, 100, 80), 16),
+                                       ((100, 30, 20), 16), ((128, 40, 30), 20)])
 def test_line_polynomial_matches_direct_evaluations(gpu, dims, rank):
     """phi(a) = f(u_bar + a d), phi'(a) = g.d from the exact line-search polynomial vs direct
     objective_and_gradient evaluations (residual form) at the same points."""
