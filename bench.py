@@ -307,6 +307,18 @@ def main():
         ncg.restart(u0, 20)
         n_ms = ncg.restart(u0, 100)
         nst = ncg.state()
+        # the reference's seed pool (bench.cpp:88-120) on one GPU: independent solves of this
+        # tensor in flight together (cpfit_solve_batch); aggregate iterations / s, wall clock
+        cstarts = np.stack([P.uniform_initial_guess(dims, R, 7_000_000 + i) for i in range(8)])
+        copts = P.NgmresOptions(window=20, max_iters=25, tol_grad=tol, gradient_scale=float(nu))
+        conc = {}
+        for cc in (1, 4):
+            P.solve_batch(t, cstarts[:cc], copts, 0, cc)
+            tc0 = time.perf_counter()
+            bb = P.solve_batch(t, cstarts, copts, 0, cc)
+            conc[f"in_flight_{cc}"] = round(float(bb.iters.sum()) / (time.perf_counter() - tc0), 1)
+        extras["concurrent_solves"] = {"iters/s": conc, "solves": 8, "iters_each": 25,
+                                       "note": "aggregate over independent solves of the same tensor (seed sweep)"}
         extras["ncg"] = {"iters/s": round(nst["iters"] / (n_ms * 1e-3), 1), "iters": nst["iters"],
                          "fevals": nst["fevals"], "ms": round(n_ms, 3),
                          "note": "device N-CG (Polak-Ribiere+, More-Thuente on the exact line polynomial for dense order 3, trial evaluations otherwise), init included"}
