@@ -181,11 +181,16 @@ struct PolyWork {
     dd* coef = nullptr;       // phi coefficients [7]
     unsigned int* counter = nullptr;
     int s8_grid = 0;
+    double* drows = nullptr;  // sparse: row-major copy of d's factors
     // the cross Grams run beside the S_d pass on their own stream (graph branch)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 bool poly_supported(const DevTensor& t);
+constexpr int kSparseLineBlocks = 592;
+// sparse order 3: the eight contractions of the line polynomial into part[nblocks][8] (sparse.cu)
+void sparse_line_contractions(const DevTensor& t, EvalWork& w, const double* ub, const double* d, double* drows,
+                              dd* part, int nblocks, cudaStream_t st);
 PolyWork* poly_create(const DevTensor& t, const EvalWork& w);
 void poly_destroy(PolyWork* p);
 // coefficients of phi from u_bar (its S in w.S) and d

@@ -376,15 +376,24 @@ void poly_point_device(EvalWork& w, const PolyWork& pw, const double* ub, const 
     CPFIT_CUDA(cudaGetLastError());
 }
 
-bool poly_supported(const DevTensor& t) { return !t.sparse && t.order == 3; }
+bool poly_supported(const DevTensor& t) { return t.order == 3; }  // dense or sparse
 
 PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {
     auto* p = new PolyWork();
     int64_t tasks = 0;
     for (int n = 0; n < 3; ++n) tasks += (int64_t)gram_chunks(t.dims[n]) * kKinds * w.R * w.R;
     p->nchunk_total = tasks;
-    p->s8_grid = s8_grid_dims(t, w).x;
-    p->S_d = w.S2;  // owned by the evaluation workspace (next to S)
+    if (t.sparse) {
+        // sparse: the eight contractions in one pass over the mode-0 sorted nonzeros, reading
+        // row-major copies of u_bar's and d's factors (drows holds d's)
+        p->s8_grid = kSparseLineBlocks;
+        int64_t rows = 0;
+        for (int n = 0; n < 3; ++n) rows += t.dims[n];
+        CPFIT_CUDA(cudaMalloc(&p->drows, sizeof(double) * (size_t)rows * w.RP));
+    } else {
+        p->s8_grid = s8_grid_dims(t, w).x;
+        p->S_d = w.S2;  // owned by the evaluation workspace (next to S)
+    }
     CPFIT_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
     CPFIT_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
     CPFIT_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
@@ -406,10 +415,24 @@ void poly_destroy(PolyWork* p) {
     cudaFree(p->coef);
     cudaFree(p->s8);
     cudaFree(p->counter);
+    cudaFree(p->drows);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
     if (p->side) cudaStreamDestroy(p->side);
     delete p;
+}
+
+void launch_coef(const DevTensor& t, const EvalWork& w, const PolyWork& pw, int s8_blocks, cudaStream_t st) {
+    CoefParams q{};
+    q.R = w.R;
+    q.RP = w.RP;
+    q.grams = pw.grams;
+    q.s8part = pw.s8part;
+    q.s8_blocks = s8_blocks;
+    q.half_norm_sq = dd{0.5 * t.norm_sq, 0.5 * t.norm_sq_lo};
+    q.coef = pw.coef;
+    coef_kernel<<<1, 256, 0, st>>>(q);
+    CPFIT_CUDA(cudaGetLastError());
 }
 
 void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const double* ub, const double* d,
@@ -431,6 +454,12 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     cross_gram_kernel<<<(ctasks + 7) / 8, 256, 0, pw.side>>>(c);
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaEventRecord(pw.ev_join, pw.side));
+    if (t.sparse) {
+        sparse_line_contractions(t, w, ub, d, pw.drows, pw.s8part, pw.s8_grid, st);
+        CPFIT_CUDA(cudaStreamWaitEvent(st, pw.ev_join, 0));  // cross Grams done
+        launch_coef(t, w, pw, pw.s8_grid, st);
+        return;
+    }
     // S_d = T x_1 D_0 (the direction's first block)
     dense_s_pass(t, w, d, pw.S_d, st);
     S8Params s{};
@@ -458,16 +487,7 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     s8_kernel<<<sg.x, 256, 0, st>>>(s);
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaStreamWaitEvent(st, pw.ev_join, 0));  // cross Grams done
-    CoefParams q{};
-    q.R = w.R;
-    q.RP = w.RP;
-    q.grams = pw.grams;
-    q.s8part = pw.s8part;
-    q.s8_blocks = sg.x;
-    q.half_norm_sq = dd{0.5 * t.norm_sq, 0.5 * t.norm_sq_lo};
-    q.coef = pw.coef;
-    coef_kernel<<<1, 256, 0, st>>>(q);
-    CPFIT_CUDA(cudaGetLastError());
+    launch_coef(t, w, pw, sg.x, st);
 }
 
 }  // namespace cpfit_gpu

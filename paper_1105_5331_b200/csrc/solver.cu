@@ -930,9 +930,13 @@ void Solver::emit_ncg_poly(cudaStream_t st, const void* ctl) {
     poly_build_device(*t_, *w_, *pw_, u_, d_, st, nullptr, nullptr);
     k_poly_ls<<<1, 1, 0, st>>>(c);
     poly_point_device(*w_, *pw_, u_, d_, &s->beta, ut_, st);
-    eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true, nullptr, nullptr);
-    const int64_t ns = t_->J * (int64_t)w_->RP;
-    k_s_axpy<<<(int)std::min<int64_t>(1184, (ns + 255) / 256), 256, 0, st>>>(s, w_->S, pw_->S_d, ns);
+    if (t_->sparse) {
+        eval_device(*t_, *w_, ut_, gt_, sc_trial, nullptr, &s->status, st, true, &s->resid, false, true);
+    } else {
+        eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true, nullptr, nullptr);
+        const int64_t ns = t_->J * (int64_t)w_->RP;
+        k_s_axpy<<<(int)std::min<int64_t>(1184, (ns + 255) / 256), 256, 0, st>>>(s, w_->S, pw_->S_d, ns);
+    }
     CPFIT_CUDA(cudaGetLastError());
 }
 
@@ -982,8 +986,11 @@ void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
     // u* and its Grams (from the cross Grams); S(u*) = S(u_bar) + beta S_d is formed on the fly
     // by the level pass
     poly_point_device(*w_, *pw_, ub_, d_, &s->beta, ut_, st);
-    eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true, defer_ ? w_->nperm : nullptr,
-                        defer_ ? w_->nscale0 : nullptr);
+    if (t_->sparse)  // one sparse evaluation at u* (its Grams came with the point)
+        eval_device(*t_, *w_, ut_, gt_, sc_trial, nullptr, &s->status, st, true, &s->resid, false, true);
+    else
+        eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true,
+                            defer_ ? w_->nperm : nullptr, defer_ ? w_->nscale0 : nullptr);
     const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, w_->m0, m0_cur_, gout_);
     k_after_rescale<<<1, 32, 0, st>>>(c, sc_next, red_, nb);
     CPFIT_CUDA(cudaGetLastError());

@@ -134,6 +134,76 @@ __global__ void frows_kernel(int order, const int64_t* dims_d, int64_t d0, int64
     }
 }
 
+
+// The eight contractions <T, [[X0, X1, X2]]> (X_n in {A_n, D_n}, index 4 b0 + 2 b1 + b2, b_n = 1
+// selects D_n) of a sparse order-3 tensor for the exact line-search polynomial (poly.cu): warp per
+// mode-0 row i over the mode-0 sorted copy, lanes spanning the rank as in sp_mttkrp_kernel; per
+// 32-nonzero chunk the four inner sums sum_nz v X1[j][r] X2[k][r] in fp64, folded into
+// double-double with X0[i][r] in {A0, D0}; per-block partials [block][8] for coef_kernel.
+template <int RP>
+__global__ void __launch_bounds__(256) sp_line8_kernel(const SpParams p, const double* a0rows, const double* d0rows,
+                                                       const double* a1, const double* e1, const double* a2,
+                                                       const double* e2, dd* part) {
+    constexpr int G = 32 / RP;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = lane % RP, g = lane / RP;
+    const bool live = r < p.R;
+    dd acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = dd{0.0, 0.0};
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = gw; i < p.In; i += nw) {
+        const double x0a = live ? a0rows[i * RP + r] : 0.0, x0d = live ? d0rows[i * RP + r] : 0.0;
+        const int64_t j0 = p.rowptr[i], j1 = p.rowptr[i + 1];
+        for (int64_t jb = j0; jb < j1; jb += 32) {
+            const int64_t jl = jb + lane;
+            const bool okl = jl < j1;
+            const double vl = okl ? __ldg(p.vals + jl) : 0.0;
+            const int cj = okl ? __ldg(p.oidx + jl) : 0, ck = okl ? __ldg(p.oidx + p.nnz + jl) : 0;
+            const int cnt = (int)imin64(32, j1 - jb);
+            double q[4] = {0.0, 0.0, 0.0, 0.0};  // X1 X2 in {AA, AD, DA, DD}
+            for (int q0 = 0; q0 < cnt; q0 += G) {
+                const int qq = q0 + g;
+                const double v = __shfl_sync(0xffffffffu, vl, qq & 31);
+                const int j = __shfl_sync(0xffffffffu, cj, qq & 31), k = __shfl_sync(0xffffffffu, ck, qq & 31);
+                if (qq < cnt && live) {
+                    const double y1a = __ldg(a1 + (int64_t)j * RP + r), y1d = __ldg(e1 + (int64_t)j * RP + r);
+                    const double y2a = __ldg(a2 + (int64_t)k * RP + r), y2d = __ldg(e2 + (int64_t)k * RP + r);
+                    const double va = v * y1a, vd = v * y1d;
+                    q[0] = fma(va, y2a, q[0]);
+                    q[1] = fma(va, y2d, q[1]);
+                    q[2] = fma(vd, y2a, q[2]);
+                    q[3] = fma(vd, y2d, q[3]);
+                }
+            }
+#pragma unroll
+            for (int b12 = 0; b12 < 4; ++b12) {
+                acc[b12] = dd_fma(acc[b12], x0a, q[b12]);
+                acc[4 + b12] = dd_fma(acc[4 + b12], x0d, q[b12]);
+            }
+        }
+    }
+    // warp tree (fixed order), then the warps in order
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const dd t{__shfl_xor_sync(0xffffffffu, acc[k].hi, o), __shfl_xor_sync(0xffffffffu, acc[k].lo, o)};
+            acc[k] = dd_add(acc[k], t);
+        }
+    __shared__ dd red[8][8];
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) red[warp][k] = acc[k];
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        dd s{0.0, 0.0};
+        for (int w8 = 0; w8 < (int)(blockDim.x >> 5); ++w8) s = dd_add(s, red[w8][threadIdx.x]);
+        part[(size_t)blockIdx.x * 8 + threadIdx.x] = s;
+    }
+}
+
 }  // namespace
 
 void upload_sparse_modes(DevTensor& t, const std::vector<int64_t>& coords, const std::vector<double>& vals,
@@ -219,4 +289,40 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
     }
 }
 
+}  // namespace cpfit_gpu
+
+namespace cpfit_gpu {
+// Row-major copies of the factors of u_bar (w.frows) and d (drows), then the eight line
+// contractions into part[nblocks][8] (poly.cu's coefficient kernel sums them in order).
+void sparse_line_contractions(const DevTensor& t, EvalWork& w, const double* ub, const double* d, double* drows,
+                              dd* part, int nblocks, cudaStream_t st) {
+    if (t.order != 3) throw std::logic_error("sparse line contractions: order 3 only");
+    int64_t total = 0;
+    for (int n = 0; n < 3; ++n) total += t.dims[n] * w.RP;
+    const int fb = (int)std::min<int64_t>(1024, (total + 255) / 256);
+    frows_kernel<<<fb, 256, 0, st>>>(3, nullptr, t.dims[0], t.dims[1], t.dims[2], 0, 0, 0, 0, 0, w.R, w.RP, ub, w.frows);
+    frows_kernel<<<fb, 256, 0, st>>>(3, nullptr, t.dims[0], t.dims[1], t.dims[2], 0, 0, 0, 0, 0, w.R, w.RP, d, drows);
+    CPFIT_CUDA(cudaGetLastError());
+    const int64_t o1 = t.dims[0] * w.RP, o2 = o1 + t.dims[1] * w.RP;
+    SpParams p{};
+    p.In = t.dims[0];
+    p.nnz = t.nnz;
+    p.rowptr = t.modes->rowptr[0];
+    p.oidx = t.modes->oidx[0];
+    p.vals = t.modes->vals[0];
+    p.nother = 2;
+    p.R = w.R;
+    switch (w.RP) {
+        case 8:
+            sp_line8_kernel<8><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part);
+            break;
+        case 16:
+            sp_line8_kernel<16><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part);
+            break;
+        default:
+            sp_line8_kernel<32><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part);
+            break;
+    }
+    CPFIT_CUDA(cudaGetLastError());
+}
 }  // namespace cpfit_gpu

@@ -301,3 +301,24 @@ def test_line_polynomial_matches_direct_evaluations(gpu, dims, rank):
         fd, gd = P.objective_and_gradient(t, ub + a * d)
         assert abs(f - fd) <= 1e-12 * abs(fd) + 1e-14 * t.norm() ** 2, (a, f, fd)
         assert abs(g - gd @ d) <= 1e-10 * (np.linalg.norm(gd) * np.linalg.norm(d) + 1e-300), (a, g, gd @ d)
+
+
+def test_sparse_ngmres_matches_oracle(gpu, O):
+    """Sparse order 3 (the exact line polynomial from one pass over the nonzeros): first 20 trace
+    rows f <= 1e-8, then the full solve's stop reason, final f and iteration count."""
+    P = gpu
+    dims, nnz, R = (40, 30, 25), 3000, 4
+    coords, vals, _ = P.random_sparse_problem(dims, nnz, R, 0.01, 3)
+    t = P.DataTensor.coo(dims, coords, vals)
+    o = O.Tensor.coo(dims, coords.reshape(-1, 3), vals)
+    u0 = P.uniform_initial_guess(dims, R, 3)
+    nu = float(sum(dims) * R)
+    ref = o.ngmres(u0, window=20, max_iters=500, tol_grad=1e-10, gradient_scale=nu)
+    res = P.ngmres_solve(t, u0, P.NgmresOptions(window=20, max_iters=500, tol_grad=1e-10, gradient_scale=nu))
+    for a, b in list(zip(res.trace, ref["trace"]))[:20]:
+        assert a["iter"] == b["iter"] and a["restart"] == b["restart"]
+        assert abs(a["f"] - b["f"]) <= 1e-8 * abs(b["f"]), (a, b)
+    assert res.stop_reason == ref["stop"]
+    n, n_ref = len(res.trace) - 1, len(ref["trace"]) - 1
+    assert abs(n - n_ref) <= max(2, 0.02 * n_ref), (n, n_ref)
+    assert abs(res.f - ref["f"]) <= 1e-8 * abs(ref["f"])
