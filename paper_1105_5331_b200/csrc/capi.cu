@@ -608,7 +608,7 @@ int cpfit_line_polynomial(cpfit_tensor t, int64_t rank, const double* u_bar, con
         std::lock_guard<std::mutex> lk(t->mu);
         check_rank(rank);
         if (!cpfit_gpu::poly_supported(*t->t))
-            throw std::invalid_argument("line polynomial: dense order-3 tensors only");
+            throw std::invalid_argument("line polynomial: order-3 (dense or sparse) or dense order-4 tensors only");
         if (n < 0) throw std::invalid_argument("line polynomial: n >= 0");
         EvalWork& w = t->work((int)rank);
         check_finite(u_bar, w.nu);

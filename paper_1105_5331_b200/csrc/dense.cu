@@ -999,8 +999,8 @@ EvalWork* work_create(const DevTensor& t, int R) {
         w->fiber_grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
         // order 3: room for the line search's S_d right after S
         const size_t sn = (size_t)t.J * w->RP;
-        CPFIT_CUDA(cudaMalloc(&w->S, sizeof(double) * sn * (t.order == 3 ? 2 : 1)));
-        if (t.order == 3) w->S2 = w->S + sn;
+        CPFIT_CUDA(cudaMalloc(&w->S, sizeof(double) * sn * (t.order <= 4 ? 2 : 1)));
+        if (t.order == 3 || t.order == 4) w->S2 = w->S + sn;
         CPFIT_CUDA(cudaMalloc(&w->m0_part, sizeof(double) * (size_t)w->fiber_grid * w->RP * 32 * w->fiber_nchunk));
         // rows >= 8 ceil(I0 / 8) of the partials are never written: keep them zero
         CPFIT_CUDA(cudaMemset(w->m0_part, 0, sizeof(double) * (size_t)w->fiber_grid * w->RP * 32 * w->fiber_nchunk));

@@ -27,10 +27,10 @@ namespace {
 constexpr int kKinds = 3;  // A^T A, A^T D, D^T D
 
 struct CrossParams {
-    int R, RP;
-    int64_t dims[3];
-    const double* a[3];
-    const double* d[3];
+    int R, RP, nmodes;
+    int64_t dims[4];
+    const double* a[4];
+    const double* d[4];
     dd* out;          // [mode][kind][RP*RP]
 };
 
@@ -38,7 +38,7 @@ struct CrossParams {
 // fixed xor tree); padded entries are written as zero by warps with q or r >= R
 __global__ void __launch_bounds__(256) cross_gram_kernel(const CrossParams p) {
     const int RR = p.RP * p.RP;
-    const int total = 3 * kKinds * RR;
+    const int total = p.nmodes * kKinds * RR;
     const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
     for (int t = warp; t < total; t += nwarps) {
@@ -236,7 +236,7 @@ struct CoefParams {
 __global__ void __launch_bounds__(256) coef_kernel(const CoefParams p) {
     dd c8[8];
 #pragma unroll
-    for (int k = 0; k <= kPolyDeg; ++k) c8[k] = dd{0.0, 0.0};
+    for (int k = 0; k <= kPolyDeg3; ++k) c8[k] = dd{0.0, 0.0};
     const int RR = p.RP * p.RP;
     for (int e = threadIdx.x; e < p.R * p.R; e += blockDim.x) {
         const int q = e / p.R, r = e % p.R;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(256) coef_kernel(const CoefParams p) {
     // fixed-order trees: a transposing shuffle reduction of the seven coefficients (plus a zero)
     // that ends with coefficient k in lane 4 k, the s8 sums over the warp's four groups, then the
     // warps in order
-    c8[kPolyDeg + 1] = dd{0.0, 0.0};
+    c8[kPolyDeg3 + 1] = dd{0.0, 0.0};
     {
         const bool b = lane & 16;
 #pragma unroll
@@ -307,30 +307,221 @@ __global__ void __launch_bounds__(256) coef_kernel(const CoefParams p) {
     c8[0] = dd_add(c8[0], dd_shfl_xor(c8[0], 1));
 #pragma unroll
     for (int o = 16; o >= 8; o >>= 1) v8 = dd_add(v8, dd_shfl_xor(v8, o));
-    __shared__ dd red[8][kPolyDeg + 1 + 8];
-    if ((lane & 3) == 0 && (lane >> 2) <= kPolyDeg) red[warp][lane >> 2] = c8[0];
-    if (lane < 8) red[warp][kPolyDeg + 1 + lane] = v8;
+    __shared__ dd red[8][kPolyDeg3 + 1 + 8];
+    if ((lane & 3) == 0 && (lane >> 2) <= kPolyDeg3) red[warp][lane >> 2] = c8[0];
+    if (lane < 8) red[warp][kPolyDeg3 + 1 + lane] = v8;
     __syncthreads();
-    __shared__ dd tot[kPolyDeg + 1 + 8];
-    if (threadIdx.x < kPolyDeg + 1 + 8) {
+    __shared__ dd tot[kPolyDeg3 + 1 + 8];
+    if (threadIdx.x < kPolyDeg3 + 1 + 8) {
         dd v{0.0, 0.0};
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = dd_add(v, red[w][threadIdx.x]);
         tot[threadIdx.x] = v;
     }
     __syncthreads();
-    const dd* s8v = tot + kPolyDeg + 1;
+    const dd* s8v = tot + kPolyDeg3 + 1;
     if (threadIdx.x == 0) {
         // <T, model(a)>: a^|S| s8[S]
         dd a[4] = {s8v[0], dd_add(dd_add(s8v[4], s8v[2]), s8v[1]), dd_add(dd_add(s8v[6], s8v[5]), s8v[3]), s8v[7]};
-        for (int k = 0; k <= kPolyDeg; ++k) {
+        for (int k = 0; k <= kPolyDeg3; ++k) {
             dd v = dd_mul(dd{0.5, 0.0}, tot[k]);
             if (k <= 3) v = dd_sub(v, a[k]);
             if (k == 0) v = dd_add(v, p.half_norm_sq);
             p.coef[k] = v;
         }
+        for (int k = kPolyDeg3 + 1; k <= kPolyDeg; ++k) p.coef[k] = dd{0.0, 0.0};
     }
 }
 
+
+// ---- order 4 (degree 8) ---------------------------------------------------------------------
+// the sixteen <T, [[X0, X1, X2, X3]]> (index 8 b0 + 4 b1 + 2 b2 + b3, b_n = 1 selects D_n) as
+//   sum_{i1, r} X1[i1][r] sum_{o} S_{b0}[i1 + I1 o][r] (X2 X3)[o][r],  o = i2 + I2 i3:
+// thread (i1, r) walks a chunk of o with the chunk's four X2[i2] X3[i3] row products (AA, AD, DA,
+// DD) staged in shared memory; fp64 runs folded into double-double as in s8_kernel.
+constexpr int kS16O = 40;  // max outer indices per block chunk (static shared memory)
+struct S16Params {
+    int oc;            // outer indices per block
+    const double* S;
+    const double* Sd;
+    int64_t I1, I2, I3;
+    int R, RP;
+    const double *A1, *D1, *A2, *D2, *A3, *D3;
+    dd* part;          // [block][16]
+    const int* perm;
+    const double* sc0;
+};
+
+__global__ void __launch_bounds__(256) s16_kernel(const S16Params p) {
+    __shared__ double x23[4][kS16O][33];
+    __shared__ dd red[8][16];
+    const int I1 = (int)p.I1, I2 = (int)p.I2;
+    const int NO = (int)(p.I2 * p.I3);
+    const int npr = I1 * p.RP;
+    const int ngx = (npr + blockDim.x - 1) / blockDim.x;
+    const int pr = (blockIdx.x % ngx) * blockDim.x + threadIdx.x;
+    const int oa = (blockIdx.x / ngx) * p.oc;
+    const int ob = min(NO, oa + p.oc);
+    const int i1 = pr / p.RP, r = pr % p.RP;
+    const bool active = pr < npr && r < p.R;
+    const int lane0 = threadIdx.x & 31;
+    const int src = (lane0 & ~(p.RP - 1)) + ((p.perm && r < p.R) ? p.perm[r] : r);
+    const double scl = (active && p.perm) ? p.sc0[r] : 1.0;
+    for (int e = threadIdx.x; e < (ob - oa) * p.RP; e += blockDim.x) {
+        const int n = ob - oa, ii = e % n, rr = e / n;
+        const int o = oa + ii, i2 = o % I2, i3 = o / I2;
+        const bool ok = rr < p.R;
+        const double a2 = ok ? p.A2[(int64_t)rr * p.I2 + i2] : 0.0, d2 = ok ? p.D2[(int64_t)rr * p.I2 + i2] : 0.0;
+        const double a3 = ok ? p.A3[(int64_t)rr * p.I3 + i3] : 0.0, d3 = ok ? p.D3[(int64_t)rr * p.I3 + i3] : 0.0;
+        x23[0][ii][rr] = a2 * a3;
+        x23[1][ii][rr] = a2 * d3;
+        x23[2][ii][rr] = d2 * a3;
+        x23[3][ii][rr] = d2 * d3;
+    }
+    const double x1a = active ? p.A1[(int64_t)r * p.I1 + i1] : 0.0;
+    const double x1d = active ? p.D1[(int64_t)r * p.I1 + i1] : 0.0;
+    __syncthreads();
+    dd q[2][4];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[b][c] = dd{0.0, 0.0};
+    for (int o0 = oa; o0 < ob; o0 += 8) {
+        double run[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+        double sv[8], dv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t f = (int64_t)i1 + (int64_t)I1 * (o0 + u);
+            const bool ok = pr < npr && o0 + u < ob;
+            sv[u] = ok ? p.S[f * p.RP + r] : 0.0;
+            dv[u] = ok ? p.Sd[f * p.RP + r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (o0 + u >= ob) break;
+            const double sa = p.perm ? __shfl_sync(0xffffffffu, sv[u], src) : sv[u];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double x = x23[c][o0 + u - oa][r];
+                run[0][c] = fma(sa, x, run[0][c]);
+                run[1][c] = fma(dv[u], x, run[1][c]);
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dd_acc(q[b][c], run[b][c]);
+    }
+    dd acc[16];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            dd v = dd_two_sum(q[b][c].hi, q[b][c].lo);
+            if (b == 0 && p.perm) v = dd_mul(v, dd{scl, 0.0});
+            if (!active) v = dd{0.0, 0.0};
+            acc[8 * b + c] = dd_mul(v, dd{x1a, 0.0});
+            acc[8 * b + 4 + c] = dd_mul(v, dd{x1d, 0.0});
+        }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[k] = dd_add(acc[k], dd_shfl_xor(acc[k], o));
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < 16; ++k) red[warp][k] = acc[k];
+    __syncthreads();
+    if (threadIdx.x < 16) {
+        dd v{0.0, 0.0};
+        for (int w8 = 0; w8 < (int)(blockDim.x >> 5); ++w8) v = dd_add(v, red[w8][threadIdx.x]);
+        p.part[(size_t)blockIdx.x * 16 + threadIdx.x] = v;
+    }
+}
+
+// order-4 phi coefficients: 1/2 ||T||^2 - sum_S a^|S| s16[S] + 1/2 sum_qr prod_n G_n(a)_qr
+__global__ void __launch_bounds__(256) coef4_kernel(const CoefParams p) {
+    dd c[kPolyDeg + 1];
+#pragma unroll
+    for (int k = 0; k <= kPolyDeg; ++k) c[k] = dd{0.0, 0.0};
+    const int RR = p.RP * p.RP;
+    for (int e = threadIdx.x; e < p.R * p.R; e += blockDim.x) {
+        const int q = e / p.R, r = e % p.R;
+        dd qc[4][3];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            const dd* g = p.grams + (size_t)n * kKinds * RR;
+            qc[n][0] = g[q * p.RP + r];
+            qc[n][1] = dd_add(g[RR + q * p.RP + r], g[RR + r * p.RP + q]);
+            qc[n][2] = g[2 * RR + q * p.RP + r];
+        }
+        dd pa[5], pb[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) pa[k] = pb[k] = dd{0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                pa[i + j] = dd_add(pa[i + j], dd_mul(qc[0][i], qc[1][j]));
+                pb[i + j] = dd_add(pb[i + j], dd_mul(qc[2][i], qc[3][j]));
+            }
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+#pragma unroll
+            for (int j = 0; j < 5; ++j) c[i + j] = dd_add(c[i + j], dd_mul(pa[i], pb[j]));
+    }
+    // the sixteen contractions: thread t folds blocks b = t / 16 mod 16 of contraction t % 16
+    dd v{0.0, 0.0};
+    {
+        const int k = threadIdx.x & 15, g = threadIdx.x >> 4;
+        for (int b = g; b < p.s8_blocks; b += 16) v = dd_add(v, p.s8part[(size_t)b * 16 + k]);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k <= kPolyDeg; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c[k] = dd_add(c[k], dd_shfl_xor(c[k], o));
+    v = dd_add(v, dd_shfl_xor(v, 16));
+    __shared__ dd red[8][kPolyDeg + 1 + 16];
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k <= kPolyDeg; ++k) red[warp][k] = c[k];
+    if (lane < 16) red[warp][kPolyDeg + 1 + lane] = v;
+    __syncthreads();
+    __shared__ dd tot[kPolyDeg + 1 + 16];
+    if (threadIdx.x < kPolyDeg + 1 + 16) {
+        dd t{0.0, 0.0};
+        for (int w8 = 0; w8 < (int)(blockDim.x >> 5); ++w8) t = dd_add(t, red[w8][threadIdx.x]);
+        tot[threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const dd* s16 = tot + kPolyDeg + 1;
+        dd a[5];
+        for (int j = 0; j < 5; ++j) a[j] = dd{0.0, 0.0};
+        for (int k = 0; k < 16; ++k) a[__popc(k)] = dd_add(a[__popc(k)], s16[k]);
+        for (int k = 0; k <= kPolyDeg; ++k) {
+            dd x = dd_mul(dd{0.5, 0.0}, tot[k]);
+            if (k <= 4) x = dd_sub(x, a[k]);
+            if (k == 0) x = dd_add(x, p.half_norm_sq);
+            p.coef[k] = x;
+        }
+    }
+}
+
+// s16 grid: (i1, r) pair blocks x outer chunks sized for one wave; returns (blocks, pair blocks, chunk)
+int3 s16_grid_dims(const DevTensor& t, const EvalWork& w) {
+    int sms = 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) {
+        (void)cudaGetLastError();
+        sms = 148;
+    }
+    const int64_t NO = t.dims[2] * t.dims[3];
+    const int ngx = (int)((t.dims[1] * w.RP + 255) / 256);
+    int64_t ngy = std::max<int64_t>(1, (int64_t)2 * sms / ngx);
+    const int64_t oc = std::min<int64_t>(kS16O, (NO + ngy - 1) / ngy);
+    ngy = (NO + oc - 1) / oc;
+    return make_int3((int)(ngx * ngy), ngx, (int)oc);
+}
 }  // namespace
 
 namespace {
@@ -352,14 +543,15 @@ void poly_eval_device(const PolyWork& pw, const double* alphas, int n, double* p
 namespace {
 // u* = u_bar + beta d (grid-stride) and, in the first block, G_n(u*) from the cross Grams
 __global__ void __launch_bounds__(256) poly_point_kernel(const double* ub, const double* d, const double* beta_p,
-                                                         double* ut, int64_t n, const dd* cg, double* gram, int RP) {
+                                                         double* ut, int64_t n, const dd* cg, double* gram, int RP,
+                                                         int nmodes) {
     const double beta = *beta_p;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         ut[i] = ub[i] + beta * d[i];
     if (blockIdx.x != 0) return;
     const int RR = RP * RP;
     const dd b{beta, 0.0}, b2 = dd_mul(b, b);
-    for (int e = threadIdx.x; e < 3 * RR; e += blockDim.x) {
+    for (int e = threadIdx.x; e < nmodes * RR; e += blockDim.x) {
         const int m = e / RR, q = (e % RR) / RP, r = e % RP;
         const dd* g = cg + (size_t)m * kKinds * RR;
         const dd ad = dd_add(g[RR + q * RP + r], g[RR + r * RP + q]);
@@ -372,16 +564,17 @@ __global__ void __launch_bounds__(256) poly_point_kernel(const double* ub, const
 void poly_point_device(EvalWork& w, const PolyWork& pw, const double* ub, const double* d, const double* beta,
                        double* ut, cudaStream_t st) {
     poly_point_kernel<<<(int)std::min<int64_t>(148, (w.nu + 255) / 256), 256, 0, st>>>(ub, d, beta, ut, w.nu,
-                                                                                        pw.grams, w.gram, w.RP);
+                                                                                        pw.grams, w.gram, w.RP,
+                                                                                        w.order);
     CPFIT_CUDA(cudaGetLastError());
 }
 
-bool poly_supported(const DevTensor& t) { return t.order == 3; }  // dense or sparse
+bool poly_supported(const DevTensor& t) { return t.order == 3 || (t.order == 4 && !t.sparse); }
 
 PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {
     auto* p = new PolyWork();
     int64_t tasks = 0;
-    for (int n = 0; n < 3; ++n) tasks += (int64_t)gram_chunks(t.dims[n]) * kKinds * w.R * w.R;
+    for (int n = 0; n < t.order; ++n) tasks += (int64_t)gram_chunks(t.dims[n]) * kKinds * w.R * w.R;
     p->nchunk_total = tasks;
     if (t.sparse) {
         // sparse: the eight contractions in one pass over the mode-0 sorted nonzeros, reading
@@ -391,15 +584,15 @@ PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {
         for (int n = 0; n < 3; ++n) rows += t.dims[n];
         CPFIT_CUDA(cudaMalloc(&p->drows, sizeof(double) * (size_t)rows * w.RP));
     } else {
-        p->s8_grid = s8_grid_dims(t, w).x;
+        p->s8_grid = t.order == 4 ? s16_grid_dims(t, w).x : s8_grid_dims(t, w).x;
         p->S_d = w.S2;  // owned by the evaluation workspace (next to S)
     }
     CPFIT_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
     CPFIT_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
     CPFIT_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
     CPFIT_CUDA(cudaMalloc(&p->gpart, sizeof(dd) * (size_t)std::max<int64_t>(tasks, 1)));
-    CPFIT_CUDA(cudaMalloc(&p->grams, sizeof(dd) * 3 * kKinds * (size_t)w.RP * w.RP));
-    CPFIT_CUDA(cudaMalloc(&p->s8part, sizeof(dd) * 8 * (size_t)p->s8_grid));
+    CPFIT_CUDA(cudaMalloc(&p->grams, sizeof(dd) * 4 * kKinds * (size_t)w.RP * w.RP));
+    CPFIT_CUDA(cudaMalloc(&p->s8part, sizeof(dd) * 16 * (size_t)p->s8_grid));
     CPFIT_CUDA(cudaMalloc(&p->coef, sizeof(dd) * (kPolyDeg + 1)));
     CPFIT_CUDA(cudaMalloc(&p->s8, sizeof(dd) * 8));
     CPFIT_CUDA(cudaMalloc(&p->counter, sizeof(unsigned int) * 2));
@@ -444,13 +637,14 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     CrossParams c{};
     c.R = w.R;
     c.RP = w.RP;
-    for (int n = 0; n < 3; ++n) {
+    c.nmodes = t.order;
+    for (int n = 0; n < t.order; ++n) {
         c.dims[n] = t.dims[n];
         c.a[n] = ub + w.off[n];
         c.d[n] = d + w.off[n];
     }
     c.out = pw.grams;
-    const int ctasks = 3 * kKinds * w.RP * w.RP;
+    const int ctasks = t.order * kKinds * w.RP * w.RP;
     cross_gram_kernel<<<(ctasks + 7) / 8, 256, 0, pw.side>>>(c);
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaEventRecord(pw.ev_join, pw.side));
@@ -462,6 +656,41 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     }
     // S_d = T x_1 D_0 (the direction's first block)
     dense_s_pass(t, w, d, pw.S_d, st);
+    if (t.order == 4) {
+        S16Params s16{};
+        const int3 sg = s16_grid_dims(t, w);
+        s16.oc = sg.z;
+        s16.S = w.S;
+        s16.Sd = pw.S_d;
+        s16.I1 = t.dims[1];
+        s16.I2 = t.dims[2];
+        s16.I3 = t.dims[3];
+        s16.R = w.R;
+        s16.RP = w.RP;
+        s16.A1 = ub + w.off[1];
+        s16.D1 = d + w.off[1];
+        s16.A2 = ub + w.off[2];
+        s16.D2 = d + w.off[2];
+        s16.A3 = ub + w.off[3];
+        s16.D3 = d + w.off[3];
+        s16.part = pw.s8part;
+        s16.perm = perm;
+        s16.sc0 = sc0;
+        s16_kernel<<<sg.x, 256, 0, st>>>(s16);
+        CPFIT_CUDA(cudaGetLastError());
+        CPFIT_CUDA(cudaStreamWaitEvent(st, pw.ev_join, 0));  // cross Grams done
+        CoefParams q{};
+        q.R = w.R;
+        q.RP = w.RP;
+        q.grams = pw.grams;
+        q.s8part = pw.s8part;
+        q.s8_blocks = sg.x;
+        q.half_norm_sq = dd{0.5 * t.norm_sq, 0.5 * t.norm_sq_lo};
+        q.coef = pw.coef;
+        coef4_kernel<<<1, 256, 0, st>>>(q);
+        CPFIT_CUDA(cudaGetLastError());
+        return;
+    }
     S8Params s{};
     s.S = w.S;
     s.Sd = pw.S_d;

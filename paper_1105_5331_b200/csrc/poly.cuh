@@ -6,7 +6,8 @@
 
 namespace cpfit_gpu {
 
-constexpr int kPolyDeg = 6;  // order 3: f is of degree 2N in a
+constexpr int kPolyDeg = 8;   // f is of degree 2N in a: 6 for order 3 (coefficients 7, 8 zero), 8 for order 4
+constexpr int kPolyDeg3 = 6;
 
 // phi(a) and phi'(a) by Horner on the double-double coefficients coef[0..kPolyDeg]
 __device__ __forceinline__ void poly_eval(const dd* coef, double a, double& f, double& g) {

@@ -244,6 +244,25 @@ __global__ void k_poly_ls(Ctl c) {
     }
 }
 
+// order 4: S(u*) = S(u_bar) + beta S_d materialised in place (the first level of an order-4
+// tensor cannot form it on the fly), with S(u_bar) = S'[.][perm r] sc0[r] when perm is set;
+// guard: only after an accepted search (N-CG keeps S(u) otherwise)
+__global__ void k_s_point(const DevState* s, int guard, double* S, const double* Sd, int64_t J, int RP, int R,
+                          const int* perm, const double* sc0) {
+    if (guard && !s->accepted) return;
+    const double b = s->beta;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
+        double* row = S + j * RP;
+        const double* drow = Sd + j * RP;
+        double v[32];
+        for (int r = 0; r < RP; ++r) v[r] = row[r];
+        for (int r = 0; r < RP; ++r) {
+            const double base = (perm && r < R) ? v[perm[r]] * sc0[r] : v[r];
+            row[r] = fma(b, drow[r], base);
+        }
+    }
+}
+
 // N-CG accepted polynomial step: S(u*) = S(u) + beta S_d for the next iteration's polynomial
 __global__ void k_s_axpy(const DevState* s, double* S, const double* Sd, int64_t n) {
     if (!s->accepted) return;
@@ -932,6 +951,12 @@ void Solver::emit_ncg_poly(cudaStream_t st, const void* ctl) {
     poly_point_device(*w_, *pw_, u_, d_, &s->beta, ut_, st);
     if (t_->sparse) {
         eval_device(*t_, *w_, ut_, gt_, sc_trial, nullptr, &s->status, st, true, &s->resid, false, true);
+    } else if (t_->order == 4) {
+        // S(u*) replaces S(u) only after an accepted search; the evaluation below then reads it
+        // (a rejected search leaves S(u) for the retry from steepest descent)
+        const int rb = (int)std::min<int64_t>(1184, (t_->J + 255) / 256);
+        k_s_point<<<rb, 256, 0, st>>>(s, 1, w_->S, pw_->S_d, t_->J, w_->RP, w_->R, nullptr, nullptr);
+        eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, nullptr, nullptr, true, nullptr, nullptr);
     } else {
         eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true, nullptr, nullptr);
         const int64_t ns = t_->J * (int64_t)w_->RP;
@@ -986,11 +1011,17 @@ void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
     // u* and its Grams (from the cross Grams); S(u*) = S(u_bar) + beta S_d is formed on the fly
     // by the level pass
     poly_point_device(*w_, *pw_, ub_, d_, &s->beta, ut_, st);
-    if (t_->sparse)  // one sparse evaluation at u* (its Grams came with the point)
+    if (t_->sparse) {  // one sparse evaluation at u* (its Grams came with the point)
         eval_device(*t_, *w_, ut_, gt_, sc_trial, nullptr, &s->status, st, true, &s->resid, false, true);
-    else
+    } else if (t_->order == 4) {
+        const int rb = (int)std::min<int64_t>(1184, (t_->J + 255) / 256);
+        k_s_point<<<rb, 256, 0, st>>>(s, 0, w_->S, pw_->S_d, t_->J, w_->RP, w_->R, defer_ ? w_->nperm : nullptr,
+                                       defer_ ? w_->nscale0 : nullptr);
+        eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, nullptr, nullptr, true, nullptr, nullptr);
+    } else {
         eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true,
                             defer_ ? w_->nperm : nullptr, defer_ ? w_->nscale0 : nullptr);
+    }
     const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, w_->m0, m0_cur_, gout_);
     k_after_rescale<<<1, 32, 0, st>>>(c, sc_next, red_, nb);
     CPFIT_CUDA(cudaGetLastError());

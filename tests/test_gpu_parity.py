@@ -285,7 +285,8 @@ def test_swamp_config_within_oracle_envelope(gpu, O, cfg):
 
 
 @pytest.mark.parametrize("dims,rank", [((20, 20, 20), 3), ((50, 50, 50), 5), ((33, 20, 17), 16), ((120, 100, 80), 16),
-                                       ((100, 30, 20), 16), ((128, 40, 30), 20)])
+                                       ((100, 30, 20), 16), ((128, 40, 30), 20), ((12, 10, 8, 6), 4),
+                                       ((64, 20, 12, 10), 10), ((40, 24, 22, 21), 20)])
 def test_line_polynomial_matches_direct_evaluations(gpu, dims, rank):
     """phi(a) = f(u_bar + a d), phi'(a) = g.d from the exact line-search polynomial vs direct
     objective_and_gradient evaluations (residual form) at the same points."""
