@@ -206,6 +206,10 @@ struct LevelParams {
     const double* beta;
     const int* perm;
     const double* sc0;
+    // optional (bulk kernel, M only): the last slab-range CTA of each pair tile sums the tile's
+    // partials in order and writes M_h col-major (I_h x R) here — the MTTKRP's final output
+    double* m_final;
+    unsigned int* tile_cnt;
 };
 
 constexpr int kLevelThreads = 256;
@@ -395,6 +399,24 @@ __global__ void __launch_bounds__(kBulkPairs) level_bulk_kernel(const LevelParam
         }
     }
     if (DO_M && live) p.m_part[(int64_t)blockIdx.y * npairs + pr] = acc;
+    if (DO_M && p.m_final) {
+        __shared__ bool last;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            last = (atomicAdd(p.tile_cnt + blockIdx.x, 1u) == gridDim.y - 1);
+            if (last) p.tile_cnt[blockIdx.x] = 0u;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        if (live && r < p.R) {
+            double v = 0.0;
+            for (int c = 0; c < (int)gridDim.y; ++c) v += __ldcg(p.m_part + (int64_t)c * npairs + pr);
+            p.m_final[(int64_t)r * p.Ih + pr / RP] = v;
+        }
+        return;
+    }
     if (DO_S) {
         __syncthreads();  // every warp is done with the Sin rows
         if (lane < RP)
@@ -634,7 +656,7 @@ void reduce_jobs(const RedJobs& jobs, cudaStream_t st) {
 void run_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const double* u, bool do_m, bool do_s,
                double* Sout, cudaStream_t st, RedJobs* defer_m = nullptr, RedJobs* defer_s = nullptr,
                const double* Sd = nullptr, const double* beta = nullptr, const int* perm = nullptr,
-               const double* sc0 = nullptr) {
+               const double* sc0 = nullptr, double* m_final = nullptr) {
     if (!do_m && !do_s) return;
     LevelParams p{};
     p.Sin = Sin;
@@ -642,6 +664,8 @@ void run_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, const 
     p.beta = beta;
     p.perm = perm;
     p.sc0 = sc0;
+    p.m_final = (m_final && do_m && !do_s && w.lvl_bulk[h]) ? m_final : nullptr;
+    p.tile_cnt = w.lvl_cnt;
     p.Ih = t.dims[h];
     p.Jt = 1;
     for (int m = h + 1; m < t.order; ++m) p.Jt *= t.dims[m];
@@ -940,6 +964,8 @@ EvalWork* work_create(const DevTensor& t, int R) {
     CPFIT_CUDA(cudaEventCreateWithFlags(&w->ev_gram, cudaEventDisableTiming));
     CPFIT_CUDA(cudaMalloc(&w->counter, sizeof(unsigned int) * kCounters));
     CPFIT_CUDA(cudaMemset(w->counter, 0, sizeof(unsigned int) * kCounters));
+    CPFIT_CUDA(cudaMalloc(&w->lvl_cnt, sizeof(unsigned int) * kLvlCounters));
+    CPFIT_CUDA(cudaMemset(w->lvl_cnt, 0, sizeof(unsigned int) * kLvlCounters));
     if (!t.sparse) {
         if (t.order < 2) throw std::invalid_argument("device dense path needs order >= 2");
         const int I0 = (int)t.dims[0];
@@ -1054,6 +1080,7 @@ void work_destroy(EvalWork* w) {
     cudaFree(w->sp_part);
     cudaFree(w->frows);
     cudaFree(w->counter);
+    cudaFree(w->lvl_cnt);
     cudaFree(w->chol);
     cudaFree(w->solve_part);
     cudaFree(w->nperm);
@@ -1324,7 +1351,11 @@ void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, d
         for (int h = 1; h <= mode && h < t.order - 1; ++h) {
             const bool last = (h == mode);
             const bool final = last || h == t.order - 2;
-            run_level(t, w, h, Sin, u, last, !last, w.lvl_S[h], st, final ? &skip : nullptr, final ? &skip : nullptr);
+            // the bulk last level can finish M_mode itself (no gather launch)
+            const bool fin = last && w.lvl_bulk[h] && w.lvl_ny[h] <= kLvlCounters;
+            run_level(t, w, h, Sin, u, last, !last, w.lvl_S[h], st, final ? &skip : nullptr, final ? &skip : nullptr,
+                      nullptr, nullptr, nullptr, nullptr, fin ? out : nullptr);
+            if (fin) return;
             Sin = w.lvl_S[h];
             if (final) {
                 if (last) {

@@ -46,6 +46,7 @@ DevTensor* tensor_create_coo(int order, const int64_t* dims, int64_t nnz, const 
 void tensor_destroy(DevTensor* t);
 
 // last-block-done counters (one per kernel family; each resets its own after use)
+constexpr int kLvlCounters = 1024;
 constexpr int kCounterGrad = 0, kCounterGram = 1, kCounterSolve = 2, kCounterNorm = 3, kCounters = 4;
 // normalisations can hand on the Grams of their output when order * RP^2 <= kGramsOutMax
 constexpr int kGramsOutMax = 4096;
@@ -79,6 +80,7 @@ struct EvalWork {
     double* lvl_m[kMaxOrder] = {};     // reduced M_h [i][r]
     double* lvl_S[kMaxOrder] = {};     // S_{h} outputs (slabs x RP)
     unsigned int* counter = nullptr;   // last-block-done counters [kCounters]
+    unsigned int* lvl_cnt = nullptr;   // per pair tile counters of the level kernel's M finish
     // Grams (gram.cuh): per-mode row chunks, dd partials [global chunk][R(R+1)/2]
     int gram_nchunk[kMaxOrder] = {}, gram_chunk0[kMaxOrder] = {};
     dd* gram_part = nullptr;
