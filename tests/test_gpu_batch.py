@@ -54,3 +54,18 @@ def test_batch_argument_errors(gpu):
     bad[2, 5] = np.nan
     with pytest.raises(ValueError):
         P.solve_batch(t, bad, P.NgmresOptions())
+
+
+def test_batch_sparse_equals_single_solves(gpu):
+    """Sparse order 3 (exact line polynomial from the nonzeros): concurrent solves equal single ones."""
+    P = gpu
+    dims, R = (30, 25, 20), 3
+    coords, vals, _ = P.random_sparse_problem(dims, 2000, R, 0.01, 4)
+    t = P.DataTensor.coo(dims, coords, vals)
+    starts = np.stack([P.uniform_initial_guess(dims, R, 40 + s) for s in range(4)])
+    o = P.NgmresOptions(window=10, max_iters=200, tol_grad=1e-9, gradient_scale=float(sum(dims) * R))
+    b = P.solve_batch(t, starts, o, method=0, concurrency=4)
+    for i, u0 in enumerate(starts):
+        r = P.ngmres_solve(t, u0, o)
+        assert b.iters[i] == len(r.trace) - 1 and b.f[i] == r.f
+        assert np.array_equal(b.solutions[i], r.solution)

@@ -97,3 +97,17 @@ def test_ncg_iterate_and_solution_layout(gpu, O):
     ref = o.ncg(u0, tol_grad=1e-12, max_iters=15)
     res = P.ncg_solve(t, u0, P.NcgOptions(tol_grad=1e-12, max_iters=15))
     assert rel(res.solution, ref["u"]) <= 1e-6
+
+
+@pytest.mark.parametrize("dims,rank", [((40, 24, 22, 21), 20), ((50, 30, 26), 24)])
+def test_ncg_rank_above_16_matches_oracle(gpu, O, dims, rank):
+    """RP = 32 (line polynomial of order 3 and 4 with 16 < R <= 32): the first 15 rows."""
+    P = gpu
+    T, _, _ = P.dense_test_problem(dims, rank, 0.5, 1.0, 1.0, 2, noise_mode=1)
+    u0 = P.uniform_initial_guess(dims, rank, 2)
+    t = P.DataTensor.dense(T, dims)
+    o = O.Tensor.dense(dims, T)
+    ref = o.ncg(u0, tol_grad=1e-12, max_iters=15)
+    res = P.ncg_solve(t, u0, P.NcgOptions(tol_grad=1e-12, max_iters=15))
+    assert len(res.trace) == len(ref["trace"])
+    _rows_match(res, ref, n_f=15)
