@@ -386,8 +386,10 @@ __global__ void normalize_kernel(const NormParams p) {
     // the iterate / gradient element and the M0 element of one index together (their loads overlap)
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + tid; e < total || e < tm; e += (int64_t)gridDim.x * blockDim.x) {
         if (e < tm) {
-            const int r = (int)(e / p.m0_ld);
-            const int64_t i = e % p.m0_ld;
+            // 32-bit index math (tm, total < 2^31 for any iterate that fits a solve): 64-bit
+            // division costs ~100 instructions and dominated the kernel at n_u = 3e5
+            const int r = (int)e / p.m0_ld;
+            const int i = (int)e - r * p.m0_ld;
             double v = 0.0;
             if (r < p.R) {
                 const int src = perm[r];
@@ -399,10 +401,10 @@ __global__ void normalize_kernel(const NormParams p) {
         if (e < total) {
             int n = 0;
             while (e >= p.off[n + 1]) ++n;
-            const int64_t loc = e - p.off[n];
-            const int64_t In = p.dims[n];
-            const int r = (int)(loc / In);
-            const int64_t i = loc % In;
+            const int loc = (int)(e - p.off[n]);
+            const int In = (int)p.dims[n];
+            const int r = loc / In;
+            const int i = loc - r * In;
             const int src = perm[r];
             const int64_t at = p.off[n] + (int64_t)src * In + i;
             const double v = p.u[at];

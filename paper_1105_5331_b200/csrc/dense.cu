@@ -934,6 +934,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
         w->off[n + 1] = w->off[n] + t.dims[n] * R;
     }
     w->nu = w->off[t.order];
+    if (w->nu >= ((int64_t)1 << 31)) throw std::invalid_argument("device path: R * sum(I_n) must be < 2^31");
     const int sms = sm_count();
     int chunks = 0;
     for (int n = 0; n < t.order; ++n) {
