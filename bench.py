@@ -330,6 +330,13 @@ def main():
     starts = [np.ascontiguousarray(P.uniform_initial_guess(dims, R, next(e_seeds))) for _ in range(64)]
     for s in starts:
         P.host_register(s)
+    # one untimed cycle of the same calls first (W warm-up steps of the e2e leg): first-touch
+    # costs of this process (device memory pool growth, lazily loaded modules) stay out of the
+    # timed region; the timed region still builds the new tensor handle's graphs
+    tw = P.DataTensor.dense(T_pin, dims)
+    P.ngmres_solve(tw, starts[-1], P.NgmresOptions(window=20, max_iters=max(args.warmup, 3), tol_grad=tol,
+                                                   gradient_scale=float(nu)))
+    tw.close()
     barrier()
     te0 = time.perf_counter()
     te = P.DataTensor.dense(T_pin, dims)
