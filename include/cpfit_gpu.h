@@ -93,6 +93,13 @@ int cpfit_mttkrp(cpfit_tensor t, int64_t rank, const double* u, int mode, double
 int cpfit_objective(cpfit_tensor t, int64_t rank, const double* u, double* f);
 /* objective_and_gradient(t, k, grad) — kruskal.hpp:43; grad in pack() layout. */
 int cpfit_objective_and_gradient(cpfit_tensor t, int64_t rank, const double* u, double* grad, double* f);
+/* objective_and_gradient with the device's objective form selected: form 0 is the reference's
+ * residual form 1/2 sum (T - model)^2 (kruskal.cpp:83-102; what cpfit_objective_and_gradient
+ * computes); form 1 is the per-fibre three-term form the solver loop evaluates with until f
+ * stagnates (dense tensors; sparse tensors always use the three-term form of kruskal.cpp:146-148).
+ * Parity hook for the loop's default objective. */
+int cpfit_objective_and_gradient_form(cpfit_tensor t, int64_t rank, const double* u, int form, double* grad,
+                                      double* f);
 /* gram_hadamard(factors, skip) — tensor.hpp:124; out R x R column-major. */
 int cpfit_gram_hadamard(int order, const int64_t* dims, int64_t rank, const double* u, int skip, double* out);
 /* normalize_and_reorder(k) — kruskal.hpp:54 */

@@ -83,6 +83,8 @@ _SIGS = {
     "cpfit_mttkrp": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_int, _f64p]),
     "cpfit_objective": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.POINTER(C.c_double)]),
     "cpfit_objective_and_gradient": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p, C.POINTER(C.c_double)]),
+    "cpfit_objective_and_gradient_form": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_int, _f64p,
+                                                    C.POINTER(C.c_double)]),
     "cpfit_gram_hadamard": (C.c_int, [C.c_int, _i64p, C.c_int64, _f64p, C.c_int, _f64p]),
     "cpfit_normalize_and_reorder": (C.c_int, [C.c_int, _i64p, C.c_int64, _f64p, _f64p]),
     "cpfit_als_sweep": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p]),
@@ -163,6 +165,21 @@ def _f64(x) -> np.ndarray:
 
 def _dims(d) -> np.ndarray:
     return np.ascontiguousarray(d, dtype=np.int64)
+
+
+def _vec(x, n: int, what: str) -> np.ndarray:
+    """Contiguous float64 vector of exactly n entries (the C side reads and writes n doubles);
+    kruskal.cpp:208-209 unpack() rejects other lengths the same way."""
+    x = _f64(x).reshape(-1)
+    if x.size != n:
+        raise ValueError(f"{what}: vector length does not match shape and rank")
+    return x
+
+
+def _packed_len(dims, rank) -> int:
+    if rank < 1:
+        raise ValueError("KruskalTensor: rank must be >= 1")
+    return int(sum(int(d) for d in dims)) * int(rank)
 
 
 # ---- pack / unpack (kruskal.cpp:195-221) ---------------------------------------------------
@@ -280,6 +297,16 @@ def objective_and_gradient(t: DataTensor, u):
     return f.value, g
 
 
+def objective_and_gradient_form(t: DataTensor, u, form: int):
+    """form 0: the reference's residual objective (= objective_and_gradient); form 1: the
+    per-fibre three-term objective the device solver loop evaluates with (dense tensors)."""
+    u, r = t._rank(u)
+    g = np.empty(u.size)
+    f = C.c_double()
+    _check(lib.cpfit_objective_and_gradient_form(t._h, r, u, int(form), g, C.byref(f)))
+    return f.value, g
+
+
 def gradient(t, u):
     return objective_and_gradient(t, u)[1]
 
@@ -287,7 +314,7 @@ def gradient(t, u):
 def line_polynomial(t: DataTensor, u_bar, d, alphas):
     """(phi, dphi) at alphas from the device line-search polynomial (dense order 3)."""
     ub, r = t._rank(u_bar)
-    dv = _f64(d)
+    dv = _vec(d, ub.size, "line_polynomial")
     al = _f64(alphas)
     phi, dphi = np.zeros(al.size), np.zeros(al.size)
     _check(lib.cpfit_line_polynomial(t._h, r, ub, dv, al if al.size else np.zeros(1), al.size, phi, dphi))
@@ -303,14 +330,15 @@ def fit_h(t: DataTensor, u) -> float:
 
 def gram_hadamard(dims, rank, u, skip=-1):
     dims = _dims(dims)
+    u = _vec(u, _packed_len(dims, rank), "gram_hadamard")
     out = np.empty(rank * rank)
-    _check(lib.cpfit_gram_hadamard(len(dims), dims, rank, _f64(u), skip, out))
+    _check(lib.cpfit_gram_hadamard(len(dims), dims, rank, u, skip, out))
     return out.reshape((rank, rank), order="F")
 
 
 def normalize_and_reorder(dims, rank, u):
     dims = _dims(dims)
-    u = _f64(u)
+    u = _vec(u, _packed_len(dims, rank), "normalize_and_reorder")
     out = np.empty_like(u)
     _check(lib.cpfit_normalize_and_reorder(len(dims), dims, rank, u, out))
     return out
@@ -335,10 +363,14 @@ def accelerate(window_u, window_g, u_bar, g_bar, epsilon_reg=1e-12) -> AccelOutc
     wu = np.ascontiguousarray(np.asarray(window_u, dtype=np.float64).reshape(len(window_u), -1))
     wg = np.ascontiguousarray(np.asarray(window_g, dtype=np.float64).reshape(len(window_g), -1))
     m, n = wu.shape
+    if wg.shape != wu.shape:
+        raise ValueError("accelerate: window iterates and gradients must have the same shape")
+    u_bar = _vec(u_bar, n, "accelerate")
+    g_bar = _vec(g_bar, n, "accelerate")
     uh = np.empty(n)
     al = np.empty(max(m, 1))
     rr = C.c_double()
-    _check(lib.cpfit_accelerate(n, m, wu.reshape(-1), wg.reshape(-1), _f64(u_bar), _f64(g_bar), epsilon_reg, uh, al,
+    _check(lib.cpfit_accelerate(n, m, wu.reshape(-1), wg.reshape(-1), u_bar, g_bar, epsilon_reg, uh, al,
                                 C.byref(rr)))
     return AccelOutcome(uh, al[:m], rr.value)
 
@@ -523,7 +555,7 @@ class Solver:
         self.max_iters = opts.max_iters
 
     def set_initial(self, u0):
-        _check(lib.cpfit_solver_set_initial(self._h, _f64(u0)))
+        _check(lib.cpfit_solver_set_initial(self._h, _vec(u0, self.t.nu(self.rank), "Solver.set_initial")))
 
     def init(self):
         _check(lib.cpfit_solver_init(self._h))
@@ -536,7 +568,8 @@ class Solver:
     def restart(self, u0, max_iters_total) -> float:
         """New start point + init + loop; CUDA-event ms for init + loop."""
         ms = C.c_float()
-        _check(lib.cpfit_solver_restart(self._h, _f64(u0), int(max_iters_total), C.byref(ms)))
+        u0 = _vec(u0, self.t.nu(self.rank), "Solver.restart")
+        _check(lib.cpfit_solver_restart(self._h, u0, int(max_iters_total), C.byref(ms)))
         return ms.value
 
     def state(self):
@@ -546,7 +579,9 @@ class Solver:
         return dict(iters=it.value, stop=st.value, f=f.value, best_f=bf.value, fevals=fe.value)
 
     def trace(self, rows):
-        buf = (TraceRow * rows)()
+        if not 0 <= rows <= self.max_iters + 1:
+            raise ValueError("Solver.trace: rows must be in [0, max_iters + 1]")
+        buf = (TraceRow * max(rows, 1))()
         _check(lib.cpfit_solver_trace(self._h, buf, rows))
         return _trace_list(buf, rows)
 
@@ -632,8 +667,9 @@ def collinear_factors(dims, rank, c, seed):
 
 def full(dims, rank, u):
     dims = _dims(dims)
+    u = _vec(u, _packed_len(dims, rank), "full")
     out = np.empty(int(np.prod(dims)))
-    _check(lib.cpfit_full(len(dims), dims, rank, _f64(u), out), True)
+    _check(lib.cpfit_full(len(dims), dims, rank, u, out), True)
     return out
 
 

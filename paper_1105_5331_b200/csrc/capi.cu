@@ -276,7 +276,7 @@ int cpfit_mttkrp(cpfit_tensor t, int64_t rank, const double* u, int mode, double
     });
 }
 
-static int eval_impl(cpfit_tensor t, int64_t rank, const double* u, double* grad, double* f) {
+static int eval_impl(cpfit_tensor t, int64_t rank, const double* u, double* grad, double* f, int form = 0) {
     return guard([&] {
         std::lock_guard<std::mutex> lk(t->mu);
         check_rank(rank);
@@ -286,8 +286,10 @@ static int eval_impl(cpfit_tensor t, int64_t rank, const double* u, double* grad
         double* dg = du + w.nu;
         EvalScalars* sc = reinterpret_cast<EvalScalars*>(dg + w.nu);
         CPFIT_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * w.nu, cudaMemcpyHostToDevice, t->st));
-        // per-call objective uses the reference's residual form (kruskal.cpp:83-102)
-        eval_device(*t->t, w, du, dg, sc, nullptr, nullptr, t->st, grad != nullptr, t->one());
+        // per-call objective uses the reference's residual form (kruskal.cpp:83-102); form 1 selects
+        // the per-fibre three-term form the solver loop evaluates with (dense only)
+        if (form != 0 && form != 1) throw std::invalid_argument("objective form must be 0 (residual) or 1 (per-fibre)");
+        eval_device(*t->t, w, du, dg, sc, nullptr, nullptr, t->st, grad != nullptr, form == 1 ? nullptr : t->one());
         EvalScalars hs;
         CPFIT_CUDA(cudaMemcpyAsync(&hs, sc, sizeof(EvalScalars), cudaMemcpyDeviceToHost, t->st));
         if (grad) CPFIT_CUDA(cudaMemcpyAsync(grad, dg, sizeof(double) * w.nu, cudaMemcpyDeviceToHost, t->st));
@@ -300,6 +302,11 @@ int cpfit_objective(cpfit_tensor t, int64_t rank, const double* u, double* f) { 
 
 int cpfit_objective_and_gradient(cpfit_tensor t, int64_t rank, const double* u, double* grad, double* f) {
     return eval_impl(t, rank, u, grad, f);
+}
+
+int cpfit_objective_and_gradient_form(cpfit_tensor t, int64_t rank, const double* u, int form, double* grad,
+                                      double* f) {
+    return eval_impl(t, rank, u, grad, f, form);
 }
 
 int cpfit_gram_hadamard(int order, const int64_t* dims, int64_t rank, const double* u, int skip, double* out) {

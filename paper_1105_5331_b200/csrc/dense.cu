@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
 
 namespace cpfit_gpu {
 
@@ -925,6 +926,8 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
 EvalWork* work_create(const DevTensor& t, int R) {
     if (R < 1 || R > kMaxRank) throw std::invalid_argument("device path supports 1 <= rank <= 32");
     auto* w = new EvalWork();
+    // freed by work_destroy if a later allocation or shape check throws
+    std::unique_ptr<EvalWork, void (*)(EvalWork*)> owner(w, work_destroy);
     w->R = R;
     w->RP = (R <= 8) ? 8 : (R <= 16 ? 16 : 32);  // power of two: per-fiber lane groups
     w->order = t.order;
@@ -1065,7 +1068,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
         CPFIT_CUDA(cudaMalloc(&w->frows, sizeof(double) * (size_t)tot));
         CPFIT_CUDA(cudaMalloc(&w->f_part, sizeof(double) * 4));
     }
-    return w;
+    return owner.release();
 }
 
 void work_destroy(EvalWork* w) {

@@ -653,6 +653,15 @@ cudaGraph_t append_conditional(cudaStream_t st, cudaGraphConditionalHandle h, cu
 
 Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     : t_(t), R_(R), opt_(o), method_(method) {
+    try {
+        construct(t, R, o);
+    } catch (...) {
+        release();  // a throwing constructor runs no destructor: free what was allocated
+        throw;
+    }
+}
+
+void Solver::construct(DevTensor* t, int R, const SolverOptions& o) {
     CPFIT_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     CPFIT_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
     CPFIT_CUDA(cudaStreamCreateWithFlags(&st3_, cudaStreamNonBlocking));
@@ -715,7 +724,9 @@ Solver::Solver(DevTensor* t, int R, const SolverOptions& o, int method)
     build_graphs();
 }
 
-Solver::~Solver() {
+Solver::~Solver() { release(); }
+
+void Solver::release() {
     if (x_init_) cudaGraphExecDestroy(x_init_);
     if (x_loop_) cudaGraphExecDestroy(x_loop_);
     if (g_init_) cudaGraphDestroy(g_init_);
@@ -730,10 +741,14 @@ Solver::~Solver() {
     accel_destroy(a_);
     poly_destroy(pw_);
     work_destroy(w_);
-    cudaStreamDestroy(st_);
-    cudaStreamDestroy(st2_);
-    cudaStreamDestroy(st3_);
-    cudaStreamDestroy(st4_);
+    for (cudaStream_t s : {st_, st2_, st3_, st4_})
+        if (s) cudaStreamDestroy(s);
+    x_init_ = x_loop_ = nullptr;
+    g_init_ = g_loop_ = nullptr;
+    pw_ = nullptr;
+    a_ = nullptr;
+    w_ = nullptr;
+    st_ = st2_ = st3_ = st4_ = nullptr;
 }
 
 void Solver::build_graphs() {
@@ -1176,6 +1191,9 @@ SolverSummary Solver::summary() {
 }
 
 void Solver::copy_trace(TraceRow* out, int rows) {
+    if (rows < 0 || rows > trace_cap_)
+        throw std::invalid_argument("solver trace: rows must be in [0, max_iters + 1]");
+    if (rows == 0) return;
     CPFIT_CUDA(cudaMemcpyAsync(out, trace_, sizeof(TraceRow) * (size_t)rows, cudaMemcpyDeviceToHost, st_));
     sync();
 }

@@ -75,6 +75,8 @@ public:
     int64_t n() const { return n_; }
 
 private:
+    void construct(DevTensor* t, int R, const SolverOptions& o);
+    void release();
     void build_graphs();
     void run_loop_eager();
     void emit_poly_accept(cudaStream_t st, const void* ctl);

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <memory>
 #include <numeric>
 #include <vector>
 
@@ -64,6 +65,7 @@ __global__ void finite_check_kernel(const double* T, int64_t ldT, int I0, int64_
 DevTensor* tensor_create_dense(int order, const int64_t* dims, const double* host_vals, cudaStream_t st) {
     if (order < 1 || order > kMaxOrder) throw std::invalid_argument("Shape: order must be in [1, 8] on device");
     auto* t = new DevTensor();
+    std::unique_ptr<DevTensor, void (*)(DevTensor*)> owner(t, tensor_destroy);  // freed if a check throws
     t->order = order;
     t->K = 1;
     for (int n = 0; n < order; ++n) {
@@ -98,22 +100,20 @@ DevTensor* tensor_create_dense(int order, const int64_t* dims, const double* hos
     CPFIT_CUDA(cudaStreamSynchronize(st));
     cudaFree(part);
     cudaFree(bad);
-    if (hbad) {
-        tensor_destroy(t);
-        throw std::invalid_argument("DenseTensor: entries must be finite");
-    }
+    if (hbad) throw std::invalid_argument("DenseTensor: entries must be finite");
     dd s{0.0, 0.0};
     for (const dd& x : hp) s = dd_add(s, x);
     t->norm_sq = s.hi + s.lo;
     t->norm_sq_lo = (s.hi - t->norm_sq) + s.lo;  // ||T||^2 = norm_sq + norm_sq_lo in double-double
     t->norm = std::sqrt(t->norm_sq);
-    return t;
+    return owner.release();
 }
 
 DevTensor* tensor_create_coo(int order, const int64_t* dims, int64_t nnz_in, const int64_t* coords,
                              const double* vals, cudaStream_t st) {
     if (order < 1 || order > kMaxOrder) throw std::invalid_argument("Shape: order must be in [1, 8] on device");
     auto* t = new DevTensor();
+    std::unique_ptr<DevTensor, void (*)(DevTensor*)> owner(t, tensor_destroy);  // freed if a check throws
     t->order = order;
     t->sparse = true;
     t->K = 1;
@@ -160,7 +160,7 @@ DevTensor* tensor_create_coo(int order, const int64_t* dims, int64_t nnz_in, con
     t->norm = std::sqrt(s2);
     t->norm_sq = t->norm * t->norm;
     upload_sparse_modes(*t, cc, vv, st);
-    return t;
+    return owner.release();
 }
 
 void tensor_destroy(DevTensor* t) {
