@@ -62,6 +62,11 @@ struct LLT {
     Matrix matrix_u() const;  // L^T
 };
 
+// Eigen makeHouseholder on x[0..n) (tau, beta; essential part left in x[1..n)) and
+// applyHouseholderOnTheLeft on rows r0..r0+n of columns [c0, c1) of m.
+void make_householder(double* x, index_t n, double& tau, double& beta);
+void apply_householder_left(Matrix& m, index_t r0, index_t n, index_t c0, index_t c1, const double* ess, double tau);
+
 // Eigen::ColPivHouseholderQR<MatrixXd>(a).solve(b) for a single right-hand side.
 Vector colpiv_qr_solve(const Matrix& a, const Vector& b);
 

@@ -105,8 +105,6 @@ Matrix LLT::matrix_u() const {
     return u;
 }
 
-namespace {
-
 // Eigen MatrixBase::makeHouseholder on x[0..n): returns tau, beta, essential in x[1..n).
 void make_householder(double* x, index_t n, double& tau, double& beta) {
     double tail = 0.0;
@@ -142,8 +140,6 @@ void apply_householder_left(Matrix& m, index_t r0, index_t n, index_t c0, index_
         for (index_t i = 1; i < n; ++i) m(r0 + i, j) -= tau * ess[i - 1] * t;
     }
 }
-
-}  // namespace
 
 // Eigen ColPivHouseholderQR::computeInPlace + _solve_impl (single rhs).
 Vector colpiv_qr_solve(const Matrix& a, const Vector& b) {

@@ -72,6 +72,12 @@ _SIGS = {
     "oracle_ngmres_linear": (C.c_int, [C.c_int64, _f64p, _f64p, C.c_double, _f64p, C.c_int, C.c_int, C.c_double,
                                        C.c_double, C.c_int, C.c_double, C.c_int, _f64p, _f64p,
                                        C.POINTER(C.c_int64)]),
+    "oracle_problems_last_error": (C.c_char_p, []),
+    "oracle_dense_test_problem": (C.c_int, [C.c_int, _i64p, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                            C.c_uint64, C.c_int, _f64p, C.c_void_p]),
+    "oracle_uniform_initial_guess": (C.c_int, [C.c_int, _i64p, C.c_int64, C.c_uint64, _f64p]),
+    "oracle_random_sparse_problem": (C.c_int, [C.c_int, _i64p, C.c_int64, C.c_int64, C.c_double, C.c_uint64,
+                                               _i64p, _f64p]),
     "oracle_ncg_cp": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_double, C.c_int, _f64p, C.POINTER(TraceOut),
                                 C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
 }
@@ -210,6 +216,41 @@ class Tensor:
         _check(lib.oracle_ncg_cp(self.h, self.rank_of(u0), u0, tol_grad, max_iters, ub, tr, cap, C.byref(rows),
                                  C.byref(stop)))
         return dict(u=ub, trace=_trace(tr, rows.value), stop=stop.value)
+
+
+def _check_problems(rc):
+    if rc == 0:
+        return
+    msg = lib.oracle_problems_last_error().decode()
+    raise (ValueError if rc == 1 else OracleError)(msg)
+
+
+def dense_test_problem(dims, rank, c, l1, l2, seed, noise_mode=1, want_truth=False):
+    """problems.cpp:63-95 restated (noise_mode 1: BASELINE's l/100 scaling). Returns (T flat
+    first-mode-fastest, truth factors in pack order or None)."""
+    dims = np.ascontiguousarray(dims, dtype=np.int64)
+    t = np.empty(int(np.prod(dims)))
+    truth = np.empty(int(dims.sum()) * rank) if want_truth else None
+    _check_problems(lib.oracle_dense_test_problem(len(dims), dims, rank, c, l1, l2, seed, noise_mode, t,
+                                                  truth.ctypes.data if truth is not None else None))
+    return t, truth
+
+
+def uniform_initial_guess(dims, rank, seed):
+    """problems.cpp:137-145 restated."""
+    dims = np.ascontiguousarray(dims, dtype=np.int64)
+    out = np.empty(int(dims.sum()) * rank)
+    _check_problems(lib.oracle_uniform_initial_guess(len(dims), dims, rank, seed, out))
+    return out
+
+
+def random_sparse_problem(dims, nnz, rank, noise, seed):
+    """BASELINE.json configs[4] generator. Returns (coords nnz x N, values)."""
+    dims = np.ascontiguousarray(dims, dtype=np.int64)
+    coords = np.empty(nnz * len(dims), dtype=np.int64)
+    vals = np.empty(nnz)
+    _check_problems(lib.oracle_random_sparse_problem(len(dims), dims, nnz, rank, noise, seed, coords, vals))
+    return coords.reshape(-1, len(dims)), vals
 
 
 def _trace(tr, rows):

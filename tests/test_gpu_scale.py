@@ -1,0 +1,146 @@
+"""GPU parity at BASELINE.json scale (configs[2] 400^3 R=16, configs[3] 64^4 R=10, configs[4] 10M-nnz
+sparse R=10) against the CPU oracle on the same seeded inputs, through the C-ABI.
+
+Gates (BASELINE north_star): per-call MTTKRP / gradient / f within 1e-12 relative; the first 20
+N-GMRES iterates within 1e-8; final f within 1e-8 and iterations-to-tolerance within 2 %.
+
+Near convergence the gradient g = -M + A Gamma is the small difference of two terms of size |M|:
+the oracle's own g carries an error of ~eps |M| / |g| relative to |g| (8e-11 at the C2 generator's
+truth factors, h = 0.014), so there the gradient gate is stated against the cancelled terms,
+|g - g_oracle| <= 1e-12 |M| (the fp64 backward-error bound of the formula); f and every MTTKRP
+keep the plain 1e-12 relative gate at both points.
+
+The oracle runs here (C2: ~95 s for 20 reference-structured iterations; C3 ~45 s; C4 ~120 s)."""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+C2 = ((400, 400, 400), 16, 0.5, 1.0, 1.0, 1e-10)
+C3 = ((64, 64, 64, 64), 10, 0.7, 5.0, 0.0, 1e-9)
+C4 = ((10000, 10000, 10000), 10_000_000, 10, 0.01)
+
+
+def _dense_case(P, O, cfg):
+    dims, R, c, l1, l2, tol = cfg
+    T, truth, _ = P.dense_test_problem(dims, R, c, l1, l2, 0, noise_mode=1, want_truth=True)
+    u0 = P.uniform_initial_guess(dims, R, 0)
+    return dict(dims=dims, R=R, tol=tol, T=T, truth=truth, u0=u0, t=P.DataTensor.dense(T, dims),
+                o=O.Tensor.dense(dims, T), nu=float(sum(dims) * R))
+
+
+@pytest.fixture(scope="module")
+def c2(gpu, O):
+    return _dense_case(gpu, O, C2)
+
+
+def _step_iterates(P, case, k, opts):
+    """Device solver stepped one iteration at a time: (trace rows, iterates) for 1..k."""
+    s = P.Solver(case["t"], case["R"], opts, 0)
+    s.set_initial(case["u0"])
+    s.init()
+    rows, its = [], []
+    for it in range(1, k + 1):
+        s.run(it)
+        st = s.state()
+        rows.append(s.trace(it + 1)[it])
+        its.append(s.iterate())
+        if st["stop"] >= 0:
+            break
+    return rows, its
+
+
+def _compare_iterates(rows, its, ref, k, check_decisions=True):
+    worst_u, worst_f = 0.0, 0.0
+    for it in range(1, min(k, len(ref["iterates"]) - 1) + 1):
+        a, b = rows[it - 1], ref["trace"][it]
+        du = rel(its[it - 1], ref["iterates"][it])
+        df = abs(a["f"] - b["f"]) / abs(b["f"])
+        print(f"it {it:2d}: iterate {du:.2e}  f {df:.2e}  restart {int(a['restart'])}/{int(b['restart'])}  "
+              f"fevals {a['fevals']}/{b['fevals']}  beta {a['beta']:.10g}/{b['beta']:.10g}")
+        worst_u, worst_f = max(worst_u, du), max(worst_f, df)
+        assert du <= 1e-8, (it, du)
+        assert df <= 1e-8, (it, df)
+        if check_decisions:
+            assert a["restart"] == b["restart"] and a["fevals"] == b["fevals"], (it, a, b)
+    print(f"max over the first {k} iterates: iterate {worst_u:.2e}, f {worst_f:.2e}")
+
+
+def test_c2_per_call_at_start_and_near_convergence(gpu, O, c2):
+    P, t, o = gpu, c2["t"], c2["o"]
+    assert abs(t.norm() - o.norm()) <= 1e-12 * o.norm()
+    for tag, u in (("u0", c2["u0"]), ("truth", c2["truth"])):
+        ms = [o.mttkrp(u, m) for m in range(3)]
+        for m in range(3):
+            e = rel(t.mttkrp(u, m), ms[m])
+            print(f"{tag} mttkrp mode {m}: {e:.2e}")
+            assert e <= 1e-12
+        fo, go = o.eval(u)
+        mnorm = float(np.sqrt(sum(np.linalg.norm(x) ** 2 for x in ms)))
+        for form in (0, 1):  # 0: residual f (per-call default), 1: per-fibre f (the solver loop's)
+            f, g = P.objective_and_gradient_form(t, u, form)
+            ef, eg, egm = abs(f - fo) / abs(fo), rel(g, go), np.linalg.norm(g - go) / mnorm
+            print(f"{tag} form {form}: f {ef:.2e}  g {eg:.2e} (of |g|)  {egm:.2e} (of |M|)  h {np.sqrt(2 * fo) / o.norm():.4f}")
+            assert ef <= 1e-12
+            assert egm <= 1e-12
+            if tag == "u0":
+                assert eg <= 1e-12
+
+
+def test_c2_first_20_iterates(gpu, O, c2):
+    P = gpu
+    k = 20
+    ref = c2["o"].ngmres(c2["u0"], window=20, max_iters=k, tol_grad=c2["tol"], gradient_scale=c2["nu"],
+                         record_iterates=k + 1)
+    opts = P.NgmresOptions(window=20, max_iters=k, tol_grad=c2["tol"], gradient_scale=c2["nu"])
+    rows, its = _step_iterates(P, c2, k, opts)
+    _compare_iterates(rows, its, ref, k)
+
+
+def test_c3_full_solve_and_first_20_iterates(gpu, O):
+    """Order 4 with the degree-8 line polynomial: the first 20 iterates, then the full solve's stop
+    reason, final f and iteration count against the oracle's reference-structured solve."""
+    P = gpu
+    case = _dense_case(P, O, C3)
+    ref = case["o"].ngmres(case["u0"], window=20, max_iters=1000, tol_grad=case["tol"], gradient_scale=case["nu"],
+                           record_iterates=21)
+    opts = P.NgmresOptions(window=20, max_iters=1000, tol_grad=case["tol"], gradient_scale=case["nu"])
+    rows, its = _step_iterates(P, case, 20, P.NgmresOptions(window=20, max_iters=20, tol_grad=case["tol"],
+                                                            gradient_scale=case["nu"]))
+    _compare_iterates(rows, its, ref, 20)
+    res = P.ngmres_solve(case["t"], case["u0"], opts)
+    n, nr = len(res.trace) - 1, len(ref["trace"]) - 1
+    print(f"C3: device {n} iterations, oracle {nr}; f {res.f:.15e} vs {ref['f']:.15e}")
+    assert res.stop_reason == ref["stop"] == P.GRAD_TOL
+    assert abs(n - nr) <= max(1, int(0.02 * nr))
+    assert abs(res.f - ref["f"]) <= 1e-8 * abs(ref["f"])
+
+
+def test_c4_per_call_and_first_20_rows(gpu, O):
+    """Sparse 10M nnz: per-call MTTKRP (all modes), gradient and f at the start; then the first 20
+    N-GMRES iterates and trace f. From iteration 2 on this fit sits at the noise floor (f decreases
+    ~1e-7 relative per iteration) and phi is flat to within the rounding of the three-term f
+    (kruskal.cpp:146-148, ~1e-12 relative at h ~ 0.01): the Moré–Thuente step lengths and trial
+    counts then follow rounding on both sides and are reported, not gated; the iterates and f are."""
+    P = gpu
+    dims, nnz, R, noise = C4
+    coords, vals, _ = P.random_sparse_problem(dims, nnz, R, noise, 0)
+    t = P.DataTensor.coo(dims, coords, vals)
+    o = O.Tensor.coo(dims, coords, vals)
+    assert t.nnz() == nnz
+    u0 = P.uniform_initial_guess(dims, R, 0)
+    for m in range(3):
+        assert rel(t.mttkrp(u0, m), o.mttkrp(u0, m)) <= 1e-12
+    f, g = P.objective_and_gradient(t, u0)
+    fo, go = o.eval(u0)
+    assert abs(f - fo) <= 1e-12 * abs(fo)
+    assert rel(g, go) <= 1e-12
+    nu = float(sum(dims) * R)
+    k = 20
+    ref = o.ngmres(u0, window=20, max_iters=k, tol_grad=1e-300, gradient_scale=nu, record_iterates=k + 1)
+    case = dict(t=t, R=R, u0=u0)
+    rows, its = _step_iterates(P, case, k, P.NgmresOptions(window=20, max_iters=k, tol_grad=1e-300, gradient_scale=nu))
+    assert rows[0]["restart"] == ref["trace"][1]["restart"] and rows[0]["fevals"] == ref["trace"][1]["fevals"]
+    _compare_iterates(rows, its, ref, k, check_decisions=False)
