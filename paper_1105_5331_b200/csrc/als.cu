@@ -56,6 +56,7 @@ void gather_m(int64_t In, EvalWork& w, const double* part, int grid, int ld, int
               cudaStream_t st);
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
 void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st);
+void rowwise_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st);
 
 namespace {
 
@@ -637,16 +638,16 @@ __global__ void s_rescale_kernel(double* S, int64_t J, int R, const int* perm, c
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
                          int* status, cudaStream_t st, const double* m0_given, bool keep_s, bool grams_given,
                          bool defer_norm) {
-    if (defer_norm && t.sparse) throw std::logic_error("als sweep: deferred normalisation needs a dense tensor");
+    if (defer_norm && rowwise(t)) throw std::logic_error("als sweep: deferred normalisation needs a dense tensor");
     CPFIT_CUDA(cudaMemcpyAsync(work, u, sizeof(double) * w.nu, cudaMemcpyDeviceToDevice, st));
     if (!grams_given) grams_device(w, work, st);
     const int N = t.order;
     // Gamma_0 from the Grams of u; each later Gamma_n as soon as G_{n-1}' exists (side stream)
     chol_mode(w, 0, -1, status, st);
-    if (t.sparse) {
+    if (rowwise(t)) {
         for (int n = 0; n < N; ++n) {
             if (n > 0) fork_chol(w, n, status, st);
-            sparse_all_modes(t, w, work, n, st);
+            rowwise_modes(t, w, work, n, st);
             int64_t off = 0;
             for (int m = 0; m < n; ++m) off += t.dims[m] * w.RP;
             if (n > 0) join_chol(w, st);
@@ -687,8 +688,8 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
     // Gram still in solve partials: finalize_gram_side) and normalises afterwards
     // (normalize_grad), so S never needs the rescale below
     if (defer_norm) return;
-    normalize_device(w, work, out, st, N - 1, keep_s && !t.sparse, grams_given);
-    if (keep_s && !t.sparse) {
+    normalize_device(w, work, out, st, N - 1, keep_s && !rowwise(t), grams_given);
+    if (keep_s && !rowwise(t)) {
         const int blocks = (int)std::min<int64_t>(8 * 148, (t.J * w.RP + 255) / 256);
         switch (w.RP) {
             case 8: s_rescale_kernel<8><<<blocks, 256, 0, st>>>(w.S, t.J, w.R, w.nperm, w.nscale0); break;

@@ -711,7 +711,7 @@ int cpfit_bench_kernel(cpfit_tensor t, int64_t rank, const double* u, int kind, 
         cudaEvent_t e0, e1;
         CPFIT_CUDA(cudaEventCreate(&e0));
         CPFIT_CUDA(cudaEventCreate(&e1));
-        if (kind >= 3 && t->t->sparse) throw std::invalid_argument("fiber-pass kinds need a dense tensor");
+        if (kind >= 3 && rowwise(*t->t)) throw std::invalid_argument("fiber-pass kinds need a dense tensor");
         if (kind >= 3) grams_device(w, du, t->st);
         auto call = [&] {
             switch (kind) {

@@ -920,6 +920,27 @@ __global__ void grad_kernel(const GradParams p) {
 // ---------------------------------------------------------------------------------------
 // sparse hooks (sparse.cu)
 void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st);
+// generic dense hooks (generic.cu)
+void generic_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st);
+void generic_plan(const DevTensor& t, int RP, int n, int* gx, int64_t* cols_per_cta, int* gy);
+
+// every mode's M_n (only_mode < 0) or one mode's into w.sp_part, for a rowwise tensor
+void rowwise_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st) {
+    if (t.generic)
+        generic_all_modes(t, w, u, only_mode, st);
+    else
+        sparse_all_modes(t, w, u, only_mode, st);
+}
+
+bool fiber_path_fits(int order, int64_t I0) {
+    if (order < 2 || I0 < 1) return false;
+    const int nchunk = (int)((I0 + 31) / 32);
+    if (nchunk > 13) return false;
+    for (int rp : {8, 16, 32})
+        if (std::max(fiber_smem(rp, nchunk, I0, kFStages), spass_smem(rp, nchunk, I0, kFStages)) > 227 * 1024)
+            return false;
+    return true;
+}
 
 // ---------------------------------------------------------------------------------------
 
@@ -949,7 +970,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
     CPFIT_CUDA(cudaMalloc(&w->gram, sizeof(double) * (size_t)t.order * w->RP * w->RP));
     w->red_grid = sms * 2;
     CPFIT_CUDA(cudaMalloc(&w->red, sizeof(double) * 3 * (size_t)w->red_grid));
-    if (!t.sparse) {  // reduce_grad: one block per 32 outputs of M_0 .. M_{N-1}
+    if (!rowwise(t)) {  // reduce_grad: one block per 32 outputs of M_0 .. M_{N-1}
         int64_t b = (w->RP * 32 * (int64_t)((t.dims[0] + 31) / 32) + 31) / 32;
         for (int n = 1; n < t.order; ++n) b += (t.dims[n] * w->RP + 31) / 32;
         w->rg_blocks = b;
@@ -970,7 +991,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
     CPFIT_CUDA(cudaMemset(w->counter, 0, sizeof(unsigned int) * kCounters));
     CPFIT_CUDA(cudaMalloc(&w->lvl_cnt, sizeof(unsigned int) * kLvlCounters));
     CPFIT_CUDA(cudaMemset(w->lvl_cnt, 0, sizeof(unsigned int) * kLvlCounters));
-    if (!t.sparse) {
+    if (!rowwise(t)) {
         if (t.order < 2) throw std::invalid_argument("device dense path needs order >= 2");
         const int I0 = (int)t.dims[0];
         w->fiber_nchunk = (I0 + 31) / 32;
@@ -1066,7 +1087,18 @@ EvalWork* work_create(const DevTensor& t, int R) {
         for (int n = 0; n < t.order; ++n) tot += t.dims[n] * w->RP;
         CPFIT_CUDA(cudaMalloc(&w->sp_part, sizeof(double) * (size_t)tot));
         CPFIT_CUDA(cudaMalloc(&w->frows, sizeof(double) * (size_t)tot));
-        CPFIT_CUDA(cudaMalloc(&w->f_part, sizeof(double) * 4));
+        if (t.generic) {
+            int64_t most = 1;
+            for (int n = 0; n < t.order; ++n) {
+                int gx, gy;
+                int64_t cpc;
+                generic_plan(t, w->RP, n, &gx, &cpc, &gy);
+                most = std::max<int64_t>(most, (int64_t)gx * t.dims[n] * w->RP);
+                if (n == 0) w->gen_fgrid = gx * gy;
+            }
+            CPFIT_CUDA(cudaMalloc(&w->gen_part, sizeof(double) * (size_t)most));
+        }
+        CPFIT_CUDA(cudaMalloc(&w->f_part, sizeof(double) * (size_t)std::max(4, w->gen_fgrid)));
     }
     return owner.release();
 }
@@ -1083,6 +1115,7 @@ void work_destroy(EvalWork* w) {
     cudaFree(w->f_part);
     cudaFree(w->sp_part);
     cudaFree(w->frows);
+    cudaFree(w->gen_part);
     cudaFree(w->counter);
     cudaFree(w->lvl_cnt);
     cudaFree(w->chol);
@@ -1126,7 +1159,7 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
     p.d = d;
     p.gram = w.gram;
     p.need_grad = need_grad ? 1 : 0;
-    if (t.sparse) {
+    if (rowwise(t)) {
         p.sp_out = w.sp_part;
         int64_t acc = 0;
         for (int n = 0; n < t.order; ++n) {
@@ -1140,7 +1173,7 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
     }
     p.red = w.red;
     p.f_part = w.f_part;
-    p.f_grid = t.sparse ? 0 : w.fiber_grid;
+    p.f_grid = t.sparse ? 0 : (t.generic ? w.gen_fgrid : w.fiber_grid);
     p.sparse = t.sparse ? 1 : 0;
     p.norm_sq = t.norm_sq;
     p.sc = sc;
@@ -1188,7 +1221,7 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
                  cudaEvent_t grad_dep) {
     (void)status;
     if (!grams_given) grams_device(w, u, st);
-    if (!t.sparse) {
+    if (!rowwise(t)) {
         // fused pass: S, M0 partials and per-fiber objective — or, when w.S already holds
         // T x_1 A0(u), M0 and the objective only (no S contraction)
         if (s_given)
@@ -1211,7 +1244,7 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
         }
         reduce_jobs(jobs, st);
     } else {
-        sparse_all_modes(t, w, u, -1, st);
+        rowwise_modes(t, w, u, -1, st);
     }
     run_grad(t, w, u, g, d, need_grad, sc, st);
 }
@@ -1323,8 +1356,8 @@ void mttkrp3_last_only(EvalWork& w, const double* u, double* out, cudaStream_t s
 void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st) {
     const int64_t In = t.dims[mode];
     const int blocks = (int)std::min<int64_t>(1024, (In * w.R + 255) / 256);
-    if (t.sparse) {
-        sparse_all_modes(t, w, u, mode, st);
+    if (rowwise(t)) {
+        rowwise_modes(t, w, u, mode, st);
         int64_t off = 0;
         for (int n = 0; n < mode; ++n) off += t.dims[n] * w.RP;
         gather_m_kernel<<<blocks, 256, 0, st>>>(In, w.R, w.RP, w.sp_part + off, 1, 0, 1, out);

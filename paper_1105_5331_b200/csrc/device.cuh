@@ -24,6 +24,9 @@ struct DevTensor {
     int64_t dims[kMaxOrder] = {};
     int64_t K = 0;
     bool sparse = false;
+    // dense, but evaluated per mode by the generic kernels (generic.cu) like a sparse tensor:
+    // order 1, or mode-0 fibres too long for the fibre tiles (see fiber_path_fits)
+    bool generic = false;
     double norm = 0.0, norm_sq = 0.0, norm_sq_lo = 0.0;  // ||T||^2 = norm_sq + norm_sq_lo (dense)
     // dense
     double* T = nullptr;
@@ -34,6 +37,11 @@ struct DevTensor {
     int64_t nnz = 0;
     struct SparseModes* modes = nullptr;
 };
+
+// per-mode ("rowwise") evaluation: sparse tensors and generic dense tensors
+inline bool rowwise(const DevTensor& t) { return t.sparse || t.generic; }
+// the fibre-tile passes take a dense tensor of this order and mode-0 length for every rank
+bool fiber_path_fits(int order, int64_t I0);
 
 int sm_count();  // SMs of the current device (cached)
 // fiber-pass barrier-wait counters (filled only by a -DCPFIT_FIBER_PROF build)
@@ -88,6 +96,9 @@ struct EvalWork {
     // sparse
     double* sp_part = nullptr;  // per-mode outputs I_n x RP
     double* frows = nullptr;    // row-major RP-padded factor copies (sum I_n x RP)
+    // generic dense (generic.cu): column-range partials of one mode, residual partials count
+    double* gen_part = nullptr;
+    int gen_fgrid = 0;
     // reductions
     double* red = nullptr;      // per-CTA partials for norms/dots
     double* rg_red = nullptr;   // reduce_grad block partials [rg_blocks][3] (dense)

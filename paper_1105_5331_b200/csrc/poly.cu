@@ -569,7 +569,9 @@ void poly_point_device(EvalWork& w, const PolyWork& pw, const double* ub, const 
     CPFIT_CUDA(cudaGetLastError());
 }
 
-bool poly_supported(const DevTensor& t) { return t.order == 3 || (t.order == 4 && !t.sparse); }
+bool poly_supported(const DevTensor& t) {
+    return !t.generic && (t.order == 3 || (t.order == 4 && !t.sparse));
+}
 
 PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {
     auto* p = new PolyWork();

@@ -692,7 +692,7 @@ void Solver::construct(DevTensor* t, int R, const SolverOptions& o) {
     if (method_ == 0) {
         alloc(&wu_, n_ * cap_);
         alloc(&wg_, n_ * cap_);
-        if (!t->sparse) {
+        if (!rowwise(*t)) {
             m0_n_ = (int64_t)w_->RP * 32 * w_->fiber_nchunk;
             alloc(&m0_cur_, m0_n_);
             alloc(&m0_bar_, m0_n_);
@@ -708,7 +708,7 @@ void Solver::construct(DevTensor* t, int R, const SolverOptions& o) {
     // Grams handed on by the normalisations (no Gram pass at the sweep start / for u_bar)
     gout_ = (int64_t)t->order * w_->RP * w_->RP <= kGramsOutMax;
     if (gout_) alloc(&gram_bar_, gram_n());
-    defer_ = method_ == 0 && !t->sparse && gout_;
+    defer_ = method_ == 0 && !rowwise(*t) && gout_;
     norm_nb_ = (int)std::min<int64_t>(296, (n_ + 255) / 256);
     // exact polynomial line search: dense order 3, default objective handling, not disabled
     const char* np = std::getenv("CPFIT_NO_POLY_LS");
@@ -933,8 +933,8 @@ void Solver::build_graphs() {
     } else {
         // stand-alone ALS iteration (als.cpp:79-95)
         // the previous evaluation (of u) left M0(u) in w.m0 for dense tensors
-        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, t_->sparse ? nullptr : w_->m0, true, gout_);
-        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid, !t_->sparse, gout_);
+        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, rowwise(*t_) ? nullptr : w_->m0, true, gout_);
+        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid, !rowwise(*t_), gout_);
     }
     if (method_ != 2) {
         k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
@@ -1011,7 +1011,7 @@ void Solver::emit_bar(cudaStream_t st, const void* ctl) {
         return;
     }
     als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st, m0_cur_, true, gout_);
-    eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st, true, &s->resid, !t_->sparse, gout_);
+    eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st, true, &s->resid, !rowwise(*t_), gout_);
     if (m0_bar_) CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st));
     if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st));
 }
@@ -1147,8 +1147,8 @@ void Solver::run_loop_eager() {
             emit_ncg_end(st_, &c, none);
             continue;
         } else {
-            als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, t_->sparse ? nullptr : w_->m0, true, gout_);
-            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid, !t_->sparse, gout_);
+            als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, rowwise(*t_) ? nullptr : w_->m0, true, gout_);
+            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid, !rowwise(*t_), gout_);
         }
         k_commit<<<1, 1, 0, st_>>>(c, none);
         k_commit_vec<<<vb, 256, 0, st_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,

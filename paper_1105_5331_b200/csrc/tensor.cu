@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 #include <memory>
 #include <numeric>
@@ -76,6 +77,10 @@ DevTensor* tensor_create_dense(int order, const int64_t* dims, const double* hos
         t->K *= dims[n];
     }
     t->sparse = false;
+    // shapes the fibre tiles do not take run the generic per-mode kernels (generic.cu);
+    // CPFIT_FORCE_GENERIC=1 at creation selects them for any shape (tests)
+    const char* fg = std::getenv("CPFIT_FORCE_GENERIC");
+    t->generic = !fiber_path_fits(order, dims[0]) || (fg && fg[0] == '1');
     t->ldT = round_up64(dims[0], 4);
     t->J = t->K / dims[0];
     const size_t bytes = sizeof(double) * (size_t)t->ldT * t->J;
