@@ -5,6 +5,7 @@
 #include "solver.cuh"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -84,6 +85,39 @@ struct cpfit_tensor_s {
         return scratch;
     }
 };
+
+// Dense tensor handles of a destroyed DataTensor are parked here (up to CPFIT_TENSOR_POOL_MB of
+// device memory, default 8192; 0 disables) with their workspaces and captured solver graphs, and
+// a new dense tensor of the same shape and kind takes one over: its values are uploaded into the
+// same device buffers (tensor_fill_dense), so the graphs — which read T, the fibre norms and
+// ||T|| through those buffers — stay valid and the new handle pays only the upload, not the
+// workspace allocation or graph capture/instantiation (tens of ms at 400^3). Graph caches are
+// thus keyed by (shape, rank, options), not by handle.
+namespace {
+struct TensorPool {
+    std::mutex mu;
+    std::vector<cpfit_tensor_s*> items;  // oldest first
+    size_t bytes = 0;
+};
+TensorPool& tensor_pool() {
+    static TensorPool* p = new TensorPool();  // never destroyed: outlives static destructors
+    return *p;
+}
+size_t pool_cap_bytes() {
+    static const size_t cap = [] {
+        const char* e = std::getenv("CPFIT_TENSOR_POOL_MB");
+        return (size_t)(e ? std::strtoull(e, nullptr, 10) : 8192ull) << 20;
+    }();
+    return cap;
+}
+size_t handle_bytes(const cpfit_tensor_s* h) { return sizeof(double) * (size_t)h->t->ldT * (size_t)h->t->J; }
+bool same_dense_kind(const DevTensor& a, int order, const int64_t* dims, bool generic) {
+    if (a.sparse || a.order != order || a.generic != generic) return false;
+    for (int n = 0; n < order; ++n)
+        if (a.dims[n] != dims[n]) return false;
+    return true;
+}
+}  // namespace
 
 struct cpfit_solver_s {
     std::unique_ptr<Solver> s;
@@ -230,6 +264,32 @@ void cpfit_default_ngmres_options(cpfit_ngmres_options* o) {
 
 int cpfit_tensor_create_dense(int order, const int64_t* dims, const double* values, cpfit_tensor* out) {
     return guard([&] {
+        if (order >= 1 && order <= kMaxOrder) {
+            bool dims_ok = true;
+            for (int n = 0; n < order; ++n) dims_ok = dims_ok && dims[n] >= 1;
+            if (dims_ok) {
+                const char* fg = std::getenv("CPFIT_FORCE_GENERIC");
+                const bool generic = !fiber_path_fits(order, dims[0]) || (fg && fg[0] == '1');
+                cpfit_tensor_s* reuse = nullptr;
+                {
+                    TensorPool& p = tensor_pool();
+                    std::lock_guard<std::mutex> lk(p.mu);
+                    for (size_t i = 0; i < p.items.size(); ++i)
+                        if (same_dense_kind(*p.items[i]->t, order, dims, generic)) {
+                            reuse = p.items[i];
+                            p.bytes -= handle_bytes(reuse);
+                            p.items.erase(p.items.begin() + (std::ptrdiff_t)i);
+                            break;
+                        }
+                }
+                if (reuse) {
+                    std::unique_ptr<cpfit_tensor_s> h(reuse);  // deleted if the new values are rejected
+                    tensor_fill_dense(*h->t, values, h->st);
+                    *out = h.release();
+                    return;
+                }
+            }
+        }
         auto h = std::make_unique<cpfit_tensor_s>();
         CPFIT_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
         h->t = tensor_create_dense(order, dims, values, h->st);
@@ -249,7 +309,29 @@ int cpfit_tensor_create_coo(int order, const int64_t* dims, int64_t nnz, const i
 }
 
 int cpfit_tensor_destroy(cpfit_tensor t) {
-    return guard([&] { delete t; });
+    return guard([&] {
+        if (!t) return;
+        const size_t cap = pool_cap_bytes();
+        if (t->t && !t->t->sparse && handle_bytes(t) <= cap) {
+            // wait for this handle's work before another thread may refill it
+            CPFIT_CUDA(cudaStreamSynchronize(t->st));
+            std::vector<cpfit_tensor_s*> evict;
+            {
+                TensorPool& p = tensor_pool();
+                std::lock_guard<std::mutex> lk(p.mu);
+                p.items.push_back(t);
+                p.bytes += handle_bytes(t);
+                while (p.bytes > cap && !p.items.empty()) {
+                    p.bytes -= handle_bytes(p.items.front());
+                    evict.push_back(p.items.front());
+                    p.items.erase(p.items.begin());
+                }
+            }
+            for (cpfit_tensor_s* e : evict) delete e;
+            return;
+        }
+        delete t;
+    });
 }
 
 int cpfit_tensor_norm(cpfit_tensor t, double* norm) {

@@ -799,7 +799,7 @@ struct GradParams {
     const double* f_part;
     int f_grid;
     int sparse;  // three-term objective (kruskal.cpp:146-148)
-    double norm_sq;
+    const double* norm_sq;  // device ||T||^2 (DevTensor::dscal + 1)
     EvalScalars* sc;
     int has_d;
     unsigned int* counter;
@@ -907,7 +907,7 @@ __global__ void grad_kernel(const GradParams p) {
         gs = warp_sum(gs);
     }
     if (lane == 0) {
-        p.sc->f = p.sparse ? 0.5 * p.norm_sq - c + 0.5 * gs : 0.5 * fs;
+        p.sc->f = p.sparse ? 0.5 * *p.norm_sq - c + 0.5 * gs : 0.5 * fs;
         p.sc->gnorm2 = a;
         p.sc->inner = c;
         if (p.has_d) p.sc->gdotd = b;
@@ -1175,7 +1175,7 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
     p.f_part = w.f_part;
     p.f_grid = t.sparse ? 0 : (t.generic ? w.gen_fgrid : w.fiber_grid);
     p.sparse = t.sparse ? 1 : 0;
-    p.norm_sq = t.norm_sq;
+    p.norm_sq = t.dscal + 1;
     p.sc = sc;
     p.has_d = d ? 1 : 0;
     p.counter = w.counter + kCounterGrad;

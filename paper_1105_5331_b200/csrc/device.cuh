@@ -28,6 +28,9 @@ struct DevTensor {
     // order 1, or mode-0 fibres too long for the fibre tiles (see fiber_path_fits)
     bool generic = false;
     double norm = 0.0, norm_sq = 0.0, norm_sq_lo = 0.0;  // ||T||^2 = norm_sq + norm_sq_lo (dense)
+    // the same three scalars in device memory: captured graphs read them from here, so a
+    // pooled tensor refilled with new values (capi.cu) keeps its graphs valid
+    double* dscal = nullptr;
     // dense
     double* T = nullptr;
     int64_t ldT = 0;  // padded fiber stride
@@ -52,6 +55,8 @@ DevTensor* tensor_create_dense(int order, const int64_t* dims, const double* hos
 DevTensor* tensor_create_coo(int order, const int64_t* dims, int64_t nnz, const int64_t* coords_aos,
                              const double* vals, cudaStream_t st);
 void tensor_destroy(DevTensor* t);
+// new values into an existing dense tensor of the same shape (upload, finite check, norms)
+void tensor_fill_dense(DevTensor& t, const double* host_vals, cudaStream_t st);
 
 // last-block-done counters (one per kernel family; each resets its own after use)
 constexpr int kLvlCounters = 1024;

@@ -228,7 +228,7 @@ struct CoefParams {
     const dd* grams;   // [mode][kind][RP*RP]
     const dd* s8part;  // [block][8] partials of the eight contractions
     int s8_blocks;
-    dd half_norm_sq;
+    const double* tn;  // device [||T||, ||T||^2 hi, lo] (DevTensor::dscal)
     dd* coef;          // [kPolyDeg + 1]
 };
 
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(256) coef_kernel(const CoefParams p) {
         for (int k = 0; k <= kPolyDeg3; ++k) {
             dd v = dd_mul(dd{0.5, 0.0}, tot[k]);
             if (k <= 3) v = dd_sub(v, a[k]);
-            if (k == 0) v = dd_add(v, p.half_norm_sq);
+            if (k == 0) v = dd_add(v, dd{0.5 * p.tn[1], 0.5 * p.tn[2]});
             p.coef[k] = v;
         }
         for (int k = kPolyDeg3 + 1; k <= kPolyDeg; ++k) p.coef[k] = dd{0.0, 0.0};
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(256) coef4_kernel(const CoefParams p) {
         for (int k = 0; k <= kPolyDeg; ++k) {
             dd x = dd_mul(dd{0.5, 0.0}, tot[k]);
             if (k <= 4) x = dd_sub(x, a[k]);
-            if (k == 0) x = dd_add(x, p.half_norm_sq);
+            if (k == 0) x = dd_add(x, dd{0.5 * p.tn[1], 0.5 * p.tn[2]});
             p.coef[k] = x;
         }
     }
@@ -624,7 +624,7 @@ void launch_coef(const DevTensor& t, const EvalWork& w, const PolyWork& pw, int 
     q.grams = pw.grams;
     q.s8part = pw.s8part;
     q.s8_blocks = s8_blocks;
-    q.half_norm_sq = dd{0.5 * t.norm_sq, 0.5 * t.norm_sq_lo};
+    q.tn = t.dscal;
     q.coef = pw.coef;
     coef_kernel<<<1, 256, 0, st>>>(q);
     CPFIT_CUDA(cudaGetLastError());
@@ -687,7 +687,7 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
         q.grams = pw.grams;
         q.s8part = pw.s8part;
         q.s8_blocks = sg.x;
-        q.half_norm_sq = dd{0.5 * t.norm_sq, 0.5 * t.norm_sq_lo};
+        q.tn = t.dscal;
         q.coef = pw.coef;
         coef4_kernel<<<1, 256, 0, st>>>(q);
         CPFIT_CUDA(cudaGetLastError());

@@ -70,7 +70,8 @@ struct Ctl {
     int bar_nb;
     TraceRow* trace;
     int trace_cap;
-    double gradient_scale, hscale, tol_grad;
+    double gradient_scale, tol_grad;
+    const double* hscale;  // device ||T|| (DevTensor::dscal): graphs stay valid when a pooled tensor is refilled
     int resid_always;
     int cap;
     int restart_on_ascent;
@@ -116,7 +117,7 @@ __global__ void k_reset(Ctl c, int max_iters) {
 // are below the per-fiber form's rounding floor (~1e-14 (0.02/h)^2 relative).
 __device__ void update_objective_form(const Ctl& c, DevState& s, double f_old) {
     if (s.resid) return;
-    if (2.0 * s.f < 1e-6 * c.hscale * c.hscale || (f_old - s.f) < 1e-8 * s.f) s.resid = 1;
+    if (2.0 * s.f < 1e-6 * *c.hscale * *c.hscale || (f_old - s.f) < 1e-8 * s.f) s.resid = 1;
 }
 
 // after canonical(u0) + eval: window seeded with (u, g), trace row 0, best = u
@@ -130,11 +131,11 @@ __global__ void k_after_init(Ctl c) {
     s.ring[1] = 0;
     s.slot = 0;
     const double gn = sqrt(s.gnorm2);
-    c.trace[0] = TraceRow{0, 0, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, c.hscale), gn / c.gradient_scale,
+    c.trace[0] = TraceRow{0, 0, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, *c.hscale), gn / c.gradient_scale,
                           0.0, s.fevals, s.gevals, 0};
     if (s.status) s.stop = 100 + s.status;
     if ((c.als_mode || c.ncg) && gn / c.gradient_scale <= c.tol_grad) s.stop = 0;  // als.cpp:74-77, ncg.cpp:34-37
-    if (2.0 * s.f < 1e-6 * c.hscale * c.hscale) s.resid = 1;
+    if (2.0 * s.f < 1e-6 * *c.hscale * *c.hscale) s.resid = 1;
 }
 
 __global__ void k_set_cond_running(Ctl c, cudaGraphConditionalHandle h) {
@@ -366,7 +367,7 @@ __global__ void k_commit(Ctl c, cudaGraphConditionalHandle loop_h) {
     s.iter += 1;
     const double gn = sqrt(s.gnorm2);
     if (s.iter < c.trace_cap)
-        c.trace[s.iter] = TraceRow{s.iter, s.restart, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, c.hscale),
+        c.trace[s.iter] = TraceRow{s.iter, s.restart, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, *c.hscale),
                                    gn / c.gradient_scale, s.beta, s.fevals, s.gevals, s.iter};
     s.is_best = (s.f < s.best_f) ? 1 : 0;
     if (s.is_best) s.best_f = s.f;
@@ -545,7 +546,7 @@ __global__ void k_ncg_commit(Ctl c, const double* red, int nb, cudaGraphConditio
         s.gnorm2 = q;
         const double gn = sqrt(q);
         if (s.rows < c.trace_cap)
-            c.trace[s.rows] = TraceRow{s.iter, s.restart, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, c.hscale),
+            c.trace[s.rows] = TraceRow{s.iter, s.restart, (globaltimer() - s.t0) * 1e-9, s.f, fit_h(s.f, *c.hscale),
                                        gn / c.gradient_scale, s.beta, s.fevals, s.gevals, 0};
         s.rows += 1;
         s.is_best = (s.f < s.best_f) ? 1 : 0;
@@ -771,7 +772,7 @@ void Solver::build_graphs() {
     c.trace = trace_;
     c.trace_cap = trace_cap_;
     c.gradient_scale = opt_.gradient_scale;
-    c.hscale = t_->norm;
+    c.hscale = t_->dscal;
     c.tol_grad = opt_.tol_grad;
     c.resid_always = opt_.residual_objective;
     c.cap = cap_;

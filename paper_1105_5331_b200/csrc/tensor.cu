@@ -23,9 +23,13 @@ namespace cpfit_gpu {
 
 namespace {
 
-__global__ void fiber_norm_kernel(const double* T, int64_t ldT, int I0, int64_t J, double* fn2, dd* block_part) {
+// one pass over T: per-fibre ||t_f||^2 and block partials of ||T||^2 in double-double, and the
+// finite check (DenseTensor's all_finite, tensor.cpp:44-54)
+__global__ void fiber_norm_kernel(const double* T, int64_t ldT, int I0, int64_t J, double* fn2, dd* block_part,
+                                  int* bad) {
     __shared__ dd red[32];
     dd acc{0.0, 0.0};
+    bool finite = true;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -33,6 +37,7 @@ __global__ void fiber_norm_kernel(const double* T, int64_t ldT, int I0, int64_t 
         dd s{0.0, 0.0};
         for (int i = lane; i < I0; i += 32) {
             const double v = T[f * ldT + i];
+            finite = finite && isfinite(v);
             s = dd_fma(s, v, v);
         }
 #pragma unroll
@@ -45,6 +50,7 @@ __global__ void fiber_norm_kernel(const double* T, int64_t ldT, int I0, int64_t 
             acc = dd_add(acc, s);
         }
     }
+    if (!finite) atomicOr(bad, 1);
     if (lane == 0) red[warp] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -54,11 +60,10 @@ __global__ void fiber_norm_kernel(const double* T, int64_t ldT, int I0, int64_t 
     }
 }
 
-__global__ void finite_check_kernel(const double* T, int64_t ldT, int I0, int64_t J, int* bad) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < J * I0; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t f = e / I0, i = e % I0;
-        if (!isfinite(T[f * ldT + i])) atomicOr(bad, 1);
-    }
+void set_device_norms(DevTensor& t, cudaStream_t st) {
+    const double h[3] = {t.norm, t.norm_sq, t.norm_sq_lo};
+    CPFIT_CUDA(cudaMemcpyAsync(t.dscal, h, sizeof(h), cudaMemcpyHostToDevice, st));
+    CPFIT_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace
@@ -85,33 +90,43 @@ DevTensor* tensor_create_dense(int order, const int64_t* dims, const double* hos
     t->J = t->K / dims[0];
     const size_t bytes = sizeof(double) * (size_t)t->ldT * t->J;
     CPFIT_CUDA(cudaMalloc(&t->T, bytes));
-    if (t->ldT != dims[0]) CPFIT_CUDA(cudaMemsetAsync(t->T, 0, bytes, st));
-    CPFIT_CUDA(cudaMemcpy2DAsync(t->T, sizeof(double) * t->ldT, host_vals, sizeof(double) * dims[0],
-                                 sizeof(double) * dims[0], t->J, cudaMemcpyHostToDevice, st));
     CPFIT_CUDA(cudaMalloc(&t->fiber_norm2, sizeof(double) * t->J));
+    CPFIT_CUDA(cudaMalloc(&t->dscal, sizeof(double) * 3));
+    if (t->ldT != dims[0]) CPFIT_CUDA(cudaMemsetAsync(t->T, 0, bytes, st));  // pads stay zero
+    tensor_fill_dense(*t, host_vals, st);
+    return owner.release();
+}
+
+void tensor_fill_dense(DevTensor& t, const double* host_vals, cudaStream_t st) {
+    const int64_t I0 = t.dims[0];
+    CPFIT_CUDA(cudaMemcpy2DAsync(t.T, sizeof(double) * t.ldT, host_vals, sizeof(double) * I0, sizeof(double) * I0, t.J,
+                                 cudaMemcpyHostToDevice, st));
     const int blocks = 592;
-    dd* part;
-    int* bad;
-    CPFIT_CUDA(cudaMalloc(&part, sizeof(dd) * blocks));
-    CPFIT_CUDA(cudaMalloc(&bad, sizeof(int)));
-    CPFIT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
-    finite_check_kernel<<<blocks, 256, 0, st>>>(t->T, t->ldT, (int)dims[0], t->J, bad);
-    fiber_norm_kernel<<<blocks, 256, 0, st>>>(t->T, t->ldT, (int)dims[0], t->J, t->fiber_norm2, part);
+    struct Scratch {
+        dd* part = nullptr;
+        int* bad = nullptr;
+        ~Scratch() {
+            cudaFree(part);
+            cudaFree(bad);
+        }
+    } sc;
+    CPFIT_CUDA(cudaMalloc(&sc.part, sizeof(dd) * blocks));
+    CPFIT_CUDA(cudaMalloc(&sc.bad, sizeof(int)));
+    CPFIT_CUDA(cudaMemsetAsync(sc.bad, 0, sizeof(int), st));
+    fiber_norm_kernel<<<blocks, 256, 0, st>>>(t.T, t.ldT, (int)I0, t.J, t.fiber_norm2, sc.part, sc.bad);
     CPFIT_CUDA(cudaGetLastError());
     std::vector<dd> hp(blocks);
     int hbad = 0;
-    CPFIT_CUDA(cudaMemcpyAsync(hp.data(), part, sizeof(dd) * blocks, cudaMemcpyDeviceToHost, st));
-    CPFIT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CPFIT_CUDA(cudaMemcpyAsync(hp.data(), sc.part, sizeof(dd) * blocks, cudaMemcpyDeviceToHost, st));
+    CPFIT_CUDA(cudaMemcpyAsync(&hbad, sc.bad, sizeof(int), cudaMemcpyDeviceToHost, st));
     CPFIT_CUDA(cudaStreamSynchronize(st));
-    cudaFree(part);
-    cudaFree(bad);
     if (hbad) throw std::invalid_argument("DenseTensor: entries must be finite");
     dd s{0.0, 0.0};
     for (const dd& x : hp) s = dd_add(s, x);
-    t->norm_sq = s.hi + s.lo;
-    t->norm_sq_lo = (s.hi - t->norm_sq) + s.lo;  // ||T||^2 = norm_sq + norm_sq_lo in double-double
-    t->norm = std::sqrt(t->norm_sq);
-    return owner.release();
+    t.norm_sq = s.hi + s.lo;
+    t.norm_sq_lo = (s.hi - t.norm_sq) + s.lo;  // ||T||^2 = norm_sq + norm_sq_lo in double-double
+    t.norm = std::sqrt(t.norm_sq);
+    set_device_norms(t, st);
 }
 
 DevTensor* tensor_create_coo(int order, const int64_t* dims, int64_t nnz_in, const int64_t* coords,
@@ -164,6 +179,8 @@ DevTensor* tensor_create_coo(int order, const int64_t* dims, int64_t nnz_in, con
     for (double v : vv) s2 += v * v;  // Eigen norm(): sqrt(squaredNorm())
     t->norm = std::sqrt(s2);
     t->norm_sq = t->norm * t->norm;
+    CPFIT_CUDA(cudaMalloc(&t->dscal, sizeof(double) * 3));
+    set_device_norms(*t, st);
     upload_sparse_modes(*t, cc, vv, st);
     return owner.release();
 }
@@ -172,6 +189,7 @@ void tensor_destroy(DevTensor* t) {
     if (!t) return;
     cudaFree(t->T);
     cudaFree(t->fiber_norm2);
+    cudaFree(t->dscal);
     free_sparse_modes(*t);
     delete t;
 }
