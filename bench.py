@@ -420,7 +420,7 @@ def main():
     tw = P.DataTensor.dense(T_pin, dims)
     P.ngmres_solve(tw, starts[-1], P.NgmresOptions(window=20, max_iters=max(args.warmup, 3), tol_grad=tol,
                                                    gradient_scale=float(nu)))
-    tw.close()
+    tw.close()  # parked (capi.cu tensor pool): the timed handle below takes over its buffers and graphs
     barrier()
     te0 = time.perf_counter()
     te = P.DataTensor.dense(T_pin, dims)

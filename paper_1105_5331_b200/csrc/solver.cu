@@ -720,7 +720,9 @@ void Solver::construct(DevTensor* t, int R, const SolverOptions& o) {
         CPFIT_CUDA(cudaMalloc(&phase_, sizeof(unsigned long long) * (2 * kPhases + 1)));
         CPFIT_CUDA(cudaMemset(phase_, 0, sizeof(unsigned long long) * (2 * kPhases + 1)));
     }
-    trace_cap_ = o.max_iters + 1;
+    // room for the reference's default budget (ngmres.hpp:52, 2000) so a cached solver serves
+    // later calls with any max_iters up to it without a rebuild (the graphs do not depend on it)
+    trace_cap_ = std::max(o.max_iters, 2000) + 1;
     CPFIT_CUDA(cudaMalloc(&trace_, sizeof(TraceRow) * (size_t)trace_cap_));
     build_graphs();
 }

@@ -3,6 +3,8 @@
 
 #include "device.cuh"
 
+#include <algorithm>
+
 namespace cpfit_gpu {
 
 // Mirrors cpfit::NgmresOptions (ngmres.hpp:50-57) + LineSearchParams (line_search.hpp:7-14)
@@ -27,7 +29,7 @@ struct SolverOptions {
     // a solver built for *this can run a solve with options o (graphs bake in everything but
     // the iteration budget, which only needs to fit the trace buffer)
     bool serves(const SolverOptions& o) const {
-        return window == o.window && o.max_iters <= max_iters && epsilon_reg == o.epsilon_reg &&
+        return window == o.window && o.max_iters <= std::max(max_iters, 2000) && epsilon_reg == o.epsilon_reg &&
                tol_grad == o.tol_grad && gradient_scale == o.gradient_scale && ftol == o.ftol && gtol == o.gtol &&
                initial_step == o.initial_step && max_evals == o.max_evals && step_min == o.step_min &&
                step_max == o.step_max && restart_on_ascent == o.restart_on_ascent &&

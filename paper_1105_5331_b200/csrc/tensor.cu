@@ -99,8 +99,11 @@ DevTensor* tensor_create_dense(int order, const int64_t* dims, const double* hos
 
 void tensor_fill_dense(DevTensor& t, const double* host_vals, cudaStream_t st) {
     const int64_t I0 = t.dims[0];
-    CPFIT_CUDA(cudaMemcpy2DAsync(t.T, sizeof(double) * t.ldT, host_vals, sizeof(double) * I0, sizeof(double) * I0, t.J,
-                                 cudaMemcpyHostToDevice, st));
+    if (t.ldT == I0)  // unpadded fibres: one linear copy (a pitched 2D copy runs below the link rate)
+        CPFIT_CUDA(cudaMemcpyAsync(t.T, host_vals, sizeof(double) * (size_t)(I0 * t.J), cudaMemcpyHostToDevice, st));
+    else
+        CPFIT_CUDA(cudaMemcpy2DAsync(t.T, sizeof(double) * t.ldT, host_vals, sizeof(double) * I0, sizeof(double) * I0,
+                                     t.J, cudaMemcpyHostToDevice, st));
     const int blocks = 592;
     struct Scratch {
         dd* part = nullptr;
