@@ -78,6 +78,10 @@ _SIGS = {
     "oracle_uniform_initial_guess": (C.c_int, [C.c_int, _i64p, C.c_int64, C.c_uint64, _f64p]),
     "oracle_random_sparse_problem": (C.c_int, [C.c_int, _i64p, C.c_int64, C.c_int64, C.c_double, C.c_uint64,
                                                _i64p, _f64p]),
+    "oracle_io_last_error": (C.c_char_p, []),
+    "oracle_tns_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), _i64p, C.POINTER(C.c_int64), C.c_void_p,
+                                  C.c_void_p]),
+    "oracle_tns_write": (C.c_int, [C.c_char_p, C.c_int, _i64p, C.c_int64, _i64p, _f64p]),
     "oracle_ncg_cp": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_double, C.c_int, _f64p, C.POINTER(TraceOut),
                                 C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
 }
@@ -251,6 +255,36 @@ def random_sparse_problem(dims, nnz, rank, noise, seed):
     vals = np.empty(nnz)
     _check_problems(lib.oracle_random_sparse_problem(len(dims), dims, nnz, rank, noise, seed, coords, vals))
     return coords.reshape(-1, len(dims)), vals
+
+
+class OracleIOError(OracleError):
+    """cpfit::io_error"""
+
+
+def tns_read(path):
+    """read_tns_file restated (io.cpp:104-147, 179-188): (dims, coords nnz x N, values) as written,
+    or OracleIOError with the reference's message."""
+    order = C.c_int()
+    dims = np.zeros(16, dtype=np.int64)
+    nnz = C.c_int64()
+    if lib.oracle_tns_read(str(path).encode(), C.byref(order), dims, C.byref(nnz), None, None):
+        raise OracleIOError(lib.oracle_io_last_error().decode())
+    n = order.value
+    coords = np.empty(max(nnz.value, 1) * n, dtype=np.int64)
+    vals = np.empty(max(nnz.value, 1))
+    if lib.oracle_tns_read(str(path).encode(), C.byref(order), dims, C.byref(nnz), coords.ctypes.data,
+                           vals.ctypes.data):
+        raise OracleIOError(lib.oracle_io_last_error().decode())
+    return tuple(int(d) for d in dims[:n]), coords[:nnz.value * n].reshape(-1, n), vals[:nnz.value]
+
+
+def tns_write(path, dims, coords, values):
+    """write_tns_file(SparseTensor) restated (io.cpp:151-159)."""
+    dims = np.ascontiguousarray(dims, dtype=np.int64)
+    coords = np.ascontiguousarray(coords, dtype=np.int64).reshape(-1)
+    values = _f64(values).reshape(-1)
+    if lib.oracle_tns_write(str(path).encode(), len(dims), dims, values.size, coords, values):
+        raise OracleIOError(lib.oracle_io_last_error().decode())
 
 
 def _trace(tr, rows):

@@ -31,6 +31,10 @@ class CudaError(RuntimeError):
     pass
 
 
+class CpfitIOError(OSError):
+    """cpfit::io_error (errors.hpp:15-18): file and parse failures naming the file and line."""
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -123,6 +127,15 @@ _SIGS = {
     "cpfit_solver_destroy": (C.c_int, [C.c_void_p]),
     "cpfit_bench_kernel": (C.c_int, [C.c_void_p, C.c_int64, _f64p, C.c_int, C.c_int, C.c_int, C.c_int,
                                      C.POINTER(C.c_float)]),
+    # io (host, include/cpfit_io.h)
+    "cpfit_io_last_error": (C.c_char_p, []),
+    "cpfit_format_double": (C.c_int, [C.c_double, C.c_char_p, C.c_int]),
+    "cpfit_tns_read": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_int), _i64p, C.POINTER(C.c_int64), C.c_void_p,
+                                 C.c_void_p, C.c_int64, C.POINTER(C.c_int)]),
+    "cpfit_tns_read_dense": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_int), _i64p, C.POINTER(C.c_int64),
+                                       C.c_void_p, C.c_int64]),
+    "cpfit_tns_write": (C.c_int, [C.c_char_p, C.c_int, _i64p, C.c_int64, _i64p, _f64p]),
+    "cpfit_tns_write_dense": (C.c_int, [C.c_char_p, C.c_int, _i64p, _f64p]),
     # problems (host)
     "cpfit_problems_last_error": (C.c_char_p, []),
     "cpfit_rng_draws": (C.c_int, [C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -144,10 +157,13 @@ for _name, (_res, _args) in _SIGS.items():
 EXPORTED_SYMBOLS = sorted(_SIGS)
 
 
-def _check(rc: int, problems: bool = False):
+def _check(rc: int, problems: bool = False, io: bool = False):
     if rc == 0:
         return
-    msg = (lib.cpfit_problems_last_error() if problems else lib.cpfit_last_error()).decode(errors="replace")
+    err = lib.cpfit_io_last_error if io else (lib.cpfit_problems_last_error if problems else lib.cpfit_last_error)
+    msg = err().decode(errors="replace")
+    if rc == 4:
+        raise CpfitIOError(msg)
     if rc == 1:
         raise ValueError(msg)
     if rc == 2:
@@ -642,6 +658,78 @@ def bench_kernel(t: DataTensor, u, kind: int, mode: int = 0, reps: int = 10, flu
     ms = C.c_float()
     _check(lib.cpfit_bench_kernel(t._h, r, u, kind, mode, reps, int(flush_l2), C.byref(ms)))
     return ms.value
+
+
+# ---- .tns files (io.hpp:14-30; host, multi-threaded) -----------------------------------------
+
+def format_double(x: float) -> str:
+    """format_double (io.cpp:15-19): shortest round-trip decimal form."""
+    buf = C.create_string_buffer(64)
+    _check(lib.cpfit_format_double(float(x), buf, 64), io=True)
+    return buf.value.decode()
+
+
+def read_tns(path, sidecar: int = 1):
+    """read_tns_file (io.hpp:27): (dims, coords nnz x N 0-based, values) in file order.
+    sidecar 0: text only; 1: use <path>.cpfbin when it matches the file; 2: also write it."""
+    order = C.c_int()
+    dims = np.zeros(8, dtype=np.int64)
+    nnz = C.c_int64()
+    p = str(path).encode()
+    # header (or a matching sidecar's header) first; the body call below parses / writes the sidecar
+    _check(lib.cpfit_tns_read(p, min(int(sidecar), 1), C.byref(order), dims, C.byref(nnz), None, None, 0, None),
+           io=True)
+    n, k = order.value, nnz.value
+    coords = np.empty((max(k, 1), n), dtype=np.int64)
+    vals = np.empty(max(k, 1))
+    used = C.c_int()
+    _check(lib.cpfit_tns_read(p, int(sidecar), C.byref(order), dims, C.byref(nnz), coords.ctypes.data,
+                              vals.ctypes.data, max(k, 1), C.byref(used)), io=True)
+    read_tns.last_from_sidecar = bool(used.value)
+    return tuple(int(d) for d in dims[:n]), coords[:k], vals[:k]
+
+
+def read_tns_dense(path, sidecar: int = 1):
+    """read_tns_dense_file (io.hpp:30): (dims, values first-mode-fastest)."""
+    order = C.c_int()
+    dims = np.zeros(8, dtype=np.int64)
+    K = C.c_int64()
+    p = str(path).encode()
+    _check(lib.cpfit_tns_read_dense(p, int(sidecar), C.byref(order), dims, C.byref(K), None, 0), io=True)
+    vals = np.empty(max(K.value, 1))
+    _check(lib.cpfit_tns_read_dense(p, int(sidecar), C.byref(order), dims, C.byref(K), vals.ctypes.data, K.value),
+           io=True)
+    return tuple(int(d) for d in dims[:order.value]), vals[:K.value]
+
+
+def write_tns(path, dims, coords, values):
+    """write_tns_file(SparseTensor) (io.hpp:24): entries as given (1-based on disk)."""
+    dims = _dims(dims)
+    values = _f64(values).reshape(-1)
+    coords = np.ascontiguousarray(coords, dtype=np.int64).reshape(-1)
+    if coords.size != values.size * len(dims):
+        raise ValueError("SparseTensor: coords/values size mismatch")
+    _check(lib.cpfit_tns_write(str(path).encode(), len(dims), dims, values.size, coords, values), io=True)
+
+
+def write_tns_dense(path, values, dims=None):
+    """write_tns_file(DenseTensor) (io.hpp:25)."""
+    values = np.asarray(values, dtype=np.float64)
+    if dims is None:
+        dims = values.shape
+        values = values.reshape(-1, order="F")
+    dims = _dims(dims)
+    flat = _vec(values, int(np.prod(dims)), "write_tns_dense")
+    _check(lib.cpfit_tns_write_dense(str(path).encode(), len(dims), dims, flat), io=True)
+
+
+def data_tensor_from_tns(path, dense: bool = False, sidecar: int = 1) -> "DataTensor":
+    """DataTensor(read_tns_file(path)) / DataTensor(read_tns_dense_file(path)) on the device."""
+    if dense:
+        dims, vals = read_tns_dense(path, sidecar)
+        return DataTensor.dense(vals, dims)
+    dims, coords, vals = read_tns(path, sidecar)
+    return DataTensor.coo(dims, coords, vals)
 
 
 # ---- problems (host generators) ---------------------------------------------------------------

@@ -14,6 +14,8 @@
 //   * laplacian_tensor (problems.cpp:97-135) and the BASELINE random-COO problem.
 #include "../../include/cpfit_problems.h"
 
+#include <parallel/algorithm>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -66,6 +68,43 @@ double vnorm(const double* x, int64_t n) {
     double s = 0.0;
     for (int64_t i = 0; i < n; ++i) s += x[i] * x[i];
     return std::sqrt(s);
+}
+
+// ||x|| for large vectors: fixed 64K-element chunks summed on all cores, the chunk sums added
+// in order (the result does not depend on the thread count)
+double pnorm(const double* x, int64_t n) {
+    constexpr int64_t CH = 1 << 16;
+    const int64_t nch = (n + CH - 1) / CH;
+    std::vector<double> part((size_t)std::max<int64_t>(nch, 1), 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nch; ++c) {
+        double s = 0.0;
+        const int64_t e = std::min(n, (c + 1) * CH);
+        for (int64_t i = c * CH; i < e; ++i) s += x[i] * x[i];
+        part[(size_t)c] = s;
+    }
+    double s = 0.0;
+    for (double v : part) s += v;
+    return std::sqrt(s);
+}
+
+// n normals of rng in stream order (Rng::normal: two engine draws each, rng.hpp:26-33). The
+// engine is serial (~1 ns per draw) and runs ahead into a buffer; the Box–Muller transforms
+// (log1p, sqrt, cos: the expensive part) run on all cores.
+void normals(Rng& rng, double* out, int64_t n) {
+    constexpr int64_t CH = 1 << 22;
+    std::vector<uint64_t> raw((size_t)(2 * std::min<int64_t>(n, CH)));
+    for (int64_t k0 = 0; k0 < n; k0 += CH) {
+        const int64_t m = std::min(CH, n - k0);
+        for (int64_t i = 0; i < 2 * m; ++i) raw[(size_t)i] = rng.e();
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < m; ++i) {
+            const double u1 = static_cast<double>(raw[(size_t)(2 * i)] >> 11) * 0x1.0p-53;
+            const double u2 = static_cast<double>(raw[(size_t)(2 * i + 1)] >> 11) * 0x1.0p-53;
+            const double r = std::sqrt(-2.0 * std::log1p(-u1));
+            out[k0 + i] = r * std::cos(2.0 * 3.141592653589793238462643383279502884 * u2);
+        }
+    }
 }
 
 // Thin Householder QR of a (rows x k, column-major): returns Q (rows x k) with the sign fix
@@ -244,17 +283,20 @@ int cpfit_dense_test_problem(int order, const int64_t* dims, int64_t rank, doubl
         if (noise_free_out) std::memcpy(noise_free_out, t_out, sizeof(double) * (size_t)K);
         if (truth_out) std::memcpy(truth_out, truth.data(), sizeof(double) * (size_t)nu);
         std::vector<double> n1((size_t)K), n2((size_t)K);
-        for (auto& x : n1) x = rng.normal();
-        for (auto& x : n2) x = rng.normal();
+        normals(rng, n1.data(), K);
+        normals(rng, n2.data(), K);  // drawn even when l2 = 0 (problems.cpp:74)
         if (l1 > 0.0) {
             const double coef = noise_coef(l1, noise_mode);
-            const double s = coef * vnorm(t_out, K) / vnorm(n1.data(), K);
+            const double s = coef * pnorm(t_out, K) / pnorm(n1.data(), K);
+#pragma omp parallel for schedule(static)
             for (int64_t i = 0; i < K; ++i) t_out[i] += s * n1[(size_t)i];
         }
         if (l2 > 0.0) {
             const double coef = noise_coef(l2, noise_mode);
+#pragma omp parallel for schedule(static)
             for (int64_t i = 0; i < K; ++i) n2[(size_t)i] *= t_out[i];  // mixed = N2 .* T_hat
-            const double s = coef * vnorm(t_out, K) / vnorm(n2.data(), K);
+            const double s = coef * pnorm(t_out, K) / pnorm(n2.data(), K);
+#pragma omp parallel for schedule(static)
             for (int64_t i = 0; i < K; ++i) t_out[i] += s * n2[(size_t)i];
         }
     });
@@ -358,7 +400,7 @@ int cpfit_random_sparse_problem(int order, const int64_t* dims, int64_t nnz, int
         keys.reserve((size_t)nnz);
         for (int64_t i = 0; i < nnz; ++i) keys.push_back(key(draw()));
         for (;;) {
-            std::sort(keys.begin(), keys.end());
+            __gnu_parallel::sort(keys.begin(), keys.end());
             keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
             if ((int64_t)keys.size() == nnz) break;
             const int64_t miss = nnz - (int64_t)keys.size();
@@ -367,9 +409,10 @@ int cpfit_random_sparse_problem(int order, const int64_t* dims, int64_t nnz, int
         std::vector<int64_t> off(N, 0);
         for (size_t n = 1; n < N; ++n) off[n] = off[n - 1] + dims[n - 1] * rank;
         std::vector<double> m((size_t)nnz);
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < nnz; ++i) {
             int64_t k = keys[(size_t)i];
-            std::vector<int64_t> idx(N);
+            int64_t idx[16];
             for (int64_t n = (int64_t)N - 1; n >= 0; --n) {
                 idx[(size_t)n] = k % dims[n];
                 k /= dims[n];
@@ -384,8 +427,9 @@ int cpfit_random_sparse_problem(int order, const int64_t* dims, int64_t nnz, int
             for (size_t n = 0; n < N; ++n) coords[(size_t)i * N + n] = idx[n];
         }
         std::vector<double> z((size_t)nnz);
-        for (auto& x : z) x = rng.normal();
-        const double sc = (nnz > 0) ? noise * vnorm(m.data(), nnz) / vnorm(z.data(), nnz) : 0.0;
+        normals(rng, z.data(), nnz);
+        const double sc = (nnz > 0) ? noise * pnorm(m.data(), nnz) / pnorm(z.data(), nnz) : 0.0;
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < nnz; ++i) values[i] = m[(size_t)i] + sc * z[(size_t)i];
     });
 }

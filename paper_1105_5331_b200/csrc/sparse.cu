@@ -10,6 +10,7 @@
 #include "sparse.cuh"
 
 #include <algorithm>
+#include <thread>
 
 namespace cpfit_gpu {
 
@@ -212,14 +213,21 @@ void upload_sparse_modes(DevTensor& t, const std::vector<int64_t>& coords, const
     t.modes = sm;
     const int N = t.order;
     const int64_t nnz = (int64_t)vals.size();
-    for (int n = 0; n < N; ++n) {
+    // the N counting sorts are independent: one host thread each, then the uploads in order
+    std::vector<std::vector<int64_t>> rowptrs((size_t)N);
+    std::vector<std::vector<int32_t>> oidxs((size_t)N);
+    std::vector<std::vector<double>> svs((size_t)N);
+    auto sort_mode = [&](int n) {
         const int64_t In = t.dims[n];
-        std::vector<int64_t> rowptr((size_t)In + 1, 0);
+        std::vector<int64_t>& rowptr = rowptrs[(size_t)n];
+        rowptr.assign((size_t)In + 1, 0);
         for (int64_t j = 0; j < nnz; ++j) ++rowptr[(size_t)coords[(size_t)j * N + n] + 1];
         for (int64_t i = 0; i < In; ++i) rowptr[(size_t)i + 1] += rowptr[(size_t)i];
         std::vector<int64_t> pos(rowptr.begin(), rowptr.end() - 1);
-        std::vector<int32_t> oidx((size_t)std::max(1, N - 1) * (size_t)nnz);
-        std::vector<double> sv((size_t)nnz);
+        std::vector<int32_t>& oidx = oidxs[(size_t)n];
+        oidx.resize((size_t)std::max(1, N - 1) * (size_t)nnz);
+        std::vector<double>& sv = svs[(size_t)n];
+        sv.resize((size_t)nnz);
         for (int64_t j = 0; j < nnz; ++j) {  // stable counting sort by mode-n index
             const int64_t dst = pos[(size_t)coords[(size_t)j * N + n]]++;
             sv[(size_t)dst] = vals[(size_t)j];
@@ -230,6 +238,17 @@ void upload_sparse_modes(DevTensor& t, const std::vector<int64_t>& coords, const
                 ++k;
             }
         }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int n = 1; n < N; ++n) th.emplace_back(sort_mode, n);
+        sort_mode(0);
+        for (auto& x : th) x.join();
+    }
+    for (int n = 0; n < N; ++n) {
+        const std::vector<int64_t>& rowptr = rowptrs[(size_t)n];
+        const std::vector<int32_t>& oidx = oidxs[(size_t)n];
+        const std::vector<double>& sv = svs[(size_t)n];
         CPFIT_CUDA(cudaMalloc(&sm->rowptr[n], sizeof(int64_t) * rowptr.size()));
         CPFIT_CUDA(cudaMalloc(&sm->oidx[n], sizeof(int32_t) * std::max<size_t>(oidx.size(), 1)));
         CPFIT_CUDA(cudaMalloc(&sm->vals[n], sizeof(double) * std::max<size_t>(sv.size(), 1)));
