@@ -19,7 +19,6 @@ def test_format_double_round_trips(P):
             x = -x
         s = P.format_double(x)
         assert float(s) == x, s
-        assert s == repr(x).replace("e+", "e").replace("e-0", "e-").replace("e0", "e") or float(s) == x
     assert P.format_double(0.0) == "0"
     assert P.format_double(0.1) == "0.1" and P.format_double(1e-7) == "1e-07"
 
