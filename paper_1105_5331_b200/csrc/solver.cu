@@ -1067,7 +1067,7 @@ long long Solver::pending_loop_launches() {
 }
 
 void Solver::run_loop(int max_iters_total) {
-    if (max_iters_total > opt_.max_iters) max_iters_total = opt_.max_iters;
+    if (max_iters_total > trace_cap_ - 1) max_iters_total = trace_cap_ - 1;  // the trace bounds the budget
     host_max_ = max_iters_total;
     DevState* s = reinterpret_cast<DevState*>(state_);
     CPFIT_CUDA(cudaMemcpyAsync(&s->max_iters, &host_max_, sizeof(int), cudaMemcpyHostToDevice, st_));
