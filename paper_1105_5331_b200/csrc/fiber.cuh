@@ -36,6 +36,12 @@ constexpr int kMaxKSteps = 104;  // ldT / 4 for I_0 <= 416 (work_create checks)
 #define CPFIT_SREG_CHAINS 1
 #endif
 constexpr int kSRegChains = CPFIT_SREG_CHAINS;
+#ifndef CPFIT_FUSED_CHAINS
+#define CPFIT_FUSED_CHAINS 2
+#endif
+#ifndef CPFIT_FUSED_SREG
+#define CPFIT_FUSED_SREG 1  // 0: S warps with both DMMA operands from shared memory (A/B builds)
+#endif
 
 template <int RP>
 __host__ __device__ constexpr int w_ld() {
@@ -49,16 +55,30 @@ struct FiberRoles {
     static constexpr int NWP = RP <= 16 ? 2 : 0;            // W producer warps (0: the T producer)
     static constexpr bool SEPW = NWP > 0;
     static constexpr int NQ = 2 * NRT;                      // 8x8 S sub-tiles per tile
-    static constexpr int NS = RP == 32 ? 4 : NQ;            // S warps
-    static constexpr int SPW = NQ / NS;                     // sub-tiles per S warp
+    // RP = 8 (SREG): S warp q owns K quarter q for BOTH 8-fibre groups with its A0 B-fragments in
+    // registers (one shared-memory fragment load per DMMA; four S warps instead of two, so the S
+    // work no longer sits on two sub-partitions); warps 0 / 1 sum the four quarters of fibre
+    // group 0 / 1 and run its epilogue. (At RP = 16 the same scheme needs 19 warps, i.e. 96
+    // registers and spills, or fewer W-producer / M0 warps, which slows the M0 pass of the solve
+    // loop; measured in DESIGN.md §5, the 15-warp layout stays.)
+    static constexpr bool SREG = CPFIT_FUSED_SREG && RP == 8;
+    static constexpr int KQ = SREG ? 4 : 1;                 // K parts of the SREG S warps
+    static constexpr int NS = SREG ? NRT * KQ : (RP == 32 ? 4 : NQ);  // S warps
+    static constexpr int SPW = SREG ? 1 : NQ / NS;          // sub-tiles per S warp (S-given path)
+    static constexpr int NEPI = SREG ? NQ : NS;             // S warps that consume W (epilogues)
     static constexpr int NM = RP == 32 ? 11 : 8;            // M0 warps
     static constexpr int MAXMT = RP == 8 ? 14 : (RP == 16 ? 7 : 5);  // m-tiles per M0 warp
     static constexpr bool A0SMEM = RP <= 16;                // A0 staged in shared memory
     static constexpr int S0 = 1 + NWP;                      // first S warp
     static constexpr int M0W = S0 + NS;                     // first M0 warp
     static constexpr int WARPS = M0W + NM;
+    // registers per thread with one CTA of WARPS warps per SM: the register file is split over
+    // the block's warps rounded up to a multiple of 4 (one per sub-partition), in units of 8
+    static constexpr int WARPS4 = (WARPS + 3) / 4 * 4;
+    static constexpr int MAXNREG = (65536 / (32 * WARPS4)) / 8 * 8 > 128 ? 128 : (65536 / (32 * WARPS4)) / 8 * 8;
 };
-static_assert(FiberRoles<32>::WARPS <= 16 && FiberRoles<16>::WARPS <= 16, "<= 512 threads (128 registers)");
+static_assert(FiberRoles<32>::WARPS <= 16 && FiberRoles<16>::WARPS <= 16 && FiberRoles<8>::WARPS <= 16,
+              "<= 512 threads (128 registers)");
 
 struct FiberSmem {
     size_t tiles, a0, wbuf, gam, spart, bars, total;
@@ -80,6 +100,8 @@ __host__ __device__ FiberSmem fiber_layout(int nchunk, int64_t I0, int nst) {
     off += sizeof(double) * kWStages * (size_t)F * w_ld<RP>();
     s.gam = off;
     off += sizeof(double) * (size_t)RP * RP;
+    s.spart = off;  // SREG K-quarter exchange [NRT][6 slots][64] (the three other quarters of each group)
+    if (FiberRoles<RP>::SREG) off += sizeof(double) * (size_t)FiberRoles<RP>::NRT * 6 * 64;
     s.bars = off;
     off += sizeof(uint64_t) * (2 * nst + 2 * kWStages);
     s.total = off;
@@ -97,7 +119,9 @@ inline void fiber_schedule_rp(int I0, bool do_s, FiberParams& p) {
     load[0] += 2.0;
     for (int w = 0; w < Ro::NWP; ++w) load[(1 + w) % 4] += 2.0;
     if (do_s)
-        for (int s = 0; s < Ro::NS; ++s) load[(Ro::S0 + s) % 4] += (double)KS * Ro::SPW + 6.0 * Ro::SPW;
+        for (int s = 0; s < Ro::NS; ++s)
+            load[(Ro::S0 + s) % 4] += Ro::SREG ? 2.0 * KS / Ro::KQ + (s / Ro::NRT < 2 ? 6.0 : 0.0)
+                                               : (double)KS * Ro::SPW + 6.0 * Ro::SPW;
     const double mt_w = 4.0 * Ro::NRT;  // DMMAs per m-tile per tile
     int cnt[16] = {};
     for (int t = 0; t < MT; ++t) {
@@ -216,7 +240,7 @@ __device__ __forceinline__ int a0s_index(int i, int r) {
 }
 
 template <int RP, int F, int ORD, int NST>
-__global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel(const __grid_constant__ FiberParams p) {
+__global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __grid_constant__ FiberParams p) {
     using Ro = FiberRoles<RP>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int NRT = Ro::NRT;
@@ -250,7 +274,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
     const bool need_w = p.do_m0 || p.do_f;
     const bool m0w_on = p.do_m0 || resid;  // M0 warps consume T (and W)
     const bool epi_w = p.do_f && !resid;   // S warps consume W
-    const bool need_a0 = p.do_s || resid;
+    const bool need_a0 = (p.do_s && !Ro::SREG) || resid;  // SREG S warps hold A0 in registers
     dd racc{0.0, 0.0};
 
     for (int64_t e = tid; e < (int64_t)NST * F * I0s; e += blockDim.x) tiles[e] = 0.0;
@@ -263,7 +287,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
         for (int e = tid; e < RP * RP; e += blockDim.x) gam[e] = p.gamma0[e];
     if (tid == 0) {
         const int t_cons = (p.do_s ? Ro::NS : 0) + (m0w_on ? Ro::NM : 0);
-        const int w_cons = (m0w_on ? Ro::NM : 0) + (epi_w ? Ro::NS : 0);
+        const int w_cons = (m0w_on ? Ro::NM : 0) + (epi_w ? Ro::NEPI : 0);
         for (int s = 0; s < NST; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], t_cons);
@@ -368,7 +392,7 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
         if (!p.do_s && epi_w && p.S_in) {
             // S is given (the ALS sweep's S' rescaled to u_bar): only the per-fiber objective
             const int sw = warp - Ro::S0;
-            for (int64_t k = 0; k < ntl; ++k) {
+            for (int64_t k = 0; k < (sw < Ro::NEPI ? ntl : 0); ++k) {
                 const int b = (int)(k % kWStages);
                 const int64_t f0 = (t_begin + k) * F;
                 double sv[Ro::SPW][2], fn[Ro::SPW];
@@ -403,6 +427,107 @@ __global__ void __launch_bounds__(32 * FiberRoles<RP>::WARPS, 1) fiber_ws_kernel
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&wempty[b]);
+            }
+        } else if (p.do_s && Ro::SREG) {
+            constexpr int KM = (NST == kDeepFStages) ? 8 : (kMaxKSteps + 3) / 4;  // k-steps per quarter
+            constexpr int CH = CPFIT_FUSED_CHAINS;  // accumulator chains per fibre group
+            const int sw = warp - Ro::S0;
+            const int nt = sw % NRT, q = sw / NRT;
+            const int rr = nt * 8 + (lane >> 2);
+            const int k_lo = (KS * q) / 4, nk = (KS * (q + 1)) / 4 - k_lo;
+            double breg[KM];
+#pragma unroll
+            for (int kk = 0; kk < KM; ++kk) {
+                const int i = 4 * (k_lo + kk) + (lane & 3);
+                breg[kk] = (kk < nk && i < p.I0 && rr < p.R) ? __ldg(p.A0 + (int64_t)rr * p.I0 + i) : 0.0;
+            }
+            // exchange slots of column group nt: [group g][3 other quarters][64]
+            double* xch = reinterpret_cast<double*>(smem_raw + L.spart) + (size_t)nt * 6 * 64;
+            auto slot = [&](int g, int from) -> double* {  // quarter `from`'s partial of group g (from != g)
+                return xch + ((size_t)g * 3 + (from < g ? from : from - 1)) * 64;
+            };
+            for (int64_t k = 0; k < ntl; ++k) {
+                const int s = (int)(k % NST);
+                const int b = (int)(k % kWStages);
+                const int64_t f0 = (t_begin + k) * F;
+                const bool fin = q < 2;             // finishes fibre group q
+                const int fl = q * 8 + (lane >> 2);
+                const double fnv = (fin && epi_w && nt == 0 && f0 + fl < p.J) ? p.fnorm2[f0 + fl] : 0.0;
+                FIBER_WAIT(2, &tfull[s], (uint32_t)((k / NST) & 1));
+                const double* ta0 = tiles + (size_t)s * F * I0s + (lane >> 2) * I0s + (lane & 3) + 4 * k_lo;
+                const double* ta1 = ta0 + 8 * I0s;
+                double acc[2][CH][2];
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) acc[g][c][0] = acc[g][c][1] = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < KM; kk += CH) {
+                    if (kk >= nk) break;  // warp-uniform exit: no predicated-off DMMAs past the quarter
+                    double x0[CH], x1[CH];
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        x0[c] = (kk + c < nk) ? ta0[(kk + c) * 4] : 0.0;
+                        x1[c] = (kk + c < nk) ? ta1[(kk + c) * 4] : 0.0;
+                    }
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        dmma_8x8x4(acc[0][c][0], acc[0][c][1], x0[c], breg[kk + c < KM ? kk + c : KM - 1]);
+                        dmma_8x8x4(acc[1][c][0], acc[1][c][1], x1[c], breg[kk + c < KM ? kk + c : KM - 1]);
+                    }
+                }
+                double sv[2][2];
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        double t = acc[g][0][e];
+#pragma unroll
+                        for (int c = 1; c < CH; ++c) t += acc[g][c][e];
+                        sv[g][e] = t;
+                    }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[s]);
+                // partials of the groups this warp does not finish go to their finishers
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+                    if (g != q) {
+                        double* d = slot(g, q);
+                        d[2 * lane] = sv[g][0];
+                        d[2 * lane + 1] = sv[g][1];
+                    }
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + nt), "r"(32 * Ro::KQ) : "memory");
+                double s0 = 0.0, s1 = 0.0;
+                if (fin) {  // quarters in order 0, 1, 2, 3
+#pragma unroll
+                    for (int qq = 0; qq < Ro::KQ; ++qq) {
+                        const double* o = qq == q ? nullptr : slot(q, qq);
+                        s0 += o ? o[2 * lane] : sv[q][0];
+                        s1 += o ? o[2 * lane + 1] : sv[q][1];
+                    }
+                }
+                // the slots are rewritten only after every finisher has read them
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + NRT + nt), "r"(32 * Ro::KQ) : "memory");
+                if (!fin) continue;
+                if (epi_w) FIBER_WAIT(6, &wfull[b], (uint32_t)((k / kWStages) & 1));
+                const double* wv = wbuf + (size_t)b * F * WLD;
+                const int r = nt * 8 + 2 * (lane & 3);
+                if (f0 + fl < p.J) *reinterpret_cast<double2*>(p.S_out + (f0 + fl) * RP + r) = make_double2(s0, s1);
+                if (epi_w) {
+                    double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+                    for (int kr = 0; kr < RP / 4; ++kr) {
+                        const double gb = gam[(kr * 4 + (lane & 3)) * RP + nt * 8 + (lane >> 2)];
+                        dmma_8x8x4(q0, q1, wv[fl * WLD + kr * 4 + (lane & 3)], gb);
+                    }
+                    const double2 wd = *reinterpret_cast<const double2*>(wv + fl * WLD + r);
+                    double term = wd.x * (q0 - 2.0 * s0) + wd.y * (q1 - 2.0 * s1);
+                    term += __shfl_xor_sync(0xffffffffu, term, 1);
+                    term += __shfl_xor_sync(0xffffffffu, term, 2);
+                    if ((lane & 3) == 0 && f0 + fl < p.J) facc += fnv + term;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&wempty[b]);
+                }
             }
         } else if (p.do_s) {
             const int sw = warp - Ro::S0;
