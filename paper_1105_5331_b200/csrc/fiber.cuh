@@ -31,6 +31,10 @@ constexpr int kFStages = 3;      // T ring depth for long fibres (a tile is ~54 
 constexpr int kDeepFStages = 8;  // short fibres (I0 <= 128): ~70 KB of T in flight per SM
 constexpr int kFiberF = 16;
 constexpr int kWStages = 4;  // W (Khatri-Rao row) ring: the gathers of a tile take about a tile's time
+// W ring depth of a T ring depth: the deep (short-fibre) ring runs M0 tile groups, where warp m
+// consumes tiles m, m + 8, ... — with 8 slots every warp owns one W slot, so each warp's waits on
+// it are in phase order (an mbarrier wait on phase parity 1 passes before phase 0 has completed)
+__host__ __device__ constexpr int wstages(int nst) { return nst == kDeepFStages ? 8 : kWStages; }
 constexpr int kMaxKSteps = 104;  // ldT / 4 for I_0 <= 416 (work_create checks)
 #ifndef CPFIT_SREG_CHAINS
 #define CPFIT_SREG_CHAINS 1
@@ -68,6 +72,10 @@ struct FiberRoles {
     static constexpr int NEPI = SREG ? NQ : NS;             // S warps that consume W (epilogues)
     static constexpr int NM = RP == 32 ? 11 : 8;            // M0 warps
     static constexpr int MAXMT = RP == 8 ? 14 : (RP == 16 ? 7 : 5);  // m-tiles per M0 warp
+    // short fibres (deep ring, ceil(I0 / 8) <= TGMT m-tiles): M0 tile groups — warp m takes whole
+    // tiles m, m + NM, ... (every m-tile of the fibre: NRT x TGMT independent accumulators, one
+    // barrier round trip per 4 NRT TGMT DMMAs) instead of its own rows of every tile
+    static constexpr int TGMT = RP == 32 ? 4 : 16 / NRT;
     static constexpr bool A0SMEM = RP <= 16;                // A0 staged in shared memory
     static constexpr int S0 = 1 + NWP;                      // first S warp
     static constexpr int M0W = S0 + NS;                     // first M0 warp
@@ -97,13 +105,13 @@ __host__ __device__ FiberSmem fiber_layout(int nchunk, int64_t I0, int nst) {
     s.a0 = off;
     if (FiberRoles<RP>::A0SMEM) off += sizeof(double) * (size_t)a0_rows(I0) * RP;
     s.wbuf = off;
-    off += sizeof(double) * kWStages * (size_t)F * w_ld<RP>();
+    off += sizeof(double) * wstages(nst) * (size_t)F * w_ld<RP>();
     s.gam = off;
     off += sizeof(double) * (size_t)RP * RP;
     s.spart = off;  // SREG K-quarter exchange [NRT][6 slots][64] (the three other quarters of each group)
     if (FiberRoles<RP>::SREG) off += sizeof(double) * (size_t)FiberRoles<RP>::NRT * 6 * 64;
     s.bars = off;
-    off += sizeof(uint64_t) * (2 * nst + 2 * kWStages);
+    off += sizeof(uint64_t) * (2 * nst + 2 * wstages(nst));
     s.total = off;
     return s;
 }
@@ -242,6 +250,7 @@ __device__ __forceinline__ int a0s_index(int i, int r) {
 template <int RP, int F, int ORD, int NST>
 __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __grid_constant__ FiberParams p) {
     using Ro = FiberRoles<RP>;
+    constexpr int WST = wstages(NST);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int NRT = Ro::NRT;
     constexpr int WLD = w_ld<RP>();
@@ -252,13 +261,13 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
     const int KS = (int)(p.ldT / 4);  // k-steps of 4 rows (ldT = I0 rounded up to 4; pad rows are 0)
     double* tiles = reinterpret_cast<double*>(smem_raw + L.tiles);
     double* a0s = reinterpret_cast<double*>(smem_raw + L.a0);    // [a0_rows][RP] swizzled
-    double* wbuf = reinterpret_cast<double*>(smem_raw + L.wbuf);  // [kWStages][F][WLD]
+    double* wbuf = reinterpret_cast<double*>(smem_raw + L.wbuf);  // [WST][F][WLD]
     double* gam = reinterpret_cast<double*>(smem_raw + L.gam);    // [RP][RP]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
     uint64_t* tfull = bars;          // [NST] tx bytes
     uint64_t* tempty = bars + NST;   // [NST] T consumers
-    uint64_t* wfull = bars + 2 * NST;               // [kWStages] W producer
-    uint64_t* wempty = bars + 2 * NST + kWStages;   // [kWStages] W consumers
+    uint64_t* wfull = bars + 2 * NST;               // [WST] W producer
+    uint64_t* wempty = bars + 2 * NST + WST;   // [WST] W consumers
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef CPFIT_FIBER_PROF
@@ -285,14 +294,18 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
         }
     if (p.do_f)
         for (int e = tid; e < RP * RP; e += blockDim.x) gam[e] = p.gamma0[e];
+    // M0 tile groups (short fibres): one M0 consumer per T stage / W slot
+    const bool m0tg = NST == kDeepFStages && (p.I0 + 7) / 8 <= Ro::TGMT &&
+                      Ro::NM * RP * 32 * p.nchunk <= NST * F * I0s;  // the final sums reuse the T ring
+    const int m0_cons = m0w_on ? (m0tg ? 1 : Ro::NM) : 0;
     if (tid == 0) {
-        const int t_cons = (p.do_s ? Ro::NS : 0) + (m0w_on ? Ro::NM : 0);
-        const int w_cons = (m0w_on ? Ro::NM : 0) + (epi_w ? Ro::NEPI : 0);
+        const int t_cons = (p.do_s ? Ro::NS : 0) + m0_cons;
+        const int w_cons = m0_cons + (epi_w ? Ro::NEPI : 0);
         for (int s = 0; s < NST; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], t_cons);
         }
-        for (int b = 0; b < kWStages; ++b) {
+        for (int b = 0; b < WST; ++b) {
             mbar_init(&wfull[b], NW);
             mbar_init(&wempty[b], w_cons);
         }
@@ -307,6 +320,7 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
     };
 
     double facc = 0.0;
+    double tacc[NRT][Ro::TGMT][2];  // M0 tile-group accumulators (short fibres, M0 warps)
     // W tile k: lane = (fiber fw, r-slice hw) of one of the NW producer warps; gathers first
     // (independent), then the buffer
     constexpr int RS = RP * F / (32 * NW);
@@ -325,8 +339,8 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
         }
     };
     auto w_store = [&](int64_t k, int fw, int hw, const double (&w)[RS]) {
-        const int b = (int)(k % kWStages);
-        if (k >= kWStages) FIBER_WAIT(1, &wempty[b], (uint32_t)(((k / kWStages) - 1) & 1));
+        const int b = (int)(k % WST);
+        if (k >= WST) FIBER_WAIT(1, &wempty[b], (uint32_t)(((k / WST) - 1) & 1));
         double* wv = wbuf + (size_t)b * F * WLD;
 #pragma unroll
         for (int j = 0; j < RS; ++j) wv[fw * WLD + hw * RS + j] = w[j];
@@ -393,7 +407,7 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
             // S is given (the ALS sweep's S' rescaled to u_bar): only the per-fiber objective
             const int sw = warp - Ro::S0;
             for (int64_t k = 0; k < (sw < Ro::NEPI ? ntl : 0); ++k) {
-                const int b = (int)(k % kWStages);
+                const int b = (int)(k % WST);
                 const int64_t f0 = (t_begin + k) * F;
                 double sv[Ro::SPW][2], fn[Ro::SPW];
 #pragma unroll
@@ -406,7 +420,7 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
                     sv[j][0] = v.x;
                     sv[j][1] = v.y;
                 }
-                FIBER_WAIT(6, &wfull[b], (uint32_t)((k / kWStages) & 1));
+                FIBER_WAIT(6, &wfull[b], (uint32_t)((k / WST) & 1));
                 const double* wv = wbuf + (size_t)b * F * WLD;
 #pragma unroll
                 for (int j = 0; j < Ro::SPW; ++j) {
@@ -448,7 +462,7 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
             };
             for (int64_t k = 0; k < ntl; ++k) {
                 const int s = (int)(k % NST);
-                const int b = (int)(k % kWStages);
+                const int b = (int)(k % WST);
                 const int64_t f0 = (t_begin + k) * F;
                 const bool fin = q < 2;             // finishes fibre group q
                 const int fl = q * 8 + (lane >> 2);
@@ -509,7 +523,7 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
                 // the slots are rewritten only after every finisher has read them
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + NRT + nt), "r"(32 * Ro::KQ) : "memory");
                 if (!fin) continue;
-                if (epi_w) FIBER_WAIT(6, &wfull[b], (uint32_t)((k / kWStages) & 1));
+                if (epi_w) FIBER_WAIT(6, &wfull[b], (uint32_t)((k / WST) & 1));
                 const double* wv = wbuf + (size_t)b * F * WLD;
                 const int r = nt * 8 + 2 * (lane & 3);
                 if (f0 + fl < p.J) *reinterpret_cast<double2*>(p.S_out + (f0 + fl) * RP + r) = make_double2(s0, s1);
@@ -533,7 +547,7 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
             const int sw = warp - Ro::S0;
             for (int64_t k = 0; k < ntl; ++k) {
                 const int s = (int)(k % NST);
-                const int b = (int)(k % kWStages);
+                const int b = (int)(k % WST);
                 const int64_t f0 = (t_begin + k) * F;
                 double fn[Ro::SPW];  // ||t_f||^2 of this lane's fiber, prefetched (r-tile 0 only)
 #pragma unroll
@@ -592,7 +606,7 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
                 // r = 8 nt + 2 (lane%4) + {0, 1}
                 // epilogue of the sub-tile(s): lane holds D fragment items f = 8 ft + lane/4,
                 // r = 8 nt + 2 (lane%4) + {0, 1}
-                if (epi_w) FIBER_WAIT(6, &wfull[b], (uint32_t)((k / kWStages) & 1));
+                if (epi_w) FIBER_WAIT(6, &wfull[b], (uint32_t)((k / WST) & 1));
                 const double* wv = wbuf + (size_t)b * F * WLD;
 #pragma unroll
                 for (int j = 0; j < Ro::SPW; ++j) {
@@ -624,6 +638,73 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
         }
     } else {
         // ---------------- M0 warps ----------------
+        if (NST == kDeepFStages && m0tg) {
+            // tile groups: warp m runs tiles m, m + NM, ... over every m-tile of the fibre
+            const int m = warp - Ro::M0W;
+            const int mt = (p.I0 + 7) / 8;
+#pragma unroll
+            for (int rt = 0; rt < NRT; ++rt)
+#pragma unroll
+                for (int nt = 0; nt < Ro::TGMT; ++nt) tacc[rt][nt][0] = tacc[rt][nt][1] = 0.0;
+            if (m0w_on) {
+                for (int64_t k = m; k < ntl; k += Ro::NM) {
+                    const int s = (int)(k % NST);
+                    const int b = (int)(k % WST);
+                    FIBER_WAIT(3, &tfull[s], (uint32_t)((k / NST) & 1));
+                    FIBER_WAIT(4, &wfull[b], (uint32_t)((k / WST) & 1));
+                    const double* tt = tiles + (size_t)s * F * I0s;
+                    const double* wv = wbuf + (size_t)b * F * WLD;
+                    if (p.do_m0) {
+#pragma unroll
+                        for (int kf = 0; kf < F / 4; ++kf) {
+                            const int f = kf * 4 + (lane & 3);
+                            double wa[NRT];
+#pragma unroll
+                            for (int rt = 0; rt < NRT; ++rt) wa[rt] = wv[f * WLD + rt * 8 + (lane >> 2)];
+                            double bb[Ro::TGMT];
+#pragma unroll
+                            for (int nt = 0; nt < Ro::TGMT; ++nt)
+                                bb[nt] = nt < mt ? tt[f * I0s + nt * 8 + (lane >> 2)] : 0.0;
+#pragma unroll
+                            for (int nt = 0; nt < Ro::TGMT; ++nt) {
+                                if (nt >= mt) break;
+#pragma unroll
+                                for (int rt = 0; rt < NRT; ++rt)
+                                    dmma_8x8x4(tacc[rt][nt][0], tacc[rt][nt][1], wa[rt], bb[nt]);
+                            }
+                        }
+                    }
+                    if (resid) {
+                        double tsum = 0.0;
+#pragma unroll
+                        for (int nt2 = 0; nt2 < Ro::TGMT; ++nt2) {
+                            if (nt2 >= mt) break;
+                            const int i = nt2 * 8 + (lane >> 2);
+                            double a0r[RP / 4];
+#pragma unroll
+                            for (int kr = 0; kr < RP / 4; ++kr) a0r[kr] = a0_at(i, kr * 4 + (lane & 3));
+#pragma unroll
+                            for (int nt = 0; nt < F / 8; ++nt) {
+                                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                                for (int kr = 0; kr < RP / 4; ++kr)
+                                    dmma_8x8x4(d0, d1, a0r[kr], wv[(nt * 8 + (lane >> 2)) * WLD + kr * 4 + (lane & 3)]);
+                                const int f = nt * 8 + 2 * (lane & 3);
+                                const double r0 = tt[f * I0s + i] - d0;
+                                const double r1 = tt[(f + 1) * I0s + i] - d1;
+                                tsum += r0 * r0 + r1 * r1;
+                            }
+                        }
+                        racc = dd_add(racc, dd{tsum, 0.0});
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&tempty[s]);
+                        mbar_arrive(&wempty[b]);
+                    }
+                }
+            }
+        } else {
         // rows [rb, rb + 8 cnt) of the fiber (cnt <= MAXMT m-tiles)
         const int m = warp - Ro::M0W;
         const int cnt = p.mt_cnt[m];
@@ -636,9 +717,9 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
         if (m0w_on) {
             for (int64_t k = 0; k < ntl; ++k) {
                 const int s = (int)(k % NST);
-                const int b = (int)(k % kWStages);
+                const int b = (int)(k % WST);
                 FIBER_WAIT(3, &tfull[s], (uint32_t)((k / NST) & 1));
-                FIBER_WAIT(4, &wfull[b], (uint32_t)((k / kWStages) & 1));
+                FIBER_WAIT(4, &wfull[b], (uint32_t)((k / WST) & 1));
                 const double* tt = tiles + (size_t)s * F * I0s;
                 const double* wv = wbuf + (size_t)b * F * WLD;
                 if (p.do_m0) {
@@ -722,6 +803,7 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
                     }
                 }
         }
+        }  // M0 rows per warp
     }
 #ifdef CPFIT_FIBER_PROF
     {
@@ -733,6 +815,36 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
                 if (prof_acc[q]) atomicAdd(p.prof + q, (unsigned long long)prof_acc[q]);
     }
 #endif
+    if (NST == kDeepFStages && m0tg && p.do_m0) {
+        // the NM tile-group partials of every m-tile, summed in warp order through shared memory
+        // (the T ring is free once every warp has left its role loop)
+        const int ld = 32 * p.nchunk;
+        const int mt = (p.I0 + 7) / 8;
+        double* red = tiles;  // [NM][RP][ld]
+        __syncthreads();
+        if (warp >= Ro::M0W) {
+            const int m = warp - Ro::M0W;
+#pragma unroll
+            for (int rt = 0; rt < NRT; ++rt)
+#pragma unroll
+                for (int nt = 0; nt < Ro::TGMT; ++nt) {
+                    if (nt < mt) {
+                        const int r = rt * 8 + (lane >> 2);
+                        const int i = nt * 8 + 2 * (lane & 3);
+                        *reinterpret_cast<double2*>(red + ((size_t)m * RP + r) * ld + i) =
+                            make_double2(tacc[rt][nt][0], tacc[rt][nt][1]);
+                    }
+                }
+        }
+        __syncthreads();
+        double* out = p.m0_part + (size_t)blockIdx.x * RP * ld;
+        for (int e = tid; e < RP * 8 * mt; e += blockDim.x) {
+            const int r = e / (8 * mt), i = e % (8 * mt);
+            double v = 0.0;
+            for (int w2 = 0; w2 < Ro::NM; ++w2) v += red[((size_t)w2 * RP + r) * ld + i];
+            out[(size_t)r * ld + i] = v;
+        }
+    }
     if (resid) facc = racc.hi + racc.lo;
     if (p.do_f) {
         __shared__ double red[32];

@@ -17,7 +17,8 @@ import numpy as np
 import paper_1105_5331_b200 as P
 from paper_1105_5331_b200.api import lib
 
-dims, R = (400, 400, 400), 16
+dims = tuple(int(x) for x in os.environ.get("DIMS", "400,400,400").split(","))
+R = int(os.environ.get("RANK", "16"))
 rng = np.random.default_rng(0)
 T = rng.random(int(np.prod(dims)))
 u = rng.random(sum(dims) * R)
@@ -37,5 +38,6 @@ for kind in [int(k) for k in os.environ.get("KINDS", "3,4,5").split(",")]:
     def sh(x, tot):
         return f"{100 * x / tot:5.1f}%" if tot else "  -  "
     print(f"  producers tempty {sh(v[0], prod)}  wempty {sh(v[1], prod)}")
-    print(f"  compute   tfull  {sh(v[2], sw)}  wfull  {sh(v[4], sw)}  parts {sh(v[3], sw)}")
+    print(f"  S warps   tfull  {sh(v[2], sw)}  wfull  {sh(v[6], sw)}")
+    print(f"  M0 warps  tfull  {sh(v[3], mw)}  wfull  {sh(v[4], mw)}")
 
