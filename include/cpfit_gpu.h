@@ -12,8 +12,13 @@
  *     2 cpfit::numerical_error (errors.hpp:9-12), 3 CUDA / other failure; the message is
  *     available from cpfit_last_error() (thread-local);
  *   - distinct tensor handles may be used from different threads concurrently.
- * Device limits: order <= 8, rank <= 32, dense I_1 <= 512 (mode-0 fibers tile in smem),
- * sparse mode sizes < 2^31.
+ * Device limits: order <= 8, rank <= 32, N-GMRES window <= 63, sparse mode sizes < 2^31,
+ * R * sum(I_n) < 2^31. Dense shapes of any mode sizes: the fibre-tile passes take mode-0 lengths
+ * up to 416 (order >= 2); order-1 tensors and longer mode-0 fibres run the generic per-mode
+ * kernels (csrc/generic.cu) with the same results and error behaviour. Shapes beyond the limits
+ * return 1 (std::invalid_argument) at the first call that needs them.
+ * Destroyed dense handles are pooled (CPFIT_TENSOR_POOL_MB, default 8192; 0 disables): a new
+ * dense tensor of the same shape reuses the device buffers and captured solver graphs.
  */
 #ifndef CPFIT_GPU_H
 #define CPFIT_GPU_H
@@ -179,6 +184,11 @@ int cpfit_solver_phase_times(cpfit_solver s, double* us, int64_t* visits);
  * 3 fused fiber pass alone (S + M0 + per-fiber f), 4 fiber pass M0 only, 5 fiber pass S only. */
 int cpfit_bench_kernel(cpfit_tensor t, int64_t rank, const double* u, int kind, int mode, int reps, int flush_l2,
                        float* ms_per_call);
+
+/* Diagnostic: in the guard-band build (make guard, -DCPFIT_GUARD) every device allocation carries
+ * 4 KB guard bands; checks them all now. *violations = guard bands found changed so far (frees
+ * included), -1 when this is not a guard build; *live_allocations = device buffers alive. */
+int cpfit_debug_guard_check(int64_t* violations, int64_t* live_allocations);
 
 /* fp64 peaks measured on the current device (DMMA m8n8k4 and DFMA issue loops), TFLOP/s */
 int cpfit_measure_fp64_peak(double* dmma_tflops, double* dfma_tflops);

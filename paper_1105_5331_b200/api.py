@@ -120,6 +120,7 @@ _SIGS = {
     "cpfit_solver_launches": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "cpfit_line_polynomial": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p, _f64p, C.c_int64, _f64p, _f64p]),
     "cpfit_solver_phase_times": (C.c_int, [C.c_void_p, _f64p, C.POINTER(C.c_int64)]),
+    "cpfit_debug_guard_check": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "cpfit_measure_fp64_peak": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "cpfit_host_register": (C.c_int, [C.c_void_p, C.c_int64]),
     "cpfit_host_unregister": (C.c_int, [C.c_void_p]),
@@ -636,6 +637,14 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def debug_guard_check():
+    """(violations, live allocations) of the guard-band build (make guard; CPFIT_GPU_LIB pointing
+    at libcpfit_gpu_guard.so); violations = -1 for a normal build."""
+    v, n = C.c_int64(), C.c_int64()
+    _check(lib.cpfit_debug_guard_check(C.byref(v), C.byref(n)))
+    return v.value, n.value
 
 
 def measure_fp64_peak():

@@ -9,6 +9,19 @@
 #include <stdexcept>
 #include <string>
 
+// Guard-band build (-DCPFIT_GUARD, `make guard`): every device allocation of the library gets
+// 4 KB guard bands of a fixed byte pattern on both sides; frees and cpfit_debug_guard_check()
+// verify them, so an out-of-bounds write past either end of any buffer is reported (guard.cu).
+// compute-sanitizer is closed on the GPU pool this was built on; this is the substitute check.
+namespace cpfit_gpu {
+cudaError_t guard_malloc(void** p, size_t bytes);
+cudaError_t guard_free(void* p);
+}  // namespace cpfit_gpu
+#if defined(CPFIT_GUARD) && !defined(CPFIT_GUARD_IMPL)
+#define cudaMalloc(p, n) ::cpfit_gpu::guard_malloc(reinterpret_cast<void**>(p), (n))
+#define cudaFree(p) ::cpfit_gpu::guard_free((void*)(p))
+#endif
+
 namespace cpfit_gpu {
 
 constexpr int kMaxOrder = 8;   // tensor order supported on device

@@ -36,7 +36,15 @@ def O():
 def gpu(P):
     if P.device_count() < 1:
         pytest.fail("gpu-marked test ran without a visible CUDA device")
-    return P
+    yield P
+    # guard-band build (CPFIT_GPU_LIB=.../libcpfit_gpu_guard.so, csrc/guard.cu): after the whole
+    # GPU session every device buffer's 4 KB guard bands must be intact
+    import gc
+    gc.collect()
+    v, n = P.debug_guard_check()
+    if v >= 0:
+        print(f"\nguard-band check: {v} violations, {n} live device buffers")
+        assert v == 0, f"{v} device buffers were written out of bounds (see stderr)"
 
 
 def random_matrix(rng, rows, cols, lo=-1.0, hi=1.0):
