@@ -143,7 +143,7 @@ def config_dict(name, cfg, ws):
                         f"w=20, More-Thuente; consecutive solves from seeded U[0,1] starts (warm-up: seed 0; timed: "
                         f"seeds 1, 2, ...) to ||g||/(R sum I_n) < {stop_tol(name):g}, each solve's init inside the "
                         "timed region",
-            "inputs": f"T = {8 * int(np.prod(dims)) / 2**20:.0f} MB" +
+            "inputs": f"T = {8 * int(np.prod(dims)) / 1e6:.0f} MB" +
                       (" > L2 126 MB (no flush needed)" if 8 * int(np.prod(dims)) > 126e6 else " (L2-resident)"),
             "parallelism": f"{ws} independent replica(s), one solve stream per GPU"}
 
