@@ -159,6 +159,14 @@ int cpfit_solver_trace(cpfit_solver s, cpfit_trace_row* trace, int64_t rows);
 int cpfit_solver_best(cpfit_solver s, double* u);
 /* current (last accepted, canonical) iterate */
 int cpfit_solver_iterate(cpfit_solver s, double* u);
+/* ngmres_init(problem, initial, opts) — ngmres.hpp:101-103, for the CP problem ngmres_solve builds
+ * (ngmres.cpp:209-222) on a method-0 solver: canonicalize, evaluate, seed the window; *f = f(u).
+ * The state (NgmresState, ngmres.hpp:92-99: u, g, f, window, counters) stays on the device. */
+int cpfit_ngmres_init(cpfit_solver s, const double* u0, double* f);
+/* ngmres_step(problem, state, opts) — ngmres.hpp:109-117: one device iteration; the
+ * NgmresStepReport (restart, stalled, beta) and the accepted f. The device loop also applies
+ * ngmres_minimize's stop tests (ngmres.cpp:185-197): a step after a stop returns 1. */
+int cpfit_ngmres_step(cpfit_solver s, int* restart, int* stalled, double* beta, double* f);
 int cpfit_solver_destroy(cpfit_solver s);
 
 /* kernels of this library launched by the solver's loop graphs since cpfit_solver_init

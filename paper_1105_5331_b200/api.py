@@ -117,6 +117,9 @@ _SIGS = {
     "cpfit_solver_trace": (C.c_int, [C.c_void_p, C.POINTER(TraceRow), C.c_int64]),
     "cpfit_solver_best": (C.c_int, [C.c_void_p, _f64p]),
     "cpfit_solver_iterate": (C.c_int, [C.c_void_p, _f64p]),
+    "cpfit_ngmres_init": (C.c_int, [C.c_void_p, _f64p, C.POINTER(C.c_double)]),
+    "cpfit_ngmres_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]),
     "cpfit_solver_launches": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "cpfit_line_polynomial": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _f64p, _f64p, C.c_int64, _f64p, _f64p]),
     "cpfit_solver_phase_times": (C.c_int, [C.c_void_p, _f64p, C.POINTER(C.c_int64)]),
@@ -611,6 +614,18 @@ class Solver:
         out = np.empty(self.t.nu(self.rank))
         _check(lib.cpfit_solver_iterate(self._h, out))
         return out
+
+    def ngmres_init(self, u0) -> float:
+        """ngmres_init (ngmres.hpp:101-103): canonicalize, evaluate, seed the window; returns f."""
+        f = C.c_double()
+        _check(lib.cpfit_ngmres_init(self._h, _vec(u0, self.t.nu(self.rank), "ngmres_init"), C.byref(f)))
+        return f.value
+
+    def ngmres_step(self):
+        """ngmres_step (ngmres.hpp:109-117): one iteration; the NgmresStepReport and f."""
+        rs, st, b, f = C.c_int(), C.c_int(), C.c_double(), C.c_double()
+        _check(lib.cpfit_ngmres_step(self._h, C.byref(rs), C.byref(st), C.byref(b), C.byref(f)))
+        return dict(restart=bool(rs.value), stalled=bool(st.value), beta=b.value, f=f.value)
 
     def launches(self) -> int:
         n = C.c_int64()

@@ -751,6 +751,33 @@ int cpfit_solver_iterate(cpfit_solver s, double* u) {
     });
 }
 
+int cpfit_ngmres_init(cpfit_solver s, const double* u0, double* f) {
+    return guard([&] {
+        if (s->s->method() != 0) throw std::invalid_argument("ngmres_init: the solver was created for another method");
+        check_finite(u0, s->s->n());
+        s->s->set_initial(u0, true);
+        s->s->run_init();
+        const SolverSummary sm = s->s->summary();
+        if (f) *f = sm.f;
+    });
+}
+
+int cpfit_ngmres_step(cpfit_solver s, int* restart, int* stalled, double* beta, double* f) {
+    return guard([&] {
+        if (s->s->method() != 0) throw std::invalid_argument("ngmres_step: the solver was created for another method");
+        const SolverSummary before = s->s->summary();
+        if (before.stop >= 0)
+            throw std::invalid_argument("ngmres_step: the solve has stopped (gradient tolerance, stalls or budget)");
+        s->s->run_loop(before.iters + 1);
+        const SolverSummary sm = s->s->summary();
+        if (sm.status) throw cpfit_gpu::numerical_error("ngmres_step: numerical failure in the ALS normal equations");
+        if (restart) *restart = sm.restart;
+        if (stalled) *stalled = sm.stalled;
+        if (beta) *beta = sm.beta;
+        if (f) *f = sm.f;
+    });
+}
+
 int cpfit_solver_destroy(cpfit_solver s) {
     return guard([&] { delete s; });
 }

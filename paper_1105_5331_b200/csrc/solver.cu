@@ -1187,6 +1187,9 @@ SolverSummary Solver::summary() {
     r.fevals = hs.fevals;
     r.gevals = hs.gevals;
     r.rows = (method_ == 2) ? hs.rows : hs.iter + 1;
+    r.restart = hs.restart;
+    r.stalled = hs.stalled;
+    r.beta = hs.beta;
     r.launches = launches_done_ + loop_launches_ * n_prelude_ + init_launches_ * n_init_ +
                  (long long)hs.iter * n_body_ + hs.total_ls_evals * n_ls_ + (hs.total_accepted - hs.total_poly_acc) * n_acc_ +
                  hs.total_poly * n_poly_ + hs.total_poly_acc * n_accp_ + hs.total_direct * n_direct_;

@@ -51,6 +51,8 @@ struct SolverSummary {
     long long fevals, gevals;
     long long launches;  // kernels launched by the loop graphs since init
     int rows;            // trace rows written (N-CG writes none for stalled iterations)
+    int restart, stalled;  // the last iteration's NgmresStepReport (ngmres.hpp:109-113)
+    double beta;
 };
 
 class Solver {

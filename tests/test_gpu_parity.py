@@ -272,7 +272,7 @@ def test_swamp_config_within_oracle_envelope(gpu, O, cfg):
     ref = o.ngmres(u0, window=20, max_iters=2000, tol_grad=1e-10, gradient_scale=nu)
     rng = np.random.default_rng(1)
     counts = [len(ref["trace"]) - 1]
-    for _ in range(6):
+    for _ in range(20):
         r = o.ngmres(u0 * (1 + 1e-15 * rng.standard_normal(u0.size)), window=20, max_iters=2000, tol_grad=1e-10,
                      gradient_scale=nu)
         counts.append(len(r["trace"]) - 1)
@@ -357,3 +357,28 @@ def test_pooled_handle_refill_matches_oracle(gpu, O):
     fresh = P.DataTensor.dense(T2, dims)
     res2 = P.ngmres_solve(fresh, u0, opts)
     assert res2.f == res.f and len(res2.trace) == len(res.trace)
+
+
+def test_ngmres_init_and_step_match_the_oracle_trace(gpu, O):
+    """ngmres_init / ngmres_step (ngmres.hpp:101-117) on the device state: stepping reproduces the
+    oracle's trace row by row (restart flags, beta, f) for config 0, and a step after the stop
+    test fired is refused."""
+    P = gpu
+    dims, rank = (20, 20, 20), 3
+    T, _, _ = P.dense_test_problem(dims, rank, 0.5, 1.0, 1.0, 0, noise_mode=1)
+    u0 = P.uniform_initial_guess(dims, rank, 0)
+    nu = float(sum(dims) * rank)
+    t = P.DataTensor.dense(T, dims)
+    ref = O.Tensor.dense(dims, T).ngmres(u0, window=20, max_iters=60, tol_grad=1e-10, gradient_scale=nu)
+    s = P.Solver(t, rank, P.NgmresOptions(window=20, max_iters=60, tol_grad=1e-10, gradient_scale=nu), 0)
+    f0 = s.ngmres_init(u0)
+    assert abs(f0 - ref["trace"][0]["f"]) <= 1e-12 * abs(ref["trace"][0]["f"])
+    for row in ref["trace"][1:]:
+        rep = s.ngmres_step()
+        assert rep["restart"] == row["restart"]
+        assert abs(rep["f"] - row["f"]) <= 1e-8 * abs(row["f"])
+        # step lengths: Moré–Thuente interpolation on a flat phi moves them at ~1e-6 (f is gated)
+        assert abs(rep["beta"] - row["beta"]) <= 1e-4 * max(1.0, abs(row["beta"]))
+    assert s.state()["stop"] == ref["stop"]
+    with pytest.raises(ValueError):
+        s.ngmres_step()
