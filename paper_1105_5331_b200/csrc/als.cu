@@ -55,8 +55,8 @@ void dense_level(const DevTensor& t, EvalWork& w, int h, const double* Sin, cons
 void gather_m(int64_t In, EvalWork& w, const double* part, int grid, int ld, int layout, double* out,
               cudaStream_t st);
 void gram_mode_device(EvalWork& w, const double* u, int mode, cudaStream_t st);
-void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st);
-void rowwise_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st);
+void rowwise_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st,
+                   int skip_mode = -1);
 
 namespace {
 
@@ -638,7 +638,6 @@ __global__ void s_rescale_kernel(double* S, int64_t J, int R, const int* perm, c
 void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, double* out, double* work, double* mbuf,
                          int* status, cudaStream_t st, const double* m0_given, bool keep_s, bool grams_given,
                          bool defer_norm) {
-    if (defer_norm && rowwise(t)) throw std::logic_error("als sweep: deferred normalisation needs a dense tensor");
     CPFIT_CUDA(cudaMemcpyAsync(work, u, sizeof(double) * w.nu, cudaMemcpyDeviceToDevice, st));
     if (!grams_given) grams_device(w, work, st);
     const int N = t.order;

@@ -919,17 +919,20 @@ __global__ void grad_kernel(const GradParams p) {
 
 // ---------------------------------------------------------------------------------------
 // sparse hooks (sparse.cu)
-void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st);
+void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st,
+                      int skip_mode = -1);
 // generic dense hooks (generic.cu)
-void generic_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st);
+void generic_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st,
+                       int skip_mode = -1);
 void generic_plan(const DevTensor& t, int RP, int n, int* gx, int64_t* cols_per_cta, int* gy);
 
 // every mode's M_n (only_mode < 0) or one mode's into w.sp_part, for a rowwise tensor
-void rowwise_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st) {
+void rowwise_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st,
+                   int skip_mode = -1) {
     if (t.generic)
-        generic_all_modes(t, w, u, only_mode, st);
+        generic_all_modes(t, w, u, only_mode, st, skip_mode);
     else
-        sparse_all_modes(t, w, u, only_mode, st);
+        sparse_all_modes(t, w, u, only_mode, st, skip_mode);
 }
 
 bool fiber_path_fits(int order, int64_t I0) {
@@ -1244,7 +1247,10 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
         }
         reduce_jobs(jobs, st);
     } else {
-        rowwise_modes(t, w, u, -1, st);
+        // s_given for a rowwise tensor: M_{N-1} at u is already in w.sp_part (the deferred ALS
+        // sweep's last mode, computed from the same factors of modes 0 .. N-2)
+        rowwise_modes(t, w, u, -1, st, s_given ? t.order - 1 : -1);
+        if (grad_dep) CPFIT_CUDA(cudaStreamWaitEvent(st, grad_dep, 0));
     }
     run_grad(t, w, u, g, d, need_grad, sc, st);
 }

@@ -184,11 +184,12 @@ void generic_plan(const DevTensor& t, int RP, int n, int* gx, int64_t* cols_per_
 
 // M_n of every mode (only_mode < 0; mode 0 also leaves the residual partials in w.f_part) or
 // of one mode, into w.sp_part [mode offset][i][RP].
-void generic_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st) {
+void generic_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st,
+                       int skip_mode) {
     int64_t off = 0;
     for (int n = 0; n < t.order; ++n) {
         const int64_t In = t.dims[n];
-        if (only_mode < 0 || n == only_mode) {
+        if ((only_mode < 0 || n == only_mode) && n != skip_mode) {
             GenParams p{};
             p.order = t.order;
             p.n = n;

@@ -709,7 +709,9 @@ void Solver::construct(DevTensor* t, int R, const SolverOptions& o) {
     // Grams handed on by the normalisations (no Gram pass at the sweep start / for u_bar)
     gout_ = (int64_t)t->order * w_->RP * w_->RP <= kGramsOutMax;
     if (gout_) alloc(&gram_bar_, gram_n());
-    defer_ = method_ == 0 && !rowwise(*t) && gout_;
+    // rowwise (sparse / generic dense) tensors defer too: the sweep's last-mode M_{N-1} is the
+    // evaluation's (the same factors), so eval(u_bar) computes modes 0 .. N-2 only
+    defer_ = method_ == 0 && gout_;
     norm_nb_ = (int)std::min<int64_t>(296, (n_ + 255) / 256);
     // exact polynomial line search: dense order 3, default objective handling, not disabled
     const char* np = std::getenv("CPFIT_NO_POLY_LS");

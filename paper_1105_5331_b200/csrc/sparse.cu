@@ -273,7 +273,8 @@ void free_sparse_modes(DevTensor& t) {
     t.modes = nullptr;
 }
 
-void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st) {
+void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st,
+                      int skip_mode) {
     const int N = t.order;
     int64_t total = 0;
     for (int n = 0; n < N; ++n) total += t.dims[n] * w.RP;
@@ -285,7 +286,7 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
     off[0] = 0;
     for (int n = 0; n < N; ++n) off[n + 1] = off[n] + t.dims[n] * w.RP;
     for (int n = 0; n < N; ++n) {
-        if (only_mode >= 0 && n != only_mode) continue;
+        if ((only_mode >= 0 && n != only_mode) || n == skip_mode) continue;
         SpParams p{};
         p.In = t.dims[n];
         p.nnz = t.nnz;
