@@ -315,6 +315,7 @@ struct NormParams {
     const double* m0;
     double* m0out;
     int m0_ld;
+    int m0_rowmajor;  // M0 as [i][RP] (rowwise tensors, m0_ld = I_0 rows) instead of [r][m0_ld]
     // optional: a Gram still in block partials (the last mode of an ALS sweep): its diagonal is
     // summed from the partials here, and block 0 finalises it into gram_w
     GramPending pend;
@@ -389,12 +390,18 @@ __global__ void normalize_kernel(const NormParams p) {
         if (e < tm) {
             // 32-bit index math (tm, total < 2^31 for any iterate that fits a solve): 64-bit
             // division costs ~100 instructions and dominated the kernel at n_u = 3e5
-            const int r = (int)e / p.m0_ld;
-            const int i = (int)e - r * p.m0_ld;
+            int r, i;
+            if (p.m0_rowmajor) {
+                i = (int)e / p.RP;
+                r = (int)e - i * p.RP;
+            } else {
+                r = (int)e / p.m0_ld;
+                i = (int)e - r * p.m0_ld;
+            }
             double v = 0.0;
             if (r < p.R) {
                 const int src = perm[r];
-                v = p.m0[(int64_t)src * p.m0_ld + i];
+                v = p.m0_rowmajor ? p.m0[(int64_t)i * p.RP + src] : p.m0[(int64_t)src * p.m0_ld + i];
                 if (lam[src] != 0.0) v /= scale[0][r];
             }
             p.m0out[e] = v;
@@ -542,7 +549,8 @@ int normalize_grad_device(EvalWork& w, const double* u, const double* g, double*
     p.red = red;
     p.m0 = m0;
     p.m0out = m0out;
-    p.m0_ld = 32 * w.fiber_nchunk;
+    p.m0_rowmajor = w.m0_rowwise ? 1 : 0;
+    p.m0_ld = w.m0_rowwise ? (int)w.dims[0] : 32 * w.fiber_nchunk;
     const int blocks = (int)std::min<int64_t>(296, (w.nu + 255) / 256);
     normalize_kernel<<<blocks, 256, 0, st>>>(p);
     CPFIT_CUDA(cudaGetLastError());
@@ -646,11 +654,12 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
     if (rowwise(t)) {
         for (int n = 0; n < N; ++n) {
             if (n > 0) fork_chol(w, n, status, st);
-            rowwise_modes(t, w, work, n, st);
+            // mode 0: the M0 the evaluation of this iterate produced ([i][RP]), when given
+            if (!(n == 0 && m0_given)) rowwise_modes(t, w, work, n, st);
             int64_t off = 0;
             for (int m = 0; m < n; ++m) off += t.dims[m] * w.RP;
             if (n > 0) join_chol(w, st);
-            solve_gram(w, n, w.sp_part + off, 1, 0, work + w.off[n], status, st);
+            solve_gram(w, n, (n == 0 && m0_given) ? m0_given : w.sp_part + off, 1, 0, work + w.off[n], status, st);
         }
     } else {
         // mode 0: tail contraction with the old modes >= 1 — or, inside the N-GMRES loop, the

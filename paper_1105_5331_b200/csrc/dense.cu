@@ -1089,6 +1089,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
         int64_t tot = 0;
         for (int n = 0; n < t.order; ++n) tot += t.dims[n] * w->RP;
         CPFIT_CUDA(cudaMalloc(&w->sp_part, sizeof(double) * (size_t)tot));
+        w->m0_rowwise = true;
         CPFIT_CUDA(cudaMalloc(&w->frows, sizeof(double) * (size_t)tot));
         if (t.generic) {
             int64_t most = 1;

@@ -100,6 +100,7 @@ struct EvalWork {
     double* gram = nullptr;     // [mode][RP*RP] (rounded from dd; padded entries 0)
     // sparse
     double* sp_part = nullptr;  // per-mode outputs I_n x RP
+    bool m0_rowwise = false;    // M0 of an evaluation lives in sp_part ([i][RP]), not m0 ([RP][ld])
     double* frows = nullptr;    // row-major RP-padded factor copies (sum I_n x RP)
     // generic dense (generic.cu): column-range partials of one mode, residual partials count
     double* gen_part = nullptr;

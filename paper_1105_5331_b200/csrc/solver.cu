@@ -693,8 +693,8 @@ void Solver::construct(DevTensor* t, int R, const SolverOptions& o) {
     if (method_ == 0) {
         alloc(&wu_, n_ * cap_);
         alloc(&wg_, n_ * cap_);
-        if (!rowwise(*t)) {
-            m0_n_ = (int64_t)w_->RP * 32 * w_->fiber_nchunk;
+        {  // M0 at the current / bar / best-trial / accepted point (rowwise: [I_0][RP] copies of sp_part)
+            m0_n_ = rowwise(*t) ? (int64_t)w_->RP * t->dims[0] : (int64_t)w_->RP * 32 * w_->fiber_nchunk;
             alloc(&m0_cur_, m0_n_);
             alloc(&m0_bar_, m0_n_);
             alloc(&m0_best_, m0_n_);
@@ -802,7 +802,7 @@ void Solver::build_graphs() {
     grams_device(*w_, u0_, st_);
     normalize_device(*w_, u0_, u_, st_);
     eval_device(*t_, *w_, u_, g_, sc_cur, nullptr, status, st_, true, &s->resid);
-    if (m0_cur_) CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
+    if (m0_cur_) CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, m0_src(), sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
     k_after_init<<<1, 1, 0, st_>>>(c);
     if (method_ == 0)
         k_seed_window<<<vb, 256, 0, st_>>>(u_, g_, wu_, wg_, ubest_, n_);
@@ -866,7 +866,7 @@ void Solver::build_graphs() {
         eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st4_, true, &s->resid);
         stamp(st4_, 3);
         k_ls_update<<<1, 1, 0, st4_>>>(c, ls_h);
-        if (!opt_.reeval_accepted) k_keep_best<<<vb, 256, 0, st4_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
+        if (!opt_.reeval_accepted) k_keep_best<<<vb, 256, 0, st4_>>>(s, ut_, gt_, ubl_, gbl_, n_, m0_src(), m0_best_, m0_n_);
         stamp(st4_, 4);
         CPFIT_CUDA(cudaGetLastError());
         CPFIT_CUDA(cudaStreamEndCapture(st4_, &lsb));
@@ -881,12 +881,12 @@ void Solver::build_graphs() {
             normalize_device(*w_, ut_, un_, st4_);
             eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st4_, true, &s->resid);
             if (m0_cur_)
-                CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st4_));
+                CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, m0_src(), sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st4_));
             k_after_next<<<1, 1, 0, st4_>>>(c);
         } else {
             // exact rescale: normalize_and_reorder scales columns by D_n with
             // prod_n D_n = I, so f is unchanged and G_n -> G_n D_n^-1 (permuted)
-            k_select_accepted<<<vb, 256, 0, st4_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
+            k_select_accepted<<<vb, 256, 0, st4_>>>(s, ubl_, gbl_, ut_, gt_, n_, m0_src(), m0_best_, m0_sel_, m0_n_);
             grams_device(*w_, ut_, st4_);
             const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st4_, m0_sel_, m0_cur_, gout_);
             k_after_rescale<<<1, 32, 0, st4_>>>(c, sc_next, red_, nb);
@@ -938,7 +938,7 @@ void Solver::build_graphs() {
     } else {
         // stand-alone ALS iteration (als.cpp:79-95)
         // the previous evaluation (of u) left M0(u) in w.m0 for dense tensors
-        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, rowwise(*t_) ? nullptr : w_->m0, true, gout_);
+        als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, m0_src(), true, gout_);
         eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid, !rowwise(*t_), gout_);
     }
     if (method_ != 2) {
@@ -1012,12 +1012,12 @@ void Solver::emit_bar(cudaStream_t st, const void* ctl) {
         // the last mode's Gram is summed beside the M0 + objective pass (only the gradient needs it)
         finalize_gram_side(*w_, t_->order - 1, st, w_->ev_gram);
         eval_device(*t_, *w_, work_, gt_, sc_bar, nullptr, status, st, true, &s->resid, true, true, w_->ev_gram);
-        normalize_grad_device(*w_, work_, gt_, ub_, gb_, red_, st, w_->m0, m0_bar_, true, true, gram_bar_);
+        normalize_grad_device(*w_, work_, gt_, ub_, gb_, red_, st, m0_src(), m0_bar_, true, true, gram_bar_);
         return;
     }
     als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st, m0_cur_, true, gout_);
     eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st, true, &s->resid, !rowwise(*t_), gout_);
-    if (m0_bar_) CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st));
+    if (m0_bar_) CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, m0_src(), sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st));
     if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st));
 }
 
@@ -1042,7 +1042,7 @@ void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
         eval_given_s_device(*t_, *w_, ut_, gt_, sc_trial, st, pw_->S_d, &s->beta, true,
                             defer_ ? w_->nperm : nullptr, defer_ ? w_->nscale0 : nullptr);
     }
-    const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, w_->m0, m0_cur_, gout_);
+    const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st, m0_src(), m0_cur_, gout_);
     k_after_rescale<<<1, 32, 0, st>>>(c, sc_next, red_, nb);
     CPFIT_CUDA(cudaGetLastError());
 }
@@ -1117,7 +1117,7 @@ void Solver::run_loop_eager() {
                 eval_device(*t_, *w_, ut_, gt_, sc_trial, d_, status, st_, true, &s->resid);
                 k_ls_update<<<1, 1, 0, st_>>>(c, none);
                 if (!opt_.reeval_accepted)
-                    k_keep_best<<<vb, 256, 0, st_>>>(s, ut_, gt_, ubl_, gbl_, n_, w_->m0, m0_best_, m0_n_);
+                    k_keep_best<<<vb, 256, 0, st_>>>(s, ut_, gt_, ubl_, gbl_, n_, m0_src(), m0_best_, m0_n_);
             }
             const DevState ha = state();
             if (ha.poly) {
@@ -1129,10 +1129,10 @@ void Solver::run_loop_eager() {
                     normalize_device(*w_, ut_, un_, st_);
                     eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid);
                     if (m0_cur_)
-                        CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, w_->m0, sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
+                        CPFIT_CUDA(cudaMemcpyAsync(m0_cur_, m0_src(), sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st_));
                     k_after_next<<<1, 1, 0, st_>>>(c);
                 } else {
-                    k_select_accepted<<<vb, 256, 0, st_>>>(s, ubl_, gbl_, ut_, gt_, n_, w_->m0, m0_best_, m0_sel_, m0_n_);
+                    k_select_accepted<<<vb, 256, 0, st_>>>(s, ubl_, gbl_, ut_, gt_, n_, m0_src(), m0_best_, m0_sel_, m0_n_);
                     grams_device(*w_, ut_, st_);
                     const int nb = normalize_grad_device(*w_, ut_, gt_, un_, gn_, red_, st_, m0_sel_, m0_cur_, gout_);
                     k_after_rescale<<<1, 32, 0, st_>>>(c, sc_next, red_, nb);
@@ -1152,7 +1152,7 @@ void Solver::run_loop_eager() {
             emit_ncg_end(st_, &c, none);
             continue;
         } else {
-            als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, rowwise(*t_) ? nullptr : w_->m0, true, gout_);
+            als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, m0_src(), true, gout_);
             eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid, !rowwise(*t_), gout_);
         }
         k_commit<<<1, 1, 0, st_>>>(c, none);

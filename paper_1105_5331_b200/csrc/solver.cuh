@@ -112,6 +112,9 @@ private:
     // dense N-GMRES: M0 = T x KR(modes >= 1) at u (cur), u_bar (bar), the best trial (best) and
     // the accepted trial (sel), so the ALS sweep reuses the evaluation's mode-0 contraction
     double *m0_cur_ = nullptr, *m0_bar_ = nullptr, *m0_best_ = nullptr, *m0_sel_ = nullptr;
+    // where an evaluation leaves M0: w.m0 ([RP][32 nchunk], fibre passes) or the mode-0 block of
+    // w.sp_part ([I_0][RP], rowwise tensors)
+    double* m0_src() const { return w_->m0_rowwise ? w_->sp_part : w_->m0; }
     int64_t m0_n_ = 0;
     unsigned long long* phase_ = nullptr;  // [kPhases] ns, [kPhases] counts, [1] last stamp
     void* sc_ = nullptr;
