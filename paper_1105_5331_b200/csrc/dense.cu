@@ -1222,7 +1222,7 @@ void reduce_grad(const DevTensor& t, EvalWork& w, const RedJobs& jobs, const dou
 
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
                  int* status, cudaStream_t st, bool need_grad, const int* resid_flag, bool s_given, bool grams_given,
-                 cudaEvent_t grad_dep) {
+                 cudaEvent_t grad_dep, int rowwise_skip) {
     (void)status;
     if (!grams_given) grams_device(w, u, st);
     if (!rowwise(t)) {
@@ -1250,7 +1250,7 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
     } else {
         // s_given for a rowwise tensor: M_{N-1} at u is already in w.sp_part (the deferred ALS
         // sweep's last mode, computed from the same factors of modes 0 .. N-2)
-        rowwise_modes(t, w, u, -1, st, s_given ? t.order - 1 : -1);
+        rowwise_modes(t, w, u, -1, st, rowwise_skip >= 0 ? rowwise_skip : (s_given ? t.order - 1 : -1));
         if (grad_dep) CPFIT_CUDA(cudaStreamWaitEvent(st, grad_dep, 0));
     }
     run_grad(t, w, u, g, d, need_grad, sc, st);

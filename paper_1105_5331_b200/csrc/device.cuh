@@ -141,7 +141,11 @@ struct EvalScalars {
 // the T pass)
 void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, EvalScalars* sc, const double* d,
                  int* status, cudaStream_t st, bool need_grad = true, const int* resid_flag = nullptr,
-                 bool s_given = false, bool grams_given = false, cudaEvent_t grad_dep = nullptr);
+                 bool s_given = false, bool grams_given = false, cudaEvent_t grad_dep = nullptr,
+                 int rowwise_skip = -1);
+// rowwise tensors: M0 at u_bar + beta d from the four mixed mode-0 products the sparse line
+// contractions leave (PolyWork::m0xy): AA + beta (AD + DA) + beta^2 DD -> w.sp_part (mode 0)
+void sparse_m0_at_point(EvalWork& w, const double* m0xy, int64_t I0, const double* beta, cudaStream_t st);
 
 // mttkrp(T, factors(u), mode) (tensor.cpp:206-259) -> out (I_mode x R col-major).
 void mttkrp3_last_only(EvalWork& w, const double* u, double* out, cudaStream_t st);
@@ -201,6 +205,7 @@ struct PolyWork {
     unsigned int* counter = nullptr;
     int s8_grid = 0;
     double* drows = nullptr;  // sparse: row-major copy of d's factors
+    double* m0xy = nullptr;   // sparse: the mode-0 products with (X1, X2) in {AA, AD, DA, DD} [4][I0][RP]
     // the cross Grams run beside the S_d pass on their own stream (graph branch)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -209,7 +214,7 @@ bool poly_supported(const DevTensor& t);
 constexpr int kSparseLineBlocks = 592;
 // sparse order 3: the eight contractions of the line polynomial into part[nblocks][8] (sparse.cu)
 void sparse_line_contractions(const DevTensor& t, EvalWork& w, const double* ub, const double* d, double* drows,
-                              dd* part, int nblocks, cudaStream_t st);
+                              dd* part, int nblocks, cudaStream_t st, double* m0xy = nullptr);
 PolyWork* poly_create(const DevTensor& t, const EvalWork& w);
 void poly_destroy(PolyWork* p);
 // coefficients of phi from u_bar (its S in w.S) and d

@@ -585,6 +585,7 @@ PolyWork* poly_create(const DevTensor& t, const EvalWork& w) {
         int64_t rows = 0;
         for (int n = 0; n < 3; ++n) rows += t.dims[n];
         CPFIT_CUDA(cudaMalloc(&p->drows, sizeof(double) * (size_t)rows * w.RP));
+        CPFIT_CUDA(cudaMalloc(&p->m0xy, sizeof(double) * 4 * (size_t)t.dims[0] * w.RP));
     } else {
         p->s8_grid = t.order == 4 ? s16_grid_dims(t, w).x : s8_grid_dims(t, w).x;
         p->S_d = w.S2;  // owned by the evaluation workspace (next to S)
@@ -611,6 +612,7 @@ void poly_destroy(PolyWork* p) {
     cudaFree(p->s8);
     cudaFree(p->counter);
     cudaFree(p->drows);
+    cudaFree(p->m0xy);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
     if (p->side) cudaStreamDestroy(p->side);
@@ -651,7 +653,7 @@ void poly_build_device(const DevTensor& t, EvalWork& w, PolyWork& pw, const doub
     CPFIT_CUDA(cudaGetLastError());
     CPFIT_CUDA(cudaEventRecord(pw.ev_join, pw.side));
     if (t.sparse) {
-        sparse_line_contractions(t, w, ub, d, pw.drows, pw.s8part, pw.s8_grid, st);
+        sparse_line_contractions(t, w, ub, d, pw.drows, pw.s8part, pw.s8_grid, st, pw.m0xy);
         CPFIT_CUDA(cudaStreamWaitEvent(st, pw.ev_join, 0));  // cross Grams done
         launch_coef(t, w, pw, pw.s8_grid, st);
         return;

@@ -1031,8 +1031,10 @@ void Solver::emit_poly_accept(cudaStream_t st, const void* ctl) {
     // u* and its Grams (from the cross Grams); S(u*) = S(u_bar) + beta S_d is formed on the fly
     // by the level pass
     poly_point_device(*w_, *pw_, ub_, d_, &s->beta, ut_, st);
-    if (t_->sparse) {  // one sparse evaluation at u* (its Grams came with the point)
-        eval_device(*t_, *w_, ut_, gt_, sc_trial, nullptr, &s->status, st, true, &s->resid, false, true);
+    if (t_->sparse) {  // one sparse evaluation at u* (its Grams came with the point); its mode 0
+        // from the mixed products the line contractions left: AA + beta (AD + DA) + beta^2 DD
+        sparse_m0_at_point(*w_, pw_->m0xy, t_->dims[0], &s->beta, st);
+        eval_device(*t_, *w_, ut_, gt_, sc_trial, nullptr, &s->status, st, true, &s->resid, false, true, nullptr, 0);
     } else if (t_->order == 4) {
         const int rb = (int)std::min<int64_t>(1184, (t_->J + 255) / 256);
         k_s_point<<<rb, 256, 0, st>>>(s, 0, w_->S, pw_->S_d, t_->J, w_->RP, w_->R, defer_ ? w_->nperm : nullptr,

@@ -144,7 +144,7 @@ __global__ void frows_kernel(int order, const int64_t* dims_d, int64_t d0, int64
 template <int RP>
 __global__ void __launch_bounds__(256) sp_line8_kernel(const SpParams p, const double* a0rows, const double* d0rows,
                                                        const double* a1, const double* e1, const double* a2,
-                                                       const double* e2, dd* part) {
+                                                       const double* e2, dd* part, double* m0xy) {
     constexpr int G = 32 / RP;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r = lane % RP, g = lane / RP;
@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(256) sp_line8_kernel(const SpParams p, const d
     for (int64_t i = gw; i < p.In; i += nw) {
         const double x0a = live ? a0rows[i * RP + r] : 0.0, x0d = live ? d0rows[i * RP + r] : 0.0;
         const int64_t j0 = p.rowptr[i], j1 = p.rowptr[i + 1];
+        double qs[4] = {0.0, 0.0, 0.0, 0.0};  // the row's mode-0 products X1 X2 (for M0 at u*)
         for (int64_t jb = j0; jb < j1; jb += 32) {
             const int64_t jl = jb + lane;
             const bool okl = jl < j1;
@@ -182,6 +183,16 @@ __global__ void __launch_bounds__(256) sp_line8_kernel(const SpParams p, const d
             for (int b12 = 0; b12 < 4; ++b12) {
                 acc[b12] = dd_fma(acc[b12], x0a, q[b12]);
                 acc[4 + b12] = dd_fma(acc[4 + b12], x0d, q[b12]);
+                qs[b12] += q[b12];
+            }
+        }
+        if (m0xy) {  // combine the lane groups (fixed order), one row of each product
+#pragma unroll
+            for (int b12 = 0; b12 < 4; ++b12) {
+                double v = qs[b12];
+#pragma unroll
+                for (int o = RP; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (g == 0) m0xy[((int64_t)b12 * p.In + i) * RP + r] = live ? v : 0.0;
             }
         }
     }
@@ -315,7 +326,7 @@ namespace cpfit_gpu {
 // Row-major copies of the factors of u_bar (w.frows) and d (drows), then the eight line
 // contractions into part[nblocks][8] (poly.cu's coefficient kernel sums them in order).
 void sparse_line_contractions(const DevTensor& t, EvalWork& w, const double* ub, const double* d, double* drows,
-                              dd* part, int nblocks, cudaStream_t st) {
+                              dd* part, int nblocks, cudaStream_t st, double* m0xy) {
     if (t.order != 3) throw std::logic_error("sparse line contractions: order 3 only");
     int64_t total = 0;
     for (int n = 0; n < 3; ++n) total += t.dims[n] * w.RP;
@@ -334,15 +345,31 @@ void sparse_line_contractions(const DevTensor& t, EvalWork& w, const double* ub,
     p.R = w.R;
     switch (w.RP) {
         case 8:
-            sp_line8_kernel<8><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part);
+            sp_line8_kernel<8><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part, m0xy);
             break;
         case 16:
-            sp_line8_kernel<16><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part);
+            sp_line8_kernel<16><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part, m0xy);
             break;
         default:
-            sp_line8_kernel<32><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part);
+            sp_line8_kernel<32><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part, m0xy);
             break;
     }
+    CPFIT_CUDA(cudaGetLastError());
+}
+}  // namespace cpfit_gpu
+
+namespace cpfit_gpu {
+namespace {
+__global__ void sp_m0_point_kernel(const double* __restrict__ q, int64_t n, const double* beta, double* out) {
+    const double b = *beta;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = q[e] + b * (q[n + e] + q[2 * n + e]) + (b * b) * q[3 * n + e];
+}
+}  // namespace
+
+void sparse_m0_at_point(EvalWork& w, const double* m0xy, int64_t I0, const double* beta, cudaStream_t st) {
+    const int64_t n = I0 * w.RP;
+    sp_m0_point_kernel<<<(int)std::min<int64_t>(1184, (n + 255) / 256), 256, 0, st>>>(m0xy, n, beta, w.sp_part);
     CPFIT_CUDA(cudaGetLastError());
 }
 }  // namespace cpfit_gpu
