@@ -388,7 +388,44 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
             FiberIndex<ORD> xw = decode_fiber<ORD>(p, t_begin * F + fw);
             // short fibres: one tile ahead — the next tile's gathers are in flight while this one
             // waits for its ring slot (the producers are latency bound there)
-            if (NST == kDeepFStages) {
+            if (NST == kDeepFStages && ORD >= 3 && p.dims[1] % F == 0) {
+                // I1 % 16 == 0: a tile's fibres share their modes >= 2 and take 16 consecutive
+                // j1, so the multi-index is a tile-uniform counter advanced without divisions or
+                // per-lane carries (the branchy per-lane advance made these warps the M0 pass's
+                // bottleneck at 64^4), and W(f, r) = A1(j1, r) * prod_{m >= 2} A_m(j_m, r)
+                FiberIndex<ORD> x0 = decode_fiber<ORD>(p, t_begin * F);
+                auto ugather = [&](int64_t k, double (&w)[RS]) {
+                    const bool valid = (t_begin + k) * F + fw < p.J;
+#pragma unroll
+                    for (int j = 0; j < RS; ++j) {
+                        const int r = hw * RS + j;
+                        const bool ok = valid && r < p.R;
+                        double tail = 1.0;
+#pragma unroll
+                        for (int m = 2; m < (ORD > 0 ? ORD : kMaxOrder); ++m)
+                            if (ok) tail = m == 2 ? __ldg(p.fac[2] + (int64_t)r * p.dims[2] + x0.j[2])
+                                                  : tail * __ldg(p.fac[m] + (int64_t)r * p.dims[m] + x0.j[m]);
+                        w[j] = ok ? __ldg(p.fac[1] + (int64_t)r * p.dims[1] + x0.j[1] + fw) * tail : 0.0;
+                    }
+                    x0.j[1] += F;  // next tile
+                    if (x0.j[1] >= (int)p.dims[1]) {
+                        x0.j[1] = 0;
+#pragma unroll
+                        for (int m = 2; m < (ORD > 0 ? ORD : kMaxOrder); ++m) {
+                            if (++x0.j[m] < (int)p.dims[m]) break;
+                            x0.j[m] = 0;
+                        }
+                    }
+                };
+                double wc[RS], wn[RS];
+                if (ntl > 0) ugather(0, wc);
+                for (int64_t k = 0; k < ntl; ++k) {
+                    if (k + 1 < ntl) ugather(k + 1, wn);
+                    w_store(k, fw, hw, wc);
+#pragma unroll
+                    for (int j = 0; j < RS; ++j) wc[j] = wn[j];
+                }
+            } else if (NST == kDeepFStages) {
                 double wc[RS], wn[RS];
                 if (ntl > 0) w_gather(0, xw, fw, hw, wc);
                 for (int64_t k = 0; k < ntl; ++k) {
