@@ -393,37 +393,78 @@ __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __gri
                 // j1, so the multi-index is a tile-uniform counter advanced without divisions or
                 // per-lane carries (the branchy per-lane advance made these warps the M0 pass's
                 // bottleneck at 64^4), and W(f, r) = A1(j1, r) * prod_{m >= 2} A_m(j_m, r)
-                FiberIndex<ORD> x0 = decode_fiber<ORD>(p, t_begin * F);
-                auto ugather = [&](int64_t k, double (&w)[RS]) {
+                // The tail product changes only when j1 wraps (every I1 / 16 tiles): it is kept in
+                // registers, the next group's factor values are loaded one wrap ahead, and a tile
+                // costs one A1 load per (fibre, r), issued a tile before the multiply that uses it.
+                FiberIndex<ORD> xn = decode_fiber<ORD>(p, t_begin * F);
+                const int I1 = (int)p.dims[1];
+                constexpr int NT = (ORD > 2 ? ORD : kMaxOrder) - 2;  // tail modes (this branch: ORD >= 3)
+                const double* a1p[RS];
+                double tail[RS], nxt[NT][RS];
+                auto next_group = [&]() {
+#pragma unroll
+                    for (int m = 2; m < (ORD > 0 ? ORD : kMaxOrder); ++m) {
+                        if (++xn.j[m] < (int)p.dims[m]) break;
+                        xn.j[m] = 0;
+                    }
+                };
+                auto load_group = [&]() {  // factor values of group xn (indices wrap: always in range)
+#pragma unroll
+                    for (int j = 0; j < RS; ++j) {
+                        const int r = hw * RS + j < p.R ? hw * RS + j : 0;
+#pragma unroll
+                        for (int m = 2; m < (ORD > 0 ? ORD : kMaxOrder); ++m)
+                            nxt[m - 2][j] = mode_active<ORD>(p, m) ? __ldg(p.fac[m] + (int64_t)r * p.dims[m] + xn.j[m]) : 1.0;
+                    }
+                };
+                auto take_group = [&]() {
+#pragma unroll
+                    for (int j = 0; j < RS; ++j) {
+                        double v = 1.0;
+#pragma unroll
+                        for (int m = 0; m < NT; ++m) v *= nxt[m][j];
+                        tail[j] = hw * RS + j < p.R ? v : 0.0;
+                    }
+                };
+#pragma unroll
+                for (int j = 0; j < RS; ++j) {
+                    const int r = hw * RS + j;
+                    a1p[j] = p.fac[1] + (int64_t)(r < p.R ? r : 0) * I1 + fw;
+                }
+                int j1 = xn.j[1];
+                load_group();
+                take_group();
+                next_group();
+                load_group();
+                // gather tile k (raw A1 values + the tail of its group)
+                auto ugather = [&](int64_t k, double (&a)[RS], double (&tl)[RS]) {
                     const bool valid = (t_begin + k) * F + fw < p.J;
 #pragma unroll
                     for (int j = 0; j < RS; ++j) {
-                        const int r = hw * RS + j;
-                        const bool ok = valid && r < p.R;
-                        double tail = 1.0;
-#pragma unroll
-                        for (int m = 2; m < (ORD > 0 ? ORD : kMaxOrder); ++m)
-                            if (ok) tail = m == 2 ? __ldg(p.fac[2] + (int64_t)r * p.dims[2] + x0.j[2])
-                                                  : tail * __ldg(p.fac[m] + (int64_t)r * p.dims[m] + x0.j[m]);
-                        w[j] = ok ? __ldg(p.fac[1] + (int64_t)r * p.dims[1] + x0.j[1] + fw) * tail : 0.0;
+                        a[j] = valid && hw * RS + j < p.R ? __ldg(a1p[j] + j1) : 0.0;
+                        tl[j] = tail[j];
                     }
-                    x0.j[1] += F;  // next tile
-                    if (x0.j[1] >= (int)p.dims[1]) {
-                        x0.j[1] = 0;
-#pragma unroll
-                        for (int m = 2; m < (ORD > 0 ? ORD : kMaxOrder); ++m) {
-                            if (++x0.j[m] < (int)p.dims[m]) break;
-                            x0.j[m] = 0;
-                        }
+                    j1 += F;  // next tile
+                    if (j1 >= I1) {
+                        j1 = 0;
+                        take_group();
+                        next_group();
+                        load_group();
                     }
                 };
-                double wc[RS], wn[RS];
-                if (ntl > 0) ugather(0, wc);
+                double ac[RS], tc[RS], an[RS], tn[RS];
+                if (ntl > 0) ugather(0, ac, tc);
                 for (int64_t k = 0; k < ntl; ++k) {
-                    if (k + 1 < ntl) ugather(k + 1, wn);
-                    w_store(k, fw, hw, wc);
+                    if (k + 1 < ntl) ugather(k + 1, an, tn);
+                    double w[RS];
 #pragma unroll
-                    for (int j = 0; j < RS; ++j) wc[j] = wn[j];
+                    for (int j = 0; j < RS; ++j) w[j] = ac[j] * tc[j];
+                    w_store(k, fw, hw, w);
+#pragma unroll
+                    for (int j = 0; j < RS; ++j) {
+                        ac[j] = an[j];
+                        tc[j] = tn[j];
+                    }
                 }
             } else if (NST == kDeepFStages) {
                 double wc[RS], wn[RS];
