@@ -2,11 +2,13 @@
 // (kruskal.cpp:106-111, 127-149).
 //
 // Each mode n has its own mode-n-sorted copy (built at upload), so M_n(i, :) is a
-// segmented sum over rows of that copy: one warp per row, lanes strided over the row's
-// nonzeros, product v * prod_{k != n} A_k(c_k, :) in the reference's mode order, then a
-// warp reduction. Deterministic (no atomics); the streamed bytes per nonzero are the
-// value plus N-1 int32 indices; the factor-row gathers hit L2 (row-major RP-padded
-// copies of the factors, rebuilt per evaluation).
+// segmented sum over rows of that copy: one warp per row, lane groups over the row's
+// nonzeros, product v * prod_{k != n} A_k(c_k, :), then a fixed-order combination of the
+// groups. Deterministic (no atomics); the streamed bytes per nonzero are the value plus the
+// other modes' indices (two 16-bit indices packed in one word for order 3 when they fit); the
+// factor-row gathers hit L2 (row-major RP-padded copies of the factors, rebuilt per
+// evaluation). At BASELINE config 4 the gathers are the bound: ~5.7 L2 sectors per nonzero
+// at ~75 % of the L2 throughput cap (profiles/r02_summary.md, "Sparse").
 #include "sparse.cuh"
 
 #include <algorithm>
@@ -103,6 +105,202 @@ __global__ void __launch_bounds__(256) sp_mttkrp_kernel(const SpParams p) {
         for (int o = RP; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (g == 0) p.out[i * RP + r] = acc;
     }
+}
+
+// Row-segment layout (the default). A factor row of RP doubles is one 128-byte line at RP = 16;
+// it is gathered by L = RP/2 lanes with one 16-byte load each, so every quarter-warp phase of a
+// 128-bit load touches exactly one line (one L1 wavefront per row; lanes past R are predicated off
+// so only the sectors holding ranks < R move). One warp step covers G = 32 / L nonzeros (RP = 16: 4).
+// Every lane of a group loads its nonzero's value and indices itself — for order 3 with both other
+// mode sizes <= 65536 the two indices come packed in one 32-bit word (one wavefront per step) — so
+// no shuffles sit between the index stream and the gathers. The previous layout (RP lanes with
+// 8-byte loads, indices broadcast by 4 shuffles per 2 nonzeros) spent a third of the L1 data path
+// on shuffles; a 5-lane layout for R = 10 straddled quarter-warp phases (1.5 wavefronts per row).
+// U steps are issued before their products; each warp owns rows_per_warp consecutive rows and one
+// lane prefetches the next row's index/value ranges into L2 with a bulk prefetch, so the dependent
+// index loads of a row's first chunk hit L2. Groups are combined in fixed order at the end of a row
+// (deterministic).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* base, int64_t bytes) {
+    // the 16-byte-aligned interior only: a prefetch reaching past the allocation faults
+    const uintptr_t a0 = (reinterpret_cast<uintptr_t>(base) + 15) & ~uintptr_t(15);
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(base) + (uintptr_t)bytes) & ~uintptr_t(15);
+    if (a1 > a0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+}
+
+// Loads through volatile asm keep their program order: the chunk's next index loads and all of
+// its gathers issue before the first product (the compiler otherwise interleaves them with the
+// multiplies to save registers, putting several L2 round trips in series per chunk).
+__device__ __forceinline__ double2 ldg_d2(const double2* a, bool on) {
+    double2 v;
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n mov.f64 %0, 0d0000000000000000;\n"
+        " mov.f64 %1, 0d0000000000000000;\n @p ld.global.nc.v2.f64 {%0, %1}, [%2];\n}"
+        : "=d"(v.x), "=d"(v.y)
+        : "l"(a), "r"((unsigned)on));
+    return v;
+}
+__device__ __forceinline__ double ldg_d(const double* a, bool on) {  // 0.0 when !on
+    double v;
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n mov.f64 %0, 0d0000000000000000;\n"
+                 " @p ld.global.nc.f64 %0, [%1];\n}"
+                 : "=d"(v)
+                 : "l"(a), "r"((unsigned)on));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_u(const uint32_t* a) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(a));
+    return v;
+}
+
+template <int RP, int NO, int U, bool PK>
+__global__ void __launch_bounds__(256) sp_mttkrp2_kernel(const SpParams p, const uint32_t* __restrict__ pidx,
+                                                         int64_t rows_per_warp) {
+    constexpr int L = RP / 2, G = 32 / L;
+    constexpr int NK = NO > 0 ? NO : kMaxOrder - 1;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / L, c = lane % L;
+    const bool live = 2 * c < p.R;
+    const int nother = NO > 0 ? NO : p.nother;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t i0 = gw * rows_per_warp, i1 = imin64(p.In, i0 + rows_per_warp);
+    const double2* fr[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) fr[k] = reinterpret_cast<const double2*>(k < nother ? p.frow[k] : p.frow[0]) + c;
+    auto prefetch_row = [&](int64_t i) {
+        const int64_t a = p.rowptr[i], b = p.rowptr[i + 1];
+        if (b > a) {
+            bulk_prefetch_l2(p.vals + a, (b - a) * 8);
+            if (PK)
+                bulk_prefetch_l2(pidx + a, (b - a) * 4);
+            else
+                for (int k = 0; k < nother; ++k) bulk_prefetch_l2(p.oidx + (int64_t)k * p.nnz + a, (b - a) * 4);
+        }
+    };
+    if (lane == 0 && i0 < i1) prefetch_row(i0);
+    for (int64_t i = i0; i < i1; ++i) {
+        if (lane == 0 && i + 1 < i1) prefetch_row(i + 1);
+        const int64_t j0 = p.rowptr[i], j1 = p.rowptr[i + 1];
+        double ax = 0.0, ay = 0.0;
+        if (j0 >= j1) {
+            if (g == 0) reinterpret_cast<double2*>(p.out + i * RP)[c] = make_double2(0.0, 0.0);
+            continue;
+        }
+        // Two-stage software pipeline over chunks of C = G*U nonzeros: in the iteration that
+        // consumes chunk m, the gathers of chunk m+1 and the index loads of chunk m+2 are issued
+        // first. Loop-carried registers keep them in flight across the products (the compiler
+        // otherwise sinks each gather next to its multiply). Slots past the row's end load an
+        // in-range address and carry v = 0.
+        constexpr int C = G * U;
+        const int n = (int)(j1 - j0);
+        const double* vrow = p.vals + j0;
+        const uint32_t* prow = PK ? pidx + j0 : nullptr;
+        auto load_idx = [&](int64_t jb, double (&vv)[U], int (&cc)[U][NK]) {
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+                const int q = (int)(jb - j0) + t * G + g;  // offset in the row (rows < 2^31 nonzeros)
+                const bool ok = q < n;
+                const int qc = ok ? q : 0;
+                vv[t] = ldg_d(vrow + qc, ok);
+                if (PK) {
+                    cc[t][0] = (int)ldg_u(prow + qc);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NK; ++k)
+                        cc[t][k] = k < nother ? __ldg(p.oidx + (int64_t)k * p.nnz + j0 + qc) : 0;
+                }
+            }
+        };
+        auto gather = [&](const int (&cc)[U][NK], double2 (&xx)[U][NK]) {
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+                int ci[NK];
+                if (PK) {
+                    const uint32_t w = (uint32_t)cc[t][0];
+                    ci[0] = (int)(w & 0xffffu);
+                    ci[1] = (int)(w >> 16);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NK; ++k) ci[k] = cc[t][k];
+                }
+#pragma unroll
+                for (int k = 0; k < NK; ++k)
+                    if (k < nother) xx[t][k] = ldg_d2(fr[k] + (int64_t)ci[k] * L, live);
+            }
+        };
+        double va[U], vb[U];
+        int ca[U][NK], cb[U][NK];
+        double2 xa[U][NK];
+        load_idx(j0, va, ca);
+        gather(ca, xa);
+        load_idx(j0 + C, vb, cb);
+        for (int64_t jb = j0; jb < j1; jb += C) {
+            double2 xb[U][NK];
+            gather(cb, xb);              // chunk m+1
+            double vc[U];
+#pragma unroll
+            for (int t = 0; t < U; ++t) vc[t] = vb[t];
+            load_idx(jb + 2 * C, vb, cb);  // chunk m+2
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+                double px = va[t], py = va[t];
+#pragma unroll
+                for (int k = 0; k < NK; ++k)
+                    if (k < nother) {
+                        px *= xa[t][k].x;
+                        py *= xa[t][k].y;
+                    }
+                ax += px;
+                ay += py;
+            }
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+                va[t] = vc[t];
+#pragma unroll
+                for (int k = 0; k < NK; ++k) xa[t][k] = xb[t][k];
+            }
+        }
+        // groups in fixed order onto group 0's lanes, which write the row (zeros past R)
+#pragma unroll
+        for (int o = L; o < 32; o <<= 1) {
+            ax += __shfl_xor_sync(0xffffffffu, ax, o);
+            ay += __shfl_xor_sync(0xffffffffu, ay, o);
+        }
+        if (g == 0) reinterpret_cast<double2*>(p.out + i * RP)[c] = make_double2(ax, ay);
+    }
+}
+
+template <int RP>
+#ifndef CPFIT_SP_U
+#define CPFIT_SP_U 2
+#endif
+void launch_sp2(const SpParams& p, const uint32_t* pidx, int order, cudaStream_t st) {
+    constexpr int U = CPFIT_SP_U;
+    // rows_per_warp from a target of 32 resident warps per SM; blocks of 8 warps
+#ifndef CPFIT_SP_WPS
+#define CPFIT_SP_WPS 24
+#endif
+    const int64_t max_warps = 148 * CPFIT_SP_WPS;
+    const int64_t rpw = std::max<int64_t>(1, (p.In + max_warps - 1) / max_warps);
+    const int64_t nwarps = (p.In + rpw - 1) / rpw;
+    const int blocks = (int)std::max<int64_t>(1, (nwarps + 7) / 8);
+    if (order == 3 && pidx)
+        sp_mttkrp2_kernel<RP, 2, U, true><<<blocks, 256, 0, st>>>(p, pidx, rpw);
+    else if (order == 3)
+        sp_mttkrp2_kernel<RP, 2, U, false><<<blocks, 256, 0, st>>>(p, nullptr, rpw);
+    else if (order == 4)
+        sp_mttkrp2_kernel<RP, 3, U, false><<<blocks, 256, 0, st>>>(p, nullptr, rpw);
+    else
+        sp_mttkrp2_kernel<RP, 0, 2, false><<<blocks, 256, 0, st>>>(p, nullptr, rpw);
+}
+
+bool sp_v1() {
+    static const bool v1 = [] {
+        const char* e = getenv("CPFIT_SP_V1");
+        return e && e[0] == '1';
+    }();
+    return v1;
 }
 
 template <int RP>
@@ -228,6 +426,7 @@ void upload_sparse_modes(DevTensor& t, const std::vector<int64_t>& coords, const
     std::vector<std::vector<int64_t>> rowptrs((size_t)N);
     std::vector<std::vector<int32_t>> oidxs((size_t)N);
     std::vector<std::vector<double>> svs((size_t)N);
+    std::vector<std::vector<uint32_t>> pidxs((size_t)N);
     auto sort_mode = [&](int n) {
         const int64_t In = t.dims[n];
         std::vector<int64_t>& rowptr = rowptrs[(size_t)n];
@@ -261,12 +460,30 @@ void upload_sparse_modes(DevTensor& t, const std::vector<int64_t>& coords, const
         const std::vector<int32_t>& oidx = oidxs[(size_t)n];
         const std::vector<double>& sv = svs[(size_t)n];
         CPFIT_CUDA(cudaMalloc(&sm->rowptr[n], sizeof(int64_t) * rowptr.size()));
-        CPFIT_CUDA(cudaMalloc(&sm->oidx[n], sizeof(int32_t) * std::max<size_t>(oidx.size(), 1)));
-        CPFIT_CUDA(cudaMalloc(&sm->vals[n], sizeof(double) * std::max<size_t>(sv.size(), 1)));
+        // one zero slot past the end (value 0, index 0): pipeline slots past a segment's end load
+        // it instead of being predicated off
+        CPFIT_CUDA(cudaMalloc(&sm->oidx[n], sizeof(int32_t) * (oidx.size() + 1)));
+        CPFIT_CUDA(cudaMalloc(&sm->vals[n], sizeof(double) * (sv.size() + 1)));
+        CPFIT_CUDA(cudaMemsetAsync(sm->oidx[n] + oidx.size(), 0, sizeof(int32_t), st));
+        CPFIT_CUDA(cudaMemsetAsync(sm->vals[n] + sv.size(), 0, sizeof(double), st));
         CPFIT_CUDA(cudaMemcpyAsync(sm->rowptr[n], rowptr.data(), sizeof(int64_t) * rowptr.size(), cudaMemcpyHostToDevice, st));
         if (nnz > 0) {
             CPFIT_CUDA(cudaMemcpyAsync(sm->oidx[n], oidx.data(), sizeof(int32_t) * oidx.size(), cudaMemcpyHostToDevice, st));
             CPFIT_CUDA(cudaMemcpyAsync(sm->vals[n], sv.data(), sizeof(double) * sv.size(), cudaMemcpyHostToDevice, st));
+        }
+        if (N == 3 && nnz > 0) {
+            bool fits = true;
+            for (int m = 0; m < 3; ++m)
+                if (m != n && t.dims[m] > 65536) fits = false;
+            if (fits) {
+                pidxs[(size_t)n].resize((size_t)nnz);
+                uint32_t* pk = pidxs[(size_t)n].data();
+                const int32_t* o = oidx.data();
+                for (int64_t j = 0; j < nnz; ++j) pk[j] = (uint32_t)o[j] | ((uint32_t)o[nnz + j] << 16);
+                CPFIT_CUDA(cudaMalloc(&sm->pidx[n], sizeof(uint32_t) * ((size_t)nnz + 1)));
+                CPFIT_CUDA(cudaMemsetAsync(sm->pidx[n] + nnz, 0, sizeof(uint32_t), st));
+                CPFIT_CUDA(cudaMemcpyAsync(sm->pidx[n], pk, sizeof(uint32_t) * (size_t)nnz, cudaMemcpyHostToDevice, st));
+            }
         }
         CPFIT_CUDA(cudaStreamSynchronize(st));  // host staging vectors go out of scope
     }
@@ -279,6 +496,7 @@ void free_sparse_modes(DevTensor& t) {
         cudaFree(t.modes->rowptr[n]);
         cudaFree(t.modes->oidx[n]);
         cudaFree(t.modes->vals[n]);
+        cudaFree(t.modes->pidx[n]);
     }
     delete t.modes;
     t.modes = nullptr;
@@ -310,6 +528,16 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
         p.nother = k;
         p.R = w.R;
         p.out = w.sp_part + off[n];
+        if (!sp_v1()) {
+            const uint32_t* pk = t.modes->pidx[n];
+            switch (w.RP) {
+                case 8: launch_sp2<8>(p, pk, N, st); break;
+                case 16: launch_sp2<16>(p, pk, N, st); break;
+                default: launch_sp2<32>(p, pk, N, st); break;
+            }
+            CPFIT_CUDA(cudaGetLastError());
+            continue;
+        }
         const int blocks = (int)std::min<int64_t>(148 * 8, (p.In * 32 + 255) / 256);
         switch (w.RP) {
             case 8: launch_sp<8>(p, blocks, N, st); break;
