@@ -248,19 +248,25 @@ __global__ void k_poly_ls(Ctl c) {
 // order 4: S(u*) = S(u_bar) + beta S_d materialised in place (the first level of an order-4
 // tensor cannot form it on the fly), with S(u_bar) = S'[.][perm r] sc0[r] when perm is set;
 // guard: only after an accepted search (N-CG keeps S(u) otherwise)
+// Coalesced: a warp covers 32 consecutive elements (32 / RP whole rows, RP in {8, 16, 32}); the
+// column permutation is a shuffle inside the row, so the in-place update has no cross-thread race.
 __global__ void k_s_point(const DevState* s, int guard, double* S, const double* Sd, int64_t J, int RP, int R,
                           const int* perm, const double* sc0) {
     if (guard && !s->accepted) return;
     const double b = s->beta;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
-        double* row = S + j * RP;
-        const double* drow = Sd + j * RP;
-        double v[32];
-        for (int r = 0; r < RP; ++r) v[r] = row[r];
-        for (int r = 0; r < RP; ++r) {
-            const double base = (perm && r < R) ? v[perm[r]] * sc0[r] : v[r];
-            row[r] = fma(b, drow[r], base);
-        }
+    const int lane = threadIdx.x & 31, r = lane % RP;
+    const bool pm = perm && r < R;
+    const int src = lane - r + (pm ? perm[r] : r);
+    const double sc = pm ? sc0[r] : 1.0;
+    const int64_t total = J * RP;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; w0 < total; w0 += nw * 32) {
+        const int64_t e = w0 + lane;
+        const bool ok = e < total;
+        const double v = ok ? S[e] : 0.0;
+        const double d = ok ? Sd[e] : 0.0;
+        const double base = __shfl_sync(0xffffffffu, v, src) * sc;
+        if (ok) S[e] = fma(b, d, base);
     }
 }
 

@@ -176,3 +176,44 @@ def test_shape_and_rank_errors(gpu):
         P.DataTensor.dense(np.ones(5), (2, 3))  # value count
     with pytest.raises(ValueError):
         P.ngmres_solve(t, np.ones(9 * 2), P.NgmresOptions(window=64))  # window above the device limit
+
+
+def test_coo_canonicalisation_and_rejections(gpu, O):
+    """COO input through the C-ABI (tensor.cpp:56-103; test_tensor.cpp:170-211): duplicates are
+    summed, explicit zeros and cancelled duplicates dropped, out-of-range coordinates and
+    non-finite values rejected (invalid_argument -> ValueError), like the reference."""
+    P = gpu
+    # the reference's own example: (1,1) = 2 and -2 cancel and are dropped; (0,0) = 5, (0,1) = 1 remain
+    coords = np.array([1, 1, 0, 0, 1, 1, 0, 1]).reshape(-1, 2)
+    t = P.DataTensor.coo((2, 2), coords, np.array([2.0, 5.0, -2.0, 1.0]))
+    o = O.Tensor.coo((2, 2), coords, [2.0, 5.0, -2.0, 1.0])
+    assert t.nnz() == 2 and abs(t.norm() - o.norm()) <= 1e-15 * o.norm()
+    # duplicates, explicit zeros and a duplicate pair that cancels, order 3, against the oracle
+    rng = np.random.default_rng(17)
+    dims = (6, 5, 4)
+    base = np.stack([rng.integers(0, d, 60) for d in dims], axis=1)
+    coords = np.concatenate([base, base[:20], base[40:45]])
+    vals = np.concatenate([rng.standard_normal(60), rng.standard_normal(20), np.zeros(5)])
+    vals[:3] = 0.0  # explicit zeros
+    vals[60:63] = 0.0
+    vals[10], vals[70] = 1.5, -1.5  # this duplicate pair cancels
+    t, o = P.DataTensor.coo(dims, coords, vals), O.Tensor.coo(dims, coords, vals)
+    oc, ov = o.sparse_contents()
+    assert t.nnz() == len(ov) and abs(t.norm() - o.norm()) <= 1e-14 * o.norm()
+    u = random_factors(rng, dims, 3)
+    for m in range(3):
+        assert rel(t.mttkrp(u, m), o.mttkrp(u, m)) <= 1e-12
+    f, g = P.objective_and_gradient(t, u)
+    fo, go = o.eval(u)
+    assert abs(f - fo) <= 1e-12 * abs(fo) and rel(g, go) <= 1e-12
+    with pytest.raises(ValueError):  # coordinate out of range
+        P.DataTensor.coo((2, 2), np.array([[2, 0]]), np.array([1.0]))
+    with pytest.raises(ValueError):
+        P.DataTensor.coo((2, 2), np.array([[0, -1]]), np.array([1.0]))
+    for bad in (np.nan, np.inf, -np.inf):  # non-finite values
+        with pytest.raises(ValueError):
+            P.DataTensor.coo((2, 2), np.array([[0, 0], [1, 1]]), np.array([1.0, bad]))
+        x = np.ones(24)
+        x[7] = bad
+        with pytest.raises(ValueError):
+            P.DataTensor.dense(x, (2, 3, 4))

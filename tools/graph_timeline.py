@@ -1,7 +1,7 @@
 """Device timeline of the N-GMRES loop as the solver runs it (CUDA graph, not eager) at C2
 (400^3, R=16) through CUPTI: per-kernel busy time, the idle time between consecutive kernels
 (launch gaps inside the graph), and one iteration's kernel sequence with start offsets.
-usage: python tools/graph_timeline.py  [ITERS=20 WARM=10 SHOW=1]"""
+usage: python tools/graph_timeline.py  [CFG=c2|c3 ITERS=20 WARM=10 SHOW=1]"""
 import os
 import sys
 from collections import defaultdict
@@ -12,11 +12,14 @@ from torch.profiler import ProfilerActivity, profile
 
 import paper_1105_5331_b200 as P
 
-dims, R = (400, 400, 400), 16
-T, _, _ = P.dense_test_problem(dims, R, 0.5, 1.0, 1.0, 0, noise_mode=1)
+import bench  # noqa: E402
+
+cfg = bench.CONFIGS[os.environ.get("CFG", "c2")]  # CFG=c3: the order-4 config
+dims, R = cfg["dims"], cfg["rank"]
+T, u0 = bench.make_problem(P, cfg, 1)
 t = P.DataTensor.dense(T, dims)
-s = P.Solver(t, R, P.NgmresOptions(tol_grad=1e-10, gradient_scale=float(sum(dims) * R), max_iters=400))
-s.set_initial(P.uniform_initial_guess(dims, R, 1))
+s = P.Solver(t, R, P.NgmresOptions(tol_grad=1e-300, gradient_scale=float(sum(dims) * R), max_iters=400))
+s.set_initial(u0)
 s.init()
 w0 = int(os.environ.get("WARM", "10"))
 n = int(os.environ.get("ITERS", "20"))
