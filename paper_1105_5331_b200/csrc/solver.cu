@@ -80,6 +80,7 @@ struct Ctl {
     int ncg;       // 1: N-CG (ncg.cpp) control flow
     int eager;     // 1: host-driven loop (no graph conditionals; profiling / launch lists)
     int poly_ok;   // the polynomial line search applies to this tensor / options
+    int poly_exact;  // sparse: f has one (three-term) form, so the residual phase keeps the polynomial
     const dd* coef;
 };
 
@@ -177,7 +178,7 @@ __global__ void k_branch(Ctl c, cudaGraphConditionalHandle br_h) {
     } else {
         s.searching = s.mt.begin(c.ls, s.f_bar, s.slope) ? 1 : 0;
     }
-    s.poly = (c.poly_ok && s.searching && !s.resid) ? 1 : 0;
+    s.poly = (c.poly_ok && s.searching && (!s.resid || c.poly_exact)) ? 1 : 0;
     if (s.poly) {
         s.searching = 0;  // no trial-evaluation loop
         s.total_poly += 1;
@@ -467,7 +468,7 @@ __global__ void k_ncg_begin(Ctl c, const double* red, int nb, cudaGraphCondition
     s.searching = s.mt.begin(c.ls, s.f, sl) ? 1 : 0;
     // branch: 0 Moré–Thuente on the exact polynomial phi (dense order 3, per-fibre objective
     // phase), 1 on trial evaluations, 2 none (NotDescent: step 0, a stall, ncg.cpp:60)
-    s.poly = (c.poly_ok && s.searching && !s.resid) ? 1 : 0;
+    s.poly = (c.poly_ok && s.searching && (!s.resid || c.poly_exact)) ? 1 : 0;
     if (s.poly) {
         s.searching = 0;
         s.total_poly += 1;
@@ -791,6 +792,10 @@ void Solver::build_graphs() {
     c.als_mode = (method_ == 1);
     c.ncg = (method_ == 2);
     c.poly_ok = pw_ ? 1 : 0;
+    // a sparse tensor's f is the reference's three-term form in every phase (the residual switch
+    // only matters for the dense per-fibre form); phi in double-double is at least as exact as a
+    // trial evaluation, so stagnation does not send the search back to trial evaluations
+    c.poly_exact = (pw_ && t_->modes) ? 1 : 0;
     c.coef = pw_ ? pw_->coef : nullptr;
     static_assert(sizeof(Ctl) <= sizeof(ctl_blob_), "ctl blob");
     std::memcpy(ctl_blob_, &c, sizeof(Ctl));

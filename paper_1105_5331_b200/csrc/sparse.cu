@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <thread>
+#include <type_traits>
 
 namespace cpfit_gpu {
 
@@ -335,62 +336,153 @@ __global__ void frows_kernel(int order, const int64_t* dims_d, int64_t d0, int64
 
 
 // The eight contractions <T, [[X0, X1, X2]]> (X_n in {A_n, D_n}, index 4 b0 + 2 b1 + b2, b_n = 1
-// selects D_n) of a sparse order-3 tensor for the exact line-search polynomial (poly.cu): warp per
-// mode-0 row i over the mode-0 sorted copy, lanes spanning the rank as in sp_mttkrp_kernel; per
-// 32-nonzero chunk the four inner sums sum_nz v X1[j][r] X2[k][r] in fp64, folded into
-// double-double with X0[i][r] in {A0, D0}; per-block partials [block][8] for coef_kernel.
-template <int RP>
-__global__ void __launch_bounds__(256) sp_line8_kernel(const SpParams p, const double* a0rows, const double* d0rows,
-                                                       const double* a1, const double* e1, const double* a2,
-                                                       const double* e2, dd* part, double* m0xy) {
-    constexpr int G = 32 / RP;
+// selects D_n) of a sparse order-3 tensor for the exact line-search polynomial (poly.cu), over the
+// mode-0 sorted copy in the layout and two-stage pipeline of sp_mttkrp2_kernel (RP/2 lanes per
+// row, 16-byte gathers of A1[j], D1[j], A2[k], D2[k]; packed indices when they fit). Each lane
+// sums v X1[j] X2[k] for its two ranks in fp64 over a window of 16 of its group's nonzeros, then
+// folds the window into double-double with X0[i] in {A0, D0} (the same 16-term fp64 sums as the
+// shuffle-broadcast kernel it replaces); per-block partials [block][8] for coef_kernel, and the
+// row's four mode-0 products X1 X2 (for M0 at u*) when m0xy is set.
+template <int RP, int U, bool PK>
+__global__ void __launch_bounds__(256, 2) sp_line8_kernel(const SpParams p, const uint32_t* __restrict__ pidx,
+                                                       int64_t rows_per_warp, const double* a0rows,
+                                                       const double* d0rows, const double* a1, const double* e1,
+                                                       const double* a2, const double* e2, dd* part, double* m0xy) {
+    constexpr int L = RP / 2, G = 32 / L, C = G * U;
+    constexpr int FOLD = 16 / U;  // chunks per fp64 window (16 nonzeros per lane group)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int r = lane % RP, g = lane / RP;
-    const bool live = r < p.R;
+    const int g = lane / L, c = lane % L;
+    const bool live = 2 * c < p.R;
     dd acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = dd{0.0, 0.0};
+    const double2* f1a = reinterpret_cast<const double2*>(a1) + c;
+    const double2* f1d = reinterpret_cast<const double2*>(e1) + c;
+    const double2* f2a = reinterpret_cast<const double2*>(a2) + c;
+    const double2* f2d = reinterpret_cast<const double2*>(e2) + c;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = gw; i < p.In; i += nw) {
-        const double x0a = live ? a0rows[i * RP + r] : 0.0, x0d = live ? d0rows[i * RP + r] : 0.0;
-        const int64_t j0 = p.rowptr[i], j1 = p.rowptr[i + 1];
-        double qs[4] = {0.0, 0.0, 0.0, 0.0};  // the row's mode-0 products X1 X2 (for M0 at u*)
-        for (int64_t jb = j0; jb < j1; jb += 32) {
-            const int64_t jl = jb + lane;
-            const bool okl = jl < j1;
-            const double vl = okl ? __ldg(p.vals + jl) : 0.0;
-            const int cj = okl ? __ldg(p.oidx + jl) : 0, ck = okl ? __ldg(p.oidx + p.nnz + jl) : 0;
-            const int cnt = (int)imin64(32, j1 - jb);
-            double q[4] = {0.0, 0.0, 0.0, 0.0};  // X1 X2 in {AA, AD, DA, DD}
-            for (int q0 = 0; q0 < cnt; q0 += G) {
-                const int qq = q0 + g;
-                const double v = __shfl_sync(0xffffffffu, vl, qq & 31);
-                const int j = __shfl_sync(0xffffffffu, cj, qq & 31), k = __shfl_sync(0xffffffffu, ck, qq & 31);
-                if (qq < cnt && live) {
-                    const double y1a = __ldg(a1 + (int64_t)j * RP + r), y1d = __ldg(e1 + (int64_t)j * RP + r);
-                    const double y2a = __ldg(a2 + (int64_t)k * RP + r), y2d = __ldg(e2 + (int64_t)k * RP + r);
-                    const double va = v * y1a, vd = v * y1d;
-                    q[0] = fma(va, y2a, q[0]);
-                    q[1] = fma(va, y2d, q[1]);
-                    q[2] = fma(vd, y2a, q[2]);
-                    q[3] = fma(vd, y2d, q[3]);
-                }
+    const int64_t i0 = gw * rows_per_warp, i1 = imin64(p.In, i0 + rows_per_warp);
+    auto prefetch_row = [&](int64_t i) {
+        const int64_t a = p.rowptr[i], b = p.rowptr[i + 1];
+        if (b > a) {
+            bulk_prefetch_l2(p.vals + a, (b - a) * 8);
+            if (PK) {
+                bulk_prefetch_l2(pidx + a, (b - a) * 4);
+            } else {
+                bulk_prefetch_l2(p.oidx + a, (b - a) * 4);
+                bulk_prefetch_l2(p.oidx + p.nnz + a, (b - a) * 4);
             }
+        }
+    };
+    if (lane == 0 && i0 < i1) prefetch_row(i0);
+    for (int64_t i = i0; i < i1; ++i) {
+        if (lane == 0 && i + 1 < i1) prefetch_row(i + 1);
+        const double2 x0a = live ? reinterpret_cast<const double2*>(a0rows + i * RP)[c] : make_double2(0.0, 0.0);
+        const double2 x0d = live ? reinterpret_cast<const double2*>(d0rows + i * RP)[c] : make_double2(0.0, 0.0);
+        const int64_t j0 = p.rowptr[i], j1 = p.rowptr[i + 1];
+        double2 qs[4], q[4];  // the row's X1 X2 products (for M0 at u*) and the current fp64 window
+#pragma unroll
+        for (int b12 = 0; b12 < 4; ++b12) qs[b12] = q[b12] = make_double2(0.0, 0.0);
+        auto fold = [&]() {
 #pragma unroll
             for (int b12 = 0; b12 < 4; ++b12) {
-                acc[b12] = dd_fma(acc[b12], x0a, q[b12]);
-                acc[4 + b12] = dd_fma(acc[4 + b12], x0d, q[b12]);
-                qs[b12] += q[b12];
+                acc[b12] = dd_fma(dd_fma(acc[b12], x0a.x, q[b12].x), x0a.y, q[b12].y);
+                acc[4 + b12] = dd_fma(dd_fma(acc[4 + b12], x0d.x, q[b12].x), x0d.y, q[b12].y);
+                qs[b12].x += q[b12].x;
+                qs[b12].y += q[b12].y;
+                q[b12] = make_double2(0.0, 0.0);
             }
+        };
+        if (j0 < j1) {
+            const int n = (int)(j1 - j0);
+            const double* vrow = p.vals + j0;
+            const uint32_t* prow = PK ? pidx + j0 : nullptr;
+            auto load_idx = [&](int64_t jb, double (&vv)[U], int (&cj)[U], int (&ck)[U]) {
+#pragma unroll
+                for (int t = 0; t < U; ++t) {
+                    const int qo = (int)(jb - j0) + t * G + g;
+                    const bool ok = qo < n;
+                    const int qc = ok ? qo : 0;
+                    vv[t] = ldg_d(vrow + qc, ok);
+                    if (PK) {
+                        cj[t] = (int)ldg_u(prow + qc);
+                        ck[t] = 0;
+                    } else {
+                        cj[t] = __ldg(p.oidx + j0 + qc);
+                        ck[t] = __ldg(p.oidx + p.nnz + j0 + qc);
+                    }
+                }
+            };
+            auto gather = [&](const int (&cj)[U], const int (&ck)[U], double2 (&xx)[U][4]) {
+#pragma unroll
+                for (int t = 0; t < U; ++t) {
+                    int j = cj[t], k = ck[t];
+                    if (PK) {
+                        k = (int)((uint32_t)j >> 16);
+                        j = (int)((uint32_t)j & 0xffffu);
+                    }
+                    xx[t][0] = ldg_d2(f1a + (int64_t)j * L, live);
+                    xx[t][1] = ldg_d2(f1d + (int64_t)j * L, live);
+                    xx[t][2] = ldg_d2(f2a + (int64_t)k * L, live);
+                    xx[t][3] = ldg_d2(f2d + (int64_t)k * L, live);
+                }
+            };
+            auto consume = [&](const double2 (&xx)[U][4], const double (&vv)[U]) {
+#pragma unroll
+                for (int t = 0; t < U; ++t) {
+                    const double vax = vv[t] * xx[t][0].x, vay = vv[t] * xx[t][0].y;
+                    const double vdx = vv[t] * xx[t][1].x, vdy = vv[t] * xx[t][1].y;
+                    q[0].x = fma(vax, xx[t][2].x, q[0].x);
+                    q[0].y = fma(vay, xx[t][2].y, q[0].y);
+                    q[1].x = fma(vax, xx[t][3].x, q[1].x);
+                    q[1].y = fma(vay, xx[t][3].y, q[1].y);
+                    q[2].x = fma(vdx, xx[t][2].x, q[2].x);
+                    q[2].y = fma(vdy, xx[t][2].y, q[2].y);
+                    q[3].x = fma(vdx, xx[t][3].x, q[3].x);
+                    q[3].y = fma(vdy, xx[t][3].y, q[3].y);
+                }
+            };
+            double va[U], vb[U], vx[U];
+            int ja[U], ka[U], jb_[U], kb[U];
+            double2 xa[U][4];
+            load_idx(j0, va, ja, ka);
+            gather(ja, ka, xa);
+#pragma unroll
+            for (int t = 0; t < U; ++t) vx[t] = va[t];
+            load_idx(j0 + C, vb, jb_, kb);
+            int nf = 0;
+            for (int64_t jb = j0; jb < j1; jb += C) {
+                double2 xb[U][4];
+                gather(jb_, kb, xb);  // chunk m+1
+                double vn[U];
+#pragma unroll
+                for (int t = 0; t < U; ++t) vn[t] = vb[t];
+                load_idx(jb + 2 * C, vb, jb_, kb);  // chunk m+2
+                consume(xa, vx);                     // chunk m
+                if (++nf == FOLD) {
+                    fold();
+                    nf = 0;
+                }
+#pragma unroll
+                for (int t = 0; t < U; ++t) {
+                    vx[t] = vn[t];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) xa[t][k] = xb[t][k];
+                }
+            }
+            if (nf) fold();
         }
         if (m0xy) {  // combine the lane groups (fixed order), one row of each product
 #pragma unroll
             for (int b12 = 0; b12 < 4; ++b12) {
-                double v = qs[b12];
+                double vx2 = qs[b12].x, vy2 = qs[b12].y;
 #pragma unroll
-                for (int o = RP; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (g == 0) m0xy[((int64_t)b12 * p.In + i) * RP + r] = live ? v : 0.0;
+                for (int o = L; o < 32; o <<= 1) {
+                    vx2 += __shfl_xor_sync(0xffffffffu, vx2, o);
+                    vy2 += __shfl_xor_sync(0xffffffffu, vy2, o);
+                }
+                if (g == 0)
+                    reinterpret_cast<double2*>(m0xy + ((int64_t)b12 * p.In + i) * RP)[c] = make_double2(vx2, vy2);
             }
         }
     }
@@ -571,16 +663,25 @@ void sparse_line_contractions(const DevTensor& t, EvalWork& w, const double* ub,
     p.vals = t.modes->vals[0];
     p.nother = 2;
     p.R = w.R;
+#ifndef CPFIT_L8_U
+#define CPFIT_L8_U 1
+#endif
+    // rows per warp so the nblocks x 8 warps cover the rows in one pass
+    const int64_t rpw = std::max<int64_t>(1, (p.In + (int64_t)nblocks * 8 - 1) / ((int64_t)nblocks * 8));
+    const uint32_t* pk = t.modes->pidx[0];
+    auto go = [&](auto tag) {
+        constexpr int RP = decltype(tag)::value;
+        if (pk)
+            sp_line8_kernel<RP, CPFIT_L8_U, true><<<nblocks, 256, 0, st>>>(p, pk, rpw, w.frows, drows, w.frows + o1, drows + o1,
+                                                                  w.frows + o2, drows + o2, part, m0xy);
+        else
+            sp_line8_kernel<RP, CPFIT_L8_U, false><<<nblocks, 256, 0, st>>>(p, nullptr, rpw, w.frows, drows, w.frows + o1,
+                                                                   drows + o1, w.frows + o2, drows + o2, part, m0xy);
+    };
     switch (w.RP) {
-        case 8:
-            sp_line8_kernel<8><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part, m0xy);
-            break;
-        case 16:
-            sp_line8_kernel<16><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part, m0xy);
-            break;
-        default:
-            sp_line8_kernel<32><<<nblocks, 256, 0, st>>>(p, w.frows, drows, w.frows + o1, drows + o1, w.frows + o2, drows + o2, part, m0xy);
-            break;
+        case 8: go(std::integral_constant<int, 8>{}); break;
+        case 16: go(std::integral_constant<int, 16>{}); break;
+        default: go(std::integral_constant<int, 32>{}); break;
     }
     CPFIT_CUDA(cudaGetLastError());
 }

@@ -14,10 +14,16 @@ import paper_1105_5331_b200 as P
 
 import bench  # noqa: E402
 
-cfg = bench.CONFIGS[os.environ.get("CFG", "c2")]  # CFG=c3: the order-4 config
-dims, R = cfg["dims"], cfg["rank"]
-T, u0 = bench.make_problem(P, cfg, 1)
-t = P.DataTensor.dense(T, dims)
+if os.environ.get("CFG") == "c4":  # the sparse config: 10000^3, 10M nnz, R = 10
+    dims, R = (10000, 10000, 10000), 10
+    coords, vals, _ = P.random_sparse_problem(dims, 10_000_000, R, 0.01, 0)
+    t = P.DataTensor.coo(dims, coords, vals)
+    u0 = P.uniform_initial_guess(dims, R, 1)
+else:
+    cfg = bench.CONFIGS[os.environ.get("CFG", "c2")]  # CFG=c3: the order-4 config
+    dims, R = cfg["dims"], cfg["rank"]
+    T, u0 = bench.make_problem(P, cfg, 1)
+    t = P.DataTensor.dense(T, dims)
 s = P.Solver(t, R, P.NgmresOptions(tol_grad=1e-300, gradient_scale=float(sum(dims) * R), max_iters=400))
 s.set_initial(u0)
 s.init()
