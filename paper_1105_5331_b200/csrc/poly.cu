@@ -422,14 +422,21 @@ __global__ void __launch_bounds__(256) s16_kernel(const S16Params p) {
             acc[8 * b + c] = dd_mul(v, dd{x1a, 0.0});
             acc[8 * b + 4 + c] = dd_mul(v, dd{x1d, 0.0});
         }
+    // transposing warp reduction (as in s8_kernel): each xor step halves the values a lane holds
+    // (8 + 4 + 2 + 1 + 1 double-double adds per lane instead of 16 x 5); contraction k ends in
+    // lanes 2k, 2k + 1
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
+    for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+        const bool up = lane & o;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[k] = dd_add(acc[k], dd_shfl_xor(acc[k], o));
-    if (lane == 0)
-#pragma unroll
-        for (int k = 0; k < 16; ++k) red[warp][k] = acc[k];
+        for (int j = 0; j < h; ++j) {
+            const dd mine = up ? acc[j + h] : acc[j], other = up ? acc[j] : acc[j + h];
+            acc[j] = dd_add(mine, dd_shfl_xor(other, o));
+        }
+    }
+    acc[0] = dd_add(acc[0], dd_shfl_xor(acc[0], 1));
+    if ((lane & 1) == 0) red[warp][lane >> 1] = acc[0];
     __syncthreads();
     if (threadIdx.x < 16) {
         dd v{0.0, 0.0};

@@ -37,8 +37,15 @@ for r in src[2:]:
         continue
     for k in hh:
         if k.startswith("stall_") and "Not Issued" not in k:
-            stalls[k] += int(r[ix[k]] or 0)
-    lines.append((int(r[ix["Warp Stall Sampling (All Samples)"]] or 0), r[ix["Instructions Executed"]], r[ix["Source"]].strip()))
+            try:
+                stalls[k] += int(float(r[ix[k]] or 0))
+            except ValueError:
+                pass
+    try:
+        lines.append((int(r[ix["Warp Stall Sampling (All Samples)"]] or 0), r[ix["Instructions Executed"]],
+                      r[ix["Source"]].strip()))
+    except ValueError:
+        continue
 tot = sum(stalls.values()) or 1
 print("stalls:", ", ".join(f"{k[6:]} {100 * c / tot:.1f}%" for k, c in stalls.most_common(8)))
 ops = collections.Counter()

@@ -21,3 +21,15 @@ o = O.Tensor.coo(dims, coords, vals)
 for a, fp in zip(al, phi):
     fo = o.eval(u + a * d)[0]
     print(f"alpha {a}: poly {fp:.15e} oracle {fo:.15e} rel {abs(fp - fo) / abs(fo):.2e}", flush=True)
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+torch.cuda.init()
+for _ in range(3):
+    P.line_polynomial(t, u, d, al)
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(10):
+        P.line_polynomial(t, u, d, al)
+ks = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and "sp_line8" in e.name]
+us = [e.time_range.end - e.time_range.start for e in ks]
+print(f"sp_line8_kernel: {len(us)} launches, mean {sum(us) / max(1, len(us)):.1f} us", flush=True)
