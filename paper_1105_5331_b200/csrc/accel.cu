@@ -14,6 +14,7 @@
 #include "device.cuh"
 
 #include <algorithm>
+#include <string>
 
 namespace cpfit_gpu {
 
@@ -21,6 +22,21 @@ namespace {
 
 constexpr int kLeafRows = 256;
 constexpr int kTsqrThreads = 512;
+constexpr size_t kTsqrSmem = 220 * 1024;  // dynamic shared memory of one TSQR block
+constexpr int kQrMaxRows = 320;           // smem_qr: kQrMaxRpl rows per lane
+
+// Leaf rows for windows of C = m + 1 columns: 256 up to C = 64 (the stacked running R + leaf rows
+// fit smem_qr's 320 rows), fewer above so (C + rows) x C doubles stay in shared memory.
+int tsqr_leaf_rows(int C) {
+    if (C <= 64) return kLeafRows;
+    return std::min<int>(kQrMaxRows - C, (int)(kTsqrSmem / (sizeof(double) * C)) - C);
+}
+// R factors stacked per merge block: (C + per C) rows within both limits, at least one
+int tsqr_merge_per(int C) {
+    if (C <= 64) return std::max(1, kLeafRows / C);
+    const int rows = std::min<int>(kQrMaxRows, (int)(kTsqrSmem / (sizeof(double) * C)));
+    return std::max(1, (rows - C) / C);
+}
 
 struct TsqrParams {
     int64_t n;
@@ -135,11 +151,12 @@ __global__ void tsqr_kernel(const TsqrParams p) {
     for (int64_t b = b0; b < b1; ++b) {
         const int top = have ? C : 0;
         if (!p.rin) {
-            // leaves hold kLeafRows rows; column j of the window sits in ring slot head + j (mod cap)
-            const int64_t r0 = b * kLeafRows;
+            // leaves hold per_block rows; column j of the window sits in ring slot head + j (mod cap)
+            const int lr = p.per_block;
+            const int64_t r0 = b * lr;
 #pragma unroll 4
-            for (int e = threadIdx.x; e < kLeafRows * C; e += blockDim.x) {
-                const int j = e / kLeafRows, ii = e % kLeafRows;
+            for (int e = threadIdx.x; e < lr * C; e += blockDim.x) {
+                const int j = e / lr, ii = e % lr;
                 const int64_t i = r0 + ii;
                 double v = 0.0;
                 if (i < p.n) {
@@ -191,9 +208,10 @@ constexpr int kSolveThreads = 512;
 
 __global__ void __launch_bounds__(kSolveThreads) accel_solve_kernel(const double* rfin, const int* ring, double eps,
                                                                     double* alpha, double* scal) {
-    extern __shared__ double sm[];  // a: 2m x m stacked system (col-major), rf: C x C
-    __shared__ double bvec[128], cvec[128], upd[64], dir[64], hc[64], rhs[64], al[64], colsq[64], yv[64];
-    __shared__ int perm[64], transp[64];
+    extern __shared__ double sm[];  // a: 2m x m stacked system (col-major); the C x C R factor stays in global
+    __shared__ double bvec[2 * kMaxWindow], cvec[2 * kMaxWindow], upd[kMaxWindow], dir[kMaxWindow], hc[kMaxWindow],
+        rhs[kMaxWindow], al[kMaxWindow], colsq[kMaxWindow], yv[kMaxWindow];
+    __shared__ int perm[kMaxWindow], transp[kMaxWindow];
     __shared__ double sh_delta, sh_rn, sh_thr_help, sh_maxpivot, sh_tau;
     __shared__ int sh_nzp, sh_nz;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -201,9 +219,7 @@ __global__ void __launch_bounds__(kSolveThreads) accel_solve_kernel(const double
     const int C = m + 1;
     const int rows = 2 * m;
     double* a = sm;
-    double* rf = sm + (size_t)rows * m;
-    for (int e = tid; e < C * C; e += blockDim.x) rf[e] = rfin[e];
-    __syncthreads();
+    const double* __restrict__ rf = rfin;  // L2-resident; read a few times
     // ||R_P e_j||^2 and rhs_j = R_P(:, j) . r_c = -(P^T g_bar)_j
     for (int j = tid; j < m; j += blockDim.x) {
         double s2 = 0.0, r = 0.0;
@@ -493,26 +509,19 @@ __global__ void accel_slope_kernel(const double* red, int nblk, double* scal) {
 }  // namespace
 
 AccelWork* accel_create(int64_t n, int cap) {
-    if (cap < 1 || cap > 63) throw std::invalid_argument("device accelerate supports window 1..63");
+    if (cap < 1 || cap > kMaxWindow)
+        throw std::invalid_argument("device accelerate supports window 1.." + std::to_string(kMaxWindow));
     auto* a = new AccelWork();
     a->n = n;
     a->cap = cap;
     const int C = cap + 1;
-    a->leaf_rows = kLeafRows;
-    const int64_t nblocks = (n + kLeafRows - 1) / kLeafRows;
+    a->leaf_rows = tsqr_leaf_rows(C);
+    const int64_t nblocks = (n + a->leaf_rows - 1) / a->leaf_rows;
     a->leaf_grid = (int)std::min<int64_t>(nblocks, 148);
-    int64_t cnt = a->leaf_grid;
-    while (cnt > 1) {
-        const int per = std::max(1, kLeafRows / C);
-        const int64_t nb = (cnt + per - 1) / per;
-        const int g = (int)std::min<int64_t>(nb, 148);
-        a->merge_grid.push_back(g);
-        cnt = g;
-    }
     const size_t rsz = sizeof(double) * (size_t)std::max<int64_t>(a->leaf_grid, 1) * C * C;
     CPFIT_CUDA(cudaMalloc(&a->rbuf[0], rsz));
     CPFIT_CUDA(cudaMalloc(&a->rbuf[1], rsz));
-    CPFIT_CUDA(cudaMalloc(&a->alpha, sizeof(double) * 64));
+    CPFIT_CUDA(cudaMalloc(&a->alpha, sizeof(double) * std::max(64, cap)));
     CPFIT_CUDA(cudaMalloc(&a->scal, sizeof(double) * 8));
     CPFIT_CUDA(cudaMalloc(&a->red, sizeof(double) * 1024));
     return a;
@@ -537,18 +546,18 @@ void accelerate_device(AccelWork& a, const double* wu, const double* wg, const i
     p.ring = ring;
     p.wg = wg;
     p.gb = gb;
-    p.per_block = kLeafRows;
-    p.nblocks = (a.n + kLeafRows - 1) / kLeafRows;
+    p.per_block = a.leaf_rows;
+    p.nblocks = (a.n + a.leaf_rows - 1) / a.leaf_rows;
     p.blocks_per_cta = (p.nblocks + a.leaf_grid - 1) / a.leaf_grid;
     p.rout = a.rbuf[0];
-    size_t smem = sizeof(double) * (size_t)(C + kLeafRows) * C;
+    size_t smem = sizeof(double) * (size_t)(C + a.leaf_rows) * C;
     CPFIT_CUDA(cudaFuncSetAttribute(tsqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int g0 = (int)((p.nblocks + p.blocks_per_cta - 1) / p.blocks_per_cta);
     tsqr_kernel<<<g0, kTsqrThreads, smem, st>>>(p);
     CPFIT_CUDA(cudaGetLastError());
     int64_t cnt = g0;
     int src = 0;
-    const int per = std::max(1, kLeafRows / C);
+    const int per = tsqr_merge_per(C);
     while (cnt > 1) {
         TsqrParams q = p;
         q.rin = a.rbuf[src];
@@ -556,7 +565,8 @@ void accelerate_device(AccelWork& a, const double* wu, const double* wg, const i
         q.rout = a.rbuf[src ^ 1];
         q.per_block = per;
         q.nblocks = (cnt + per - 1) / per;
-        const int gmax = 148;
+        // one R per block (wide windows): every CTA merges at least two blocks so cnt shrinks
+        const int64_t gmax = per == 1 ? std::max<int64_t>(1, q.nblocks / 2) : 148;
         q.blocks_per_cta = (q.nblocks + gmax - 1) / gmax;
         const int g = (int)((q.nblocks + q.blocks_per_cta - 1) / q.blocks_per_cta);
         smem = sizeof(double) * (size_t)(C + per * C) * C;
@@ -565,7 +575,7 @@ void accelerate_device(AccelWork& a, const double* wu, const double* wg, const i
         cnt = g;
         src ^= 1;
     }
-    const size_t ssmem = sizeof(double) * (2 * (size_t)a.cap * a.cap + (size_t)C * C);
+    const size_t ssmem = sizeof(double) * (2 * (size_t)a.cap * a.cap);
     CPFIT_CUDA(cudaFuncSetAttribute(accel_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
     accel_solve_kernel<<<1, kSolveThreads, ssmem, st>>>(a.rbuf[src], ring, eps, a.alpha, a.scal);
     CPFIT_CUDA(cudaGetLastError());

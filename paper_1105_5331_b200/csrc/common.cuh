@@ -26,6 +26,7 @@ namespace cpfit_gpu {
 
 constexpr int kMaxOrder = 8;   // tensor order supported on device
 constexpr int kMaxRank = 32;   // R <= 32 (RP = R rounded up to 8)
+constexpr int kMaxWindow = 112;  // N-GMRES window: the 2m x m damped system of accelerate in shared memory
 
 struct cuda_error : std::runtime_error {
     explicit cuda_error(const std::string& w) : std::runtime_error(w) {}

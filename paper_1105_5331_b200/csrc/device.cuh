@@ -233,7 +233,6 @@ struct AccelWork {
     int64_t n = 0;
     int cap = 0;
     int leaf_grid = 0, leaf_rows = 0;
-    std::vector<int> merge_grid;  // per merge level
     double* rbuf[2] = {nullptr, nullptr};
     double* alpha = nullptr;  // cap
     double* scal = nullptr;   // [0] residual_rel, [1] slope, [2] delta, [3] m

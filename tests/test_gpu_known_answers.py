@@ -175,7 +175,7 @@ def test_shape_and_rank_errors(gpu):
     with pytest.raises(ValueError):
         P.DataTensor.dense(np.ones(5), (2, 3))  # value count
     with pytest.raises(ValueError):
-        P.ngmres_solve(t, np.ones(9 * 2), P.NgmresOptions(window=64))  # window above the device limit
+        P.ngmres_solve(t, np.ones(9 * 2), P.NgmresOptions(window=113))  # window above the device limit
 
 
 def test_coo_canonicalisation_and_rejections(gpu, O):

@@ -119,7 +119,8 @@ def test_als_singular_raises(gpu):
         P.als_sweep(t, np.zeros(12))
 
 
-@pytest.mark.parametrize("n,m", [(5, 1), (5, 4), (180, 20), (19200, 20), (1000, 7)])
+@pytest.mark.parametrize("n,m", [(5, 1), (5, 4), (180, 20), (19200, 20), (1000, 7), (19200, 64), (19200, 100),
+                                 (3000, 112), (60, 80)])
 def test_accelerate_matches_oracle(gpu, O, n, m):
     P = gpu
     rng = np.random.default_rng(n + m)
@@ -227,6 +228,28 @@ def test_ngmres_full_solve_matches_oracle(gpu, O, cfg):
     n_ref, n_got = len(ref["trace"]) - 1, len(res.trace) - 1
     assert abs(n_got - n_ref) <= max(1, int(0.02 * n_ref)), (n_got, n_ref)
     assert abs(res.f - ref["f"]) <= 1e-8 * ref["f"]
+
+
+@pytest.mark.parametrize("window", [64, 112])
+def test_ngmres_wide_window_matches_oracle(gpu, O, window):
+    """Windows above 63 (the reference's acceptance test uses 64, acceptance.cpp:343): the wide
+    TSQR geometry (fewer leaf rows, one R per merge block) and the 2m x m damped system. C0 with
+    the window filling past 63 entries: trace rows and final f against the oracle."""
+    P = gpu
+    cfg = ((20, 20, 20), 3, 0.5, 1.0, 1.0)
+    dims, rank = cfg[0], cfg[1]
+    T, u0 = _baseline_case(P, cfg)
+    nu = float(sum(dims) * rank)
+    t = P.DataTensor.dense(T, dims)
+    o = O.Tensor.dense(dims, T)
+    k = 90
+    ref = o.ngmres(u0, window=window, max_iters=k, tol_grad=1e-300, gradient_scale=nu)
+    res = P.ngmres_solve(t, u0, P.NgmresOptions(window=window, max_iters=k, tol_grad=1e-300, gradient_scale=nu))
+    n = min(len(ref["trace"]), len(res.trace), 21)
+    for it in range(1, n):
+        assert res.trace[it]["restart"] == ref["trace"][it]["restart"], it
+        assert abs(res.trace[it]["f"] - ref["trace"][it]["f"]) <= 1e-8 * ref["trace"][it]["f"], it
+    assert abs(res.f - ref["f"]) <= 1e-8 * ref["f"], (res.f, ref["f"])
 
 
 def test_ngmres_stationary_start_stops_at_iteration_one(gpu):
