@@ -122,6 +122,8 @@ void reduce_m0(EvalWork& w, cudaStream_t st) {
 void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool do_m0, bool do_f,
                const double* gamma0, cudaStream_t st, const int* resid_flag = nullptr, double* s_out = nullptr,
                const double* s_in = nullptr) {
+    // M0 only, short fibres with 16 | I_1: the slab pass (slab.cu) writes the same partials
+    if (do_m0 && !do_s && !do_f && dense_m0_slab(t, w, u, st)) return;
     FiberParams p{};
     p.T = t.T;
     p.ldT = t.ldT;

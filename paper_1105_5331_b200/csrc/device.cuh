@@ -47,6 +47,9 @@ inline bool rowwise(const DevTensor& t) { return t.sparse || t.generic; }
 bool fiber_path_fits(int order, int64_t I0);
 
 int sm_count();  // SMs of the current device (cached)
+struct EvalWork;
+// slab.cu: the M0 pass of short-fibre tensors with 16 | I_1 (false: shape does not qualify)
+bool dense_m0_slab(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st);
 // fiber-pass barrier-wait counters (filled only by a -DCPFIT_FIBER_PROF build)
 constexpr int kFiberProfSlots = 12;
 unsigned long long* fiber_prof_buffer();
@@ -78,6 +81,9 @@ struct EvalWork {
     bool fiber_tmap = false;
     int sreg_groups = 0;  // S pass tile groups for short fibres (0: K split)
     CUtensorMap tmap_fws{}, tmap_sreg{};
+    // slab M0 pass (slab.cu): a box of 16 fibres x half a (padded) row; -1 not tried, 0 none, 1 ok
+    CUtensorMap tmap_slab{};
+    int slab_tmap = -1;
     size_t fiber_smem = 0;
     double* S = nullptr;        // J x RP
     double* S2 = nullptr;       // (dense order 3) a second J x RP right after S: the line search's S_d

@@ -14,7 +14,10 @@ SHAPES = [((3, 4, 2), 3), ((4, 3, 5), 2), ((5, 5, 5, 5), 3), ((20, 20, 20), 3), 
           # RP = 32 (spass_kernel), RP = 8 tile groups, the last J tile partial (J % 16 != 0)
           ((100, 30, 20), 16), ((128, 9, 11), 20), ((36, 40, 7), 5), ((20, 7, 3, 5), 9),
           # RP = 32 level contractions (the factor staging once covered only 16 of 32 columns)
-          ((200, 30, 20), 20), ((40, 30, 20, 6), 24)]
+          ((200, 30, 20), 20), ((40, 30, 20, 6), 24),
+          # the slab M0 pass (16 | I_0 <= 64, 16 | I_1 <= 64): tiles per slab 1..4, row tiles per
+          # warp 1..4, order 3..5, RP 8 and 16
+          ((64, 16, 5), 7), ((32, 48, 3, 4), 16), ((16, 32, 10), 3), ((48, 64, 7), 12), ((32, 16, 4, 3, 2), 9)]
 
 
 def _dense(P, O, dims, seed=0):
