@@ -60,6 +60,7 @@ struct alignas(64) FiberParams {
     const double* gamma0;          // RP x RP
     const double* fnorm2;          // J
     const int* resid_flag;         // device flag: residual-form objective when nonzero
+    int only_resid;                // exit at once unless *resid_flag (the slab passes did M0 + f)
     int64_t tiles_per_cta;
     int64_t ntiles;
     unsigned long long* prof;  // diagnostic build only (fiber.cuh FIBER_WAIT)
@@ -123,8 +124,13 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
                const double* gamma0, cudaStream_t st, const int* resid_flag = nullptr, double* s_out = nullptr,
                const double* s_in = nullptr) {
     // M0 only, short fibres with 16 | I_1: the slab pass (slab.cu) writes the same partials
-    if (do_m0 && !do_s && !do_f && dense_m0_slab(t, w, u, st)) return;
+    if (do_m0 && !do_s && !do_f && dense_m0_slab(t, w, u, st, nullptr)) return;
+    // M0 + per-fibre objective with S given, same shapes: the slab pass and a per-fibre objective
+    // kernel (S, the fibre norms and the factor rows; T is not read twice); under the residual form
+    // (a device flag) both exit and the fibre kernel below does the pass instead
+    const bool slab_f = do_m0 && !do_s && do_f && s_in && m0_slab_applies(t, w);
     FiberParams p{};
+    p.only_resid = 0;
     p.T = t.T;
     p.ldT = t.ldT;
     p.I0 = (int)t.dims[0];
@@ -167,6 +173,12 @@ void run_fiber(const DevTensor& t, EvalWork& w, const double* u, bool do_s, bool
             CPFIT_CUDA(cudaMemsetAsync(w.m0_part + (size_t)grid * w.RP * 32 * w.fiber_nchunk, 0,
                                        sizeof(double) * (size_t)(w.fiber_grid - grid) * w.RP * 32 * w.fiber_nchunk, st));
         if (do_f) CPFIT_CUDA(cudaMemsetAsync(w.f_part + grid, 0, sizeof(double) * (w.fiber_grid - grid), st));
+    }
+    if (slab_f) {
+        dense_m0_slab(t, w, u, st, resid_flag);
+        dense_fobj_slab(t, w, u, s_in, gamma0, st, resid_flag);
+        if (!resid_flag) return;  // the per-fibre form always: no residual fallback needed
+        p.only_resid = 1;
     }
     if (do_s && !do_m0 && !do_f) {  // S only: every warp on S
         switch (w.RP) {

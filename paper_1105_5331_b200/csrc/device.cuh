@@ -49,7 +49,12 @@ bool fiber_path_fits(int order, int64_t I0);
 int sm_count();  // SMs of the current device (cached)
 struct EvalWork;
 // slab.cu: the M0 pass of short-fibre tensors with 16 | I_1 (false: shape does not qualify)
-bool dense_m0_slab(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st);
+// resid_flag: a device flag; when nonzero at run time the slab kernels exit without writing
+bool dense_m0_slab(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st, const int* resid_flag);
+bool m0_slab_applies(const DevTensor& t, const EvalWork& w);
+// the per-fibre objective partials (w.f_part) of the slab shapes with S given
+void dense_fobj_slab(const DevTensor& t, EvalWork& w, const double* u, const double* S, const double* gamma0,
+                     cudaStream_t st, const int* resid_flag);
 // fiber-pass barrier-wait counters (filled only by a -DCPFIT_FIBER_PROF build)
 constexpr int kFiberProfSlots = 12;
 unsigned long long* fiber_prof_buffer();

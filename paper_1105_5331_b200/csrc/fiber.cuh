@@ -249,6 +249,7 @@ __device__ __forceinline__ int a0s_index(int i, int r) {
 
 template <int RP, int F, int ORD, int NST>
 __global__ void __maxnreg__(FiberRoles<RP>::MAXNREG) fiber_ws_kernel(const __grid_constant__ FiberParams p) {
+    if (p.only_resid && !*p.resid_flag) return;  // the slab passes did this evaluation (slab.cu)
     using Ro = FiberRoles<RP>;
     constexpr int WST = wstages(NST);
     extern __shared__ __align__(128) unsigned char smem_raw[];

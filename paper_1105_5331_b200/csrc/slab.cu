@@ -14,7 +14,12 @@
 // and the CTA's warps sum their M0 in fixed order into the same per-CTA partial layout the fibre
 // kernels write (m0_part[cta][r][32 nchunk]), so the reduction downstream is unchanged.
 // The fibre kernels' M0 warps wait on their two W-producer warps for short fibres (C3: 44 us for
-// a pass whose HBM floor is 20.5 us, profiles/r02_summary.md); this pass has no producer role.
+// a pass whose HBM floor is 20.5 us, profiles/r02_summary.md); this pass has no producer role
+// (C3: 29 us, DMMA sub-pipe ~60 % busy with RP = 16 for R = 10).
+// The evaluation at u_bar (M0 + per-fibre objective, S given) runs this pass plus
+// fobj_slab_kernel (the per-fibre objective from S, the fibre norms and the factor rows) in place
+// of the fibre kernel; both exit at once when the residual form is on (a device flag read at run
+// time in the captured graph), and the fibre kernel then runs instead (FiberParams::only_resid).
 #include "device.cuh"
 
 #include <cstdlib>
@@ -38,6 +43,7 @@ struct SlabParams {
     double* m0_part;               // [grid][RP][ld]
     int ld;                        // 32 * nchunk
     int64_t tiles_per_warp;
+    const int* resid_flag;         // exit at once when set (the residual form runs the fibre kernel)
     int use_tmap;                  // one TMA box (I0s x 16 at column h I0h, pads arrive as zeros) per tile
     int I0h;                       // rows of M0 per warp (a half of I0)
     CUtensorMap tmap;
@@ -48,6 +54,7 @@ struct SlabParams {
 template <int RP, int NQ, int NMT>
 __global__ void __launch_bounds__(kSlabWarps * 32, 1) m0slab_kernel(const __grid_constant__ SlabParams p) {
     constexpr int NRT = RP / 8;
+    if (p.resid_flag && *p.resid_flag) return;
     extern __shared__ __align__(128) double slab_raw[];
     __shared__ uint64_t full[kSlabWarps][kSlabStages];
     // TMA destinations need 128-byte alignment (the dynamic region follows the static barriers)
@@ -256,9 +263,10 @@ bool m0_slab_applies(const DevTensor& t, const EvalWork& w) {
 
 // M0 partials of T x KR(modes >= 1) at u into w.m0_part (w.fiber_grid CTAs, the fibre kernels'
 // layout); false when the shape does not qualify (the caller runs the fibre kernel instead)
-bool dense_m0_slab(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st) {
+bool dense_m0_slab(const DevTensor& t, EvalWork& w, const double* u, cudaStream_t st, const int* resid_flag) {
     if (!m0_slab_applies(t, w)) return false;
     SlabParams p{};
+    p.resid_flag = resid_flag;
     p.T = t.T;
     p.ldT = t.ldT;
     p.I0 = (int)t.dims[0];
@@ -291,6 +299,128 @@ bool dense_m0_slab(const DevTensor& t, EvalWork& w, const double* u, cudaStream_
     }
     CPFIT_CUDA(cudaGetLastError());
     return ok;
+}
+
+namespace {
+
+constexpr int kFobjThreads = 1024;
+
+struct FobjParams {
+    int64_t J;
+    int I1, order, R;
+    int64_t dims[kMaxOrder];
+    const double* fac[kMaxOrder];
+    const double* S;       // J x RP (S = T x_1 A_0)
+    const double* fnorm2;  // ||t_f||^2 per fibre
+    const double* gamma0;  // A_0^T A_0, RP x RP
+    double* f_part;        // [grid]
+    const int* resid_flag;
+};
+
+// Per-fibre objective with S given (the fibre kernels' S-given epilogue, fiber.cuh): for fibre f
+// with w_f = A_1(i_1, :) * prod_{m >= 2} A_m(i_m, :), the partial sum of
+// ||t_f||^2 + w_f^T (Gamma_0 w_f - 2 s_f); RP lanes per fibre (Gamma_0 row r on lane r), the
+// block's fibres contiguous, fixed-order sums -> f_part[block].
+template <int RP>
+__global__ void __launch_bounds__(kFobjThreads) fobj_slab_kernel(const FobjParams p) {
+    if (p.resid_flag && *p.resid_flag) return;
+    // lane per fibre: w_f, s_f in registers, Gamma_0 from shared memory (broadcast loads);
+    // a warp takes 32 consecutive fibres of one slab (I_1 % 16 == 0: a half warp never crosses)
+    __shared__ double gam[RP * RP];
+    __shared__ double red[kFobjThreads / 32];
+    extern __shared__ double wsh[];  // per warp [r][lane]
+    for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) gam[e] = p.gamma0[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+    const int R = p.R;
+    // fibre indices fit 32 bits (m0_slab_applies: J / I_1 < 2^31, I_1 <= 64)
+    const int f_lo = (int)((int64_t)blockIdx.x * p.J / gridDim.x), f_hi = (int)((int64_t)(blockIdx.x + 1) * p.J / gridDim.x);
+    double acc = 0.0;
+    for (int f = f_lo + warp * 32 + lane; f - lane < f_hi; f += nw * 32) {  // warp-uniform
+        const bool ok = f < f_hi;
+        const int fc = ok ? f : f_lo;
+        const int i1 = fc % p.I1;
+        int rem = fc / p.I1;
+        double w[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) w[r] = r < R ? p.fac[1][(int64_t)r * p.I1 + i1] : 0.0;
+        for (int m = 2; m < p.order; ++m) {
+            const int dm = (int)p.dims[m];
+            const int im = rem % dm;
+            rem /= dm;
+            const double* am = p.fac[m] + im;
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+                if (r < R) w[r] *= am[(int64_t)r * dm];
+        }
+        const double2* srow = reinterpret_cast<const double2*>(p.S + (int64_t)fc * RP);
+        double t = 0.0;
+#pragma unroll
+        for (int r2 = 0; r2 < RP / 2; ++r2) {
+            if (2 * r2 < R) {
+                const double2 sv = srow[r2];
+                t = fma(w[2 * r2], -2.0 * sv.x, t);
+                t = fma(w[2 * r2 + 1], -2.0 * sv.y, t);
+            }
+        }
+        // w^T Gamma_0 w: the q loop stays rolled (w_q from this lane's shared-memory copy) so the
+        // Gamma_0 loads are not all hoisted into registers
+        double* wq = wsh + (size_t)warp * RP * 32 + lane;
+#pragma unroll
+        for (int r = 0; r < RP; ++r) wq[r * 32] = w[r];
+#pragma unroll 1
+        for (int q = 0; q < R; ++q) {
+            double g = 0.0;
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+                if (r < R) g = fma(gam[q * RP + r], w[r], g);
+            t = fma(wq[q * 32], g, t);
+        }
+        if (ok) acc += p.fnorm2[fc] + t;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w2 = 0; w2 < nw; ++w2) s += red[w2];
+        p.f_part[blockIdx.x] = s;
+    }
+}
+
+}  // namespace
+
+void dense_fobj_slab(const DevTensor& t, EvalWork& w, const double* u, const double* S, const double* gamma0,
+                     cudaStream_t st, const int* resid_flag) {
+    FobjParams p{};
+    p.J = t.J;
+    p.I1 = (int)t.dims[1];
+    p.order = t.order;
+    p.R = w.R;
+    for (int m = 0; m < t.order; ++m) {
+        p.dims[m] = t.dims[m];
+        p.fac[m] = u + w.off[m];
+    }
+    p.S = S;
+    p.fnorm2 = t.fiber_norm2;
+    p.gamma0 = gamma0;
+    p.f_part = w.f_part;
+    p.resid_flag = resid_flag;
+    switch (w.RP) {
+        case 8: {
+            const size_t sm = sizeof(double) * (kFobjThreads / 32) * 8 * 32;
+            CPFIT_CUDA(cudaFuncSetAttribute(fobj_slab_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            fobj_slab_kernel<8><<<w.fiber_grid, kFobjThreads, sm, st>>>(p);
+            break;
+        }
+        default: {
+            const size_t sm = sizeof(double) * (kFobjThreads / 32) * 16 * 32;
+            CPFIT_CUDA(cudaFuncSetAttribute(fobj_slab_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            fobj_slab_kernel<16><<<w.fiber_grid, kFobjThreads, sm, st>>>(p);
+            break;
+        }
+    }
+    CPFIT_CUDA(cudaGetLastError());
 }
 
 }  // namespace cpfit_gpu

@@ -233,6 +233,27 @@ def test_ngmres_full_solve_matches_oracle(gpu, O, cfg):
     assert abs(res.f - ref["f"]) <= 1e-8 * ref["f"]
 
 
+@pytest.mark.parametrize("dims,rank", [((32, 48, 10), 5), ((64, 16, 8, 6), 6), ((16, 32, 6, 5), 3), ((48, 32, 20), 12)])
+def test_ngmres_slab_shapes_match_oracle(gpu, O, dims, rank):
+    """Shapes on the slab passes (16 | I_0 <= 64, 16 | I_1 <= 64: slab M0 and the per-fibre
+    objective kernel in the evaluation at u_bar, the slab M0 at the accepted point): trace rows
+    and final f against the oracle."""
+    P = gpu
+    T, _, _ = P.dense_test_problem(dims, rank, 0.5, 1.0, 1.0, 3, noise_mode=1)
+    u0 = P.uniform_initial_guess(dims, rank, 3)
+    nu = float(sum(dims) * rank)
+    t = P.DataTensor.dense(T, dims)
+    o = O.Tensor.dense(dims, T)
+    k = 30
+    ref = o.ngmres(u0, window=20, max_iters=k, tol_grad=1e-300, gradient_scale=nu)
+    res = P.ngmres_solve(t, u0, P.NgmresOptions(window=20, max_iters=k, tol_grad=1e-300, gradient_scale=nu))
+    n = min(len(ref["trace"]), len(res.trace), 21)
+    for it in range(1, n):
+        assert res.trace[it]["restart"] == ref["trace"][it]["restart"], it
+        assert abs(res.trace[it]["f"] - ref["trace"][it]["f"]) <= 1e-8 * ref["trace"][it]["f"], it
+    assert abs(res.f - ref["f"]) <= 1e-8 * ref["f"], (res.f, ref["f"])
+
+
 @pytest.mark.parametrize("window", [64, 112])
 def test_ngmres_wide_window_matches_oracle(gpu, O, window):
     """Windows above 63 (the reference's acceptance test uses 64, acceptance.cpp:343): the wide
