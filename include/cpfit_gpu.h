@@ -12,7 +12,7 @@
  *     2 cpfit::numerical_error (errors.hpp:9-12), 3 CUDA / other failure; the message is
  *     available from cpfit_last_error() (thread-local);
  *   - distinct tensor handles may be used from different threads concurrently.
- * Device limits: order <= 8, rank <= 32, N-GMRES window <= 112, sparse mode sizes < 2^31,
+ * Device limits: order <= 8, rank <= 64 (ranks above 32 on the per-mode path), N-GMRES window <= 112, sparse mode sizes < 2^31,
  * R * sum(I_n) < 2^31. Dense shapes of any mode sizes: the fibre-tile passes take mode-0 lengths
  * up to 416 (order >= 2); order-1 tensors and longer mode-0 fibres run the generic per-mode
  * kernels (csrc/generic.cu) with the same results and error behaviour. Shapes beyond the limits

@@ -70,6 +70,7 @@ namespace {
 // solve has no grid-wide step (its Gram is finished by the next consumer).
 constexpr int kCholThreads = 256;
 constexpr int kSolveThreads = 256;
+constexpr int kSolveWideRows = 64;  // rows per block step of solve_gram_wide_kernel (ranks > 32)
 constexpr int kSolveMaxBlocks = 148;
 
 struct GramPending {
@@ -191,6 +192,76 @@ __global__ void __launch_bounds__(kCholThreads) chol_kernel(const CholParams p) 
     }
 }
 
+// Ranks above 32 (RP = 64): the same left-looking LLT with the same operation order (l_ik =
+// (g_ik - sum_{j<k} l_ij l_kj) / l_kk, j ascending, the division a multiplication by rsqrt, one
+// ridge retry), a column per step over the block's threads with L in shared memory instead of a
+// lane per row. Latency-bound (R dependent steps); only the wide-rank path uses it.
+__global__ void __launch_bounds__(kCholThreads) chol_wide_kernel(const CholParams p) {
+    constexpr int RP = kMaxRankWide;
+    extern __shared__ double cwsm[];  // gam [RP * RP], l [RP * RP]
+    double* gam = cwsm;
+    double* l = cwsm + RP * RP;
+    __shared__ double dv[RP];
+    __shared__ int okf;
+    const int R = p.R, tid = threadIdx.x;
+    finalize_pending(p.pend, R, RP, p.gram);
+    __syncthreads();
+    for (int e = tid; e < RP * RP; e += blockDim.x) {
+        const int q = e / RP, r = e % RP;
+        double v = 0.0;
+        if (q < R && r < R) {
+            v = 1.0;
+            for (int m = 0; m < p.order; ++m)
+                if (m != p.mode) v *= p.gram[(size_t)m * RP * RP + e];
+        }
+        gam[e] = v;
+    }
+    __syncthreads();
+    double ridge = 0.0;
+    bool ok = false;
+    for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+        if (attempt == 1) {
+            double tr = 0.0;
+            for (int j = 0; j < R; ++j) tr += gam[j * RP + j];  // diagonal, j ascending
+            ridge = 1e-12 * tr;
+            if (!(ridge > 0.0)) break;
+        }
+        if (tid == 0) okf = 1;
+        for (int e = tid; e < RP * RP; e += blockDim.x) l[e] = 0.0;
+        __syncthreads();
+        for (int k = 0; k < R; ++k) {
+            // pivot (thread 0) then column k below it, every row against the finished columns j < k
+            if (tid == 0) {
+                double s2 = gam[k * RP + k] + ridge;
+                for (int j = 0; j < k; ++j) s2 -= l[k * RP + j] * l[k * RP + j];
+                if (s2 <= 0.0) okf = 0;
+                const double inv = rsqrt(s2);
+                l[k * RP + k] = s2 * inv;
+                dv[k] = inv;
+            }
+            __syncthreads();
+            if (!okf) break;
+            for (int i = k + 1 + tid; i < R; i += blockDim.x) {
+                double s2 = gam[i * RP + k];
+                for (int j = 0; j < k; ++j) s2 -= l[i * RP + j] * l[k * RP + j];
+                l[i * RP + k] = s2 * dv[k];
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        ok = okf != 0;
+    }
+    for (int e = tid; e < R * R; e += blockDim.x) {
+        const int i = e / R, j = e % R;
+        p.fac[e] = (j <= i) ? l[i * RP + j] : 0.0;
+    }
+    for (int i = tid; i < R; i += blockDim.x) p.fac[R * R + i] = dv[i];
+    if (tid == 0) {
+        p.fac[R * R + R] = ok ? 1.0 : 0.0;
+        if (!ok) atomicOr(p.status, 1);
+    }
+}
+
 struct SolveGramParams {
     int R, mode;
     int64_t In;
@@ -298,6 +369,95 @@ __global__ void __launch_bounds__(kSolveThreads) solve_gram_kernel(const SolveGr
     }
 }
 
+// Ranks above 32: a thread per row i with the row in registers (m_i summed from the partials in
+// order, then L y = m and L^T x = y by columns in the same operation order as solve_gram_kernel),
+// the block's rows staged in shared memory for the double-double Gram partials of the output.
+__global__ void __launch_bounds__(kSolveWideRows) solve_gram_wide_kernel(const SolveGramParams p) {
+    constexpr int RP = kMaxRankWide;
+    extern __shared__ double swsm[];  // l [RP * RP], then xs [kSolveWideRows][RP + 1]
+    double* l = swsm;
+    double (*xs)[RP + 1] = reinterpret_cast<double (*)[RP + 1]>(swsm + RP * RP);
+    __shared__ double dinv[RP];
+    const int R = p.R, tid = threadIdx.x;
+    if (p.fac[R * R + R] == 0.0) return;  // factorisation failed (status set): uniform exit
+    for (int e = tid; e < R * R; e += blockDim.x) l[(e / R) * RP + e % R] = p.fac[e];
+    for (int e = tid; e < R; e += blockDim.x) dinv[e] = p.fac[R * R + e];
+    const int npair = R * (R + 1) / 2;
+    constexpr int NPT = (RP * (RP + 1) / 2 + kSolveWideRows - 1) / kSolveWideRows;
+    dd acc[NPT];
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) acc[k] = dd{0.0, 0.0};
+    __syncthreads();
+    bool fin = true;
+    for (int64_t i0 = (int64_t)blockIdx.x * kSolveWideRows; i0 < p.In; i0 += (int64_t)gridDim.x * kSolveWideRows) {
+        const int64_t i = i0 + tid;
+        const bool live = i < p.In;
+        double s[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+            double v = 0.0;
+            if (live && r < R) {
+                const double* m = p.M + (p.layout == 0 ? (int64_t)r * p.ld + i : i * p.RP + r);
+                for (int c = 0; c < p.nparts; ++c) v += m[(int64_t)c * p.pstride];
+            }
+            s[r] = v;
+        }
+        double y[RP];
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+            y[j] = 0.0;
+            if (j < R) {
+                y[j] = s[j] * dinv[j];
+#pragma unroll
+                for (int r = j + 1; r < RP; ++r)
+                    if (r < R) s[r] -= l[r * RP + j] * y[j];
+            }
+        }
+#pragma unroll
+        for (int j = RP - 1; j >= 0; --j) {
+            if (j < R) {
+                const double xj = y[j] * dinv[j];
+#pragma unroll
+                for (int r = 0; r < j; ++r) y[r] -= l[j * RP + r] * xj;
+                y[j] = xj;
+            }
+        }
+        __syncthreads();  // the previous step's Gram reads of xs are done
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+            const double x = (live && r < R) ? y[r] : 0.0;
+            if (live && r < R) {
+                p.out[(int64_t)r * p.In + i] = x;
+                fin = fin && isfinite(x);
+            }
+            xs[tid][r] = x;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NPT; ++k) {
+            const int q = tid + k * kSolveWideRows;
+            if (q < npair) {
+                int a, b;
+                pair_rq(q, R, a, b);
+                for (int rr = 0; rr < kSolveWideRows; ++rr) acc[k] = dd_fma(acc[k], xs[rr][a], xs[rr][b]);
+            }
+        }
+    }
+    if (!fin) atomicOr(p.status, 2);
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        const int q = tid + k * kSolveWideRows;
+        if (q < npair) p.part[(size_t)blockIdx.x * npair + q] = acc[k];
+    }
+    if (p.fin_counter && last_block_arrives(p.fin_counter)) {
+        GramPending g{};
+        g.mode = p.mode;
+        g.part = p.part;
+        g.nblk = (int)gridDim.x;
+        finalize_pending(g, R, p.RP, p.gram);
+    }
+}
+
 struct NormParams {
     int order, R, RP;
     int64_t dims[kMaxOrder];
@@ -333,11 +493,11 @@ struct NormParams {
 // prod_n ||a_r^(n)||, stable sort by decreasing lambda, scale to lambda^(1/N); zero-lambda
 // terms keep their columns and sort last (kruskal.cpp:156-193).
 __global__ void normalize_kernel(const NormParams p) {
-    __shared__ double nrm[kMaxOrder][kMaxRank];
-    __shared__ double lam[kMaxRank];
-    __shared__ int perm[kMaxRank];
-    __shared__ double scale[kMaxOrder][kMaxRank];
-    __shared__ double diag[kMaxOrder][kMaxRank];
+    __shared__ double nrm[kMaxOrder][kMaxRankWide];
+    __shared__ double lam[kMaxRankWide];
+    __shared__ int perm[kMaxRankWide];
+    __shared__ double scale[kMaxOrder][kMaxRankWide];
+    __shared__ double diag[kMaxOrder][kMaxRankWide];
     const int tid = threadIdx.x;
     NSTAMP(0);
     for (int e = tid; e < p.order * p.R; e += blockDim.x) {  // Gram diagonals, independent loads
@@ -348,7 +508,40 @@ __global__ void normalize_kernel(const NormParams p) {
     if (blockIdx.x == 0) finalize_pending(p.pend, p.R, p.RP, p.gram_w);
     __syncthreads();
     NSTAMP(1);
-    if (tid < 32) {
+    if (p.R > 32) {
+        // ranks above 32: thread r, the same stable descending order through shared memory
+        const int r = tid;
+        const bool on = r < p.R;
+        double l = 1.0;
+        if (on) {
+            for (int n = 0; n < p.order; ++n) {
+                const double v = sqrt(diag[n][r]);
+                nrm[n][r] = v;
+                l *= v;
+            }
+            lam[r] = l;
+        }
+        __syncthreads();
+        if (on) {
+            int pos = 0;
+            for (int q = 0; q < p.R; ++q) {
+                const double lq = lam[q];
+                if (lq > l || (q < r && !(l > lq) && !(lq > l))) ++pos;
+            }
+            perm[pos] = r;
+        }
+        __syncthreads();
+        if (on) {
+            const int src = perm[r];
+            const double ls = lam[src];
+            const double root = (ls == 0.0) ? 0.0 : (p.order == 3 ? cbrt(ls) : pow(ls, 1.0 / p.order));
+            for (int n = 0; n < p.order; ++n) scale[n][r] = (ls == 0.0) ? 1.0 : root / nrm[n][src];
+            if (blockIdx.x == 0 && p.perm_out) {
+                p.perm_out[r] = src;
+                p.scale0_out[r] = scale[0][r];
+            }
+        }
+    } else if (tid < 32) {
         // warp 0, lane r: rank r's norms (shared memory) and lambda, the stable sort by shuffles
         const int r = tid;
         const bool on = r < p.R;
@@ -476,7 +669,7 @@ __global__ void gram_hadamard_kernel(const double* gram, int order, int R, int R
 
 namespace {
 int solve_blocks(const EvalWork& w, int n) {
-    const int rpb = kSolveThreads / w.RP;
+    const int rpb = w.RP > kMaxRank ? kSolveWideRows : kSolveThreads / w.RP;
     return (int)std::max<int64_t>(1, std::min<int64_t>((w.dims[n] + rpb - 1) / rpb, kSolveMaxBlocks));
 }
 GramPending pending_of(const EvalWork& w, int n) {
@@ -572,7 +765,13 @@ void chol_mode(EvalWork& w, int n, int pending, int* status, cudaStream_t st) {
     switch (w.RP) {
         case 8: chol_kernel<8><<<1, kCholThreads, 0, st>>>(p); break;
         case 16: chol_kernel<16><<<1, kCholThreads, 0, st>>>(p); break;
-        default: chol_kernel<32><<<1, kCholThreads, 0, st>>>(p); break;
+        case 32: chol_kernel<32><<<1, kCholThreads, 0, st>>>(p); break;
+        default: {
+            const size_t sm = sizeof(double) * 2 * kMaxRankWide * kMaxRankWide;
+            CPFIT_CUDA(cudaFuncSetAttribute(chol_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            chol_wide_kernel<<<1, kCholThreads, sm, st>>>(p);
+            break;
+        }
     }
     CPFIT_CUDA(cudaGetLastError());
 }
@@ -602,7 +801,13 @@ void solve_gram(EvalWork& w, int n, const double* M, int layout, int64_t ld, dou
     switch (w.RP) {
         case 8: solve_gram_kernel<8><<<grid, kSolveThreads, 0, st>>>(p); break;
         case 16: solve_gram_kernel<16><<<grid, kSolveThreads, 0, st>>>(p); break;
-        default: solve_gram_kernel<32><<<grid, kSolveThreads, 0, st>>>(p); break;
+        case 32: solve_gram_kernel<32><<<grid, kSolveThreads, 0, st>>>(p); break;
+        default: {
+            const size_t sm = sizeof(double) * (kMaxRankWide * kMaxRankWide + kSolveWideRows * (kMaxRankWide + 1));
+            CPFIT_CUDA(cudaFuncSetAttribute(solve_gram_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            solve_gram_wide_kernel<<<grid, kSolveWideRows, sm, st>>>(p);
+            break;
+        }
     }
     CPFIT_CUDA(cudaGetLastError());
 }
@@ -651,7 +856,7 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
     const int N = t.order;
     // Gamma_0 from the Grams of u; each later Gamma_n as soon as G_{n-1}' exists (side stream)
     chol_mode(w, 0, -1, status, st);
-    if (rowwise(t)) {
+    if (rowwise(t, w)) {
         for (int n = 0; n < N; ++n) {
             if (n > 0) fork_chol(w, n, status, st);
             // mode 0: the M0 the evaluation of this iterate produced ([i][RP]), when given
@@ -696,8 +901,8 @@ void als_sweep_device_ws(const DevTensor& t, EvalWork& w, const double* u, doubl
     // Gram still in solve partials: finalize_gram_side) and normalises afterwards
     // (normalize_grad), so S never needs the rescale below
     if (defer_norm) return;
-    normalize_device(w, work, out, st, N - 1, keep_s && !rowwise(t), grams_given);
-    if (keep_s && !rowwise(t)) {
+    normalize_device(w, work, out, st, N - 1, keep_s && !rowwise(t, w), grams_given);
+    if (keep_s && !rowwise(t, w)) {
         const int blocks = (int)std::min<int64_t>(8 * 148, (t.J * w.RP + 255) / 256);
         switch (w.RP) {
             case 8: s_rescale_kernel<8><<<blocks, 256, 0, st>>>(w.S, t.J, w.R, w.nperm, w.nscale0); break;

@@ -156,7 +156,7 @@ int64_t packed_len(int order, const int64_t* dims, int64_t R) {
 
 void check_rank(int64_t R) {
     if (R < 1) throw std::invalid_argument("KruskalTensor: rank must be >= 1");
-    if (R > kMaxRank) throw std::invalid_argument("device path supports rank <= 32");
+    if (R > kMaxRankWide) throw std::invalid_argument("device path supports rank <= 64");
 }
 
 void check_finite(const double* u, int64_t n) {
@@ -696,8 +696,9 @@ int cpfit_line_polynomial(cpfit_tensor t, int64_t rank, const double* u_bar, con
     return guard([&] {
         std::lock_guard<std::mutex> lk(t->mu);
         check_rank(rank);
-        if (!cpfit_gpu::poly_supported(*t->t))
-            throw std::invalid_argument("line polynomial: order-3 (dense or sparse) or dense order-4 tensors only");
+        if (!cpfit_gpu::poly_supported(*t->t) || rank > cpfit_gpu::kMaxRank)
+            throw std::invalid_argument(
+                "line polynomial: order-3 (dense or sparse) or dense order-4 tensors, rank <= 32, only");
         if (n < 0) throw std::invalid_argument("line polynomial: n >= 0");
         EvalWork& w = t->work((int)rank);
         check_finite(u_bar, w.nu);
@@ -820,7 +821,8 @@ int cpfit_bench_kernel(cpfit_tensor t, int64_t rank, const double* u, int kind, 
         cudaEvent_t e0, e1;
         CPFIT_CUDA(cudaEventCreate(&e0));
         CPFIT_CUDA(cudaEventCreate(&e1));
-        if (kind >= 3 && rowwise(*t->t)) throw std::invalid_argument("fiber-pass kinds need a dense tensor");
+        if (kind >= 3 && (rowwise(*t->t) || rank > kMaxRank))
+            throw std::invalid_argument("fiber-pass kinds need a dense tensor and rank <= 32");
         if (kind >= 3) grams_device(w, du, t->st);
         auto call = [&] {
             switch (kind) {

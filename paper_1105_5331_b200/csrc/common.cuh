@@ -25,7 +25,8 @@ cudaError_t guard_free(void* p);
 namespace cpfit_gpu {
 
 constexpr int kMaxOrder = 8;   // tensor order supported on device
-constexpr int kMaxRank = 32;   // R <= 32 (RP = R rounded up to 8)
+constexpr int kMaxRank = 32;   // the fibre-tile / level / polynomial kernels: R <= 32 (RP = R rounded up to 8)
+constexpr int kMaxRankWide = 64;  // ranks 33..64 (RP = 64) run the per-mode ("rowwise") path
 constexpr int kMaxWindow = 112;  // N-GMRES window: the 2m x m damped system of accelerate in shared memory
 
 struct cuda_error : std::runtime_error {

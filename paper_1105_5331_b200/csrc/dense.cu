@@ -857,13 +857,15 @@ __global__ void grad_kernel(const GradParams p) {
         if (n == 0) inner += m * p.u[e];
         if (p.need_grad) {
             const double* a = p.u + p.off[n];
-            double av[kMaxRank];  // row i of A_n, loaded before the in-order dot product
-#pragma unroll
-            for (int q = 0; q < kMaxRank; ++q) av[q] = q < p.R ? a[(int64_t)q * In + i] : 0.0;
             double ag = 0.0;
+            for (int q0 = 0; q0 < p.R; q0 += kMaxRank) {  // one chunk for R <= 32, two above
+                double av[kMaxRank];  // row i of A_n, loaded before the in-order dot product
 #pragma unroll
-            for (int q = 0; q < kMaxRank; ++q)
-                if (q < p.R) ag += av[q] * gsm[n * RR + q * p.R + r];
+                for (int q = 0; q < kMaxRank; ++q) av[q] = q0 + q < p.R ? a[(int64_t)(q0 + q) * In + i] : 0.0;
+#pragma unroll
+                for (int q = 0; q < kMaxRank; ++q)
+                    if (q0 + q < p.R) ag += av[q] * gsm[n * RR + (q0 + q) * p.R + r];
+            }
             const double gv = -m + ag;
             p.g[e] = gv;
             g2 += gv * gv;
@@ -943,7 +945,7 @@ void generic_plan(const DevTensor& t, int RP, int n, int* gx, int64_t* cols_per_
 // every mode's M_n (only_mode < 0) or one mode's into w.sp_part, for a rowwise tensor
 void rowwise_modes(const DevTensor& t, EvalWork& w, const double* u, int only_mode, cudaStream_t st,
                    int skip_mode = -1) {
-    if (t.generic)
+    if (generic_dense(t, w))
         generic_all_modes(t, w, u, only_mode, st, skip_mode);
     else
         sparse_all_modes(t, w, u, only_mode, st, skip_mode);
@@ -962,12 +964,15 @@ bool fiber_path_fits(int order, int64_t I0) {
 // ---------------------------------------------------------------------------------------
 
 EvalWork* work_create(const DevTensor& t, int R) {
-    if (R < 1 || R > kMaxRank) throw std::invalid_argument("device path supports 1 <= rank <= 32");
+    if (R < 1 || R > kMaxRankWide) throw std::invalid_argument("device path supports 1 <= rank <= 64");
     auto* w = new EvalWork();
     // freed by work_destroy if a later allocation or shape check throws
     std::unique_ptr<EvalWork, void (*)(EvalWork*)> owner(w, work_destroy);
     w->R = R;
-    w->RP = (R <= 8) ? 8 : (R <= 16 ? 16 : 32);  // power of two: per-fiber lane groups
+    // power of two: per-fiber lane groups; ranks above 32 (RP = 64) run the per-mode path
+    w->RP = (R <= 8) ? 8 : (R <= 16 ? 16 : (R <= 32 ? 32 : 64));
+    if (sizeof(double) * t.order * R * R > 220 * 1024)  // grad_kernel stages every Gamma_n
+        throw std::invalid_argument("device path: order * rank^2 too large for the gradient epilogue");
     w->order = t.order;
     w->off[0] = 0;
     for (int n = 0; n < t.order; ++n) {
@@ -987,7 +992,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
     CPFIT_CUDA(cudaMalloc(&w->gram, sizeof(double) * (size_t)t.order * w->RP * w->RP));
     w->red_grid = sms * 2;
     CPFIT_CUDA(cudaMalloc(&w->red, sizeof(double) * 3 * (size_t)w->red_grid));
-    if (!rowwise(t)) {  // reduce_grad: one block per 32 outputs of M_0 .. M_{N-1}
+    if (!rowwise(t, *w)) {  // reduce_grad: one block per 32 outputs of M_0 .. M_{N-1}
         int64_t b = (w->RP * 32 * (int64_t)((t.dims[0] + 31) / 32) + 31) / 32;
         for (int n = 1; n < t.order; ++n) b += (t.dims[n] * w->RP + 31) / 32;
         w->rg_blocks = b;
@@ -996,8 +1001,8 @@ EvalWork* work_create(const DevTensor& t, int R) {
     // ALS solve Gram partials: <= 148 blocks per mode (als.cu solve_blocks)
     w->solve_part_stride = (int64_t)148 * (R * (R + 1) / 2);
     CPFIT_CUDA(cudaMalloc(&w->solve_part, sizeof(dd) * (size_t)t.order * w->solve_part_stride));
-    CPFIT_CUDA(cudaMalloc(&w->nperm, sizeof(int) * kMaxRank));
-    CPFIT_CUDA(cudaMalloc(&w->nscale0, sizeof(double) * kMaxRank));
+    CPFIT_CUDA(cudaMalloc(&w->nperm, sizeof(int) * kMaxRankWide));
+    CPFIT_CUDA(cudaMalloc(&w->nscale0, sizeof(double) * kMaxRankWide));
     w->chol_stride = (int64_t)R * R + R + 1;
     CPFIT_CUDA(cudaMalloc(&w->chol, sizeof(double) * (size_t)t.order * w->chol_stride));
     CPFIT_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
@@ -1008,7 +1013,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
     CPFIT_CUDA(cudaMemset(w->counter, 0, sizeof(unsigned int) * kCounters));
     CPFIT_CUDA(cudaMalloc(&w->lvl_cnt, sizeof(unsigned int) * kLvlCounters));
     CPFIT_CUDA(cudaMemset(w->lvl_cnt, 0, sizeof(unsigned int) * kLvlCounters));
-    if (!rowwise(t)) {
+    if (!rowwise(t, *w)) {
         if (t.order < 2) throw std::invalid_argument("device dense path needs order >= 2");
         const int I0 = (int)t.dims[0];
         w->fiber_nchunk = (I0 + 31) / 32;
@@ -1105,7 +1110,7 @@ EvalWork* work_create(const DevTensor& t, int R) {
         CPFIT_CUDA(cudaMalloc(&w->sp_part, sizeof(double) * (size_t)tot));
         w->m0_rowwise = true;
         CPFIT_CUDA(cudaMalloc(&w->frows, sizeof(double) * (size_t)tot));
-        if (t.generic) {
+        if (generic_dense(t, *w)) {
             int64_t most = 1;
             for (int n = 0; n < t.order; ++n) {
                 int gx, gy;
@@ -1177,7 +1182,7 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
     p.d = d;
     p.gram = w.gram;
     p.need_grad = need_grad ? 1 : 0;
-    if (rowwise(t)) {
+    if (rowwise(t, w)) {
         p.sp_out = w.sp_part;
         int64_t acc = 0;
         for (int n = 0; n < t.order; ++n) {
@@ -1191,7 +1196,7 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
     }
     p.red = w.red;
     p.f_part = w.f_part;
-    p.f_grid = t.sparse ? 0 : (t.generic ? w.gen_fgrid : w.fiber_grid);
+    p.f_grid = t.sparse ? 0 : (generic_dense(t, w) ? w.gen_fgrid : w.fiber_grid);
     p.sparse = t.sparse ? 1 : 0;
     p.norm_sq = t.dscal + 1;
     p.sc = sc;
@@ -1199,7 +1204,10 @@ void run_grad(const DevTensor& t, EvalWork& w, const double* u, double* g, const
     p.counter = w.counter + kCounterGrad;
     // enough blocks to cover n_u once (latency-bound epilogue, no grid-stride tail)
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(w.red_grid, (w.nu + 255) / 256));
-    grad_kernel<<<blocks, 256, sizeof(double) * t.order * w.R * w.R, st>>>(p);
+    const size_t gsmem = sizeof(double) * t.order * w.R * w.R;  // > 48 KB only for ranks above 32
+    if (gsmem > 48 * 1024)
+        CPFIT_CUDA(cudaFuncSetAttribute(grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
+    grad_kernel<<<blocks, 256, gsmem, st>>>(p);
     CPFIT_CUDA(cudaGetLastError());
 }
 }  // namespace
@@ -1239,7 +1247,7 @@ void eval_device(const DevTensor& t, EvalWork& w, const double* u, double* g, Ev
                  cudaEvent_t grad_dep, int rowwise_skip) {
     (void)status;
     if (!grams_given) grams_device(w, u, st);
-    if (!rowwise(t)) {
+    if (!rowwise(t, w)) {
         // fused pass: S, M0 partials and per-fiber objective — or, when w.S already holds
         // T x_1 A0(u), M0 and the objective only (no S contraction)
         if (s_given)
@@ -1377,7 +1385,7 @@ void mttkrp3_last_only(EvalWork& w, const double* u, double* out, cudaStream_t s
 void mttkrp_device(const DevTensor& t, EvalWork& w, const double* u, int mode, double* out, cudaStream_t st) {
     const int64_t In = t.dims[mode];
     const int blocks = (int)std::min<int64_t>(1024, (In * w.R + 255) / 256);
-    if (rowwise(t)) {
+    if (rowwise(t, w)) {
         rowwise_modes(t, w, u, mode, st);
         int64_t off = 0;
         for (int n = 0; n < mode; ++n) off += t.dims[n] * w.RP;

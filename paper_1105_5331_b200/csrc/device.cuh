@@ -239,6 +239,11 @@ void poly_point_device(EvalWork& w, const PolyWork& pw, const double* ub, const 
 // phi(alphas[i]), phi'(alphas[i]) (device arrays)
 void poly_eval_device(const PolyWork& pw, const double* alphas, int n, double* phi, double* dphi, cudaStream_t st);
 
+// Routing with the workspace's rank: ranks above kMaxRank (RP = 64) take the per-mode path on
+// every tensor (a dense one through the generic kernels, csrc/generic.cu)
+inline bool rowwise(const DevTensor& t, const EvalWork& w) { return rowwise(t) || w.RP > kMaxRank; }
+inline bool generic_dense(const DevTensor& t, const EvalWork& w) { return t.generic || (!t.sparse && w.RP > kMaxRank); }
+
 // Accelerate (ngmres.cpp:27-63) on device.
 struct AccelWork {
     int64_t n = 0;

@@ -68,12 +68,16 @@ __device__ __forceinline__ int64_t column_base(const GenParams& p, int64_t c, in
     return idx[0] + p.ldT * (lp + p.Lp * p.In * t);
 }
 
+// RP = 64 (ranks above 32): the residual's A_0 row lives in shared memory ([r][thread], the
+// accumulators alone fill half the register file)
 template <int RP>
 __global__ void __launch_bounds__(kGenThreads) gen_mttkrp_kernel(const GenParams p) {
+    constexpr bool A0S = RP > 32;
     __shared__ double Ws[kCols][RP + 1];
     __shared__ int64_t base[kCols];
     __shared__ int cidx[kCols][kMaxOrder];
     __shared__ double fred[kGenThreads / 32];
+    extern __shared__ double a0sm[];  // A0S: [RP][blockDim.x]
     const int tid = threadIdx.x;
     const int64_t i = (int64_t)blockIdx.y * blockDim.x + tid;
     const bool row_ok = i < p.In;
@@ -82,12 +86,19 @@ __global__ void __launch_bounds__(kGenThreads) gen_mttkrp_kernel(const GenParams
     double acc[RP];
 #pragma unroll
     for (int r = 0; r < RP; ++r) acc[r] = 0.0;
-    double a0[RP];
+    double a0[A0S ? 1 : RP];
     double fs = 0.0;
     if (p.fpart) {
 #pragma unroll
-        for (int r = 0; r < RP; ++r) a0[r] = (row_ok && r < p.R) ? p.u[p.uoff[0] + (int64_t)r * p.In + i] : 0.0;
+        for (int r = 0; r < RP; ++r) {
+            const double v = (row_ok && r < p.R) ? p.u[p.uoff[0] + (int64_t)r * p.In + i] : 0.0;
+            if (A0S)
+                a0sm[r * blockDim.x + tid] = v;
+            else
+                a0[r] = v;
+        }
     }
+    auto a0v = [&](int r) { return A0S ? a0sm[r * blockDim.x + tid] : a0[r]; };
     for (int64_t cc = c0; cc < c1; cc += kCols) {
         const int nc = (int)((c1 - cc < kCols) ? c1 - cc : kCols);
         __syncthreads();  // the previous chunk's W is consumed
@@ -116,7 +127,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mttkrp_kernel(const GenParams
                     if (p.fpart) {
                         double m = 0.0;
 #pragma unroll
-                        for (int r = 0; r < RP; ++r) m += a0[r] * Ws[k + q][r];
+                        for (int r = 0; r < RP; ++r) m += a0v(r) * Ws[k + q][r];
                         const double d = x[q] - m;
                         fs += d * d;
                     }
@@ -129,7 +140,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_mttkrp_kernel(const GenParams
                 if (p.fpart) {
                     double m = 0.0;
 #pragma unroll
-                    for (int r = 0; r < RP; ++r) m += a0[r] * Ws[k][r];
+                    for (int r = 0; r < RP; ++r) m += a0v(r) * Ws[k][r];
                     const double d = x - m;
                     fs += d * d;
                 }
@@ -216,7 +227,14 @@ void generic_all_modes(const DevTensor& t, EvalWork& w, const double* u, int onl
             switch (w.RP) {
                 case 8: gen_mttkrp_kernel<8><<<grid, th, 0, st>>>(p); break;
                 case 16: gen_mttkrp_kernel<16><<<grid, th, 0, st>>>(p); break;
-                default: gen_mttkrp_kernel<32><<<grid, th, 0, st>>>(p); break;
+                case 32: gen_mttkrp_kernel<32><<<grid, th, 0, st>>>(p); break;
+                default: {
+                    const size_t sm = p.fpart ? sizeof(double) * 64 * th : 0;
+                    CPFIT_CUDA(cudaFuncSetAttribute(gen_mttkrp_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)sm));
+                    gen_mttkrp_kernel<64><<<grid, th, sm, st>>>(p);
+                    break;
+                }
             }
             CPFIT_CUDA(cudaGetLastError());
             const int64_t ne = In * w.RP;

@@ -701,7 +701,7 @@ void Solver::construct(DevTensor* t, int R, const SolverOptions& o) {
         alloc(&wu_, n_ * cap_);
         alloc(&wg_, n_ * cap_);
         {  // M0 at the current / bar / best-trial / accepted point (rowwise: [I_0][RP] copies of sp_part)
-            m0_n_ = rowwise(*t) ? (int64_t)w_->RP * t->dims[0] : (int64_t)w_->RP * 32 * w_->fiber_nchunk;
+            m0_n_ = rowwise(*t, *w_) ? (int64_t)w_->RP * t->dims[0] : (int64_t)w_->RP * 32 * w_->fiber_nchunk;
             alloc(&m0_cur_, m0_n_);
             alloc(&m0_bar_, m0_n_);
             alloc(&m0_best_, m0_n_);
@@ -722,7 +722,8 @@ void Solver::construct(DevTensor* t, int R, const SolverOptions& o) {
     norm_nb_ = (int)std::min<int64_t>(296, (n_ + 255) / 256);
     // exact polynomial line search: dense order 3, default objective handling, not disabled
     const char* np = std::getenv("CPFIT_NO_POLY_LS");
-    if ((method_ == 0 || method_ == 2) && poly_supported(*t) && !o.reeval_accepted && !o.residual_objective &&
+    if ((method_ == 0 || method_ == 2) && poly_supported(*t) && w_->RP <= kMaxRank && !o.reeval_accepted &&
+        !o.residual_objective &&
         !(np && np[0] == '1'))
         pw_ = poly_create(*t, *w_);
     if (const char* e = std::getenv("CPFIT_PHASE_PROFILE"); e && e[0] == '1') {
@@ -950,7 +951,7 @@ void Solver::build_graphs() {
         // stand-alone ALS iteration (als.cpp:79-95)
         // the previous evaluation (of u) left M0(u) in w.m0 for dense tensors
         als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st2_, m0_src(), true, gout_);
-        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid, !rowwise(*t_), gout_);
+        eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st2_, true, &s->resid, !rowwise(*t_, *w_), gout_);
     }
     if (method_ != 2) {
         k_commit<<<1, 1, 0, st2_>>>(c, loop_h);
@@ -1027,7 +1028,7 @@ void Solver::emit_bar(cudaStream_t st, const void* ctl) {
         return;
     }
     als_sweep_device_ws(*t_, *w_, u_, ub_, work_, mbuf_, status, st, m0_cur_, true, gout_);
-    eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st, true, &s->resid, !rowwise(*t_), gout_);
+    eval_device(*t_, *w_, ub_, gb_, sc_bar, nullptr, status, st, true, &s->resid, !rowwise(*t_, *w_), gout_);
     if (m0_bar_) CPFIT_CUDA(cudaMemcpyAsync(m0_bar_, m0_src(), sizeof(double) * m0_n_, cudaMemcpyDeviceToDevice, st));
     if (gout_) CPFIT_CUDA(cudaMemcpyAsync(gram_bar_, w_->gram, gram_bytes(), cudaMemcpyDeviceToDevice, st));
 }
@@ -1166,7 +1167,7 @@ void Solver::run_loop_eager() {
             continue;
         } else {
             als_sweep_device_ws(*t_, *w_, u_, un_, work_, mbuf_, status, st_, m0_src(), true, gout_);
-            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid, !rowwise(*t_), gout_);
+            eval_device(*t_, *w_, un_, gn_, sc_next, nullptr, status, st_, true, &s->resid, !rowwise(*t_, *w_), gout_);
         }
         k_commit<<<1, 1, 0, st_>>>(c, none);
         k_commit_vec<<<vb, 256, 0, st_>>>(s, method_ == 1, ub_, gb_, un_, gn_, u_, g_, wu_, wg_, ubest_, n_, m0_bar_,

@@ -620,12 +620,13 @@ void sparse_all_modes(const DevTensor& t, EvalWork& w, const double* u, int only
         p.nother = k;
         p.R = w.R;
         p.out = w.sp_part + off[n];
-        if (!sp_v1()) {
+        if (!sp_v1() || w.RP > 32) {
             const uint32_t* pk = t.modes->pidx[n];
             switch (w.RP) {
                 case 8: launch_sp2<8>(p, pk, N, st); break;
                 case 16: launch_sp2<16>(p, pk, N, st); break;
-                default: launch_sp2<32>(p, pk, N, st); break;
+                case 32: launch_sp2<32>(p, pk, N, st); break;
+                default: launch_sp2<64>(p, pk, N, st); break;
             }
             CPFIT_CUDA(cudaGetLastError());
             continue;

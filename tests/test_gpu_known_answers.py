@@ -171,7 +171,7 @@ def test_shape_and_rank_errors(gpu):
     with pytest.raises(ValueError):
         t.mttkrp(np.ones(9 * 2), 3)  # mode out of range
     with pytest.raises(ValueError):
-        P.objective(t, np.ones(9 * 33))  # rank above the device limit
+        P.objective(t, np.ones(9 * 65))  # rank above the device limit (64)
     with pytest.raises(ValueError):
         P.DataTensor.dense(np.ones(5), (2, 3))  # value count
     with pytest.raises(ValueError):
