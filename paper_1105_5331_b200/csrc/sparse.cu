@@ -552,12 +552,8 @@ void upload_sparse_modes(DevTensor& t, const std::vector<int64_t>& coords, const
         const std::vector<int32_t>& oidx = oidxs[(size_t)n];
         const std::vector<double>& sv = svs[(size_t)n];
         CPFIT_CUDA(cudaMalloc(&sm->rowptr[n], sizeof(int64_t) * rowptr.size()));
-        // one zero slot past the end (value 0, index 0): pipeline slots past a segment's end load
-        // it instead of being predicated off
-        CPFIT_CUDA(cudaMalloc(&sm->oidx[n], sizeof(int32_t) * (oidx.size() + 1)));
-        CPFIT_CUDA(cudaMalloc(&sm->vals[n], sizeof(double) * (sv.size() + 1)));
-        CPFIT_CUDA(cudaMemsetAsync(sm->oidx[n] + oidx.size(), 0, sizeof(int32_t), st));
-        CPFIT_CUDA(cudaMemsetAsync(sm->vals[n] + sv.size(), 0, sizeof(double), st));
+        CPFIT_CUDA(cudaMalloc(&sm->oidx[n], sizeof(int32_t) * std::max<size_t>(oidx.size(), 1)));
+        CPFIT_CUDA(cudaMalloc(&sm->vals[n], sizeof(double) * std::max<size_t>(sv.size(), 1)));
         CPFIT_CUDA(cudaMemcpyAsync(sm->rowptr[n], rowptr.data(), sizeof(int64_t) * rowptr.size(), cudaMemcpyHostToDevice, st));
         if (nnz > 0) {
             CPFIT_CUDA(cudaMemcpyAsync(sm->oidx[n], oidx.data(), sizeof(int32_t) * oidx.size(), cudaMemcpyHostToDevice, st));
@@ -572,8 +568,7 @@ void upload_sparse_modes(DevTensor& t, const std::vector<int64_t>& coords, const
                 uint32_t* pk = pidxs[(size_t)n].data();
                 const int32_t* o = oidx.data();
                 for (int64_t j = 0; j < nnz; ++j) pk[j] = (uint32_t)o[j] | ((uint32_t)o[nnz + j] << 16);
-                CPFIT_CUDA(cudaMalloc(&sm->pidx[n], sizeof(uint32_t) * ((size_t)nnz + 1)));
-                CPFIT_CUDA(cudaMemsetAsync(sm->pidx[n] + nnz, 0, sizeof(uint32_t), st));
+                CPFIT_CUDA(cudaMalloc(&sm->pidx[n], sizeof(uint32_t) * (size_t)nnz));
                 CPFIT_CUDA(cudaMemcpyAsync(sm->pidx[n], pk, sizeof(uint32_t) * (size_t)nnz, cudaMemcpyHostToDevice, st));
             }
         }
